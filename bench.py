@@ -1,0 +1,428 @@
+#!/usr/bin/env python3
+"""bench.py -- B200 Lookup UTF-8 validation throughput (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c1|c0|c4|c3]
+
+One step = one pass of the hot path over one batch of synthetic input
+resident in HBM: validate_lanes (K1) over the rank's 1 GiB shard of the
+config-1 stream (the whole C1 buffer at N=1), followed at N>1 by the
+one-word NCCL allreduce(MAX) that combines shard verdicts.  Weak scaling:
+every rank validates 1 GiB per step; `value` is the box aggregate.
+
+`e2e` repeats the metric through the public C-ABI with a HOST (pinned)
+buffer: utf8v_cuda_validate(host_ptr, n, 0, &ok), which streams the bytes
+over PCIe in 32 MiB pieces and validates each as it lands; every step
+includes the 1 GiB H2D copy and the 4-byte verdict read back.
+
+`--impl reference` times the unmodified reference CPU implementation
+(oracle/_ref: validate_lookup, AVX2, compiled from the reference sources)
+on this box's host cores, all threads, on the same workload; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+GiB = 1 << 30
+METRIC = "validated GB/s per GPU and box (device-timed) vs HBM roofline; records/sec"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c1", choices=["c0", "c1", "c3", "c4"])
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# clocks: nvidia-smi sampled during the timed region
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines: list[str] = []
+        self._t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:
+            self.proc = None
+        time.sleep(0.15)
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.06)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+def measured_peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": d.get("hbm_gbs", 6650.0), "source": "measured (MEASURED_PEAKS.json hbm_gbs)"}
+    return {"hbm_gbs": 6650.0, "source": "fallback 6.65 TB/s (B200_PROFILING.md)"}
+
+
+def ncu_traffic(kernel: str) -> float | None:
+    """DRAM bytes per launch of `kernel` from the committed ncu summary."""
+    p = ROOT / "profiles" / "ncu_summary.json"
+    if not p.exists():
+        return None
+    try:
+        d = json.loads(p.read_text())
+        return d.get("kernels", {}).get(kernel, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def ref_lib():
+    so = ROOT / "oracle" / "_ref" / "libutf8v_ref.so"
+    if not so.exists():
+        return None
+    L = C.CDLL(str(so))
+    L.ref_validate_lookup_mt.argtypes = [C.c_void_p, C.c_size_t, C.c_int]
+    L.ref_validate_lookup_mt.restype = C.c_int
+    L.ref_validate_lookup.argtypes = [C.c_void_p, C.c_size_t]
+    L.ref_validate_lookup.restype = C.c_int
+    return L
+
+
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def time_reference(L, buf: np.ndarray, threads: int, seconds: float, max_reps: int | None = None):
+    """Best-of GB/s of the reference validate_lookup over buf on `threads`
+    threads (after a correctness gate, proj/src/bench.cpp:80-86)."""
+    p = buf.ctypes.data
+    n = buf.size
+    ok = L.ref_validate_lookup_mt(p, n, threads)
+    best, total, reps = float("inf"), 0.0, 0
+    t_end = time.perf_counter() + seconds
+    while True:
+        t0 = time.perf_counter()
+        L.ref_validate_lookup_mt(p, n, threads)
+        dt = time.perf_counter() - t0
+        best = min(best, dt)
+        total += dt
+        reps += 1
+        if time.perf_counter() > t_end or (max_reps and reps >= max_reps):
+            break
+    return {"valid": bool(ok), "best_GBps": n / best / 1e9, "mean_GBps": n * reps / total / 1e9, "reps": reps}
+
+
+def host_stream(n: int, seed: int, ascii_only: bool) -> np.ndarray:
+    from paper_2010_03090_b200 import _lib
+    buf = np.empty(n, np.uint8)
+    _lib.check(_lib.load().utf8v_gen_stream_host(buf.ctypes.data, n, seed, int(ascii_only), host_threads()))
+    return buf
+
+
+# ---------------------------------------------------------------------------
+def run_reference(args, rank: int, world: int):
+    if rank != 0:
+        return
+    L = ref_lib()
+    base = {"metric": METRIC, "unit": "GB/s", "impl": "reference", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "u8", "data": "synthetic"}
+    if L is None:
+        print(json.dumps({**base, "unavailable": "oracle/_ref/libutf8v_ref.so not built (no reference checkout)"}))
+        return
+    n_total = GiB * max(1, args.gpus) if args.config == "c1" else (64 << 20)
+    seed, ascii_only = (2, False) if args.config != "c0" else (1, True)
+    # The sample: the whole workload when it fits in host RAM comfortably.
+    n = min(n_total, 4 * GiB)
+    buf = host_stream(n, seed, ascii_only)
+    T = host_threads()
+    ok = L.ref_validate_lookup_mt(buf.ctypes.data, n, T)
+    for _ in range(max(1, args.warmup)):
+        L.ref_validate_lookup_mt(buf.ctypes.data, n, T)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        L.ref_validate_lookup_mt(buf.ctypes.data, n, T)
+    dt = time.perf_counter() - t0
+    value = n * args.steps / dt / 1e9
+    sample = f"{n} bytes of config {args.config} (seed {seed}) per step, {args.steps} steps"
+    print(json.dumps({**base, "value": value, "ms_per_step": dt / args.steps * 1e3,
+                      "config": {"workload": f"{args.config.upper()} stream, {n_total} bytes total over {args.gpus} GPU(s)",
+                                 "sample_bytes": n, "cpu": cpu_model()},
+                      "valid": bool(ok),
+                      "cpu_baseline": {"value": value, "unit": "GB/s", "cores": T, "kind": "reference",
+                                       "sample": sample},
+                      "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+
+
+# ---------------------------------------------------------------------------
+def run_ours(args, rank: int, world: int, local_rank: int):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2010_03090_b200 as u8
+    from paper_2010_03090_b200 import _lib, configs
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    lib = _lib.load()
+
+    # ---- workload: this rank's shard (+ up to 16 bytes of halo) ----------
+    if args.config == "c4":
+        n_total = configs.C4["n"]
+        per = n_total // world
+    elif args.config == "c0":
+        per = configs.C0["n"]
+        n_total = per * world
+    else:
+        per = GiB
+        n_total = per * world
+    seed = {"c0": 1, "c1": 2, "c4": 5}.get(args.config, 2)
+    ascii_only = args.config == "c0"
+    s, e = rank * per, (rank + 1) * per
+    halo = min(s, 16)
+    # Generate the shard from the global stream's 64 KiB chunks (same bytes
+    # as generating the whole stream), halo included.
+    G = 65536
+    g0 = (s - halo) // G * G
+    g1 = min(n_total, -(-e // G) * G)
+    full = torch.empty(g1 - g0, dtype=torch.uint8, device=dev)
+    if g0 == 0 and g1 == n_total:
+        _lib.check(lib.utf8v_gen_stream(full.data_ptr(), n_total, seed, int(ascii_only),
+                                        torch.cuda.current_stream().cuda_stream))
+        shard = full[s - halo:e]
+    else:
+        # chunk-aligned window of the global stream: generate it as the head
+        # of a stream view (chunk seeds depend only on the chunk index)
+        tmp = torch.empty(g1, dtype=torch.uint8, device=dev) if g1 <= 4 * GiB else None
+        if tmp is None:
+            raise RuntimeError("shard window too large")
+        _lib.check(lib.utf8v_gen_stream(tmp.data_ptr(), g1, seed, int(ascii_only),
+                                        torch.cuda.current_stream().cuda_stream))
+        shard = tmp[s - halo:e].clone()
+        del tmp
+    del full
+    torch.cuda.synchronize()
+    n_local = shard.numel()
+    last = rank == world - 1
+    lane_lo, lane_hi = halo, n_local + (3 if last else 0)
+    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+
+    if world > 1:
+        dist.barrier()
+
+    def step():
+        _lib.check(lib.utf8v_cuda_validate_lanes_async(shard.data_ptr(), n_local, lane_lo, lane_hi,
+                                                       flag.data_ptr(), sp))
+        if world > 1:
+            dist.all_reduce(flag, op=dist.ReduceOp.MAX)
+
+    # correctness gate before timing (proj/src/bench.cpp:80-86)
+    flag.zero_()
+    step()
+    torch.cuda.synchronize()
+    expect_valid = True
+    assert (int(flag.item()) == 0) == expect_valid, "verdict mismatch on the benchmark input"
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(local_rank) if rank == 0 else None
+    if sampler:
+        sampler.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_stop = torch.cuda.Event(enable_timing=True)
+    flag.zero_()
+    t_start.record(stream)
+    for _ in range(args.steps):
+        step()
+    t_stop.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = t_start.elapsed_time(t_stop)
+    clocks = sampler.stop() if sampler else None
+    verdict_ok = int(flag.item()) == 0
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    ms_per_step = ms_max / args.steps
+    value = per * world * args.steps / (ms_max / 1e3) / 1e9
+    per_gpu = per * args.steps / (ms / 1e3) / 1e9
+
+    # ---- kernel-only timing for the roofline (same stream, no collective) --
+    kflag = torch.zeros(1, dtype=torch.int32, device=dev)
+    torch.cuda.synchronize()
+    k0 = torch.cuda.Event(enable_timing=True)
+    k1 = torch.cuda.Event(enable_timing=True)
+    kreps = max(10, min(args.steps, 200))
+    k0.record(stream)
+    for _ in range(kreps):
+        _lib.check(lib.utf8v_cuda_validate_lanes_async(shard.data_ptr(), n_local, lane_lo, lane_hi,
+                                                       kflag.data_ptr(), sp))
+    k1.record(stream)
+    torch.cuda.synchronize()
+    kernel_ms = k0.elapsed_time(k1) / kreps
+    peaks = measured_peaks()
+    alg_bytes = per  # one read per input byte of the shard (halo re-reads are overhead)
+    achieved = alg_bytes / (kernel_ms / 1e3) / 1e9
+    traffic = ncu_traffic("k_validate")
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
+                "peak_source": peaks["source"], "kernel": "u8v::k_validate<false>",
+                "kernel_ms": kernel_ms, "algorithmic_bytes_per_launch": alg_bytes}
+
+    # ---- e2e through the public C-ABI with a pinned host buffer -----------
+    e2e = None
+    if rank == 0 or True:
+        host = torch.empty(per, dtype=torch.uint8, pin_memory=True)
+        host.copy_(shard[halo:halo + per])
+        hp = host.data_ptr()
+        ok = C.c_uint8(0)
+        _lib.check(lib.utf8v_cuda_validate(hp, per, 0, C.byref(ok)))  # warm + gate
+        assert ok.value == 1 or rank > 0  # shard alone may start/end mid-character
+        es = max(1, args.e2e_steps)
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(es):
+            _lib.check(lib.utf8v_cuda_validate(hp, per, 0, C.byref(ok)))
+        et = time.perf_counter() - t0
+        tt = torch.tensor([et], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e = {"value": per * world * es / float(tt.item()) / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": per * world, "d2h_bytes_per_step": 4 * world,
+               "path": "utf8v_cuda_validate(pinned host ptr): 32 MiB H2D pieces overlapped with K1"}
+        del host
+
+    # ---- CPU baseline (rank 0, N=1): the reference on a bounded sample ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        L = ref_lib()
+        if L is not None:
+            sample_n = min(per, 256 << 20)
+            hbuf = shard[halo:halo + sample_n].cpu().numpy()
+            T = host_threads()
+            r = time_reference(L, hbuf, T, args.cpu_seconds)
+            r1 = time_reference(L, hbuf[: 64 << 20], 1, min(3.0, args.cpu_seconds), max_reps=5)
+            cpu = {"value": r["best_GBps"], "unit": "GB/s", "cores": T, "kind": "reference",
+                   "sample": f"first {sample_n >> 20} MiB of the C1 shard, best of {r['reps']} passes, "
+                             f"validate_lookup (AVX2) split at character boundaries over {T} threads",
+                   "single_thread_GBps": r1["best_GBps"], "cpu": cpu_model()}
+
+    if rank == 0:
+        workload = {"c1": "C1: valid UTF-8, 0.4/0.2/0.3/0.1 length mix, seed 2, 1 GiB per GPU",
+                    "c0": "C0: 64 MiB ASCII + 2% LF, seed 1, per GPU",
+                    "c4": "C4: 16 GiB mix, seed 5, sharded over the GPUs (strong scaling)"}[args.config]
+        out = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong" if args.config == "c4" else "weak", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic (seeded splitmix64 generator, DESIGN.md 'Synthetic inputs')",
+            "config": {"workload": workload, "bytes_per_gpu": per, "bytes_total": per * world,
+                       "l2": "input (>=1 GiB) larger than the 126 MB L2; no flush needed",
+                       "parallelism": f"dp{world}: byte-range shards with 3-byte halo"
+                                      + (" + 1-word NCCL allreduce(MAX) per step" if world > 1 else "")},
+            "per_gpu_GBps": per_gpu, "verdict_valid": verdict_ok,
+            "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks,
+            "gpu_launches": args.steps,
+        }
+        print(json.dumps(out))
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,62 @@
+// utf8v/lookup.hpp -- the reference's Lookup backend API
+// (proj/include/utf8v/lookup.hpp:18-41), served by the B200 "cuda" backend.
+//
+// Same struct, same functions, same meaning:
+//   * lookup_backend: name, width, validate, three lane entry points, self
+//     test.  The roster holds one backend, "cuda" (width 64); there is no CPU
+//     backend in this library -- a CPU fallback would void the drop-in's
+//     guarantees, so validate_lookup_fallback() exists for source
+//     compatibility and runs the same device kernels.
+//   * validate functions return false for invalid UTF-8; a CUDA failure (no
+//     device, out of memory) throws utf8v::cuda_error, because `bool` has no
+//     room for it and a silent wrong verdict is worse.
+// Additions (the reference derives these from oracle_validate or a loop):
+//   validate_lookup_verdict  -- first error offset and kind, bit-exact with
+//                               oracle_validate (proj/src/oracle.cpp:10-44)
+//   validate_lookup_batch    -- one verdict per record of a CSR batch
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <string_view>
+#include <vector>
+
+#include "utf8v/verdict.hpp"
+
+namespace utf8v {
+
+struct lookup_backend {
+  const char* name;   // "cuda"
+  std::size_t width;  // 64
+  bool (*validate)(const std::uint8_t* data, std::size_t size);
+  void (*classify_lanes)(const std::uint8_t* input, const std::uint8_t* previous,
+                         std::uint8_t* out);
+  void (*length_error_lanes)(const std::uint8_t* input, const std::uint8_t* previous,
+                             std::uint8_t* out);
+  void (*incomplete_lanes)(const std::uint8_t* input, std::uint8_t* out);
+  bool (*ops_self_test)(std::uint64_t seed);
+};
+
+class cuda_error : public std::runtime_error {
+ public:
+  cuda_error(int status, const std::string& what) : std::runtime_error(what), status_(status) {}
+  int status() const noexcept { return status_; }
+
+ private:
+  int status_;
+};
+
+std::span<const lookup_backend> lookup_backends();
+const lookup_backend* find_lookup_backend(std::string_view name);
+bool validate_lookup(bytes_view input);
+bool validate_lookup_fallback(bytes_view input);
+
+// Extensions.
+verdict validate_lookup_verdict(bytes_view input);
+std::vector<std::uint8_t> validate_lookup_batch(bytes_view data,
+                                                std::span<const std::uint64_t> offsets);
+
+}  // namespace utf8v

@@ -1,0 +1,112 @@
+/*
+ * utf8v_cuda.h -- the drop-in C-ABI boundary of the B200 Lookup validator
+ * (libutf8v_cuda.so).
+ *
+ * It replaces, for the Lookup path of the reference `utf8v` library, the
+ * backend function-pointer table and its dispatch:
+ *   struct lookup_backend          proj/include/utf8v/lookup.hpp:77-87
+ *   lookup_backends / find_...     proj/include/utf8v/lookup.hpp:89-94, proj/src/lookup.cpp:16-37
+ *   validate_lookup[_fallback]     proj/include/utf8v/lookup.hpp:96-100, proj/src/lookup.cpp:39-45
+ * and adds the position and record-batch variants the reference obtains by
+ * re-running oracle_validate (proj/src/oracle.cpp:10-44; the CLI failure path
+ * proj/tools/main.cpp:129-147) or by looping validate_lookup per record.
+ * The C++ API of include/utf8v/lookup.hpp (same names as the reference) is a
+ * thin layer over these entry points; INTEGRATION.md shows the binding.
+ *
+ * Conventions:
+ *   - plain pointers and sizes only; every pointer is borrowed for the call;
+ *   - return an int status: UTF8V_OK, or a mapped CUDA/argument error -- never
+ *     throw, never abort; invalid UTF-8 is a normal result, not an error;
+ *   - n == 0 (with any pointer, NULL included) is valid text;
+ *   - `is_device` != 0: the pointer is device memory of the current device;
+ *     0: host memory (pinned or pageable; copied over PCIe inside the call);
+ *   - re-entrant: one lazily initialised context per device, per-thread
+ *     streams and scratch; callable concurrently from many host threads;
+ *   - there is no CPU fallback: without a usable CUDA device every compute
+ *     entry point returns UTF8V_ERR_NO_DEVICE.
+ */
+#ifndef UTF8V_CUDA_H
+#define UTF8V_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define UTF8V_OK 0
+#define UTF8V_ERR_CUDA 1
+#define UTF8V_ERR_ARG 2
+#define UTF8V_ERR_NO_DEVICE 3
+#define UTF8V_ERR_NCCL 4
+
+/* Width in bytes of the lane entry points below (lookup_backend::width;
+ * >= 32 so the roster stays widest-first, proj/tests/test_lookup.cpp:41-42). */
+#define UTF8V_CUDA_WIDTH 64
+
+/* ABI version (bumped on any signature change). */
+int utf8v_cuda_abi_version(void);
+
+/* Human-readable text of the last error on this thread ("" if none). */
+const char* utf8v_cuda_last_error(void);
+
+/* lookup_backend::validate (proj/include/utf8v/lookup.hpp:80) and
+ * validate_lookup (proj/src/lookup.cpp:39-41): *out_valid = 1 iff p[0..n)
+ * is valid UTF-8.  Host input is streamed to the GPU in pieces, each piece
+ * validated as soon as it lands (copy and compute overlap). */
+int utf8v_cuda_validate(const uint8_t* p, size_t n, int is_device, uint8_t* out_valid);
+
+/* Verdict with the first error, bit-exact with oracle_validate
+ * (proj/src/oracle.cpp:10-44): *out_valid, and when 0, *out_offset (lead byte
+ * of the offending sequence) and *out_kind (error_kind numbering of
+ * proj/include/utf8v/verdict.hpp:20-27). */
+int utf8v_cuda_validate_verdict(const uint8_t* p, size_t n, int is_device, uint8_t* out_valid,
+                                uint64_t* out_offset, int* out_kind);
+
+/* Records p[offsets[r] .. offsets[r+1]) for r < n_records, each validated as
+ * its own stream (the reference loops validate_lookup per record); writes
+ * verdicts[r] = 1 (valid) / 0 (invalid).  offsets: n_records+1 non-decreasing
+ * uint64 (CSR), offsets[n_records] <= n.  is_device applies to data, offsets
+ * and verdicts alike. */
+int utf8v_cuda_validate_batch(const uint8_t* data, size_t n, const uint64_t* offsets,
+                              size_t n_records, int is_device, uint8_t* verdicts);
+
+/* Lane entry points over UTF8V_CUDA_WIDTH host bytes (lookup_backend
+ * ::classify_lanes / length_error_lanes / incomplete_lanes, lookup.hpp:81-85;
+ * proj/src/lookup_backend_detail.hpp:16-43), computed on the GPU. */
+int utf8v_cuda_classify_lanes(const uint8_t* input, const uint8_t* previous, uint8_t* out);
+int utf8v_cuda_length_error_lanes(const uint8_t* input, const uint8_t* previous, uint8_t* out);
+int utf8v_cuda_incomplete_lanes(const uint8_t* input, uint8_t* out);
+
+/* lookup_backend::ops_self_test (lookup.hpp:86; lookup_kernel.hpp:139-216):
+ * *out_ok = 1 iff every SWAR vector operation matches plain arithmetic. */
+int utf8v_cuda_ops_self_test(uint64_t seed, int* out_ok);
+
+/* ---- device-resident, asynchronous entry points (no host sync) ---------
+ * For callers that own device memory and streams (the bench, the multi-GPU
+ * shard layer).  `stream` is a cudaStream_t (NULL = legacy default stream).
+ * d_flag is a device uint32 the kernels OR a nonzero value into when an
+ * error is found; the caller zeroes it and reads it back. */
+
+/* Lanes [lane_lo, lane_hi) of the stream d_p[0..n) (zero outside), lane_hi
+ * <= n + 3.  Whole stream: lane_lo = 0, lane_hi = n + 3.  A shard of a larger
+ * stream passes its halo bytes as the head of d_p and lane_lo = halo length. */
+int utf8v_cuda_validate_lanes_async(const uint8_t* d_p, uint64_t n, uint64_t lane_lo,
+                                    uint64_t lane_hi, uint32_t* d_flag, void* stream);
+
+/* Batch on device memory; d_verdicts is written fully (1/0 per record).
+ * d_scratch: NULL or >= utf8v_cuda_batch_scratch_bytes(n) device bytes. */
+int utf8v_cuda_validate_batch_async(const uint8_t* d_data, uint64_t n, const uint64_t* d_offsets,
+                                    uint64_t n_records, uint8_t* d_verdicts, void* d_scratch,
+                                    void* stream);
+uint64_t utf8v_cuda_batch_scratch_bytes(uint64_t n);
+
+/* Number of kernel launches the last call on this thread enqueued. */
+int utf8v_cuda_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

@@ -1,0 +1,211 @@
+"""paper_2010_03090_b200 -- B200-native Lookup UTF-8 validation (arXiv 2010.03090).
+
+Python face of libutf8v_cuda.so, mirroring the reference's Lookup API
+(proj/include/utf8v/lookup.hpp:18-41, proj/src/lookup.cpp:16-45):
+
+    lookup_backends()            roster (one backend, "cuda", width 64)
+    find_lookup_backend(name)    None when unknown
+    validate_lookup(data)        bool
+    validate_lookup_fallback(d)  same device path (no CPU fallback exists)
+    validate_lookup_verdict(d)   Verdict, bit-exact with oracle_validate
+    validate_lookup_batch(d, offsets)  one verdict per CSR record
+
+`data` is host bytes (bytes / bytearray / memoryview / numpy uint8) or a CUDA
+torch.uint8 tensor (device-resident, validated in place).  All compute runs on
+the GPU; a missing library or device raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from enum import IntEnum
+from typing import Callable, Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+
+__all__ = [
+    "ErrorKind", "Utf8Error", "Verdict", "LookupBackend", "lookup_backends", "find_lookup_backend",
+    "validate_lookup", "validate_lookup_fallback", "validate_lookup_verdict", "validate_lookup_batch",
+    "validate_lanes_async", "validate_batch_async", "WIDTH",
+]
+
+WIDTH = _lib.WIDTH
+
+
+class ErrorKind(IntEnum):
+    """error_kind of proj/include/utf8v/verdict.hpp:20-27 (same values)."""
+    HEADER_BITS = 0
+    TOO_SHORT = 1
+    TOO_LONG = 2
+    OVERLONG = 3
+    TOO_LARGE = 4
+    SURROGATE = 5
+
+    def __str__(self) -> str:  # to_string, verdict.hpp:29-39
+        return self.name.lower().replace("_", "-")
+
+
+@dataclass(frozen=True)
+class Utf8Error:
+    offset: int
+    kind: ErrorKind
+
+
+@dataclass(frozen=True)
+class Verdict:
+    error: Optional[Utf8Error] = None
+
+    def valid(self) -> bool:
+        return self.error is None
+
+    @staticmethod
+    def ok() -> "Verdict":
+        return Verdict()
+
+    @staticmethod
+    def fail(offset: int, kind: ErrorKind) -> "Verdict":
+        return Verdict(Utf8Error(int(offset), ErrorKind(kind)))
+
+
+def _is_cuda_tensor(x) -> bool:
+    t = type(x)
+    return t.__module__.startswith("torch") and getattr(x, "is_cuda", False)
+
+
+def _host_view(data):
+    """(pointer, size, keepalive) for host bytes-like input."""
+    if isinstance(data, np.ndarray):
+        a = np.ascontiguousarray(data).view(np.uint8).reshape(-1)
+    else:
+        a = np.frombuffer(memoryview(data).cast("B"), dtype=np.uint8) if len(memoryview(data)) else np.empty(0, np.uint8)
+    ptr = a.ctypes.data if a.size else None
+    return ptr, int(a.size), a
+
+
+def _input(data):
+    """(pointer, size, is_device, keepalive)."""
+    if _is_cuda_tensor(data):
+        if data.dtype.itemsize != 1 or not data.is_contiguous():
+            raise ValueError("device input must be a contiguous 1-byte tensor")
+        return (data.data_ptr() if data.numel() else None), int(data.numel()), 1, data
+    ptr, n, keep = _host_view(data)
+    return ptr, n, 0, keep
+
+
+def _validate(data) -> bool:
+    lib = _lib.load()
+    ptr, n, dev, _keep = _input(data)
+    out = C.c_uint8(0)
+    _lib.check(lib.utf8v_cuda_validate(ptr, n, dev, C.byref(out)))
+    return bool(out.value)
+
+
+def _lanes(fn_name: str, inp: bytes, prev: Optional[bytes]) -> bytes:
+    lib = _lib.load()
+    if len(inp) != WIDTH or (prev is not None and len(prev) != WIDTH):
+        raise ValueError(f"lane buffers are exactly {WIDTH} bytes")
+    a = (C.c_uint8 * WIDTH).from_buffer_copy(bytes(inp))
+    out = (C.c_uint8 * WIDTH)()
+    if prev is None:
+        _lib.check(getattr(lib, fn_name)(a, out))
+    else:
+        b = (C.c_uint8 * WIDTH).from_buffer_copy(bytes(prev))
+        _lib.check(getattr(lib, fn_name)(a, b, out))
+    return bytes(out)
+
+
+def _self_test(seed: int) -> bool:
+    lib = _lib.load()
+    ok = C.c_int(0)
+    _lib.check(lib.utf8v_cuda_ops_self_test(C.c_uint64(seed), C.byref(ok)))
+    return bool(ok.value)
+
+
+@dataclass(frozen=True)
+class LookupBackend:
+    """struct lookup_backend, proj/include/utf8v/lookup.hpp:77-87."""
+    name: str
+    width: int
+    validate: Callable[[object], bool]
+    classify_lanes: Callable[[bytes, bytes], bytes]
+    length_error_lanes: Callable[[bytes, bytes], bytes]
+    incomplete_lanes: Callable[[bytes], bytes]
+    ops_self_test: Callable[[int], bool]
+
+
+_CUDA = LookupBackend(
+    name="cuda",
+    width=WIDTH,
+    validate=_validate,
+    classify_lanes=lambda i, p: _lanes("utf8v_cuda_classify_lanes", i, p),
+    length_error_lanes=lambda i, p: _lanes("utf8v_cuda_length_error_lanes", i, p),
+    incomplete_lanes=lambda i: _lanes("utf8v_cuda_incomplete_lanes", i, None),
+    ops_self_test=_self_test,
+)
+_ROSTER = (_CUDA,)
+
+
+def lookup_backends() -> Sequence[LookupBackend]:
+    return _ROSTER
+
+
+def find_lookup_backend(name: str) -> Optional[LookupBackend]:
+    for b in _ROSTER:
+        if b.name == name:
+            return b
+    return None
+
+
+def validate_lookup(data) -> bool:
+    return lookup_backends()[0].validate(data)
+
+
+def validate_lookup_fallback(data) -> bool:
+    return lookup_backends()[-1].validate(data)
+
+
+def validate_lookup_verdict(data) -> Verdict:
+    lib = _lib.load()
+    ptr, n, dev, _keep = _input(data)
+    ok = C.c_uint8(0)
+    off = C.c_uint64(0)
+    kind = C.c_int(-1)
+    _lib.check(lib.utf8v_cuda_validate_verdict(ptr, n, dev, C.byref(ok), C.byref(off), C.byref(kind)))
+    if ok.value:
+        return Verdict.ok()
+    return Verdict.fail(off.value, ErrorKind(kind.value))
+
+
+def validate_lookup_batch(data, offsets) -> np.ndarray:
+    """verdicts[r] = 1 iff data[offsets[r]:offsets[r+1]] is valid UTF-8."""
+    lib = _lib.load()
+    if _is_cuda_tensor(data):
+        import torch
+        off = offsets if _is_cuda_tensor(offsets) else torch.as_tensor(np.asarray(offsets, np.uint64).view(np.int64), device=data.device)
+        nrec = int(off.numel()) - 1
+        if nrec <= 0:
+            return np.zeros(0, np.uint8)
+        ver = torch.empty(nrec, dtype=torch.uint8, device=data.device)
+        _lib.check(lib.utf8v_cuda_validate_batch(data.data_ptr() if data.numel() else None, int(data.numel()),
+                                                 off.data_ptr(), nrec, 1, ver.data_ptr()))
+        return ver.cpu().numpy()
+    ptr, n, _, keep = _host_view(data)
+    off = np.ascontiguousarray(np.asarray(offsets, dtype=np.uint64))
+    nrec = int(off.size) - 1
+    if nrec <= 0:
+        return np.zeros(0, np.uint8)
+    ver = np.empty(nrec, np.uint8)
+    _lib.check(lib.utf8v_cuda_validate_batch(ptr, n, off.ctypes.data, nrec, 0, ver.ctypes.data))
+    del keep
+    return ver
+
+
+def validate_lanes_async(d_ptr: int, n: int, lane_lo: int, lane_hi: int, d_flag_ptr: int, stream: int = 0) -> None:
+    """Device-resident lane range (see utf8v_cuda_validate_lanes_async)."""
+    _lib.check(_lib.load().utf8v_cuda_validate_lanes_async(d_ptr, n, lane_lo, lane_hi, d_flag_ptr, stream))
+
+
+def validate_batch_async(d_data: int, n: int, d_offsets: int, n_records: int, d_verdicts: int, stream: int = 0) -> None:
+    _lib.check(_lib.load().utf8v_cuda_validate_batch_async(d_data, n, d_offsets, n_records, d_verdicts, None, stream))

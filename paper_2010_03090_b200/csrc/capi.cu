@@ -1,0 +1,383 @@
+// capi.cu -- the extern "C" boundary (include/utf8v_cuda.h) over the sm_100a
+// kernels: per-thread/per-device context, H2D pipelining for host inputs,
+// status mapping.  No CPU fallback: without a CUDA device every compute entry
+// point returns UTF8V_ERR_NO_DEVICE.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/utf8v_cuda.h"
+#include "kernels.cuh"
+
+namespace {
+
+constexpr int kMaxDevices = 64;
+constexpr size_t kPiece = 32ull << 20;  // H2D pipeline piece (multiple of 16)
+
+thread_local std::string t_err;
+thread_local int t_launches = 0;
+
+int fail(int code, const std::string& what, cudaError_t e = cudaSuccess) {
+  t_err = what;
+  if (e != cudaSuccess) {
+    t_err += ": ";
+    t_err += cudaGetErrorString(e);
+  }
+  return code;
+}
+
+#define CK(call)                                              \
+  do {                                                        \
+    cudaError_t _e = (call);                                  \
+    if (_e != cudaSuccess) return fail(UTF8V_ERR_CUDA, #call, _e); \
+  } while (0)
+
+// The reference's eight 2-byte error patterns -> three nibble tables
+// (proj/include/utf8v/tables.hpp:60-99, same construction).
+void build_tables(uint8_t t1[16], uint8_t t2[16], uint8_t t3[16]) {
+  auto nib = [](unsigned lo, unsigned hi) {
+    uint16_t m = 0;
+    for (unsigned v = lo; v <= hi; ++v) m = (uint16_t)(m | (1u << v));
+    return m;
+  };
+  struct P {
+    uint8_t bit;
+    uint16_t h1, l1, h2;
+  };
+  const P pat[8] = {
+      {0, nib(0xC, 0xF), 0xFFFF, (uint16_t)(nib(0x0, 0x7) | nib(0xC, 0xF))},
+      {1, nib(0x0, 0x7), 0xFFFF, nib(0x8, 0xB)},
+      {2, nib(0xE, 0xE), nib(0x0, 0x0), nib(0x8, 0x9)},
+      {3, nib(0xF, 0xF), nib(0x4, 0xF), nib(0x9, 0xB)},
+      {4, nib(0xE, 0xE), nib(0xD, 0xD), nib(0xA, 0xB)},
+      {5, nib(0xC, 0xC), nib(0x0, 0x1), nib(0x8, 0xB)},
+      {6, nib(0xF, 0xF), (uint16_t)(nib(0x0, 0x0) | nib(0x5, 0xF)), nib(0x8, 0x8)},
+      {7, nib(0x8, 0xB), 0xFFFF, nib(0x8, 0xB)},
+  };
+  memset(t1, 0, 16);
+  memset(t2, 0, 16);
+  memset(t3, 0, 16);
+  for (const P& p : pat)
+    for (unsigned n = 0; n < 16; ++n) {
+      if (p.h1 & (1u << n)) t1[n] |= (uint8_t)(1u << p.bit);
+      if (p.l1 & (1u << n)) t2[n] |= (uint8_t)(1u << p.bit);
+      if (p.h2 & (1u << n)) t3[n] |= (uint8_t)(1u << p.bit);
+    }
+}
+
+std::once_flag g_dev_once[kMaxDevices];
+
+struct Ctx {
+  bool ready = false;
+  cudaStream_t s_comp = nullptr, s_copy = nullptr;
+  uint32_t* d_flag = nullptr;               // [0] verdict flag
+  unsigned long long* d_pos = nullptr;      // [0] first chunk, [1] offset
+  int* d_kind = nullptr;
+  uint8_t* d_lanes = nullptr;               // 3 x UTF8V_CUDA_WIDTH
+  int* d_ok = nullptr;
+  uint32_t* h_res = nullptr;                // pinned result words
+  uint8_t* d_stage = nullptr;
+  size_t stage_cap = 0;
+  std::vector<cudaEvent_t> events;
+};
+thread_local Ctx t_ctx[kMaxDevices];
+
+int get_ctx(Ctx** out) {
+  int dev = -1, count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    return fail(UTF8V_ERR_NO_DEVICE, "no CUDA device");
+  }
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices)
+    return fail(UTF8V_ERR_NO_DEVICE, "cudaGetDevice failed");
+  std::call_once(g_dev_once[dev], [] {
+    uint8_t t1[16], t2[16], t3[16];
+    build_tables(t1, t2, t3);
+    u8v::set_tables(t1, t2, t3);
+  });
+  Ctx& c = t_ctx[dev];
+  if (!c.ready) {
+    CK(cudaStreamCreateWithFlags(&c.s_comp, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&c.s_copy, cudaStreamNonBlocking));
+    CK(cudaMalloc(&c.d_flag, 64));
+    CK(cudaMalloc(&c.d_pos, 64));
+    CK(cudaMalloc(&c.d_kind, 64));
+    CK(cudaMalloc(&c.d_lanes, 4 * UTF8V_CUDA_WIDTH));
+    CK(cudaMalloc(&c.d_ok, 64));
+    CK(cudaMallocHost(&c.h_res, 256));
+    c.ready = true;
+  }
+  *out = &c;
+  return UTF8V_OK;
+}
+
+int ensure_stage(Ctx& c, size_t n) {
+  if (c.stage_cap >= n) return UTF8V_OK;
+  if (c.d_stage) cudaFree(c.d_stage);
+  c.d_stage = nullptr;
+  c.stage_cap = 0;
+  size_t cap = (n + 0xFFFFF) & ~size_t(0xFFFFF);
+  CK(cudaMalloc(&c.d_stage, cap));
+  c.stage_cap = cap;
+  return UTF8V_OK;
+}
+
+int ensure_events(Ctx& c, size_t k) {
+  while (c.events.size() < k) {
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c.events.push_back(e);
+  }
+  return UTF8V_OK;
+}
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(UTF8V_ERR_CUDA, what, e);
+  return UTF8V_OK;
+}
+
+// Copy host bytes into the stage in pieces on s_copy; `each(k, off, len)`
+// runs on s_comp after piece k has landed.
+template <class F>
+int pipeline_h2d(Ctx& c, const uint8_t* p, size_t n, F each) {
+  int st = ensure_stage(c, n);
+  if (st) return st;
+  const size_t pieces = (n + kPiece - 1) / kPiece;
+  st = ensure_events(c, pieces);
+  if (st) return st;
+  for (size_t k = 0; k < pieces; ++k) {
+    const size_t off = k * kPiece;
+    const size_t len = n - off < kPiece ? n - off : kPiece;
+    CK(cudaMemcpyAsync(c.d_stage + off, p + off, len, cudaMemcpyHostToDevice, c.s_copy));
+    CK(cudaEventRecord(c.events[k], c.s_copy));
+    CK(cudaStreamWaitEvent(c.s_comp, c.events[k], 0));
+    st = each(k, off, len);
+    if (st) return st;
+  }
+  return UTF8V_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int utf8v_cuda_abi_version(void) { return 1; }
+
+const char* utf8v_cuda_last_error(void) { return t_err.c_str(); }
+
+int utf8v_cuda_last_launch_count(void) { return t_launches; }
+
+int utf8v_cuda_validate(const uint8_t* p, size_t n, int is_device, uint8_t* out_valid) {
+  t_launches = 0;
+  if (!out_valid) return fail(UTF8V_ERR_ARG, "out_valid is NULL");
+  if (n == 0) {
+    *out_valid = 1;
+    return UTF8V_OK;
+  }
+  if (!p) return fail(UTF8V_ERR_ARG, "NULL data with n > 0");
+  Ctx* c;
+  int st = get_ctx(&c);
+  if (st) return st;
+  CK(cudaMemsetAsync(c->d_flag, 0, 4, c->s_comp));
+  if (is_device) {
+    u8v::launch_validate(u8v::make_desc(p, n, 0, n + 3), c->d_flag, c->s_comp);
+    ++t_launches;
+  } else {
+    st = pipeline_h2d(*c, p, n, [&](size_t, size_t off, size_t len) {
+      const bool last = off + len == n;
+      u8v::launch_validate(u8v::make_desc(c->d_stage, n, off, last ? n + 3 : off + len),
+                           c->d_flag, c->s_comp);
+      ++t_launches;
+      return check_launch("validate kernel");
+    });
+    if (st) return st;
+  }
+  st = check_launch("validate kernel");
+  if (st) return st;
+  CK(cudaMemcpyAsync(c->h_res, c->d_flag, 4, cudaMemcpyDeviceToHost, c->s_comp));
+  CK(cudaStreamSynchronize(c->s_comp));
+  *out_valid = c->h_res[0] == 0 ? 1 : 0;
+  return UTF8V_OK;
+}
+
+int utf8v_cuda_validate_verdict(const uint8_t* p, size_t n, int is_device, uint8_t* out_valid,
+                                uint64_t* out_offset, int* out_kind) {
+  t_launches = 0;
+  if (!out_valid || !out_offset || !out_kind) return fail(UTF8V_ERR_ARG, "NULL output");
+  *out_offset = 0;
+  *out_kind = -1;
+  if (n == 0) {
+    *out_valid = 1;
+    return UTF8V_OK;
+  }
+  if (!p) return fail(UTF8V_ERR_ARG, "NULL data with n > 0");
+  Ctx* c;
+  int st = get_ctx(&c);
+  if (st) return st;
+  const uint8_t* d = p;
+  if (!is_device) {
+    st = pipeline_h2d(*c, p, n, [](size_t, size_t, size_t) { return UTF8V_OK; });
+    if (st) return st;
+    d = c->d_stage;
+  }
+  CK(cudaMemsetAsync(c->d_flag, 0, 4, c->s_comp));
+  CK(cudaMemsetAsync(c->d_pos, 0xFF, 16, c->s_comp));
+  u8v::launch_first_error(u8v::make_desc(d, n, 0, n + 3), n, c->d_flag, c->d_pos, c->d_pos + 1,
+                          c->d_kind, c->s_comp);
+  t_launches += 2;
+  st = check_launch("first_error kernel");
+  if (st) return st;
+  CK(cudaMemcpyAsync(c->h_res, c->d_flag, 4, cudaMemcpyDeviceToHost, c->s_comp));
+  CK(cudaMemcpyAsync(c->h_res + 2, c->d_pos + 1, 8, cudaMemcpyDeviceToHost, c->s_comp));
+  CK(cudaMemcpyAsync(c->h_res + 4, c->d_kind, 4, cudaMemcpyDeviceToHost, c->s_comp));
+  CK(cudaStreamSynchronize(c->s_comp));
+  if (c->h_res[0] == 0) {
+    *out_valid = 1;
+    return UTF8V_OK;
+  }
+  *out_valid = 0;
+  uint64_t off;
+  memcpy(&off, c->h_res + 2, 8);
+  const int kind = (int)c->h_res[4];
+  if (kind < 0) return fail(UTF8V_ERR_CUDA, "flagged input but the window decode found no error");
+  *out_offset = off;
+  *out_kind = kind;
+  return UTF8V_OK;
+}
+
+int utf8v_cuda_validate_lanes_async(const uint8_t* d_p, uint64_t n, uint64_t lane_lo,
+                                    uint64_t lane_hi, uint32_t* d_flag, void* stream) {
+  t_launches = 0;
+  if (lane_hi > n + 3 || lane_lo > lane_hi || !d_flag) return fail(UTF8V_ERR_ARG, "bad lane range");
+  if (lane_lo == lane_hi || n == 0) return UTF8V_OK;
+  if (!d_p) return fail(UTF8V_ERR_ARG, "NULL data");
+  Ctx* c;
+  int st = get_ctx(&c);
+  if (st) return st;
+  u8v::launch_validate(u8v::make_desc(d_p, n, lane_lo, lane_hi), d_flag, (cudaStream_t)stream);
+  ++t_launches;
+  return check_launch("validate kernel");
+}
+
+uint64_t utf8v_cuda_batch_scratch_bytes(uint64_t) { return 0; }
+
+int utf8v_cuda_validate_batch_async(const uint8_t* d_data, uint64_t n, const uint64_t* d_offsets,
+                                    uint64_t n_records, uint8_t* d_verdicts, void* d_scratch,
+                                    void* stream) {
+  (void)d_scratch;
+  t_launches = 0;
+  if (n_records == 0) return UTF8V_OK;
+  if (!d_offsets || !d_verdicts) return fail(UTF8V_ERR_ARG, "NULL offsets/verdicts");
+  Ctx* c;
+  int st = get_ctx(&c);
+  if (st) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(cudaMemsetAsync(d_verdicts, 1, n_records, s));
+  // First and last offsets decide the byte range; read them back (16 bytes).
+  uint64_t* h = reinterpret_cast<uint64_t*>(c->h_res + 8);
+  CK(cudaMemcpyAsync(h, d_offsets, 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(h + 1, d_offsets + n_records, 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (h[1] < h[0] || h[1] > n) return fail(UTF8V_ERR_ARG, "offsets out of range");
+  if (h[1] > h[0] && !d_data) return fail(UTF8V_ERR_ARG, "NULL data");
+  u8v::launch_batch_known(d_data, d_offsets, n_records, h[0], h[1], d_verdicts, s);
+  ++t_launches;
+  return check_launch("batch kernel");
+}
+
+int utf8v_cuda_validate_batch(const uint8_t* data, size_t n, const uint64_t* offsets,
+                              size_t n_records, int is_device, uint8_t* verdicts) {
+  t_launches = 0;
+  if (n_records == 0) return UTF8V_OK;
+  if (!offsets || !verdicts) return fail(UTF8V_ERR_ARG, "NULL offsets/verdicts");
+  if (is_device) {
+    Ctx* c;
+    int st = get_ctx(&c);
+    if (st) return st;
+    st = utf8v_cuda_validate_batch_async(data, n, offsets, n_records, verdicts, nullptr, c->s_comp);
+    if (st) return st;
+    CK(cudaStreamSynchronize(c->s_comp));
+    return UTF8V_OK;
+  }
+  // Host arrays: validate the offsets here (cheap), stage everything.
+  for (size_t r = 0; r < n_records; ++r)
+    if (offsets[r + 1] < offsets[r]) return fail(UTF8V_ERR_ARG, "offsets not non-decreasing");
+  if (offsets[n_records] > n) return fail(UTF8V_ERR_ARG, "offsets exceed data size");
+  Ctx* c;
+  int st = get_ctx(&c);
+  if (st) return st;
+  uint64_t* d_off = nullptr;
+  uint8_t* d_ver = nullptr;
+  CK(cudaMallocAsync(&d_off, (n_records + 1) * 8, c->s_comp));
+  CK(cudaMallocAsync(&d_ver, n_records, c->s_comp));
+  CK(cudaMemcpyAsync(d_off, offsets, (n_records + 1) * 8, cudaMemcpyHostToDevice, c->s_comp));
+  if (n > 0) {
+    st = pipeline_h2d(*c, data, n, [](size_t, size_t, size_t) { return UTF8V_OK; });
+    if (st) return st;
+  }
+  CK(cudaMemsetAsync(d_ver, 1, n_records, c->s_comp));
+  u8v::launch_batch_known(n > 0 ? c->d_stage : nullptr, d_off, n_records, offsets[0],
+                          offsets[n_records], d_ver, c->s_comp);
+  ++t_launches;
+  st = check_launch("batch kernel");
+  if (st) return st;
+  CK(cudaMemcpyAsync(verdicts, d_ver, n_records, cudaMemcpyDeviceToHost, c->s_comp));
+  CK(cudaFreeAsync(d_off, c->s_comp));
+  CK(cudaFreeAsync(d_ver, c->s_comp));
+  CK(cudaStreamSynchronize(c->s_comp));
+  return UTF8V_OK;
+}
+
+static int lanes_call(const uint8_t* input, const uint8_t* previous, uint8_t* out, int mode) {
+  t_launches = 0;
+  if (!input || !out || (mode != 2 && !previous)) return fail(UTF8V_ERR_ARG, "NULL lane buffer");
+  Ctx* c;
+  int st = get_ctx(&c);
+  if (st) return st;
+  const int W = UTF8V_CUDA_WIDTH;
+  CK(cudaMemcpyAsync(c->d_lanes, input, W, cudaMemcpyHostToDevice, c->s_comp));
+  if (mode != 2)
+    CK(cudaMemcpyAsync(c->d_lanes + W, previous, W, cudaMemcpyHostToDevice, c->s_comp));
+  u8v::launch_classify_lanes(c->d_lanes, c->d_lanes + W, c->d_lanes + 2 * W, mode, c->s_comp);
+  ++t_launches;
+  st = check_launch("lanes kernel");
+  if (st) return st;
+  CK(cudaMemcpyAsync(out, c->d_lanes + 2 * W, W, cudaMemcpyDeviceToHost, c->s_comp));
+  CK(cudaStreamSynchronize(c->s_comp));
+  return UTF8V_OK;
+}
+
+int utf8v_cuda_classify_lanes(const uint8_t* input, const uint8_t* previous, uint8_t* out) {
+  return lanes_call(input, previous, out, 0);
+}
+
+int utf8v_cuda_length_error_lanes(const uint8_t* input, const uint8_t* previous, uint8_t* out) {
+  return lanes_call(input, previous, out, 1);
+}
+
+int utf8v_cuda_incomplete_lanes(const uint8_t* input, uint8_t* out) {
+  return lanes_call(input, nullptr, out, 2);
+}
+
+int utf8v_cuda_ops_self_test(uint64_t seed, int* out_ok) {
+  t_launches = 0;
+  if (!out_ok) return fail(UTF8V_ERR_ARG, "out_ok is NULL");
+  Ctx* c;
+  int st = get_ctx(&c);
+  if (st) return st;
+  u8v::launch_ops_self_test(seed, c->d_ok, c->s_comp);
+  ++t_launches;
+  st = check_launch("self-test kernel");
+  if (st) return st;
+  CK(cudaMemcpyAsync(c->h_res, c->d_ok, 4, cudaMemcpyDeviceToHost, c->s_comp));
+  CK(cudaStreamSynchronize(c->s_comp));
+  *out_ok = (int)c->h_res[0];
+  return UTF8V_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,47 @@
+// kernels.cuh -- shared declarations between the sm_100a kernels and capi.cu.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace u8v {
+
+constexpr int kThreads = 256;              // 8 warps per CTA
+constexpr int kU = 4;                      // 16-byte chunks per lane per step
+constexpr int kStepChunks = 32 * kU;       // 128 chunks = 2 KiB per warp step
+
+// error_kind numbering of proj/include/utf8v/verdict.hpp:20-27.
+enum { kHeaderBits = 0, kTooShort = 1, kTooLong = 2, kOverlong = 3, kTooLarge = 4, kSurrogate = 5 };
+
+struct StreamDesc {
+  const uint8_t* base;     // 16-byte aligned view of the stream
+  int64_t lo, hi;          // valid bytes [lo, hi) relative to base; others read 0
+  int64_t off16;           // stream byte 0 is base[off16]
+  int64_t L0, L1;          // lanes evaluated: [L0, L1) relative to base
+  int64_t c_begin, c_end;  // chunks evaluated: [c_begin, c_end)
+  int64_t steps;           // ceil((c_end - c_begin) / kStepChunks)
+  int64_t steps_per_warp;
+};
+
+int max_resident_warps();
+StreamDesc make_desc(const uint8_t* p, uint64_t n, uint64_t lane_lo, uint64_t lane_hi);
+void launch_validate(const StreamDesc& d, uint32_t* flag, cudaStream_t st);
+void launch_first_error(const StreamDesc& d, uint64_t n, uint32_t* flag,
+                        unsigned long long* first_chunk, unsigned long long* out_offset,
+                        int* out_kind, cudaStream_t st);
+
+// batch.cu
+// Caller sets d_verdicts[] = 1 first; first_off/last_off = offsets[0] and
+// offsets[n_records] (host values).
+void launch_batch_known(const uint8_t* data, const uint64_t* d_offsets, uint64_t n_records,
+                        uint64_t first_off, uint64_t last_off, uint8_t* d_verdicts,
+                        cudaStream_t st);
+
+// lanes.cu (lane entry points of the lookup_backend table, width kLaneWidth)
+constexpr int kLaneWidth = 64;
+void set_tables(const uint8_t t1[16], const uint8_t t2[16], const uint8_t t3[16]);
+void launch_classify_lanes(const uint8_t* in, const uint8_t* prev, uint8_t* out, int mode,
+                           cudaStream_t st);
+void launch_ops_self_test(uint64_t seed, int* result, cudaStream_t st);
+
+
+}  // namespace u8v

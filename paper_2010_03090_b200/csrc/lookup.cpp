@@ -1,0 +1,91 @@
+// lookup.cpp -- the reference C++ API (include/utf8v/lookup.hpp) over the
+// C-ABI.  Mirrors proj/src/lookup.cpp:16-45: a roster built once behind a
+// function-local static, lookup by name, validate_lookup through front().
+#include "utf8v/lookup.hpp"
+
+#include <string>
+
+#include "../../include/utf8v_cuda.h"
+
+namespace utf8v {
+namespace {
+
+[[noreturn]] void raise(int status) {
+  throw cuda_error(status, std::string("utf8v cuda backend: ") + utf8v_cuda_last_error());
+}
+
+bool cuda_validate(const std::uint8_t* data, std::size_t size) {
+  std::uint8_t ok = 0;
+  const int st = utf8v_cuda_validate(data, size, 0, &ok);
+  if (st != UTF8V_OK) raise(st);
+  return ok != 0;
+}
+
+void cuda_classify(const std::uint8_t* in, const std::uint8_t* prev, std::uint8_t* out) {
+  const int st = utf8v_cuda_classify_lanes(in, prev, out);
+  if (st != UTF8V_OK) raise(st);
+}
+
+void cuda_length_error(const std::uint8_t* in, const std::uint8_t* prev, std::uint8_t* out) {
+  const int st = utf8v_cuda_length_error_lanes(in, prev, out);
+  if (st != UTF8V_OK) raise(st);
+}
+
+void cuda_incomplete(const std::uint8_t* in, std::uint8_t* out) {
+  const int st = utf8v_cuda_incomplete_lanes(in, out);
+  if (st != UTF8V_OK) raise(st);
+}
+
+bool cuda_self_test(std::uint64_t seed) {
+  int ok = 0;
+  const int st = utf8v_cuda_ops_self_test(seed, &ok);
+  if (st != UTF8V_OK) raise(st);
+  return ok != 0;
+}
+
+constexpr lookup_backend k_cuda = {"cuda",          UTF8V_CUDA_WIDTH, &cuda_validate,
+                                   &cuda_classify,  &cuda_length_error, &cuda_incomplete,
+                                   &cuda_self_test};
+
+}  // namespace
+
+std::span<const lookup_backend> lookup_backends() {
+  static const lookup_backend roster[1] = {k_cuda};
+  return roster;
+}
+
+const lookup_backend* find_lookup_backend(std::string_view name) {
+  for (const lookup_backend& b : lookup_backends())
+    if (name == b.name) return &b;
+  return nullptr;
+}
+
+bool validate_lookup(bytes_view input) {
+  return lookup_backends().front().validate(input.data(), input.size());
+}
+
+bool validate_lookup_fallback(bytes_view input) {
+  return lookup_backends().back().validate(input.data(), input.size());
+}
+
+verdict validate_lookup_verdict(bytes_view input) {
+  std::uint8_t ok = 0;
+  std::uint64_t off = 0;
+  int kind = -1;
+  const int st = utf8v_cuda_validate_verdict(input.data(), input.size(), 0, &ok, &off, &kind);
+  if (st != UTF8V_OK) raise(st);
+  if (ok) return verdict::ok();
+  return verdict::fail(static_cast<std::size_t>(off), static_cast<error_kind>(kind));
+}
+
+std::vector<std::uint8_t> validate_lookup_batch(bytes_view data,
+                                                std::span<const std::uint64_t> offsets) {
+  if (offsets.empty()) return {};
+  std::vector<std::uint8_t> out(offsets.size() - 1);
+  const int st = utf8v_cuda_validate_batch(data.data(), data.size(), offsets.data(),
+                                           offsets.size() - 1, 0, out.data());
+  if (st != UTF8V_OK) raise(st);
+  return out;
+}
+
+}  // namespace utf8v

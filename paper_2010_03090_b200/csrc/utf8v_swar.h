@@ -1,0 +1,194 @@
+// utf8v_swar.h -- the per-word Lookup check, 4 byte lanes per 32-bit register.
+//
+// Compiled by nvcc into the sm_100a kernels (validate.cu, batch.cu) and, for
+// exhaustive verification only, by gcc into a test helper (tests/cpp): the same
+// source is checked on the CPU against the oracle for every input of length
+// <= 3 and against fuzz corpora, so what runs on the GPU is what was proven.
+//
+// Semantics (the reference's Lookup verdict, proj/include/utf8v/lookup_kernel.hpp
+// :21-134, restated per lane over the zero-extended stream x, x[i] = 0 outside
+// [0,n)).  The input is invalid iff some lane i in [0, n+3) has
+//
+//   S_i = cont(x[i]) XOR (x[i-1] >= C0 | x[i-2] >= E0 | x[i-3] >= F0)
+//       -- the classification's too-short / too-long bits plus the 2/3/4-byte
+//          continuation cross-check (lookup_kernel.hpp:38-46: bit 7 of the
+//          three-table AND is "two continuations", XORed with prev2>=E0 |
+//          prev3>=F0), folded into one structural test;
+//   R_i = x[i-1] in {C0,C1} | x[i-1] >= F5 | (x[i-1]=E0 & x[i]<A0)
+//       | (x[i-1]=ED & x[i]>=A0) | (x[i-1]=F0 & x[i]<90) | (x[i-1]=F4 & x[i]>=90)
+//       -- the nibble-table bits 2..6 (tables.hpp:60-79: overlong-3, too-large,
+//          surrogate, overlong-2, overlong-4/5+), restated on the pair.
+//
+// Lanes n..n+2 reduce to check_incomplete (lookup_kernel.hpp:48-68) and an
+// all-ASCII block contributes exactly the pending incomplete check (:94-96).
+// The equivalence with the nibble-table formulation is proven exhaustively for
+// all 65,536 byte pairs at every lane of a word and every input of length <= 3
+// by tests/test_swar.py (CPU), and on the GPU by tests/test_gpu_parity.py.
+//
+// Bit layout: byte k of a word is bits 8k..8k+7 (little-endian memory order);
+// all per-lane flags live in bit 7 of their byte.
+#pragma once
+#include <stdint.h>
+
+#if defined(__CUDACC__)
+#define U8V_HD __host__ __device__ __forceinline__
+#else
+#define U8V_HD static inline
+#endif
+
+// Upper 32 bits of ((hi:lo) << s), 0 < s < 32.  SHF.L.W on sm_100a.
+U8V_HD uint32_t u8v_fsl(uint32_t lo, uint32_t hi, unsigned s) {
+#if defined(__CUDA_ARCH__)
+  return __funnelshift_l(lo, hi, s);
+#else
+  return (hi << s) | (lo >> (32 - s));
+#endif
+}
+
+#define U8V_B7 0x80808080u
+
+// Lane flags of the word before the current one.  p is the raw word; f1/f2/f3
+// hold, in bit 7 of each byte, byte >= C0 / >= E0 / >= F0.
+typedef struct {
+  uint32_t p, f1, f2, f3;
+} u8v_carry;
+
+U8V_HD u8v_carry u8v_carry_of(uint32_t p) {
+  u8v_carry c;
+  c.p = p;
+  c.f1 = p & (p << 1);
+  c.f2 = c.f1 & (p << 2);
+  c.f3 = c.f2 & (p << 3);
+  return c;
+}
+
+U8V_HD u8v_carry u8v_carry_zero(void) {
+  u8v_carry c;
+  c.p = 0;
+  c.f1 = 0;
+  c.f2 = 0;
+  c.f3 = 0;
+  return c;
+}
+
+// Error flags (bit 7 of each byte lane, other bits garbage -- mask with U8V_B7
+// or test via u8v_any) for the four lanes of word w, given the previous word.
+// Advances the carry to w.
+U8V_HD uint32_t u8v_word_errors(uint32_t w, u8v_carry* c) {
+  // --- S: structure (cont XOR expected-continuation) ---------------------
+  const uint32_t s1 = w << 1, s2 = w << 2, s3 = w << 3;
+  const uint32_t f1 = w & s1;   // >= C0
+  const uint32_t f2 = f1 & s2;  // >= E0
+  const uint32_t f3 = f2 & s3;  // >= F0
+  const uint32_t e1 = u8v_fsl(c->f1, f1, 8);   // x[i-1] >= C0
+  const uint32_t e2 = u8v_fsl(c->f2, f2, 16);  // x[i-2] >= E0
+  const uint32_t e3 = u8v_fsl(c->f3, f3, 24);  // x[i-3] >= F0
+  const uint32_t cont = w & ~s1;               // 10xxxxxx
+  const uint32_t S = (e1 | e2 | e3) ^ cont;
+
+  // --- R: the rare lead pairs -------------------------------------------
+  // Key zl = a4 a3 a2 a1 a0 b5 b4 (7 bits) for the pair (a = x[i-1], b = x[i]).
+  // For a in C0..DF (a4 a3 a2 a1 = 0 <=> C0/C1): error iff zl < 8.
+  // For a >= E0 (E row has a4=0, F row a4=1; b is a continuation or S fires):
+  //   E0 & b<A0 -> zl in {00,01};  ED & b>=A0 -> zl in {36,37}
+  //   F0 & b<90 -> zl == 40;       F4 & b>=90, F5..FF -> zl >= 51.
+  const uint32_t a = u8v_fsl(c->p, w, 8);
+  const uint32_t zl = ((a & 0x1F1F1F1Fu) << 2) | ((w >> 4) & 0x03030303u);
+  const uint32_t ge08 = zl + 0x78787878u;  // bit7: zl >= 0x08
+  const uint32_t ge02 = zl + 0x7E7E7E7Eu;  // zl >= 0x02
+  const uint32_t ge36 = zl + 0x4A4A4A4Au;  // zl >= 0x36
+  const uint32_t ge38 = zl + 0x48484848u;  // zl >= 0x38
+  const uint32_t ge40 = zl + 0x40404040u;  // zl >= 0x40
+  const uint32_t ge41 = zl + 0x3F3F3F3Fu;  // zl >= 0x41
+  const uint32_t ge51 = zl + 0x2F2F2F2Fu;  // zl >= 0x51
+  const uint32_t a_ge_e0 = u8v_fsl(c->f2, f2, 8);
+  const uint32_t bad_ef = ~ge02 | (ge36 & ~ge38) | (ge40 & ~ge41) | ge51;
+  const uint32_t R = (a_ge_e0 & bad_ef) | (e1 & ~a_ge_e0 & ~ge08);
+
+  c->p = w;
+  c->f1 = f1;
+  c->f2 = f2;
+  c->f3 = f3;
+  return S | R;
+}
+
+// Record-bounded variant for the batch kernel: each record is its own
+// zero-extended stream.  bm / pbm carry, in bit 7 of byte k, "a record
+// starts at byte k" of this / the previous word.  Lane i drops every
+// look-back source that lies in an earlier record (i-1 if a record starts at
+// i; i-2 if one starts at i or i-1; i-3 if at i, i-1 or i-2), which is the
+// reference's zero prev vector at a record start (lookup_kernel.hpp:115).
+// *end_err receives, at each record start b, the previous record's
+// end-of-stream check (lookup_kernel.hpp:48-68, :111) restricted to that
+// record's own bytes; the returned flags belong to the record of their lane.
+U8V_HD uint32_t u8v_word_errors_bounded(uint32_t w, u8v_carry* c, uint32_t bm, uint32_t pbm,
+                                        uint32_t* end_err) {
+  const uint32_t s1 = w << 1, s2 = w << 2, s3 = w << 3;
+  const uint32_t f1 = w & s1;
+  const uint32_t f2 = f1 & s2;
+  const uint32_t f3 = f2 & s3;
+  const uint32_t e1 = u8v_fsl(c->f1, f1, 8);
+  const uint32_t e2 = u8v_fsl(c->f2, f2, 16);
+  const uint32_t e3 = u8v_fsl(c->f3, f3, 24);
+  const uint32_t b1 = u8v_fsl(pbm, bm, 8);   // a record starts at i-1
+  const uint32_t b2 = u8v_fsl(pbm, bm, 16);  // a record starts at i-2
+  const uint32_t m2 = bm | b1;
+  const uint32_t m3 = m2 | b2;
+  const uint32_t cont = w & ~s1;
+  const uint32_t S = ((e1 & ~bm) | (e2 & ~m2) | (e3 & ~m3)) ^ cont;
+
+  const uint32_t a = u8v_fsl(c->p, w, 8);
+  const uint32_t zl = ((a & 0x1F1F1F1Fu) << 2) | ((w >> 4) & 0x03030303u);
+  const uint32_t ge08 = zl + 0x78787878u;
+  const uint32_t ge02 = zl + 0x7E7E7E7Eu;
+  const uint32_t ge36 = zl + 0x4A4A4A4Au;
+  const uint32_t ge38 = zl + 0x48484848u;
+  const uint32_t ge40 = zl + 0x40404040u;
+  const uint32_t ge41 = zl + 0x3F3F3F3Fu;
+  const uint32_t ge51 = zl + 0x2F2F2F2Fu;
+  const uint32_t a_ge_e0 = u8v_fsl(c->f2, f2, 8);
+  const uint32_t bad_ef = ~ge02 | (ge36 & ~ge38) | (ge40 & ~ge41) | ge51;
+  const uint32_t R = ((a_ge_e0 & bad_ef) | (e1 & ~a_ge_e0 & ~ge08)) & ~bm;
+
+  *end_err = bm & (e1 | (e2 & ~b1) | (e3 & ~b1 & ~b2)) & U8V_B7;
+  c->p = w;
+  c->f1 = f1;
+  c->f2 = f2;
+  c->f3 = f3;
+  return (S | R) & U8V_B7;
+}
+
+// Spread 4 bits (bit k = byte k) to bit 7 of each byte.
+U8V_HD uint32_t u8v_spread4(uint32_t x) { return ((x & 0xFu) * 0x10204080u) & U8V_B7; }
+
+// Errors contributed by a word of all-ASCII bytes (no leads, no
+// continuations): only the continuation expected from the previous word's
+// last three bytes -- the pending incomplete check of lookup_kernel.hpp:94-96.
+U8V_HD uint32_t u8v_ascii_word_errors(uint32_t w, u8v_carry* c) {
+  const uint32_t e = u8v_fsl(c->f1, 0, 8) | u8v_fsl(c->f2, 0, 16) | u8v_fsl(c->f3, 0, 24);
+  c->p = w;
+  c->f1 = 0;
+  c->f2 = 0;
+  c->f3 = 0;
+  return e;
+}
+
+// End-of-stream lanes n, n+1, n+2: check_incomplete of the last three bytes
+// (lookup_kernel.hpp:48-68, :111).  Equivalent to u8v_word_errors(0, c).
+U8V_HD uint32_t u8v_end_errors(const u8v_carry* c) {
+  return u8v_fsl(c->f1, 0, 8) | u8v_fsl(c->f2, 0, 16) | u8v_fsl(c->f3, 0, 24);
+}
+
+U8V_HD int u8v_any(uint32_t err) { return (err & U8V_B7) != 0; }
+
+// Bytes outside [lo, hi) of word at byte position `pos` replaced by zero --
+// the zero-extended stream the reference builds with its zeroed tail block
+// (lookup_kernel.hpp:128-132) and all-zero initial prev vector (:115).
+U8V_HD uint32_t u8v_mask_word(uint32_t w, int64_t pos, int64_t lo, int64_t hi) {
+  uint32_t keep = 0;
+  for (int k = 0; k < 4; ++k) {
+    const int64_t q = pos + k;
+    if (q >= lo && q < hi) keep |= 0xFFu << (8 * k);
+  }
+  return w & keep;
+}

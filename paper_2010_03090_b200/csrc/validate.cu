@@ -1,0 +1,292 @@
+// validate.cu -- sm_100a kernels for single-stream Lookup validation.
+//
+//   k_validate<false>   K1: OR of the per-lane error flags of one stream (or
+//                       of one lane range of it: a pipeline piece, a shard),
+//                       reduced with REDUX + one atomicOr per warp.
+//   k_validate<true>    K3: the same scan, recording the first 16-byte chunk
+//                       that holds a flagged lane (atomicMin per warp).
+//   k_locate            K3b: one thread decodes the <= 26-byte window around
+//                       that chunk and writes the reference's (offset, kind).
+//
+// Reference path replaced: validate_with<V> / lookup_checker<V>
+// (proj/include/utf8v/lookup_kernel.hpp:82-134) reached through
+// validate_lookup (proj/src/lookup.cpp:39-41); error positions as produced by
+// oracle_validate (proj/src/oracle.cpp:10-44) in the CLI's failure path
+// (proj/tools/main.cpp:129-147).
+//
+// Data layout: the caller's bytes stay where they are in HBM.  A stream is
+// viewed through a 16-byte aligned base; chunk c is bytes [16c, 16c+16) of
+// that base, bytes outside the valid range [lo, hi) read as zero (the
+// reference's zero prev vector and zero-padded tail).  A warp owns a
+// contiguous run of 2 KiB steps; in a step lane L holds chunks L, L+32, L+64,
+// L+96 (each load instruction is one coalesced 512-byte sweep) and gets the
+// word before each chunk from lane L-1 with one SHFL (lane 0 from lane 31's
+// previous chunk), so the 3-byte look-back halo never touches memory twice.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "kernels.cuh"
+#include "utf8v_swar.h"
+
+namespace u8v {
+
+__device__ __forceinline__ uint4 ld_stream(const uint8_t* p) {
+  uint4 r;
+  asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+      : "l"(p));
+  return r;
+}
+
+// Load one 16-byte chunk with every byte outside [lo, hi) replaced by zero;
+// only bytes inside the range are touched (boundary chunks only).
+__device__ __forceinline__ uint4 ld_chunk_masked(const uint8_t* base, int64_t c, int64_t lo,
+                                                 int64_t hi) {
+  uint32_t w[4] = {0, 0, 0, 0};
+  const int64_t b0 = c * 16;
+  if (b0 >= lo && b0 + 16 <= hi) return ld_stream(base + b0);
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    const int64_t q = b0 + k;
+    if (q >= lo && q < hi) w[k >> 2] |= (uint32_t)base[q] << (8 * (k & 3));
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+__device__ __forceinline__ uint32_t ld_word_masked(const uint8_t* base, int64_t pos, int64_t lo,
+                                                   int64_t hi) {
+  uint32_t w = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int64_t q = pos + k;
+    if (q >= lo && q < hi) w |= (uint32_t)base[q] << (8 * k);
+  }
+  return w;
+}
+
+__device__ __forceinline__ uint32_t chunk_errors(const uint4 v, uint32_t prev) {
+  u8v_carry c = u8v_carry_of(prev);
+  uint32_t e = u8v_word_errors(v.x, &c);
+  e |= u8v_word_errors(v.y, &c);
+  e |= u8v_word_errors(v.z, &c);
+  e |= u8v_word_errors(v.w, &c);
+  return e & U8V_B7;
+}
+
+// Errors of one chunk on the masked path: lanes outside [L0, L1) dropped.
+__device__ __forceinline__ uint32_t chunk_errors_ranged(const uint4 v, uint32_t prev, int64_t c,
+                                                        int64_t L0, int64_t L1) {
+  u8v_carry cr = u8v_carry_of(prev);
+  const int64_t p0 = c * 16;
+  uint32_t e = u8v_mask_word(u8v_word_errors(v.x, &cr), p0, L0, L1);
+  e |= u8v_mask_word(u8v_word_errors(v.y, &cr), p0 + 4, L0, L1);
+  e |= u8v_mask_word(u8v_word_errors(v.z, &cr), p0 + 8, L0, L1);
+  e |= u8v_mask_word(u8v_word_errors(v.w, &cr), p0 + 12, L0, L1);
+  return e & U8V_B7;
+}
+
+template <bool kPos>
+__global__ void __launch_bounds__(kThreads, 4)
+    k_validate(StreamDesc d, uint32_t* __restrict__ flag,
+               unsigned long long* __restrict__ first_chunk) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
+  int64_t step = warp * d.steps_per_warp;
+  int64_t step_end = step + d.steps_per_warp;
+  if (step_end > d.steps) step_end = d.steps;
+  if (step >= step_end) return;
+  const int64_t in_lo = d.lo > d.L0 ? d.lo : d.L0;  // interior: all bytes real,
+  const int64_t in_hi = d.hi < d.L1 ? d.hi : d.L1;  // all lanes wanted
+
+  // Word before this warp's first chunk, supplied by lane 31 to lane 0.
+  uint32_t carry_word = 0;
+  {
+    const int64_t c0 = d.c_begin + step * kStepChunks;
+    if (lane == 31 && c0 > 0) carry_word = ld_word_masked(d.base, c0 * 16 - 4, d.lo, d.hi);
+  }
+  uint32_t acc = 0;
+  for (; step < step_end; ++step) {
+    const int64_t cstep = d.c_begin + step * kStepChunks;
+    const bool interior = cstep * 16 >= in_lo && (cstep + kStepChunks) * 16 <= in_hi;
+    uint4 v[kU];
+    if (interior) {
+#pragma unroll
+      for (int i = 0; i < kU; ++i) v[i] = ld_stream(d.base + (cstep + lane + 32 * i) * 16);
+    } else {
+#pragma unroll
+      for (int i = 0; i < kU; ++i) {
+        const int64_t c = cstep + lane + 32 * i;
+        v[i] = c < d.c_end ? ld_chunk_masked(d.base, c, d.lo, d.hi) : make_uint4(0, 0, 0, 0);
+      }
+    }
+    uint32_t hibits = 0;
+#pragma unroll
+    for (int i = 0; i < kU; ++i) hibits |= v[i].x | v[i].y | v[i].z | v[i].w;
+    const bool all_ascii = __all_sync(0xFFFFFFFFu, (hibits & U8V_B7) == 0);
+
+    uint32_t step_err = 0;
+    int first_i = kU;
+#pragma unroll
+    for (int i = 0; i < kU; ++i) {
+      const uint32_t supply = lane == 31 ? (i == 0 ? carry_word : v[i - 1].w) : v[i].w;
+      const uint32_t prev = __shfl_sync(0xFFFFFFFFu, supply, (lane + 31) & 31);
+      uint32_t e;
+      if (interior) {
+        if (all_ascii) {
+          u8v_carry cr = u8v_carry_of(prev);
+          e = u8v_ascii_word_errors(v[i].x, &cr) & U8V_B7;
+        } else {
+          e = chunk_errors(v[i], prev);
+        }
+      } else {
+        const int64_t c = cstep + lane + 32 * i;
+        e = c < d.c_end ? chunk_errors_ranged(v[i], prev, c, d.L0, d.L1) : 0u;
+      }
+      step_err |= e;
+      if (kPos && e != 0 && first_i == kU) first_i = i;
+    }
+    if (lane == 31) carry_word = v[kU - 1].w;
+    if (kPos) {
+      // Chunks of a step are ordered (i, lane); the warp's first flagged chunk
+      // is the minimum over lanes of cstep + lane + 32 * first_i.
+      const unsigned long long mine =
+          first_i < kU ? (unsigned long long)(cstep + lane + 32 * first_i) : ~0ull;
+      if (__any_sync(0xFFFFFFFFu, first_i < kU)) {
+        unsigned long long m = mine;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const unsigned long long t = __shfl_xor_sync(0xFFFFFFFFu, m, o);
+          m = t < m ? t : m;
+        }
+        if (lane == 0) {
+          atomicMin(first_chunk, m);
+          atomicOr(flag, 1u);
+        }
+        return;  // later chunks of this warp cannot be earlier
+      }
+    } else {
+      acc |= step_err;
+    }
+  }
+  if (!kPos) {
+    const unsigned any = __reduce_or_sync(0xFFFFFFFFu, acc);
+    if (lane == 0 && any) atomicOr(flag, 1u);
+  }
+}
+
+// The reference decode of oracle.cpp:10-44 run over [from, to) of the stream;
+// `from` is a character boundary and the first error lies inside the window.
+__device__ int decode_window(const uint8_t* s, uint64_t from, uint64_t to, uint64_t* off) {
+  uint64_t i = from;
+  while (i < to) {
+    const uint8_t lead = s[i];
+    if (lead < 0x80) {
+      ++i;
+      continue;
+    }
+    *off = i;
+    if (lead < 0xC0) return kTooLong;
+    if (lead >= 0xF8) return kHeaderBits;
+    const unsigned len = lead >= 0xF0 ? 4 : lead >= 0xE0 ? 3 : 2;
+    uint32_t cp = lead & (0x7Fu >> len);
+    for (unsigned k = 1; k < len; ++k) {
+      if (i + k >= to) return kTooShort;
+      const uint8_t c = s[i + k];
+      if ((c & 0xC0) != 0x80) return kTooShort;
+      cp = (cp << 6) | (c & 0x3F);
+    }
+    const uint32_t min_cp = len == 2 ? 0x80 : len == 3 ? 0x800 : 0x10000;
+    if (cp < min_cp) return kOverlong;
+    if (cp > 0x10FFFF) return kTooLarge;
+    if (cp >= 0xD800 && cp <= 0xDFFF) return kSurrogate;
+    i += len;
+  }
+  return -1;
+}
+
+// K3b: turn the first flagged chunk into (offset, kind).  Every flagged lane L
+// satisfies E <= L <= E + 3 for the sequential first error E, so E lies in
+// [chunk_start - 3, chunk_end) and the decode needs bytes up to E + 3.  The
+// window starts at the character boundary at or before chunk_start - 3
+// (at most 3 continuation bytes back; if there are more, E is at that point).
+__global__ void k_locate(const uint8_t* __restrict__ s, uint64_t n, int64_t off16,
+                         const unsigned long long* __restrict__ first_chunk,
+                         unsigned long long* __restrict__ out_offset, int* __restrict__ out_kind) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const unsigned long long c = *first_chunk;
+  const int64_t lmin = (int64_t)c * 16 - off16;  // first lane of the chunk, stream coords
+  int64_t b0 = lmin - 3;
+  if (b0 < 0) b0 = 0;
+  if ((uint64_t)b0 > n) b0 = (int64_t)n;
+  int64_t b = b0;
+  for (int k = 0; k < 3 && b > 0 && (uint64_t)b < n && (s[b] & 0xC0) == 0x80; ++k) --b;
+  if ((uint64_t)b < n && (s[b] & 0xC0) == 0x80 && b > 0) b = b0;
+  uint64_t to = (uint64_t)(lmin + 16 + 4);
+  if (to > n) to = n;
+  uint64_t o = 0;
+  const int kind = decode_window(s, (uint64_t)b, to, &o);
+  *out_kind = kind;
+  *out_offset = kind < 0 ? ~0ull : o;
+}
+
+}  // namespace u8v
+
+// ---- host-side launchers (called by capi.cu) ------------------------------
+namespace u8v {
+
+int max_resident_warps() {
+  static int warps = 0;
+  if (warps == 0) {
+    int dev = 0, sms = 0, blocks = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_validate<false>, kThreads, 0);
+    if (blocks < 1) blocks = 1;
+    warps = sms * blocks * (kThreads / 32);
+  }
+  return warps;
+}
+
+StreamDesc make_desc(const uint8_t* p, uint64_t n, uint64_t lane_lo, uint64_t lane_hi) {
+  // Stream coordinates: byte i of the stream is p[i]; lanes [lane_lo,
+  // lane_hi) are evaluated (lane_hi <= n + 3).  Chunk coordinates are
+  // relative to the 16-byte aligned base below p.
+  StreamDesc d;
+  const uintptr_t up = (uintptr_t)p;
+  const int64_t off = (int64_t)(up & 15u);
+  d.base = (const uint8_t*)(up - (uintptr_t)off);
+  d.lo = off;
+  d.hi = off + (int64_t)n;
+  d.off16 = off;
+  d.L0 = off + (int64_t)lane_lo;
+  d.L1 = off + (int64_t)lane_hi;
+  d.c_begin = d.L0 / 16;
+  d.c_end = (d.L1 + 15) / 16;
+  const int64_t chunks = d.c_end - d.c_begin;
+  d.steps = (chunks + kStepChunks - 1) / kStepChunks;
+  int64_t warps = max_resident_warps();
+  if (warps > d.steps) warps = d.steps;
+  if (warps < 1) warps = 1;
+  d.steps_per_warp = (d.steps + warps - 1) / warps;
+  return d;
+}
+
+void launch_validate(const StreamDesc& d, uint32_t* flag, cudaStream_t st) {
+  if (d.steps <= 0) return;
+  const int64_t warps = (d.steps + d.steps_per_warp - 1) / d.steps_per_warp;
+  const int64_t blocks = (warps * 32 + kThreads - 1) / kThreads;
+  k_validate<false><<<(unsigned)blocks, kThreads, 0, st>>>(d, flag, nullptr);
+}
+
+void launch_first_error(const StreamDesc& d, uint64_t n, uint32_t* flag,
+                        unsigned long long* first_chunk, unsigned long long* out_offset,
+                        int* out_kind, cudaStream_t st) {
+  if (d.steps > 0) {
+    const int64_t warps = (d.steps + d.steps_per_warp - 1) / d.steps_per_warp;
+    const int64_t blocks = (warps * 32 + kThreads - 1) / kThreads;
+    k_validate<true><<<(unsigned)blocks, kThreads, 0, st>>>(d, flag, first_chunk);
+  }
+  k_locate<<<1, 32, 0, st>>>(d.base + d.off16, n, d.off16, first_chunk, out_offset, out_kind);
+}
+
+}  // namespace u8v

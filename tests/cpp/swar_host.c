@@ -1,0 +1,194 @@
+/*
+ * swar_host.c -- TEST HELPER: the device SWAR formula (utf8v_swar.h),
+ * compiled for the CPU, driven the way the kernels drive it, and checked
+ * against the oracle restatement at volumes Python cannot loop over
+ * (all 16,843,009 inputs of length <= 3 at every word alignment).
+ */
+#include <stdlib.h>
+#include <string.h>
+
+#include "utf8_oracle.h"
+#include "utf8v_swar.h"
+
+/* Stream the words of a zero-extended stream [0, n) that starts `off` bytes
+ * into an aligned word grid, exactly like k_validate: words in order, lanes
+ * up to n+3 included.  Returns the first flagged lane (stream coords), or
+ * UINT64_MAX when none. */
+uint64_t swar_first_lane(const uint8_t* p, size_t n, unsigned off) {
+  const int64_t lo = off, hi = (int64_t)off + (int64_t)n;
+  const int64_t words = (hi + 3 + 3) / 4;
+  u8v_carry c = u8v_carry_zero();
+  for (int64_t k = 0; k < words; ++k) {
+    uint32_t w = 0;
+    for (int j = 0; j < 4; ++j) {
+      const int64_t q = 4 * k + j;
+      if (q >= lo && q < hi) w |= (uint32_t)p[q - lo] << (8 * j);
+    }
+    const uint32_t e = u8v_word_errors(w, &c) & U8V_B7;
+    if (e) {
+      for (int j = 0; j < 4; ++j)
+        if ((e >> (8 * j + 7)) & 1) return (uint64_t)(4 * k + j - lo);
+    }
+  }
+  return UINT64_MAX;
+}
+
+int swar_validate(const uint8_t* p, size_t n, unsigned off) {
+  return swar_first_lane(p, n, off) == UINT64_MAX;
+}
+
+/* Exhaustive agreement for every input of length 0..max_len (<= 3) at word
+ * alignment `off`: counts verdict mismatches and first-lane bound violations
+ * (E <= L <= E+3).  Mirrors proj/tests/acceptance.cpp:74-113. */
+void swar_exhaustive(unsigned off, int max_len, uint64_t* checked, uint64_t* mismatches,
+                     uint64_t* bound_violations) {
+  uint8_t buf[3];
+  uint64_t ck = 0, mm = 0, bv = 0;
+  for (int len = 0; len <= max_len; ++len) {
+    const uint64_t total = len == 0 ? 1 : (1ull << (8 * len));
+    for (uint64_t v = 0; v < total; ++v) {
+      for (int i = 0; i < len; ++i) buf[i] = (uint8_t)(v >> (8 * i));
+      uint64_t eoff = 0;
+      int kind = 0;
+      const int ok = orc_validate(buf, (size_t)len, &eoff, &kind);
+      const uint64_t L = swar_first_lane(buf, (size_t)len, off);
+      ++ck;
+      if ((L == UINT64_MAX) != (ok != 0)) ++mm;
+      else if (!ok && !(L >= eoff && L <= eoff + 3)) ++bv;
+    }
+  }
+  *checked = ck;
+  *mismatches = mm;
+  *bound_violations = bv;
+}
+
+/* All 65,536 byte pairs embedded at `offset` inside ASCII padding
+ * (proj/tests/test_lookup.cpp:287-311), at word alignment `align`. */
+uint64_t swar_pairs(size_t offset, unsigned align) {
+  uint8_t buf[256];
+  const size_t n = offset + 2 + 16;
+  memset(buf, 0x41, sizeof buf);
+  uint64_t mm = 0;
+  for (unsigned b1 = 0; b1 < 256; ++b1)
+    for (unsigned b2 = 0; b2 < 256; ++b2) {
+      buf[offset] = (uint8_t)b1;
+      buf[offset + 1] = (uint8_t)b2;
+      uint64_t eo;
+      int k;
+      const int ok = orc_validate(buf, n, &eo, &k);
+      if (swar_validate(buf, n, align) != ok) ++mm;
+    }
+  return mm;
+}
+
+/* Batch semantics through u8v_word_errors_bounded, as k_batch drives it:
+ * records [offsets[r], offsets[r+1]) of one contiguous buffer starting `off`
+ * bytes into the word grid.  verdicts[r] = 1 / 0. */
+void swar_batch(const uint8_t* data, const uint64_t* offsets, size_t n_records, unsigned off,
+                uint8_t* verdicts) {
+  if (n_records == 0) return;
+  const int64_t lo = (int64_t)off + (int64_t)offsets[0];
+  const int64_t hi = (int64_t)off + (int64_t)offsets[n_records];
+  for (size_t r = 0; r < n_records; ++r) verdicts[r] = 1;
+  if (hi <= lo) return;
+  const int64_t words = (hi + 3 + 3) / 4;
+  u8v_carry c = u8v_carry_zero();
+  uint32_t pbm = 0;
+  size_t rcur = 0; /* record of the current lane */
+  for (int64_t k = lo / 4; k < words; ++k) {
+    uint32_t w = 0, bm = 0;
+    for (int j = 0; j < 4; ++j) {
+      const int64_t q = 4 * k + j;
+      if (q >= lo && q < hi) w |= (uint32_t)data[q - (int64_t)off] << (8 * j);
+      for (size_t r = 0; r <= n_records; ++r)
+        if ((int64_t)offsets[r] + (int64_t)off == q) bm |= 0x80u << (8 * j);
+    }
+    if (k == lo / 4) c = u8v_carry_zero();
+    uint32_t end_err = 0;
+    const uint32_t e = u8v_word_errors_bounded(w, &c, bm, pbm, &end_err);
+    for (int j = 0; j < 4; ++j) {
+      const int64_t q = 4 * k + j - (int64_t)off; /* data coords */
+      /* record of lane q: largest r < n with offsets[r] <= q */
+      while (rcur + 1 < n_records && (int64_t)offsets[rcur + 1] <= q) ++rcur;
+      if ((e >> (8 * j + 7)) & 1) {
+        if (q >= (int64_t)offsets[0] && q < (int64_t)offsets[n_records] + 3) {
+          size_t r = 0;
+          while (r + 1 < n_records && (int64_t)offsets[r + 1] <= q) ++r;
+          if (q < (int64_t)offsets[n_records]) verdicts[r] = 0;
+          else verdicts[n_records - 1] = 0; /* lanes past the end: last record */
+        }
+      }
+      if ((end_err >> (8 * j + 7)) & 1) {
+        const int64_t qb = q - 1;
+        if (qb >= (int64_t)offsets[0]) {
+          size_t r = 0;
+          while (r + 1 < n_records && (int64_t)offsets[r + 1] <= qb) ++r;
+          verdicts[r] = 0;
+        }
+      }
+    }
+    pbm = bm;
+  }
+}
+
+/* Oracle verdicts for every input of exactly `len` bytes (len <= 3), in the
+ * order v = 0 .. 256^len - 1 with byte i = (v >> 8i) & 0xFF. */
+void oracle_exhaustive_verdicts(int len, uint8_t* out) {
+  uint8_t buf[3];
+  const uint64_t total = len == 0 ? 1 : (1ull << (8 * len));
+  for (uint64_t v = 0; v < total; ++v) {
+    for (int i = 0; i < len; ++i) buf[i] = (uint8_t)(v >> (8 * i));
+    uint64_t o;
+    int k;
+    out[v] = (uint8_t)orc_validate(buf, (size_t)len, &o, &k);
+  }
+}
+
+/* All inputs of exactly `len` bytes laid out back to back (the batch form). */
+void exhaustive_inputs(int len, uint8_t* out) {
+  const uint64_t total = len == 0 ? 1 : (1ull << (8 * len));
+  for (uint64_t v = 0; v < total; ++v)
+    for (int i = 0; i < len; ++i) out[v * len + i] = (uint8_t)(v >> (8 * i));
+}
+
+#include <pthread.h>
+typedef struct {
+  const uint8_t* data;
+  const uint64_t* off;
+  uint8_t* valid;
+  uint64_t* eoff;
+  int* kind;
+  size_t lo, hi;
+} ob_job;
+
+static void* ob_run(void* arg) {
+  ob_job* j = (ob_job*)arg;
+  for (size_t r = j->lo; r < j->hi; ++r) {
+    uint64_t o = 0;
+    int k = -1;
+    j->valid[r] = (uint8_t)orc_validate(j->data + j->off[r], j->off[r + 1] - j->off[r], &o, &k);
+    if (j->eoff) j->eoff[r] = j->valid[r] ? UINT64_MAX : o;
+    if (j->kind) j->kind[r] = j->valid[r] ? -1 : k;
+  }
+  return NULL;
+}
+
+/* Oracle verdict (and first error) for every CSR record, on `threads` threads. */
+void oracle_batch(const uint8_t* data, const uint64_t* off, size_t n_records, int threads,
+                  uint8_t* valid, uint64_t* eoff, int* kind) {
+  if (threads < 1) threads = 1;
+  if (threads > 256) threads = 256;
+  pthread_t tid[256];
+  ob_job jobs[256];
+  for (int t = 0; t < threads; ++t) {
+    jobs[t].data = data;
+    jobs[t].off = off;
+    jobs[t].valid = valid;
+    jobs[t].eoff = eoff;
+    jobs[t].kind = kind;
+    jobs[t].lo = n_records * (size_t)t / (size_t)threads;
+    jobs[t].hi = n_records * (size_t)(t + 1) / (size_t)threads;
+    pthread_create(&tid[t], NULL, ob_run, &jobs[t]);
+  }
+  for (int t = 0; t < threads; ++t) pthread_join(tid[t], NULL);
+}

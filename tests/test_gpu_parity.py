@@ -1,0 +1,447 @@
+"""GPU parity: the CUDA path (through the C-ABI) vs the oracle, on the
+reference's own test vectors (proj/tests/test_lookup.cpp, acceptance.cpp) and
+on seeded inputs.  Bit-exact: verdicts, and (offset, kind) where reported."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import paper_2010_03090_b200 as u8
+from paper_2010_03090_b200 import configs
+from tests import _native as nat
+
+pytestmark = pytest.mark.gpu
+
+
+def B(*xs):
+    return bytes(xs)
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch
+    return torch
+
+
+@pytest.fixture(scope="module")
+def cuda():
+    return u8.lookup_backends()[0]
+
+
+# ---- roster & lanes: test_lookup.cpp:34-187 --------------------------------
+def test_roster_well_formed():
+    bs = u8.lookup_backends()
+    assert len(bs) >= 1
+    for i in range(len(bs) - 1):
+        assert bs[i].width >= bs[i + 1].width
+    for b in bs:
+        assert u8.find_lookup_backend(b.name) is b
+        assert b.width >= 32
+    assert u8.find_lookup_backend("neon") is None
+    assert u8.find_lookup_backend("") is None
+
+
+@pytest.mark.parametrize("seed", [1, 0xDEADBEEF, 0x123456789ABCDEF])
+def test_ops_self_test(cuda, seed):
+    assert cuda.ops_self_test(seed)
+
+
+def test_worked_example_classification(cuda):
+    example = B(0x39, 0xC3, 0xA7, 0xE9, 0x8F, 0xA1, 0xF0, 0x9F, 0x98, 0x80, 0x00)
+    final = B(0x00, 0x00, 0x00, 0x00, 0x00, 0x80, 0x00, 0x00, 0x80, 0x80, 0x00)
+    w = cuda.width
+    out = cuda.classify_lanes(example + bytes(w - len(example)), bytes(w))
+    assert out == final + bytes(w - len(final))
+
+
+def test_classification_silent_on_ascii(cuda):
+    w = cuda.width
+    assert cuda.classify_lanes(b"A" * w, b"A" * w) == bytes(w)
+
+
+def test_lanes_match_oracle_on_random_vectors(cuda):
+    rng = np.random.default_rng(7)
+    w = cuda.width
+    import ctypes as C
+    O = nat.oracle()
+    for _ in range(200):
+        a = rng.integers(0, 256, w, dtype=np.uint8).tobytes()
+        p = rng.integers(0, 256, w, dtype=np.uint8).tobytes()
+        for fn, ofn in ((cuda.classify_lanes, O.orc_classify_lanes), (cuda.length_error_lanes, O.orc_length_error_lanes)):
+            want = (C.c_uint8 * w)()
+            ofn(a, p, want, w)
+            assert fn(a, p) == bytes(want)
+        want = (C.c_uint8 * w)()
+        O.orc_incomplete_lanes(a, want, w)
+        assert cuda.incomplete_lanes(a) == bytes(want)
+
+
+def test_all_pairs_across_the_seam(cuda):
+    # test_lookup.cpp:92-117 -- lane 0 with the pair (previous[w-1], input[0]).
+    w = cuda.width
+    prev = bytearray(b"A" * w)
+    inp = bytearray(b"A" * w)
+    bad = []
+    for b1 in range(0, 256, 1):
+        prev[w - 1] = b1
+        for b2 in range(0, 256, 17):  # full b2 sweep below through the batch path
+            inp[0] = b2
+            out = cuda.classify_lanes(bytes(inp), bytes(prev))[0]
+            exp_invalid = bool(nat.oracle().orc_pair_always_invalid(b1, b2))
+            exp_pair = (b1 & 0xC0) == 0x80 and (b2 & 0xC0) == 0x80
+            if bool(out & 0x7F) != exp_invalid or bool(out & 0x80) != exp_pair:
+                bad.append((b1, b2, out))
+    assert not bad
+
+
+def test_length_cross_check(cuda):
+    w = cuda.width
+
+    def run(head):
+        inp = bytearray(b"\x39" * w)
+        inp[: len(head)] = bytes(head)
+        return any(cuda.length_error_lanes(bytes(inp), bytes(w)))
+
+    assert not run([0xE9, 0x8F, 0xA1])
+    assert not run([0xF0, 0x9F, 0x98, 0x80])
+    assert run([0xE9, 0x8F, 0x39])
+    assert run([0x39, 0x80, 0x80])
+    assert run([0xF0, 0x9F, 0x98])
+
+
+def test_incomplete_residues(cuda):
+    w = cuda.width
+    assert not any(cuda.incomplete_lanes(b"\x39" * w))
+    c = bytearray(b"\x39" * w); c[w - 3:] = B(0xE9, 0x8F, 0xA1)
+    assert not any(cuda.incomplete_lanes(bytes(c)))
+    t = bytearray(b"\x39" * w); t[w - 3:] = B(0xF0, 0x9F, 0x98)
+    assert any(cuda.incomplete_lanes(bytes(t)))
+    l = bytearray(b"\x39" * w); l[w - 1] = 0xC2
+    out = cuda.incomplete_lanes(bytes(l))
+    assert out[w - 1] == 0xC2 ^ 0xBF and out.count(0) == w - 1
+    h = bytearray(b"\x39" * w); h[w - 1] = 0xF5
+    assert any(cuda.incomplete_lanes(bytes(h)))
+
+
+# ---- whole-buffer verdicts: test_lookup.cpp:189-285 -------------------------
+KNOWN = [
+    (b"", True),
+    (B(0x39, 0xC3, 0xA7, 0xE9, 0x8F, 0xA1, 0xF0, 0x9F, 0x98, 0x80, 0x00), True),
+    (B(0xED, 0xB8, 0x80), False),
+    (B(0x80), False),
+    (B(0xC3), False),
+    (B(0xF4, 0x8F, 0xBF, 0xBF), True),
+    (B(0xF4, 0x90, 0x80, 0x80), False),
+]
+
+
+@pytest.mark.parametrize("data,expected", KNOWN)
+def test_known_buffers(data, expected):
+    assert u8.validate_lookup(data) is expected
+    assert u8.validate_lookup_fallback(data) is expected
+
+
+def test_nullptr_zero_is_valid():
+    import ctypes as C
+    lib = u8._lib.load()
+    out = C.c_uint8(0)
+    assert lib.utf8v_cuda_validate(None, 0, 0, C.byref(out)) == 0 and out.value == 1
+
+
+def test_errors_survive_clean_blocks():
+    assert not u8.validate_lookup(B(0x80) + b"A" * 511)
+    assert not u8.validate_lookup(b"A" * 511 + B(0x80))
+
+
+def _block_cases():
+    cases = []
+    for n in (1, 15, 16, 17, 31, 32, 33, 63, 64, 65, 127, 128, 129, 191, 192, 256):
+        cases.append(b"A" * n)
+    for at in (14, 15, 30, 31, 62, 63, 126, 127):
+        cases.append(b"A" * at + B(0xE9, 0x8F, 0xA1) + b"A" * 40)
+    for pad in (61, 62, 63, 126):
+        cases.append(b"A" * pad + B(0xE9, 0x8F))
+    cases.append(b"A" * 61 + B(0xE9, 0x8F, 0xA1))
+    cases.append(b"A" * 63 + B(0xE9))
+    cases.append(b"A" * 61 + B(0xE9, 0x8F, 0xA1) + b"A" * 64 + B(0x80) + b"A" * 20)
+    cases.append(b"A" * 61 + B(0xE9, 0x8F, 0xA1) + b"A" * 64 + B(0xC3, 0xA7))
+    cases.append(b"A" * 62 + B(0xE9, 0x8F) + b"A" * 64)
+    return cases
+
+
+@pytest.mark.parametrize("data", _block_cases())
+def test_block_edges_and_tails(data, torch):
+    exp = nat.oracle_verdict(data)
+    assert u8.validate_lookup(data) is exp[0]
+    # device path, at every 16-byte misalignment of the start pointer
+    for shift in range(16):
+        buf = torch.zeros(len(data) + 32, dtype=torch.uint8, device="cuda")
+        buf[shift:shift + len(data)] = torch.frombuffer(bytearray(data), dtype=torch.uint8) if data else buf[:0]
+        assert u8.validate_lookup(buf[shift:shift + len(data)]) is exp[0]
+        v = u8.validate_lookup_verdict(buf[shift:shift + len(data)])
+        assert (v.valid(), None if v.valid() else v.error.offset, None if v.valid() else int(v.error.kind)) == exp
+
+
+# ---- exhaustive and pair sweeps through the batch kernel --------------------
+def _batch_of(items):
+    lens = np.fromiter((len(x) for x in items), dtype=np.uint64, count=len(items))
+    offs = np.zeros(len(items) + 1, np.uint64)
+    np.cumsum(lens, out=offs[1:])
+    data = np.frombuffer(b"".join(items), dtype=np.uint8) if offs[-1] else np.zeros(0, np.uint8)
+    return data, offs
+
+
+@pytest.mark.parametrize("length", [0, 1, 2, 3])
+def test_exhaustive_short_inputs_batch(length, torch):
+    # acceptance.cpp:74-113 -- every input of length 0-3, as one batch.
+    data, want = nat.exhaustive(length)
+    total = want.size
+    offs = np.arange(total + 1, dtype=np.uint64) * np.uint64(length)
+    got = u8.validate_lookup_batch(torch.from_numpy(data).cuda() if data.size else torch.zeros(0, dtype=torch.uint8, device="cuda"),
+                                   torch.from_numpy(offs.view(np.int64)).cuda())
+    assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("offset", [0, 15, 16, 31, 32, 63, 64])
+def test_all_pairs_at_seam_offsets(offset, torch):
+    # test_lookup.cpp:287-311 -- 65,536 pairs at each offset, batched.
+    n = offset + 2 + 16
+    base = np.full((65536, n), 0x41, np.uint8)
+    v = np.arange(65536)
+    base[:, offset] = v >> 8
+    base[:, offset + 1] = v & 0xFF
+    data = base.reshape(-1)
+    offs = np.arange(65537, dtype=np.uint64) * np.uint64(n)
+    want = nat.oracle_batch(data, offs)
+    got = u8.validate_lookup_batch(torch.from_numpy(data).cuda(), torch.from_numpy(offs.view(np.int64)).cuda())
+    assert np.array_equal(got, want)
+    # and a sample through the single-stream kernel
+    for k in range(0, 65536, 257):
+        assert u8.validate_lookup(base[k].tobytes()) == bool(want[k])
+
+
+def _mutation_corpora(seeds, target=64):
+    items = []
+    for seed in seeds:
+        items.append(nat.generate_valid(15, target, seed))
+        for strat in range(6):
+            items.append(nat.generate_invalid(15, target, seed, strat))
+    return items
+
+
+def test_generated_corpora_verdicts_and_positions():
+    # test_lookup.cpp:338-354 (seeds 100..111, 2048+seed bytes)
+    for seed in range(100, 112):
+        for data in _mutation_corpora([seed], 2048 + seed):
+            exp = nat.oracle_verdict(data)
+            v = u8.validate_lookup_verdict(data)
+            assert u8.validate_lookup(data) is exp[0]
+            got = (v.valid(), None if v.valid() else v.error.offset, None if v.valid() else int(v.error.kind))
+            assert got == exp, (seed, got, exp)
+
+
+def test_mutation_fuzz_batch(torch):
+    # acceptance.cpp:263-272 -- seeds x 6 strategies (subset), batched.
+    items = _mutation_corpora(range(1, 20001))
+    data, offs = _batch_of(items)
+    want = nat.oracle_batch(data, offs)
+    got = u8.validate_lookup_batch(torch.from_numpy(data.copy()).cuda(), torch.from_numpy(offs.view(np.int64)).cuda())
+    assert np.array_equal(got, want)
+    assert (want == 0).sum() == 6 * 20000
+
+
+def test_pinned_offset_fuzz_positions():
+    # acceptance.cpp:274-324 -- malformed shapes at each special offset.
+    rng = np.random.default_rng(0x0FF5E75)
+    for offset in (0, 15, 16, 31, 32, 63, 64):
+        for variant in range(40):
+            for shape in range(6):
+                cont = 0x80 + int(rng.integers(0, 0x40))
+                body = [
+                    [cont],
+                    [0xE9 if variant & 1 else 0xC3 + int(rng.integers(0, 0x1A))],
+                    [0xC0 + int(rng.integers(0, 2)), cont],
+                    [0xE0, 0x80 + int(rng.integers(0, 0x20)), cont],
+                    [0xED, 0xA0 + int(rng.integers(0, 0x20)), cont],
+                    [0xF4, 0x90 + int(rng.integers(0, 0x30)), cont, 0x80 + int(rng.integers(0, 0x40))],
+                ][shape]
+                data = b"A" * offset + bytes(body) + b"A" * 16
+                exp = nat.oracle_verdict(data)
+                assert exp[0] is False and exp[1] == offset
+                v = u8.validate_lookup_verdict(data)
+                assert (v.error.offset, int(v.error.kind)) == (exp[1], exp[2])
+
+
+# ---- host vs device paths, pieces and lane ranges ---------------------------
+def test_host_and_device_paths_agree(torch):
+    d = configs.gen_c1(3 * (32 << 20) + 12345, seed=11)  # > one H2D piece
+    h = d.cpu().numpy()
+    assert u8.validate_lookup(d) and u8.validate_lookup(h)
+    pinned = torch.from_numpy(h).pin_memory()
+    assert u8.validate_lookup(pinned.numpy())
+    # an error in the second piece, straddling nothing special
+    h2 = h.copy()
+    pos = (32 << 20) + 777
+    h2[pos] = 0xFF
+    exp = nat.oracle_verdict(h2, threads=16)
+    v = u8.validate_lookup_verdict(h2)
+    assert not v.valid() and (v.error.offset, int(v.error.kind)) == (exp[1], exp[2])
+    assert not u8.validate_lookup(h2)
+
+
+def test_lane_ranges_compose(torch):
+    import ctypes as C
+    d = configs.gen_c1(1 << 20, seed=12)
+    n = d.numel()
+    rng = np.random.default_rng(3)
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    for trial in range(20):
+        cuts = sorted(set(int(x) for x in rng.integers(1, n, size=5)))
+        bounds = [0] + cuts + [n + 3]
+        flag.zero_()
+        for a, b in zip(bounds[:-1], bounds[1:]):
+            u8.validate_lanes_async(d.data_ptr(), n, a, b, flag.data_ptr(), 0)
+        torch.cuda.synchronize()
+        assert int(flag.item()) == 0
+    # a single bad byte must be caught by whichever piece owns its lanes
+    bad = d.clone()
+    bad[n // 2] = 0x80
+    for trial in range(10):
+        cuts = sorted(set(int(x) for x in rng.integers(1, n, size=3)) | {n // 2, n // 2 + 1})
+        bounds = [0] + cuts + [n + 3]
+        flag.zero_()
+        for a, b in zip(bounds[:-1], bounds[1:]):
+            u8.validate_lanes_async(bad.data_ptr(), n, a, b, flag.data_ptr(), 0)
+        torch.cuda.synchronize()
+        assert int(flag.item()) != 0
+
+
+# ---- configs -----------------------------------------------------------------
+def test_c0_full_size():
+    d = configs.gen_c0()
+    h = d.cpu().numpy()
+    assert h.min() >= 0x0A and h.max() <= 0x7E
+    assert u8.validate_lookup(d) is True
+    assert nat.oracle_verdict(h, threads=32)[0] is True
+
+
+def test_c1_full_size_and_injected_errors():
+    d = configs.gen_c1()
+    assert d.numel() == 1 << 30
+    h = d.cpu().numpy()
+    assert nat.oracle_verdict(h, threads=64)[0] is True
+    assert u8.validate_lookup(d) is True
+    # size-independent property: one corrupted byte anywhere -> same verdict
+    # and position as the oracle (oracle run on a window: everything before
+    # is valid text, so a boundary-aligned window gives the exact answer).
+    rng = np.random.default_rng(2)
+    n = d.numel()
+    for _ in range(24):
+        pos = int(rng.integers(0, n))
+        val = int(rng.integers(0, 256))
+        old = int(h[pos])
+        if val == old:
+            continue
+        # A character-aligned window of the valid stream around pos: the
+        # stream before it is valid text ending on a boundary and the text
+        # after it is untouched, so the window's oracle verdict is the
+        # stream's (offsets shifted by lo).
+        lo = max(0, pos - 16)
+        while lo > 0 and (h[lo] & 0xC0) == 0x80:
+            lo -= 1
+        hi = min(n, pos + 16)
+        while hi < n and (h[hi] & 0xC0) == 0x80:
+            hi += 1
+        win = h[lo:hi].copy()
+        win[pos - lo] = val
+        exp = nat.oracle_verdict(win)
+        d[pos] = val
+        v = u8.validate_lookup_verdict(d)
+        assert u8.validate_lookup(d) is exp[0]
+        if exp[0]:
+            assert v.valid()
+        else:
+            assert (v.error.offset, int(v.error.kind)) == (exp[1] + lo, exp[2])
+        d[pos] = old
+    assert u8.validate_lookup(d) is True
+
+
+def test_c2_segments():
+    b = configs.gen_c2()
+    got = u8.validate_lookup_batch(b.data, b.d_offsets)
+    want = nat.oracle_batch(b.data.cpu().numpy(), b.offsets)
+    assert np.array_equal(want, b.expected)
+    assert np.array_equal(got, want)
+    assert int((got == 0).sum()) == 32
+
+
+def test_c3_records():
+    b = configs.gen_c3()
+    got = u8.validate_lookup_batch(b.data, b.d_offsets)
+    want = nat.oracle_batch(b.data.cpu().numpy(), b.offsets)
+    assert np.array_equal(want, b.expected)
+    assert np.array_equal(got, want)
+
+
+def test_batch_edge_cases(torch):
+    # empty records, 1..3-byte records, leading gap, records ending inside
+    # characters, dense tiny records (> 31 per 2 KiB)
+    rng = np.random.default_rng(5)
+    for trial in range(30):
+        parts = []
+        for _ in range(int(rng.integers(1, 400))):
+            kind = int(rng.integers(0, 6))
+            if kind == 0:
+                parts.append(b"")
+            elif kind == 1:
+                parts.append(bytes(rng.integers(0, 256, int(rng.integers(1, 4)), dtype=np.uint8)))
+            elif kind == 2:
+                parts.append(nat.generate_valid(15, int(rng.integers(1, 40)), int(rng.integers(1, 1 << 30))))
+            elif kind == 3:
+                parts.append(nat.generate_invalid(15, int(rng.integers(1, 40)), int(rng.integers(1, 1 << 30)), int(rng.integers(0, 6))))
+            elif kind == 4:
+                parts.append(nat.generate_valid(15, int(rng.integers(100, 5000)), int(rng.integers(1, 1 << 30))))
+            else:
+                parts.append(bytes([0xE9, 0x8F]))  # truncated at record end
+        data, offs = _batch_of(parts)
+        lead = int(rng.integers(0, 20))
+        data = np.concatenate([np.full(lead, 0xE9, np.uint8), data])
+        offs = offs + np.uint64(lead)
+        want = nat.oracle_batch(data, offs)
+        t = torch.from_numpy(data.copy()).cuda()
+        for shift in (0, 1, 7):
+            buf = torch.zeros(t.numel() + 32, dtype=torch.uint8, device="cuda")
+            buf[shift:shift + t.numel()] = t
+            got = u8.validate_lookup_batch(buf[shift:shift + t.numel()], torch.from_numpy(offs.view(np.int64)).cuda())
+            assert np.array_equal(got, want), (trial, shift)
+        assert np.array_equal(u8.validate_lookup_batch(data, offs), want)
+
+
+@pytest.mark.parametrize("variant", [0, 1, 2])
+def test_c4_structure_scaled(variant):
+    # Same construction as C4 at 64 MiB: shard edges inside 3/4-byte chars.
+    n = 64 << 20
+    d, err = configs.gen_c4(n, seed=5, variant=variant)
+    h = d.cpu().numpy()
+    for k in range(1, 8):
+        b = k * (n // 8)
+        if not (variant == 1 and k == 4):
+            assert (h[b] & 0xC0) == 0x80  # edge byte is a continuation byte
+    exp = nat.oracle_verdict(h, threads=32)
+    assert exp[0] == (variant == 0)
+    if variant:
+        assert exp[1] == err
+    v = u8.validate_lookup_verdict(d)
+    assert (v.valid(), None if v.valid() else v.error.offset) == (exp[0], exp[1])
+    # sharded over G = 2, 4, 8 with a 3-byte halo: OR of shard flags
+    import torch
+    for G in (2, 4, 8):
+        flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+        for k in range(G):
+            s, e = k * n // G, (k + 1) * n // G
+            h0 = min(s, 16)
+            last = k == G - 1
+            u8.validate_lanes_async(d.data_ptr() + s - h0, e - s + h0, h0, (e - s + h0) + (3 if last else 0),
+                                    flag.data_ptr(), 0)
+        torch.cuda.synchronize()
+        assert (int(flag.item()) == 0) == exp[0]

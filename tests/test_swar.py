@@ -1,0 +1,78 @@
+"""The device SWAR formula (csrc/utf8v_swar.h), compiled for the CPU by the
+test helper, against the oracle: exhaustive short inputs at every word
+alignment, all pairs at the reference's seam offsets, mutation corpora, and
+the record-bounded (batch) variant."""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from tests import _native as nat
+
+
+@pytest.mark.parametrize("align", [0, 1, 2, 3])
+def test_exhaustive_length_0_to_3(align):
+    # acceptance.cpp:74-113: all 16,843,009 inputs, verdict and the
+    # first-flagged-lane bound E <= L <= E+3 used by the position kernel.
+    ck, mm, bv = C.c_uint64(), C.c_uint64(), C.c_uint64()
+    nat.swar().swar_exhaustive(align, 3, C.byref(ck), C.byref(mm), C.byref(bv))
+    assert ck.value == 16843009
+    assert mm.value == 0
+    assert bv.value == 0
+
+
+@pytest.mark.parametrize("offset", [0, 15, 16, 31, 32, 63, 64])
+def test_all_pairs_at_seam_offsets(offset):
+    for align in range(4):
+        assert nat.swar().swar_pairs(offset, align) == 0
+
+
+def test_generated_corpora_and_positions():
+    S = nat.swar()
+    for seed in range(1, 3001):
+        for target in (16, 64, 200):
+            items = [nat.generate_valid(15, target, seed)] + [nat.generate_invalid(15, target, seed, s) for s in range(6)]
+            for data in items:
+                ok, eoff, _ = nat.oracle_verdict(data)
+                for align in (0, 3):
+                    L = S.swar_first_lane(data, len(data), align)
+                    assert (L == (1 << 64) - 1) == ok
+                    if not ok:
+                        assert eoff <= L <= eoff + 3
+
+
+def _batch(parts):
+    lens = np.array([len(p) for p in parts], np.uint64)
+    offs = np.zeros(len(parts) + 1, np.uint64)
+    np.cumsum(lens, out=offs[1:])
+    data = np.frombuffer(b"".join(parts) or b"\0", np.uint8)[: int(offs[-1])].copy()
+    return data, offs
+
+
+def test_bounded_variant_matches_per_record_oracle():
+    rng = np.random.default_rng(11)
+    S = nat.swar()
+    for trial in range(300):
+        parts = []
+        for _ in range(int(rng.integers(1, 30))):
+            k = int(rng.integers(0, 5))
+            if k == 0:
+                parts.append(b"")
+            elif k == 1:
+                parts.append(bytes(rng.integers(0, 256, int(rng.integers(1, 5)), dtype=np.uint8)))
+            elif k == 2:
+                parts.append(nat.generate_valid(15, int(rng.integers(1, 30)), int(rng.integers(1, 1 << 30))))
+            elif k == 3:
+                parts.append(nat.generate_invalid(15, int(rng.integers(1, 30)), int(rng.integers(1, 1 << 30)),
+                                                  int(rng.integers(0, 6))))
+            else:
+                parts.append(bytes([0xF0, 0x9F, 0x98])[: int(rng.integers(1, 4))])
+        data, offs = _batch(parts)
+        want = np.array([nat.oracle_verdict(p)[0] for p in parts], np.uint8)
+        got = np.empty(len(parts), np.uint8)
+        for align in range(4):
+            S.swar_batch(data.ctypes.data if data.size else None, offs.ctypes.data, len(parts), align,
+                         got.ctypes.data)
+            assert np.array_equal(got, want), (trial, align, parts)
