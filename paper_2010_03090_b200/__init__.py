@@ -191,7 +191,7 @@ def validate_lookup_batch(data, offsets) -> np.ndarray:
         _lib.check(lib.utf8v_cuda_validate_batch(data.data_ptr() if data.numel() else None, int(data.numel()),
                                                  off.data_ptr(), nrec, 1, ver.data_ptr()))
         return ver.cpu().numpy()
-    ptr, n, _, keep = _host_view(data)
+    ptr, n, keep = _host_view(data)
     off = np.ascontiguousarray(np.asarray(offsets, dtype=np.uint64))
     nrec = int(off.size) - 1
     if nrec <= 0:
