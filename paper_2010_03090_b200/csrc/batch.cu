@@ -33,6 +33,7 @@ struct BatchDesc {
   int64_t c_begin, c_end;
   int64_t steps, steps_per_warp;
   int64_t n_records;
+  u8v_consts k;  // runtime multipliers (FMA-pipe routing, utf8v_swar.h)
 };
 
 __device__ __forceinline__ uint4 ld_stream_b(const uint8_t* p) {
@@ -122,7 +123,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
   if (step >= step_end) return;
 
   uint32_t carry_word = 0;
-  int64_t cstep = d.c_begin + step * kStepChunks;
+  int64_t cstep = d.c_begin + step * kBStepChunks;
   if (lane == 31 && cstep > 0) {
     const int64_t pos = cstep * 16 - 4;
 #pragma unroll
@@ -132,9 +133,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
   int64_t r0 = find_record(d, cstep * 16 - 4);
 
   for (; step < step_end; ++step) {
-    cstep = d.c_begin + step * kStepChunks;
+    cstep = d.c_begin + step * kBStepChunks;
     const int64_t hs = cstep * 16 - 4;                  // first halo byte of the step
-    const int64_t se = (cstep + kStepChunks) * 16;       // step end (exclusive)
+    const int64_t se = (cstep + kBStepChunks) * 16;       // step end (exclusive)
     // Window of record starts: O_k = start(r0 + k).
     const int64_t ok = rec_start(d, r0 + lane);
     const unsigned inside = __ballot_sync(0xFFFFFFFFu, ok < se);
@@ -142,13 +143,13 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
     const bool dense = nb == 32;    // window may not hold every start of the step
 
     const bool interior = cstep * 16 >= d.lo && se <= d.hi;
-    uint4 v[kU];
+    uint4 v[kBU];
     if (interior) {
 #pragma unroll
-      for (int i = 0; i < kU; ++i) v[i] = ld_stream_b(d.base + (cstep + lane + 32 * i) * 16);
+      for (int i = 0; i < kBU; ++i) v[i] = ld_stream_b(d.base + (cstep + lane + 32 * i) * 16);
     } else {
 #pragma unroll
-      for (int i = 0; i < kU; ++i) {
+      for (int i = 0; i < kBU; ++i) {
         const int64_t c = cstep + lane + 32 * i;
         v[i] = c < d.c_end ? ld_chunk_masked_b(d.base, c, d.lo, d.hi) : make_uint4(0, 0, 0, 0);
       }
@@ -156,11 +157,11 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
     const bool single = !dense && nb == 1;  // the whole step lies in record r0
     uint32_t hibits = 0;
 #pragma unroll
-    for (int i = 0; i < kU; ++i) hibits |= v[i].x | v[i].y | v[i].z | v[i].w;
+    for (int i = 0; i < kBU; ++i) hibits |= v[i].x | v[i].y | v[i].z | v[i].w;
     const bool all_ascii = single && __all_sync(0xFFFFFFFFu, (hibits & U8V_B7) == 0);
 
 #pragma unroll
-    for (int i = 0; i < kU; ++i) {
+    for (int i = 0; i < kBU; ++i) {
       const uint32_t supply = lane == 31 ? (i == 0 ? carry_word : v[i - 1].w) : v[i].w;
       const uint32_t prev = __shfl_sync(0xFFFFFFFFu, supply, (lane + 31) & 31);
       const int64_t c = cstep + lane + 32 * i;
@@ -196,7 +197,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
         const uint32_t w4[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          const uint32_t e = u8v_word_errors(w4[k], &cr) & U8V_B7;
+          const uint32_t e = u8v_word_errors_k(w4[k], &cr, d.k) & U8V_B7;
           if (e) attribute(d, rc, c * 16 + 4 * k, e, 0);
         }
       } else {
@@ -207,14 +208,14 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
           const uint32_t bm = u8v_spread4(mask >> (4 + 4 * k));
           const uint32_t pbm = u8v_spread4(mask >> (4 * k));
           uint32_t end_err;
-          const uint32_t e = u8v_word_errors_bounded(w4[k], &cr, bm, pbm, &end_err);
+          const uint32_t e = u8v_word_errors_bounded_k(w4[k], &cr, bm, pbm, &end_err, d.k);
           if (e | end_err) attribute(d, rc, c * 16 + 4 * k, e, end_err);
         }
       }
     }
-    if (lane == 31) carry_word = v[kU - 1].w;
+    if (lane == 31) carry_word = v[kBU - 1].w;
     // Advance the record pointer to the record holding the next step's halo.
-    const int64_t nhs = hs + kStepChunks * 16;
+    const int64_t nhs = hs + kBStepChunks * 16;
     if (!dense) {
       const unsigned le = __ballot_sync(0xFFFFFFFFu, ok <= nhs);
       r0 += (31 - __clz(le));
@@ -241,11 +242,12 @@ void launch_batch_known(const uint8_t* data, const uint64_t* d_offsets, uint64_t
   d.lo = d.off16 + (int64_t)first_off;
   d.hi = d.off16 + (int64_t)last_off;
   d.n_records = (int64_t)n_records;
+  d.k = u8v_make_consts();
   if (d.hi <= d.lo) return;  // every record empty: all valid
   d.c_begin = d.lo / 16;
   d.c_end = (d.hi + 3 + 15) / 16;
   const int64_t chunks = d.c_end - d.c_begin;
-  d.steps = (chunks + kStepChunks - 1) / kStepChunks;
+  d.steps = (chunks + kBStepChunks - 1) / kBStepChunks;
   int64_t warps = max_resident_warps();
   if (warps > d.steps) warps = d.steps;
   if (warps < 1) warps = 1;

@@ -3,11 +3,19 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "utf8v_swar.h"
+
 namespace u8v {
 
 constexpr int kThreads = 256;              // 8 warps per CTA
-constexpr int kU = 4;                      // 16-byte chunks per lane per step
-constexpr int kStepChunks = 32 * kU;       // 128 chunks = 2 KiB per warp step
+// K1/K3 (validate.cu): 32-byte lane chunks, one 256-bit LDG each.
+constexpr int kChunkBytes = 32;
+constexpr int kChunkWords = kChunkBytes / 4;
+constexpr int kU = 2;                      // chunks per lane per step
+constexpr int kStepChunks = 32 * kU;       // 64 chunks = 2 KiB per warp step
+// K2 (batch.cu): 16-byte lane chunks.
+constexpr int kBU = 4;
+constexpr int kBStepChunks = 32 * kBU;     // 128 chunks = 2 KiB per warp step
 
 // error_kind numbering of proj/include/utf8v/verdict.hpp:20-27.
 enum { kHeaderBits = 0, kTooShort = 1, kTooLong = 2, kOverlong = 3, kTooLarge = 4, kSurrogate = 5 };
@@ -20,6 +28,7 @@ struct StreamDesc {
   int64_t c_begin, c_end;  // chunks evaluated: [c_begin, c_end)
   int64_t steps;           // ceil((c_end - c_begin) / kStepChunks)
   int64_t steps_per_warp;
+  u8v_consts k;  // runtime multipliers (FMA-pipe routing, utf8v_swar.h)
 };
 
 int max_resident_warps();

@@ -47,10 +47,51 @@ U8V_HD uint32_t u8v_fsl(uint32_t lo, uint32_t hi, unsigned s) {
 
 #define U8V_B7 0x80808080u
 
+// Integer multiply-add / multiply-high routed to the FMA pipe.  On sm_100a
+// LOP3/SHF/IADD3/VIADD share the ALU pipe (16 lanes/clk/SMSP), which the
+// per-byte logic saturates; IMAD runs on the FMA pipe at the same rate.
+// The multipliers come from kernel arguments (u8v_consts) so ptxas cannot
+// strength-reduce "x*1+K" back into an ALU add or "mulhi(x, 2^k)" into a
+// shift.  Host builds (the CPU checker) compute the same values in C.
+typedef struct {
+  uint32_t one;    // 1
+  uint32_t m256;   // 1 << 8
+  uint32_t mshr4;  // 1 << 28: mulhi(x, 1<<28) == x >> 4
+} u8v_consts;
+
+U8V_HD u8v_consts u8v_make_consts(void) {
+  u8v_consts k;
+  k.one = 1u;
+  k.m256 = 256u;
+  k.mshr4 = 1u << 28;
+  return k;
+}
+
+U8V_HD uint32_t u8v_mad(uint32_t a, uint32_t b, uint32_t c) {
+#if defined(__CUDA_ARCH__)
+  uint32_t d;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+#else
+  return a * b + c;
+#endif
+}
+
+U8V_HD uint32_t u8v_mulhi(uint32_t a, uint32_t b) {
+#if defined(__CUDA_ARCH__)
+  uint32_t d;
+  asm("mul.hi.u32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+#else
+  return (uint32_t)(((uint64_t)a * b) >> 32);
+#endif
+}
+
 // Lane flags of the word before the current one.  p is the raw word; f1/f2/f3
 // hold, in bit 7 of each byte, byte >= C0 / >= E0 / >= F0.
 typedef struct {
   uint32_t p, f1, f2, f3;
+  uint32_t ph;  // p >> 24: the byte that precedes the current word
 } u8v_carry;
 
 U8V_HD u8v_carry u8v_carry_of(uint32_t p) {
@@ -59,6 +100,7 @@ U8V_HD u8v_carry u8v_carry_of(uint32_t p) {
   c.f1 = p & (p << 1);
   c.f2 = c.f1 & (p << 2);
   c.f3 = c.f2 & (p << 3);
+  c.ph = p >> 24;
   return c;
 }
 
@@ -68,13 +110,39 @@ U8V_HD u8v_carry u8v_carry_zero(void) {
   c.f1 = 0;
   c.f2 = 0;
   c.f3 = 0;
+  c.ph = 0;
   return c;
+}
+
+// R: the rare lead pairs, for the pair (a = x[i-1], b = x[i]) in every lane.
+// Key zl = a4 a3 a2 a1 a0 b5 b4 (7 bits); bit 7 of a*4 is a5.
+//   a in C0..DF (a5 = 0): error iff a4 a3 a2 a1 = 0 (C0/C1)  <=>  zl < 08
+//   a >= E0 (a5 = 1; E row a4 = 0, F row a4 = 1; b is a continuation or S
+//   fires): E0 & b<A0 -> zl in {00,01}, ED & b>=A0 -> zl in {36,37},
+//           F0 & b<90 -> zl == 40, F4 & b>=90 or F5..FF -> zl >= 51.
+// Each threshold is one add into bit 7 (zl < 0x80, addend <= 0x7E: no carry
+// leaves a lane), issued as IMAD on the FMA pipe.  `a`, the word of previous
+// bytes, is w*256 + (byte before w), also on the FMA pipe.  Gated by e1
+// (x[i-1] >= C0); flags in bit 7, garbage elsewhere.
+U8V_HD uint32_t u8v_rare_pairs(uint32_t w, uint32_t ph, uint32_t e1, u8v_consts k) {
+  const uint32_t a = u8v_mad(w, k.m256, ph);
+  const uint32_t a4 = a << 2;  // bits 7..2 = a5..a0
+  const uint32_t zl = (a4 & 0x7C7C7C7Cu) | (u8v_mulhi(w, k.mshr4) & 0x03030303u);
+  const uint32_t ge08 = u8v_mad(zl, k.one, 0x78787878u);  // bit7: zl >= 0x08
+  const uint32_t ge02 = u8v_mad(zl, k.one, 0x7E7E7E7Eu);  // zl >= 0x02
+  const uint32_t ge36 = u8v_mad(zl, k.one, 0x4A4A4A4Au);  // zl >= 0x36
+  const uint32_t ge38 = u8v_mad(zl, k.one, 0x48484848u);  // zl >= 0x38
+  const uint32_t ge40 = u8v_mad(zl, k.one, 0x40404040u);  // zl >= 0x40
+  const uint32_t ge41 = u8v_mad(zl, k.one, 0x3F3F3F3Fu);  // zl >= 0x41
+  const uint32_t ge51 = u8v_mad(zl, k.one, 0x2F2F2F2Fu);  // zl >= 0x51
+  const uint32_t bad_ef = ~ge02 | (ge36 & ~ge38) | (ge40 & ~ge41) | ge51;
+  return e1 & ((a4 & bad_ef) | (~a4 & ~ge08));
 }
 
 // Error flags (bit 7 of each byte lane, other bits garbage -- mask with U8V_B7
 // or test via u8v_any) for the four lanes of word w, given the previous word.
 // Advances the carry to w.
-U8V_HD uint32_t u8v_word_errors(uint32_t w, u8v_carry* c) {
+U8V_HD uint32_t u8v_word_errors_k(uint32_t w, u8v_carry* c, u8v_consts k) {
   // --- S: structure (cont XOR expected-continuation) ---------------------
   const uint32_t s1 = w << 1, s2 = w << 2, s3 = w << 3;
   const uint32_t f1 = w & s1;   // >= C0
@@ -85,31 +153,17 @@ U8V_HD uint32_t u8v_word_errors(uint32_t w, u8v_carry* c) {
   const uint32_t e3 = u8v_fsl(c->f3, f3, 24);  // x[i-3] >= F0
   const uint32_t cont = w & ~s1;               // 10xxxxxx
   const uint32_t S = (e1 | e2 | e3) ^ cont;
-
-  // --- R: the rare lead pairs -------------------------------------------
-  // Key zl = a4 a3 a2 a1 a0 b5 b4 (7 bits) for the pair (a = x[i-1], b = x[i]).
-  // For a in C0..DF (a4 a3 a2 a1 = 0 <=> C0/C1): error iff zl < 8.
-  // For a >= E0 (E row has a4=0, F row a4=1; b is a continuation or S fires):
-  //   E0 & b<A0 -> zl in {00,01};  ED & b>=A0 -> zl in {36,37}
-  //   F0 & b<90 -> zl == 40;       F4 & b>=90, F5..FF -> zl >= 51.
-  const uint32_t a = u8v_fsl(c->p, w, 8);
-  const uint32_t zl = ((a & 0x1F1F1F1Fu) << 2) | ((w >> 4) & 0x03030303u);
-  const uint32_t ge08 = zl + 0x78787878u;  // bit7: zl >= 0x08
-  const uint32_t ge02 = zl + 0x7E7E7E7Eu;  // zl >= 0x02
-  const uint32_t ge36 = zl + 0x4A4A4A4Au;  // zl >= 0x36
-  const uint32_t ge38 = zl + 0x48484848u;  // zl >= 0x38
-  const uint32_t ge40 = zl + 0x40404040u;  // zl >= 0x40
-  const uint32_t ge41 = zl + 0x3F3F3F3Fu;  // zl >= 0x41
-  const uint32_t ge51 = zl + 0x2F2F2F2Fu;  // zl >= 0x51
-  const uint32_t a_ge_e0 = u8v_fsl(c->f2, f2, 8);
-  const uint32_t bad_ef = ~ge02 | (ge36 & ~ge38) | (ge40 & ~ge41) | ge51;
-  const uint32_t R = (a_ge_e0 & bad_ef) | (e1 & ~a_ge_e0 & ~ge08);
-
+  const uint32_t R = u8v_rare_pairs(w, c->ph, e1, k);
   c->p = w;
   c->f1 = f1;
   c->f2 = f2;
   c->f3 = f3;
+  c->ph = u8v_mulhi(w, k.m256);
   return S | R;
+}
+
+U8V_HD uint32_t u8v_word_errors(uint32_t w, u8v_carry* c) {
+  return u8v_word_errors_k(w, c, u8v_make_consts());
 }
 
 // Record-bounded variant for the batch kernel: each record is its own
@@ -121,8 +175,8 @@ U8V_HD uint32_t u8v_word_errors(uint32_t w, u8v_carry* c) {
 // *end_err receives, at each record start b, the previous record's
 // end-of-stream check (lookup_kernel.hpp:48-68, :111) restricted to that
 // record's own bytes; the returned flags belong to the record of their lane.
-U8V_HD uint32_t u8v_word_errors_bounded(uint32_t w, u8v_carry* c, uint32_t bm, uint32_t pbm,
-                                        uint32_t* end_err) {
+U8V_HD uint32_t u8v_word_errors_bounded_k(uint32_t w, u8v_carry* c, uint32_t bm, uint32_t pbm,
+                                          uint32_t* end_err, u8v_consts k) {
   const uint32_t s1 = w << 1, s2 = w << 2, s3 = w << 3;
   const uint32_t f1 = w & s1;
   const uint32_t f2 = f1 & s2;
@@ -137,25 +191,20 @@ U8V_HD uint32_t u8v_word_errors_bounded(uint32_t w, u8v_carry* c, uint32_t bm, u
   const uint32_t cont = w & ~s1;
   const uint32_t S = ((e1 & ~bm) | (e2 & ~m2) | (e3 & ~m3)) ^ cont;
 
-  const uint32_t a = u8v_fsl(c->p, w, 8);
-  const uint32_t zl = ((a & 0x1F1F1F1Fu) << 2) | ((w >> 4) & 0x03030303u);
-  const uint32_t ge08 = zl + 0x78787878u;
-  const uint32_t ge02 = zl + 0x7E7E7E7Eu;
-  const uint32_t ge36 = zl + 0x4A4A4A4Au;
-  const uint32_t ge38 = zl + 0x48484848u;
-  const uint32_t ge40 = zl + 0x40404040u;
-  const uint32_t ge41 = zl + 0x3F3F3F3Fu;
-  const uint32_t ge51 = zl + 0x2F2F2F2Fu;
-  const uint32_t a_ge_e0 = u8v_fsl(c->f2, f2, 8);
-  const uint32_t bad_ef = ~ge02 | (ge36 & ~ge38) | (ge40 & ~ge41) | ge51;
-  const uint32_t R = ((a_ge_e0 & bad_ef) | (e1 & ~a_ge_e0 & ~ge08)) & ~bm;
+  const uint32_t R = u8v_rare_pairs(w, c->ph, e1, k) & ~bm;
 
   *end_err = bm & (e1 | (e2 & ~b1) | (e3 & ~b1 & ~b2)) & U8V_B7;
   c->p = w;
   c->f1 = f1;
   c->f2 = f2;
   c->f3 = f3;
+  c->ph = u8v_mulhi(w, k.m256);
   return (S | R) & U8V_B7;
+}
+
+U8V_HD uint32_t u8v_word_errors_bounded(uint32_t w, u8v_carry* c, uint32_t bm, uint32_t pbm,
+                                        uint32_t* end_err) {
+  return u8v_word_errors_bounded_k(w, c, bm, pbm, end_err, u8v_make_consts());
 }
 
 // Spread 4 bits (bit k = byte k) to bit 7 of each byte.
@@ -170,6 +219,7 @@ U8V_HD uint32_t u8v_ascii_word_errors(uint32_t w, u8v_carry* c) {
   c->f1 = 0;
   c->f2 = 0;
   c->f3 = 0;
+  c->ph = w >> 24;
   return e;
 }
 

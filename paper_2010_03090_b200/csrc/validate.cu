@@ -3,9 +3,9 @@
 //   k_validate<false>   K1: OR of the per-lane error flags of one stream (or
 //                       of one lane range of it: a pipeline piece, a shard),
 //                       reduced with REDUX + one atomicOr per warp.
-//   k_validate<true>    K3: the same scan, recording the first 16-byte chunk
+//   k_validate<true>    K3: the same scan, recording the first 32-byte chunk
 //                       that holds a flagged lane (atomicMin per warp).
-//   k_locate            K3b: one thread decodes the <= 26-byte window around
+//   k_locate            K3b: one thread decodes the <= 42-byte window around
 //                       that chunk and writes the reference's (offset, kind).
 //
 // Reference path replaced: validate_with<V> / lookup_checker<V>
@@ -15,13 +15,14 @@
 // (proj/tools/main.cpp:129-147).
 //
 // Data layout: the caller's bytes stay where they are in HBM.  A stream is
-// viewed through a 16-byte aligned base; chunk c is bytes [16c, 16c+16) of
+// viewed through a 32-byte aligned base; chunk c is bytes [32c, 32c+32) of
 // that base, bytes outside the valid range [lo, hi) read as zero (the
 // reference's zero prev vector and zero-padded tail).  A warp owns a
-// contiguous run of 2 KiB steps; in a step lane L holds chunks L, L+32, L+64,
-// L+96 (each load instruction is one coalesced 512-byte sweep) and gets the
-// word before each chunk from lane L-1 with one SHFL (lane 0 from lane 31's
-// previous chunk), so the 3-byte look-back halo never touches memory twice.
+// contiguous run of 2 KiB steps; in a step lane L holds chunks L and L+32,
+// each fetched by one 256-bit LDG (LDG.E.ENL2.256: a warp instruction is one
+// fully coalesced 1 KiB sweep) and gets the word before each chunk from lane
+// L-1 with one SHFL (lane 0 from lane 31's previous chunk), so the 3-byte
+// look-back halo never touches memory twice.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -30,27 +31,33 @@
 
 namespace u8v {
 
-__device__ __forceinline__ uint4 ld_stream(const uint8_t* p) {
-  uint4 r;
-  asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+struct Chunk {
+  uint32_t w[kChunkWords];
+};
+
+__device__ __forceinline__ Chunk ld_chunk(const uint8_t* p) {
+  Chunk c;
+  asm("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=r"(c.w[0]), "=r"(c.w[1]), "=r"(c.w[2]), "=r"(c.w[3]), "=r"(c.w[4]), "=r"(c.w[5]),
+        "=r"(c.w[6]), "=r"(c.w[7])
       : "l"(p));
-  return r;
+  return c;
 }
 
-// Load one 16-byte chunk with every byte outside [lo, hi) replaced by zero;
-// only bytes inside the range are touched (boundary chunks only).
-__device__ __forceinline__ uint4 ld_chunk_masked(const uint8_t* base, int64_t c, int64_t lo,
+// One chunk with every byte outside [lo, hi) replaced by zero; only bytes
+// inside the range are touched (edge chunks only).
+__device__ __forceinline__ Chunk ld_chunk_masked(const uint8_t* base, int64_t c, int64_t lo,
                                                  int64_t hi) {
-  uint32_t w[4] = {0, 0, 0, 0};
-  const int64_t b0 = c * 16;
-  if (b0 >= lo && b0 + 16 <= hi) return ld_stream(base + b0);
+  const int64_t b0 = c * kChunkBytes;
+  if (b0 >= lo && b0 + kChunkBytes <= hi) return ld_chunk(base + b0);
+  Chunk r;
 #pragma unroll
-  for (int k = 0; k < 16; ++k) {
+  for (int j = 0; j < kChunkWords; ++j) r.w[j] = 0;
+  for (int k = 0; k < kChunkBytes; ++k) {
     const int64_t q = b0 + k;
-    if (q >= lo && q < hi) w[k >> 2] |= (uint32_t)base[q] << (8 * (k & 3));
+    if (q >= lo && q < hi) r.w[k >> 2] |= (uint32_t)base[q] << (8 * (k & 3));
   }
-  return make_uint4(w[0], w[1], w[2], w[3]);
+  return r;
 }
 
 __device__ __forceinline__ uint32_t ld_word_masked(const uint8_t* base, int64_t pos, int64_t lo,
@@ -64,25 +71,58 @@ __device__ __forceinline__ uint32_t ld_word_masked(const uint8_t* base, int64_t 
   return w;
 }
 
-__device__ __forceinline__ uint32_t chunk_errors(const uint4 v, uint32_t prev) {
-  u8v_carry c = u8v_carry_of(prev);
-  uint32_t e = u8v_word_errors(v.x, &c);
-  e |= u8v_word_errors(v.y, &c);
-  e |= u8v_word_errors(v.z, &c);
-  e |= u8v_word_errors(v.w, &c);
+// Edge chunks: lanes outside [L0, L1) dropped.
+__device__ __forceinline__ uint32_t chunk_errors_ranged(const Chunk& v, uint32_t prev, int64_t c,
+                                                        u8v_consts k, int64_t L0, int64_t L1) {
+  u8v_carry cr = u8v_carry_of(prev);
+  const int64_t p0 = c * kChunkBytes;
+  uint32_t e = 0;
+#pragma unroll
+  for (int j = 0; j < kChunkWords; ++j)
+    e |= u8v_mask_word(u8v_word_errors_k(v.w[j], &cr, k), p0 + 4 * j, L0, L1);
   return e & U8V_B7;
 }
 
-// Errors of one chunk on the masked path: lanes outside [L0, L1) dropped.
-__device__ __forceinline__ uint32_t chunk_errors_ranged(const uint4 v, uint32_t prev, int64_t c,
-                                                        int64_t L0, int64_t L1) {
-  u8v_carry cr = u8v_carry_of(prev);
-  const int64_t p0 = c * 16;
-  uint32_t e = u8v_mask_word(u8v_word_errors(v.x, &cr), p0, L0, L1);
-  e |= u8v_mask_word(u8v_word_errors(v.y, &cr), p0 + 4, L0, L1);
-  e |= u8v_mask_word(u8v_word_errors(v.z, &cr), p0 + 8, L0, L1);
-  e |= u8v_mask_word(u8v_word_errors(v.w, &cr), p0 + 12, L0, L1);
-  return e & U8V_B7;
+__device__ __forceinline__ uint32_t chunk_hibits(const Chunk& v) {
+  uint32_t h = 0;
+#pragma unroll
+  for (int j = 0; j < kChunkWords; ++j) h |= v.w[j];
+  return h;
+}
+
+// One step of the interior (all bytes real, all lanes wanted): the hot loop.
+// Returns the step's error bits; flags the warp's first chunk in kPos mode.
+template <bool kPos>
+__device__ __forceinline__ uint32_t interior_step(const StreamDesc& d, int64_t cstep, int lane,
+                                                  uint32_t& carry_word, int& first_i) {
+  Chunk v[kU];
+#pragma unroll
+  for (int i = 0; i < kU; ++i) v[i] = ld_chunk(d.base + (cstep + lane + 32 * i) * kChunkBytes);
+  uint32_t hibits = 0;
+#pragma unroll
+  for (int i = 0; i < kU; ++i) hibits |= chunk_hibits(v[i]);
+  const bool all_ascii = __all_sync(0xFFFFFFFFu, (hibits & U8V_B7) == 0);
+  uint32_t step_err = 0;
+#pragma unroll
+  for (int i = 0; i < kU; ++i) {
+    const uint32_t supply =
+        lane == 31 ? (i == 0 ? carry_word : v[i - 1].w[kChunkWords - 1]) : v[i].w[kChunkWords - 1];
+    const uint32_t prev = __shfl_sync(0xFFFFFFFFu, supply, (lane + 31) & 31);
+    uint32_t e;
+    if (all_ascii) {
+      u8v_carry cr = u8v_carry_of(prev);
+      e = u8v_ascii_word_errors(v[i].w[0], &cr);
+    } else {
+      u8v_carry c = u8v_carry_of(prev);
+      e = 0;
+#pragma unroll
+      for (int j = 0; j < kChunkWords; ++j) e |= u8v_word_errors_k(v[i].w[j], &c, d.k);
+    }
+    step_err |= e;
+    if (kPos && (e & U8V_B7) != 0 && first_i == kU) first_i = i;
+  }
+  if (lane == 31) carry_word = v[kU - 1].w[kChunkWords - 1];
+  return step_err & U8V_B7;
 }
 
 template <bool kPos>
@@ -97,55 +137,86 @@ __global__ void __launch_bounds__(kThreads, 4)
   if (step >= step_end) return;
   const int64_t in_lo = d.lo > d.L0 ? d.lo : d.L0;  // interior: all bytes real,
   const int64_t in_hi = d.hi < d.L1 ? d.hi : d.L1;  // all lanes wanted
+  // Interior steps form one contiguous run [int_b, int_e) of step indices.
+  const int64_t sb = kStepChunks * (int64_t)kChunkBytes;
+  int64_t int_b = (in_lo - d.c_begin * kChunkBytes + sb - 1) / sb;
+  int64_t int_e = (in_hi - d.c_begin * kChunkBytes) / sb;
+  if (int_b < 0) int_b = 0;
+  if (int_e < int_b) int_e = int_b;
 
   // Word before this warp's first chunk, supplied by lane 31 to lane 0.
   uint32_t carry_word = 0;
   {
     const int64_t c0 = d.c_begin + step * kStepChunks;
-    if (lane == 31 && c0 > 0) carry_word = ld_word_masked(d.base, c0 * 16 - 4, d.lo, d.hi);
+    if (lane == 31 && c0 > 0) carry_word = ld_word_masked(d.base, c0 * kChunkBytes - 4, d.lo, d.hi);
   }
   uint32_t acc = 0;
+  if (!kPos) {
+    // Hot path: edge steps (stream head / tail only) are peeled off so the
+    // interior loop carries no range tests.
+    const int64_t a = step > int_b ? step : int_b;
+    const int64_t b = step_end < int_e ? step_end : int_e;
+    if (a < b && step == a && step_end == b) {
+      int unused = kU;
+      for (; step < step_end; ++step)
+        acc |= interior_step<false>(d, d.c_begin + step * kStepChunks, lane, carry_word, unused);
+      const unsigned any = __reduce_or_sync(0xFFFFFFFFu, acc & U8V_B7);
+      if (lane == 0 && any) atomicOr(flag, 1u);
+      return;
+    }
+  }
   for (; step < step_end; ++step) {
     const int64_t cstep = d.c_begin + step * kStepChunks;
-    const bool interior = cstep * 16 >= in_lo && (cstep + kStepChunks) * 16 <= in_hi;
-    uint4 v[kU];
+    const bool interior = step >= int_b && step < int_e;
     if (interior) {
+      int first_i = kU;
+      const uint32_t e = interior_step<kPos>(d, cstep, lane, carry_word, first_i);
+      if (!kPos) {
+        acc |= e;
+        continue;
+      }
+      const unsigned long long mine =
+          first_i < kU ? (unsigned long long)(cstep + lane + 32 * first_i) : ~0ull;
+      if (__any_sync(0xFFFFFFFFu, first_i < kU)) {
+        unsigned long long m = mine;
 #pragma unroll
-      for (int i = 0; i < kU; ++i) v[i] = ld_stream(d.base + (cstep + lane + 32 * i) * 16);
-    } else {
+        for (int o = 16; o > 0; o >>= 1) {
+          const unsigned long long t = __shfl_xor_sync(0xFFFFFFFFu, m, o);
+          m = t < m ? t : m;
+        }
+        if (lane == 0) {
+          atomicMin(first_chunk, m);
+          atomicOr(flag, 1u);
+        }
+        return;  // later chunks of this warp cannot be earlier
+      }
+      continue;
+    }
+    // Edge step (stream head or tail): masked loads and lane ranges.
+    Chunk v[kU];
 #pragma unroll
-      for (int i = 0; i < kU; ++i) {
-        const int64_t c = cstep + lane + 32 * i;
-        v[i] = c < d.c_end ? ld_chunk_masked(d.base, c, d.lo, d.hi) : make_uint4(0, 0, 0, 0);
+    for (int i = 0; i < kU; ++i) {
+      const int64_t c = cstep + lane + 32 * i;
+      if (c < d.c_end) {
+        v[i] = ld_chunk_masked(d.base, c, d.lo, d.hi);
+      } else {
+#pragma unroll
+        for (int j = 0; j < kChunkWords; ++j) v[i].w[j] = 0;
       }
     }
-    uint32_t hibits = 0;
-#pragma unroll
-    for (int i = 0; i < kU; ++i) hibits |= v[i].x | v[i].y | v[i].z | v[i].w;
-    const bool all_ascii = __all_sync(0xFFFFFFFFu, (hibits & U8V_B7) == 0);
-
     uint32_t step_err = 0;
     int first_i = kU;
 #pragma unroll
     for (int i = 0; i < kU; ++i) {
-      const uint32_t supply = lane == 31 ? (i == 0 ? carry_word : v[i - 1].w) : v[i].w;
+      const uint32_t supply =
+          lane == 31 ? (i == 0 ? carry_word : v[i - 1].w[kChunkWords - 1]) : v[i].w[kChunkWords - 1];
       const uint32_t prev = __shfl_sync(0xFFFFFFFFu, supply, (lane + 31) & 31);
-      uint32_t e;
-      if (interior) {
-        if (all_ascii) {
-          u8v_carry cr = u8v_carry_of(prev);
-          e = u8v_ascii_word_errors(v[i].x, &cr) & U8V_B7;
-        } else {
-          e = chunk_errors(v[i], prev);
-        }
-      } else {
-        const int64_t c = cstep + lane + 32 * i;
-        e = c < d.c_end ? chunk_errors_ranged(v[i], prev, c, d.L0, d.L1) : 0u;
-      }
+      const int64_t c = cstep + lane + 32 * i;
+      const uint32_t e = c < d.c_end ? chunk_errors_ranged(v[i], prev, c, d.k, d.L0, d.L1) : 0u;
       step_err |= e;
       if (kPos && e != 0 && first_i == kU) first_i = i;
     }
-    if (lane == 31) carry_word = v[kU - 1].w;
+    if (lane == 31) carry_word = v[kU - 1].w[kChunkWords - 1];
     if (kPos) {
       // Chunks of a step are ordered (i, lane); the warp's first flagged chunk
       // is the minimum over lanes of cstep + lane + 32 * first_i.
@@ -205,23 +276,24 @@ __device__ int decode_window(const uint8_t* s, uint64_t from, uint64_t to, uint6
 }
 
 // K3b: turn the first flagged chunk into (offset, kind).  Every flagged lane L
-// satisfies E <= L <= E + 3 for the sequential first error E, so E lies in
-// [chunk_start - 3, chunk_end) and the decode needs bytes up to E + 3.  The
-// window starts at the character boundary at or before chunk_start - 3
-// (at most 3 continuation bytes back; if there are more, E is at that point).
-__global__ void k_locate(const uint8_t* __restrict__ s, uint64_t n, int64_t off16,
+// satisfies E <= L <= E + 3 for the sequential first error E (proven for the
+// lane formula by tests/test_swar.py), so E lies in [chunk_start - 3,
+// chunk_end) and the decode needs bytes up to E + 3.  The window starts at
+// the character boundary at or before chunk_start - 3 (at most 3
+// continuation bytes back; if there are more, E is at that point).
+__global__ void k_locate(const uint8_t* __restrict__ s, uint64_t n, int64_t off,
                          const unsigned long long* __restrict__ first_chunk,
                          unsigned long long* __restrict__ out_offset, int* __restrict__ out_kind) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   const unsigned long long c = *first_chunk;
-  const int64_t lmin = (int64_t)c * 16 - off16;  // first lane of the chunk, stream coords
+  const int64_t lmin = (int64_t)c * kChunkBytes - off;  // first lane of the chunk
   int64_t b0 = lmin - 3;
   if (b0 < 0) b0 = 0;
   if ((uint64_t)b0 > n) b0 = (int64_t)n;
   int64_t b = b0;
   for (int k = 0; k < 3 && b > 0 && (uint64_t)b < n && (s[b] & 0xC0) == 0x80; ++k) --b;
   if ((uint64_t)b < n && (s[b] & 0xC0) == 0x80 && b > 0) b = b0;
-  uint64_t to = (uint64_t)(lmin + 16 + 4);
+  uint64_t to = (uint64_t)(lmin + kChunkBytes + 4);
   if (to > n) to = n;
   uint64_t o = 0;
   const int kind = decode_window(s, (uint64_t)b, to, &o);
@@ -250,18 +322,19 @@ int max_resident_warps() {
 StreamDesc make_desc(const uint8_t* p, uint64_t n, uint64_t lane_lo, uint64_t lane_hi) {
   // Stream coordinates: byte i of the stream is p[i]; lanes [lane_lo,
   // lane_hi) are evaluated (lane_hi <= n + 3).  Chunk coordinates are
-  // relative to the 16-byte aligned base below p.
+  // relative to the 32-byte aligned base below p.
   StreamDesc d;
   const uintptr_t up = (uintptr_t)p;
-  const int64_t off = (int64_t)(up & 15u);
+  const int64_t off = (int64_t)(up & (kChunkBytes - 1));
   d.base = (const uint8_t*)(up - (uintptr_t)off);
   d.lo = off;
   d.hi = off + (int64_t)n;
   d.off16 = off;
+  d.k = u8v_make_consts();
   d.L0 = off + (int64_t)lane_lo;
   d.L1 = off + (int64_t)lane_hi;
-  d.c_begin = d.L0 / 16;
-  d.c_end = (d.L1 + 15) / 16;
+  d.c_begin = d.L0 / kChunkBytes;
+  d.c_end = (d.L1 + kChunkBytes - 1) / kChunkBytes;
   const int64_t chunks = d.c_end - d.c_begin;
   d.steps = (chunks + kStepChunks - 1) / kStepChunks;
   int64_t warps = max_resident_warps();
