@@ -246,31 +246,17 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     ascii_only = args.config == "c0"
     s, e = rank * per, (rank + 1) * per
     halo = min(s, 16)
-    # Generate the shard from the global stream's 64 KiB chunks (same bytes
-    # as generating the whole stream), halo included.
-    G = 65536
-    g0 = (s - halo) // G * G
-    g1 = min(n_total, -(-e // G) * G)
-    full = torch.empty(g1 - g0, dtype=torch.uint8, device=dev)
-    if g0 == 0 and g1 == n_total:
-        _lib.check(lib.utf8v_gen_stream(full.data_ptr(), n_total, seed, int(ascii_only),
-                                        torch.cuda.current_stream().cuda_stream))
-        shard = full[s - halo:e]
-    else:
-        # chunk-aligned window of the global stream: generate it as the head
-        # of a stream view (chunk seeds depend only on the chunk index)
-        tmp = torch.empty(g1, dtype=torch.uint8, device=dev) if g1 <= 4 * GiB else None
-        if tmp is None:
-            raise RuntimeError("shard window too large")
-        _lib.check(lib.utf8v_gen_stream(tmp.data_ptr(), g1, seed, int(ascii_only),
-                                        torch.cuda.current_stream().cuda_stream))
-        shard = tmp[s - halo:e].clone()
-        del tmp
-    del full
+    last = rank == world - 1
+    tail = 0 if last else 1  # the byte after the shard: lane e-1's lookahead
+    # The shard [s - halo, e + tail) of the global stream, generated in place
+    # (chunk seeds depend only on the chunk index: same bytes as generating
+    # the whole stream).
+    shard = torch.empty(e + tail - (s - halo), dtype=torch.uint8, device=dev)
+    _lib.check(lib.utf8v_gen_stream_range(shard.data_ptr(), n_total, s - halo, e + tail, seed, int(ascii_only),
+                                          torch.cuda.current_stream().cuda_stream))
     torch.cuda.synchronize()
     n_local = shard.numel()
-    last = rank == world - 1
-    lane_lo, lane_hi = halo, n_local + (3 if last else 0)
+    lane_lo, lane_hi = halo, (n_local + 3) if last else (halo + per)
     flag = torch.zeros(1, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream()
     sp = stream.cuda_stream

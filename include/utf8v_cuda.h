@@ -90,8 +90,11 @@ int utf8v_cuda_ops_self_test(uint64_t seed, int* out_ok);
  * error is found; the caller zeroes it and reads it back. */
 
 /* Lanes [lane_lo, lane_hi) of the stream d_p[0..n) (zero outside), lane_hi
- * <= n + 3.  Whole stream: lane_lo = 0, lane_hi = n + 3.  A shard of a larger
- * stream passes its halo bytes as the head of d_p and lane_lo = halo length. */
+ * <= n + 3.  Lane j reads bytes j-3 .. j+1.  Whole stream: lane_lo = 0,
+ * lane_hi = n + 3.  A shard [s, e) of a larger stream passes its 3 (or up to
+ * 16) preceding bytes as the head of d_p and the 1 byte after it as the tail:
+ * lane_lo = head length, lane_hi = head length + (e - s), n = head + (e - s)
+ * + 1 (the last shard: no tail byte, lane_hi = n + 3). */
 int utf8v_cuda_validate_lanes_async(const uint8_t* d_p, uint64_t n, uint64_t lane_lo,
                                     uint64_t lane_hi, uint32_t* d_flag, void* stream);
 

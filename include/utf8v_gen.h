@@ -35,6 +35,12 @@ enum {
  * (0x20..0x7E + 2% 0x0A), 0 -> the config-1 length mix. */
 int utf8v_gen_stream(uint8_t* d_out, uint64_t n, uint64_t seed, int ascii_only, void* stream);
 
+/* Bytes [lo, hi) of the n-byte stream utf8v_gen_stream(n, seed, ...) would
+ * produce, written to d_out[0 .. hi-lo) (lo % 4 == 0): the shard a rank of
+ * a multi-GPU run holds, without generating the rest. */
+int utf8v_gen_stream_range(uint8_t* d_out, uint64_t n, uint64_t lo, uint64_t hi, uint64_t seed,
+                           int ascii_only, void* stream);
+
 /* Host (CPU) twin of utf8v_gen_stream writing host memory -- identical
  * bytes; used where no GPU may be touched (bench.py --impl reference). */
 int utf8v_gen_stream_host(uint8_t* out, uint64_t n, uint64_t seed, int ascii_only, int threads);

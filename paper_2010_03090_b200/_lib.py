@@ -42,6 +42,8 @@ SIGNATURES: dict[str, tuple] = {
                                                   C.c_void_p, C.c_void_p, C.c_void_p]),
     "utf8v_cuda_batch_scratch_bytes": (C.c_uint64, [C.c_uint64]),
     "utf8v_gen_stream": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_int, C.c_void_p]),
+    "utf8v_gen_stream_range": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int,
+                                         C.c_void_p]),
     "utf8v_gen_stream_host": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_int, C.c_int]),
     "utf8v_gen_c2": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint64, C.c_void_p,
                                C.c_void_p, C.c_void_p]),

@@ -188,14 +188,25 @@ int utf8v_cuda_validate(const uint8_t* p, size_t n, int is_device, uint8_t* out_
     u8v::launch_validate(u8v::make_desc(p, n, 0, n + 3), c->d_flag, c->s_comp);
     ++t_launches;
   } else {
+    // Piece k's lanes read one byte of piece k+1 (a rare pair is tested at
+    // its lead's lane), so piece k is validated once piece k+1 has landed:
+    // the callback for piece k launches piece k-1; the last piece follows.
+    size_t prev_off = 0, prev_len = 0;
+    bool have_prev = false;
     st = pipeline_h2d(*c, p, n, [&](size_t, size_t off, size_t len) {
-      const bool last = off + len == n;
-      u8v::launch_validate(u8v::make_desc(c->d_stage, n, off, last ? n + 3 : off + len),
-                           c->d_flag, c->s_comp);
-      ++t_launches;
+      if (have_prev) {
+        u8v::launch_validate(u8v::make_desc(c->d_stage, n, prev_off, prev_off + prev_len),
+                             c->d_flag, c->s_comp);
+        ++t_launches;
+      }
+      prev_off = off;
+      prev_len = len;
+      have_prev = true;
       return check_launch("validate kernel");
     });
     if (st) return st;
+    u8v::launch_validate(u8v::make_desc(c->d_stage, n, prev_off, n + 3), c->d_flag, c->s_comp);
+    ++t_launches;
   }
   st = check_launch("validate kernel");
   if (st) return st;

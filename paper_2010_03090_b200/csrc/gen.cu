@@ -196,6 +196,38 @@ void gen_chunks_host(uint8_t* out, uint64_t n, uint64_t seed, int ascii_only, ui
   }
 }
 
+// Bytes [lo, hi) of the n-byte stream (lo % 4 == 0) into out[0 .. hi-lo):
+// chunks inside the window write through the aligned writer, the (at most
+// two) chunks cut by the window regenerate the chunk and keep their part.
+__global__ void k_gen_stream_range(uint8_t* __restrict__ out, uint64_t n, uint64_t lo, uint64_t hi,
+                                   uint64_t seed, int ascii_only) {
+  const uint64_t j = lo / kGenChunk + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t cs = j * kGenChunk;
+  if (cs >= hi || cs >= n) return;
+  const uint64_t ce = cs + kGenChunk < n ? cs + kGenChunk : n;
+  Rng r{chunk_seed(seed, j)};
+  if (cs >= lo && ce <= hi) {
+    fill_range(out - lo, cs, ce, r, ascii_only);
+    return;
+  }
+  // Cut chunk: generate sequentially, store only the window's bytes.
+  uint8_t buf[4];
+  uint64_t p = cs;
+  auto put = [&](uint8_t v) {
+    if (p >= lo && p < hi) out[p - lo] = v;
+    ++p;
+  };
+  if (ascii_only) {
+    while (p < ce) put(rng_below(r, 100) < 2 ? (uint8_t)0x0A : (uint8_t)(0x20 + rng_below(r, 95)));
+  } else {
+    while (ce - p >= 4) {
+      const int len = encode_cp(random_cp(mix_kind(r), r), buf);
+      for (int i = 0; i < len; ++i) put(buf[i]);
+    }
+    while (p < ce) put((uint8_t)(0x20 + rng_below(r, 95)));
+  }
+}
+
 __global__ void k_write_patches(uint8_t* __restrict__ out, const DevPatch* __restrict__ patches,
                                 int npatches) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -369,6 +401,19 @@ extern "C" {
 
 int utf8v_gen_stream(uint8_t* d_out, uint64_t n, uint64_t seed, int ascii_only, void* stream) {
   return gen_stream_impl(d_out, n, seed, ascii_only, {}, (cudaStream_t)stream);
+}
+
+int utf8v_gen_stream_range(uint8_t* d_out, uint64_t n, uint64_t lo, uint64_t hi, uint64_t seed,
+                           int ascii_only, void* stream) {
+  if (lo % 4 != 0 || hi < lo || hi > n) return 2;
+  if (hi == lo) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  const uint64_t chunks = (hi + kGenChunk - 1) / kGenChunk - lo / kGenChunk;
+  const unsigned threads = 64;
+  k_gen_stream_range<<<(unsigned)((chunks + threads - 1) / threads), threads, 0, st>>>(
+      d_out, n, lo, hi, seed, ascii_only);
+  cudaError_t e = cudaStreamSynchronize(st);
+  return cuda_status(e == cudaSuccess ? cudaGetLastError() : e);
 }
 
 int utf8v_gen_stream_host(uint8_t* out, uint64_t n, uint64_t seed, int ascii_only, int threads) {

@@ -11,8 +11,8 @@ constexpr int kThreads = 256;              // 8 warps per CTA
 // K1/K3 (validate.cu): 32-byte lane chunks, one 256-bit LDG each.
 constexpr int kChunkBytes = 32;
 constexpr int kChunkWords = kChunkBytes / 4;
-constexpr int kU = 2;                      // chunks per lane per step
-constexpr int kStepChunks = 32 * kU;       // 64 chunks = 2 KiB per warp step
+constexpr int kU = 4;                      // chunks per lane per step
+constexpr int kStepChunks = 32 * kU;       // 128 chunks = 4 KiB per warp step
 // K2 (batch.cu): 16-byte lane chunks.
 constexpr int kBU = 4;
 constexpr int kBStepChunks = 32 * kBU;     // 128 chunks = 2 KiB per warp step

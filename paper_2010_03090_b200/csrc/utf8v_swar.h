@@ -124,10 +124,7 @@ U8V_HD u8v_carry u8v_carry_zero(void) {
 // leaves a lane), issued as IMAD on the FMA pipe.  `a`, the word of previous
 // bytes, is w*256 + (byte before w), also on the FMA pipe.  Gated by e1
 // (x[i-1] >= C0); flags in bit 7, garbage elsewhere.
-U8V_HD uint32_t u8v_rare_pairs(uint32_t w, uint32_t ph, uint32_t e1, u8v_consts k) {
-  const uint32_t a = u8v_mad(w, k.m256, ph);
-  const uint32_t a4 = a << 2;  // bits 7..2 = a5..a0
-  const uint32_t zl = (a4 & 0x7C7C7C7Cu) | (u8v_mulhi(w, k.mshr4) & 0x03030303u);
+U8V_HD uint32_t u8v_rare_key(uint32_t a4, uint32_t zl, uint32_t e1, u8v_consts k) {
   const uint32_t ge08 = u8v_mad(zl, k.one, 0x78787878u);  // bit7: zl >= 0x08
   const uint32_t ge02 = u8v_mad(zl, k.one, 0x7E7E7E7Eu);  // zl >= 0x02
   const uint32_t ge36 = u8v_mad(zl, k.one, 0x4A4A4A4Au);  // zl >= 0x36
@@ -137,6 +134,51 @@ U8V_HD uint32_t u8v_rare_pairs(uint32_t w, uint32_t ph, uint32_t e1, u8v_consts 
   const uint32_t ge51 = u8v_mad(zl, k.one, 0x2F2F2F2Fu);  // zl >= 0x51
   const uint32_t bad_ef = ~ge02 | (ge36 & ~ge38) | (ge40 & ~ge41) | ge51;
   return e1 & ((a4 & bad_ef) | (~a4 & ~ge08));
+}
+
+// Lag form: the pair ending at each lane of w (a = previous byte), flags at b.
+U8V_HD uint32_t u8v_rare_pairs(uint32_t w, uint32_t ph, uint32_t e1, u8v_consts k) {
+  const uint32_t a = u8v_mad(w, k.m256, ph);
+  const uint32_t a4 = a << 2;  // bits 7..2 = a5..a0
+  const uint32_t zl = (a4 & 0x7C7C7C7Cu) | (u8v_mulhi(w, k.mshr4) & 0x03030303u);
+  return u8v_rare_key(a4, zl, e1, k);
+}
+
+// Upper 32 bits of ((hi:lo) >> s), 0 < s < 32.  SHF.R.W on sm_100a.
+U8V_HD uint32_t u8v_fsr(uint32_t lo, uint32_t hi, unsigned s) {
+#if defined(__CUDA_ARCH__)
+  return __funnelshift_r(lo, hi, s);
+#else
+  return (lo >> s) | (hi << (32 - s));
+#endif
+}
+
+// Lead form (K1's hot loop): the same S, but each rare pair (a, b) is tested
+// at the lane of its lead a, from w itself and the next word wn -- w << 2 is
+// already needed by S and the lead flag f1 is unshifted, so the pair key
+// costs one funnel shift instead of four IMADs.  The flag of pair (j, j+1)
+// sits at lane j; lane j therefore reads byte j+1 (zero past the stream end).
+// Position bound: a flagged lead j is at or after the sequential first
+// error E (a bad pair at a character start is E itself; a lead inside
+// another character's continuation region also fails S there), so the first
+// flagged lane still satisfies E <= L <= E+3 (tests/test_swar.py).
+U8V_HD uint32_t u8v_word_errors_lead(uint32_t w, uint32_t wn, u8v_carry* c, u8v_consts k) {
+  const uint32_t s1 = w << 1, s2 = w << 2, s3 = w << 3;
+  const uint32_t f1 = w & s1;   // >= C0
+  const uint32_t f2 = f1 & s2;  // >= E0
+  const uint32_t f3 = f2 & s3;  // >= F0
+  const uint32_t e1 = u8v_fsl(c->f1, f1, 8);
+  const uint32_t e2 = u8v_fsl(c->f2, f2, 16);
+  const uint32_t e3 = u8v_fsl(c->f3, f3, 24);
+  const uint32_t S = (e1 | e2 | e3) ^ (w & ~s1);
+  const uint32_t t = u8v_fsr(w, wn, 12);  // bits 1,0 of lane j = bits 5,4 of byte j+1
+  const uint32_t zl = (s2 & 0x7C7C7C7Cu) | (t & 0x03030303u);
+  const uint32_t R = u8v_rare_key(s2, zl, f1, k);
+  c->p = w;
+  c->f1 = f1;
+  c->f2 = f2;
+  c->f3 = f3;
+  return S | R;
 }
 
 // Error flags (bit 7 of each byte lane, other bits garbage -- mask with U8V_B7

@@ -18,7 +18,7 @@
 // viewed through a 32-byte aligned base; chunk c is bytes [32c, 32c+32) of
 // that base, bytes outside the valid range [lo, hi) read as zero (the
 // reference's zero prev vector and zero-padded tail).  A warp owns a
-// contiguous run of 2 KiB steps; in a step lane L holds chunks L and L+32,
+// contiguous run of 4 KiB steps; in a step lane L holds chunks L, L+32, L+64, L+96,
 // each fetched by one 256-bit LDG (LDG.E.ENL2.256: a warp instruction is one
 // fully coalesced 1 KiB sweep) and gets the word before each chunk from lane
 // L-1 with one SHFL (lane 0 from lane 31's previous chunk), so the 3-byte
@@ -71,15 +71,27 @@ __device__ __forceinline__ uint32_t ld_word_masked(const uint8_t* base, int64_t 
   return w;
 }
 
-// Edge chunks: lanes outside [L0, L1) dropped.
-__device__ __forceinline__ uint32_t chunk_errors_ranged(const Chunk& v, uint32_t prev, int64_t c,
-                                                        u8v_consts k, int64_t L0, int64_t L1) {
-  u8v_carry cr = u8v_carry_of(prev);
-  const int64_t p0 = c * kChunkBytes;
+// One 32-bit word, zero outside [lo, hi); a single LDG when fully inside.
+__device__ __forceinline__ uint32_t ld_word_guarded(const uint8_t* base, int64_t pos, int64_t lo,
+                                                    int64_t hi) {
+  if (pos >= lo && pos + 4 <= hi) return __ldg(reinterpret_cast<const uint32_t*>(base + pos));
+  return ld_word_masked(base, pos, lo, hi);
+}
+
+// Errors of one chunk given the word before it and the word after it (lead
+// form, utf8v_swar.h); kRanged drops lanes outside [L0, L1).
+template <bool kRanged>
+__device__ __forceinline__ uint32_t chunk_errors(const Chunk& v, uint32_t prev, uint32_t next,
+                                                 u8v_consts k, int64_t p0, int64_t L0, int64_t L1) {
+  u8v_carry c = u8v_carry_of(prev);
   uint32_t e = 0;
 #pragma unroll
-  for (int j = 0; j < kChunkWords; ++j)
-    e |= u8v_mask_word(u8v_word_errors_k(v.w[j], &cr, k), p0 + 4 * j, L0, L1);
+  for (int j = 0; j < kChunkWords; ++j) {
+    const uint32_t wn = j + 1 < kChunkWords ? v.w[j + 1] : next;
+    uint32_t ej = u8v_word_errors_lead(v.w[j], wn, &c, k);
+    if (kRanged) ej = u8v_mask_word(ej, p0 + 4 * j, L0, L1);
+    e |= ej;
+  }
   return e & U8V_B7;
 }
 
@@ -90,43 +102,66 @@ __device__ __forceinline__ uint32_t chunk_hibits(const Chunk& v) {
   return h;
 }
 
+// Errors of one step's chunks v[i] (chunk cstep + lane + 32 i).  The word
+// before each chunk comes from lane L-1 (lane 0: lane 31's previous chunk,
+// or carry_word), the word after from lane L+1 (lane 31: lane 0's next
+// chunk, or nsw = the next step's first word, loaded by lane 0).
+template <bool kPos, bool kRanged>
+__device__ __forceinline__ uint32_t step_errors(const StreamDesc& d, const Chunk (&v)[kU],
+                                                int64_t cstep, int lane, uint32_t& carry_word,
+                                                uint32_t nsw, int& first_i) {
+  bool all_ascii = false;
+  if (!kRanged) {
+    uint32_t hibits = 0;
+#pragma unroll
+    for (int i = 0; i < kU; ++i) hibits |= chunk_hibits(v[i]);
+    all_ascii = __all_sync(0xFFFFFFFFu, (hibits & U8V_B7) == 0);
+  }
+  uint32_t step_err = 0;
+#pragma unroll
+  for (int i = 0; i < kU; ++i) {
+    const uint32_t up =
+        lane == 31 ? (i == 0 ? carry_word : v[i - 1].w[kChunkWords - 1]) : v[i].w[kChunkWords - 1];
+    const uint32_t prev = __shfl_sync(0xFFFFFFFFu, up, (lane + 31) & 31);
+    const uint32_t dn = lane == 0 ? (i + 1 < kU ? v[i + 1].w[0] : nsw) : v[i].w[0];
+    const uint32_t next = __shfl_sync(0xFFFFFFFFu, dn, (lane + 1) & 31);
+    uint32_t e;
+    if (all_ascii) {
+      // No leads in the step: only continuations expected by the bytes
+      // before it (the pending incomplete check, lookup_kernel.hpp:94-96).
+      u8v_carry cr = u8v_carry_of(prev);
+      e = u8v_ascii_word_errors(v[i].w[0], &cr) & U8V_B7;
+    } else {
+      const int64_t c = cstep + lane + 32 * i;
+      e = (kRanged && c >= d.c_end)
+              ? 0u
+              : chunk_errors<kRanged>(v[i], prev, next, d.k, c * kChunkBytes, d.L0, d.L1);
+    }
+    step_err |= e;
+    if (kPos && e != 0 && first_i == kU) first_i = i;
+  }
+  if (lane == 31) carry_word = v[kU - 1].w[kChunkWords - 1];
+  return step_err;
+}
+
 // One step of the interior (all bytes real, all lanes wanted): the hot loop.
-// Returns the step's error bits; flags the warp's first chunk in kPos mode.
-template <bool kPos>
+// kDirect: the next step's first word is known to be inside [lo, hi).
+template <bool kPos, bool kDirect>
 __device__ __forceinline__ uint32_t interior_step(const StreamDesc& d, int64_t cstep, int lane,
                                                   uint32_t& carry_word, int& first_i) {
   Chunk v[kU];
 #pragma unroll
   for (int i = 0; i < kU; ++i) v[i] = ld_chunk(d.base + (cstep + lane + 32 * i) * kChunkBytes);
-  uint32_t hibits = 0;
-#pragma unroll
-  for (int i = 0; i < kU; ++i) hibits |= chunk_hibits(v[i]);
-  const bool all_ascii = __all_sync(0xFFFFFFFFu, (hibits & U8V_B7) == 0);
-  uint32_t step_err = 0;
-#pragma unroll
-  for (int i = 0; i < kU; ++i) {
-    const uint32_t supply =
-        lane == 31 ? (i == 0 ? carry_word : v[i - 1].w[kChunkWords - 1]) : v[i].w[kChunkWords - 1];
-    const uint32_t prev = __shfl_sync(0xFFFFFFFFu, supply, (lane + 31) & 31);
-    uint32_t e;
-    if (all_ascii) {
-      u8v_carry cr = u8v_carry_of(prev);
-      e = u8v_ascii_word_errors(v[i].w[0], &cr);
-    } else {
-      u8v_carry c = u8v_carry_of(prev);
-      e = 0;
-#pragma unroll
-      for (int j = 0; j < kChunkWords; ++j) e |= u8v_word_errors_k(v[i].w[j], &c, d.k);
-    }
-    step_err |= e;
-    if (kPos && (e & U8V_B7) != 0 && first_i == kU) first_i = i;
-  }
-  if (lane == 31) carry_word = v[kU - 1].w[kChunkWords - 1];
-  return step_err & U8V_B7;
+  const int64_t npos = (cstep + kStepChunks) * kChunkBytes;
+  uint32_t nsw = 0;
+  if (lane == 0)
+    nsw = kDirect ? __ldg(reinterpret_cast<const uint32_t*>(d.base + npos))
+                  : ld_word_guarded(d.base, npos, d.lo, d.hi);
+  return step_errors<kPos, false>(d, v, cstep, lane, carry_word, nsw, first_i);
 }
 
 template <bool kPos>
-__global__ void __launch_bounds__(kThreads, 4)
+__global__ void __launch_bounds__(kThreads, 3)
     k_validate(StreamDesc d, uint32_t* __restrict__ flag,
                unsigned long long* __restrict__ first_chunk) {
   const int lane = threadIdx.x & 31;
@@ -143,6 +178,10 @@ __global__ void __launch_bounds__(kThreads, 4)
   int64_t int_e = (in_hi - d.c_begin * kChunkBytes) / sb;
   if (int_b < 0) int_b = 0;
   if (int_e < int_b) int_e = int_b;
+  // ... of which those whose lookahead word (the next step's first word) is
+  // inside [lo, hi) take a plain load.
+  int64_t int_d = (d.hi - 4 - d.c_begin * kChunkBytes) / sb;
+  if (int_d > int_e) int_d = int_e;
 
   // Word before this warp's first chunk, supplied by lane 31 to lane 0.
   uint32_t carry_word = 0;
@@ -155,11 +194,11 @@ __global__ void __launch_bounds__(kThreads, 4)
     // Hot path: edge steps (stream head / tail only) are peeled off so the
     // interior loop carries no range tests.
     const int64_t a = step > int_b ? step : int_b;
-    const int64_t b = step_end < int_e ? step_end : int_e;
+    const int64_t b = step_end < int_d ? step_end : int_d;
     if (a < b && step == a && step_end == b) {
       int unused = kU;
       for (; step < step_end; ++step)
-        acc |= interior_step<false>(d, d.c_begin + step * kStepChunks, lane, carry_word, unused);
+        acc |= interior_step<false, true>(d, d.c_begin + step * kStepChunks, lane, carry_word, unused);
       const unsigned any = __reduce_or_sync(0xFFFFFFFFu, acc & U8V_B7);
       if (lane == 0 && any) atomicOr(flag, 1u);
       return;
@@ -170,7 +209,7 @@ __global__ void __launch_bounds__(kThreads, 4)
     const bool interior = step >= int_b && step < int_e;
     if (interior) {
       int first_i = kU;
-      const uint32_t e = interior_step<kPos>(d, cstep, lane, carry_word, first_i);
+      const uint32_t e = interior_step<kPos, false>(d, cstep, lane, carry_word, first_i);
       if (!kPos) {
         acc |= e;
         continue;
@@ -192,31 +231,24 @@ __global__ void __launch_bounds__(kThreads, 4)
       }
       continue;
     }
-    // Edge step (stream head or tail): masked loads and lane ranges.
+    // Edge step (stream head or tail): masked loads and lane ranges.  The
+    // chunk after the last evaluated one is loaded too: its first byte is
+    // the lookahead of the last evaluated lane (lead form).
     Chunk v[kU];
 #pragma unroll
     for (int i = 0; i < kU; ++i) {
       const int64_t c = cstep + lane + 32 * i;
-      if (c < d.c_end) {
+      if (c <= d.c_end) {
         v[i] = ld_chunk_masked(d.base, c, d.lo, d.hi);
       } else {
 #pragma unroll
         for (int j = 0; j < kChunkWords; ++j) v[i].w[j] = 0;
       }
     }
-    uint32_t step_err = 0;
+    const uint32_t nsw =
+        lane == 0 ? ld_word_guarded(d.base, (cstep + kStepChunks) * kChunkBytes, d.lo, d.hi) : 0u;
     int first_i = kU;
-#pragma unroll
-    for (int i = 0; i < kU; ++i) {
-      const uint32_t supply =
-          lane == 31 ? (i == 0 ? carry_word : v[i - 1].w[kChunkWords - 1]) : v[i].w[kChunkWords - 1];
-      const uint32_t prev = __shfl_sync(0xFFFFFFFFu, supply, (lane + 31) & 31);
-      const int64_t c = cstep + lane + 32 * i;
-      const uint32_t e = c < d.c_end ? chunk_errors_ranged(v[i], prev, c, d.k, d.L0, d.L1) : 0u;
-      step_err |= e;
-      if (kPos && e != 0 && first_i == kU) first_i = i;
-    }
-    if (lane == 31) carry_word = v[kU - 1].w[kChunkWords - 1];
+    const uint32_t step_err = step_errors<kPos, true>(d, v, cstep, lane, carry_word, nsw, first_i);
     if (kPos) {
       // Chunks of a step are ordered (i, lane); the warp's first flagged chunk
       // is the minimum over lanes of cstep + lane + 32 * first_i.

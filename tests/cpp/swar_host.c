@@ -14,17 +14,27 @@
  * into an aligned word grid, exactly like k_validate: words in order, lanes
  * up to n+3 included.  Returns the first flagged lane (stream coords), or
  * UINT64_MAX when none. */
+static uint32_t word_at(const uint8_t* p, int64_t k, int64_t lo, int64_t hi) {
+  uint32_t w = 0;
+  for (int j = 0; j < 4; ++j) {
+    const int64_t q = 4 * k + j;
+    if (q >= lo && q < hi) w |= (uint32_t)p[q - lo] << (8 * j);
+  }
+  return w;
+}
+
+/* K1 drives the lead form (u8v_word_errors_lead: rare pairs flagged at the
+ * lead's lane, reading the next word); the batch kernel the lag form. */
 uint64_t swar_first_lane(const uint8_t* p, size_t n, unsigned off) {
   const int64_t lo = off, hi = (int64_t)off + (int64_t)n;
   const int64_t words = (hi + 3 + 3) / 4;
+  const u8v_consts kc = u8v_make_consts();
   u8v_carry c = u8v_carry_zero();
+  uint32_t w = word_at(p, 0, lo, hi);
   for (int64_t k = 0; k < words; ++k) {
-    uint32_t w = 0;
-    for (int j = 0; j < 4; ++j) {
-      const int64_t q = 4 * k + j;
-      if (q >= lo && q < hi) w |= (uint32_t)p[q - lo] << (8 * j);
-    }
-    const uint32_t e = u8v_word_errors(w, &c) & U8V_B7;
+    const uint32_t wn = word_at(p, k + 1, lo, hi);
+    const uint32_t e = u8v_word_errors_lead(w, wn, &c, kc) & U8V_B7;
+    w = wn;
     if (e) {
       for (int j = 0; j < 4; ++j)
         if ((e >> (8 * j + 7)) & 1) return (uint64_t)(4 * k + j - lo);

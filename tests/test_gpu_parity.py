@@ -441,7 +441,21 @@ def test_c4_structure_scaled(variant):
             s, e = k * n // G, (k + 1) * n // G
             h0 = min(s, 16)
             last = k == G - 1
-            u8.validate_lanes_async(d.data_ptr() + s - h0, e - s + h0, h0, (e - s + h0) + (3 if last else 0),
+            tail = 0 if last else 1  # the byte after the shard (lane e-1's lookahead)
+            nl = e - s + h0 + tail
+            u8.validate_lanes_async(d.data_ptr() + s - h0, nl, h0, (nl + 3) if last else (e - s + h0),
                                     flag.data_ptr(), 0)
         torch.cuda.synchronize()
         assert (int(flag.item()) == 0) == exp[0]
+
+
+def test_stream_range_generator_matches_full_stream(torch):
+    import ctypes as C
+    from paper_2010_03090_b200 import _lib
+    n = (5 << 20) + 4321
+    full = configs.gen_c1(n, seed=9)
+    lib = _lib.load()
+    for lo, hi in [(0, n), (16, 1000), (65536 - 4, 65536 + 7), (131072, 3 << 20), (4 << 20, n), (100, 100)]:
+        out = torch.empty(max(hi - lo, 1), dtype=torch.uint8, device="cuda")
+        _lib.check(lib.utf8v_gen_stream_range(out.data_ptr(), n, lo, hi, 9, 0, torch.cuda.current_stream().cuda_stream))
+        assert torch.equal(out[: hi - lo], full[lo:hi]), (lo, hi)

@@ -127,6 +127,38 @@ __device__ __forceinline__ uint32_t word(uint32_t w, Carry& c, const Cfg& k) {
   }
 }
 
+// V4: R evaluated at the lead's own lane: key from w (s2 = w<<2 gives a5..a0)
+// and the next byte's bits 5,4 via a right funnel with the next word.
+__device__ __forceinline__ uint32_t word4(uint32_t w, uint32_t wn, Carry& c, const Cfg& k) {
+  const uint32_t s1 = w << 1, s2 = w << 2, s3 = w << 3;
+  const uint32_t f1 = w & s1, f2 = f1 & s2, f3 = f2 & s3;
+  const uint32_t e1 = __funnelshift_l(c.f1, f1, 8);
+  const uint32_t e2 = __funnelshift_l(c.f2, f2, 16);
+  const uint32_t e3 = __funnelshift_l(c.f3, f3, 24);
+  const uint32_t S = (e1 | e2 | e3) ^ (w & ~s1);
+  const uint32_t t = __funnelshift_r(w, wn, 12);
+  const uint32_t zl = (s2 & 0x7C7C7C7Cu) | (t & 0x03030303u);
+  const uint32_t R = rare(s2, zl, f1, k);
+  c.f1 = f1; c.f2 = f2; c.f3 = f3;
+  return S | R;
+}
+
+// V5: V4 with the e1 funnel and the next-byte funnel on the FMA pipe.
+__device__ __forceinline__ uint32_t word5(uint32_t w, uint32_t wn, Carry& c, const Cfg& k) {
+  const uint32_t s1 = w << 1, s2 = w << 2, s3 = w << 3;
+  const uint32_t f1 = w & s1, f2 = f1 & s2, f3 = f2 & s3;
+  const uint32_t e1 = mad(f1, k.m256, c.h1);                 // f1<<8 | prev f1>>24
+  const uint32_t e2 = __funnelshift_l(c.f2, f2, 16);
+  const uint32_t e3 = __funnelshift_l(c.f3, f3, 24);
+  const uint32_t S = (e1 | e2 | e3) ^ (w & ~s1);
+  const uint32_t t = mad(wn, 1u << 20, mulhi(w, 1u << 20));  // (wn:w) >> 12
+  const uint32_t zl = (s2 & 0x7C7C7C7Cu) | (t & 0x03030303u);
+  const uint32_t R = rare(s2, zl, f1, k);
+  c.f2 = f2; c.f3 = f3;
+  c.h1 = mulhi(f1, k.m256);
+  return S | R;
+}
+
 template <int V, int U>
 __device__ __forceinline__ void body(const uint8_t* base, int64_t steps, int64_t spw, uint32_t* flag,
                                      const Cfg& k) {
@@ -152,8 +184,18 @@ __device__ __forceinline__ void body(const uint8_t* base, int64_t steps, int64_t
       const uint32_t prev = __shfl_sync(0xFFFFFFFFu, supply, (lane + 31) & 31);
       Carry c = carry_of(prev);
       uint32_t e = 0;
+      if (V == 4) {
+        const uint32_t nextw = __shfl_down_sync(0xFFFFFFFFu, v[i][0], 1);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) e |= word<V>(v[i][j], c, k);
+        for (int j = 0; j < 8; ++j) e |= word4(v[i][j], j < 7 ? v[i][j + 1] : nextw, c, k);
+      } else if (V == 5) {
+        const uint32_t nextw = __shfl_down_sync(0xFFFFFFFFu, v[i][0], 1);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) e |= word5(v[i][j], j < 7 ? v[i][j + 1] : nextw, c, k);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) e |= word<V>(v[i][j], c, k);
+      }
       acc |= e;
     }
     if (lane == 31) carry_word = v[U - 1][7];
@@ -177,6 +219,12 @@ KB_KERNEL(1, 1, 6)
 KB_KERNEL(2, 2, 4)
 KB_KERNEL(2, 1, 6)
 KB_KERNEL(3, 2, 4)
+KB_KERNEL(4, 2, 4)
+KB_KERNEL(0, 4, 3)
+KB_KERNEL(4, 4, 3)
+KB_KERNEL(4, 2, 5)
+KB_KERNEL(5, 2, 4)
+KB_KERNEL(5, 4, 3)
 
 typedef void (*KFn)(const uint8_t*, int64_t, int64_t, uint32_t*, Cfg);
 struct Entry {
@@ -188,6 +236,8 @@ static const Entry kEntries[] = {
     {"v0_u2_b4", k_v0_u2_b4, 2}, {"v0_u1_b4", k_v0_u1_b4, 1}, {"v0_u1_b6", k_v0_u1_b6, 1},
     {"v0_u2_b5", k_v0_u2_b5, 2}, {"v1_u2_b4", k_v1_u2_b4, 2}, {"v1_u1_b6", k_v1_u1_b6, 1},
     {"v2_u2_b4", k_v2_u2_b4, 2}, {"v2_u1_b6", k_v2_u1_b6, 1}, {"v3_u2_b4", k_v3_u2_b4, 2},
+    {"v4_u2_b4", k_v4_u2_b4, 2}, {"v0_u4_b3", k_v0_u4_b3, 4}, {"v4_u4_b3", k_v4_u4_b3, 4},
+    {"v4_u2_b5", k_v4_u2_b5, 2}, {"v5_u2_b4", k_v5_u2_b4, 2}, {"v5_u4_b3", k_v5_u4_b3, 4},
 };
 
 }  // namespace kb
