@@ -103,6 +103,7 @@ def swar():
     L.oracle_exhaustive_verdicts.argtypes = [C.c_int, u8p]
     L.exhaustive_inputs.argtypes = [C.c_int, u8p]
     L.oracle_batch.argtypes = [u8p, u8p, C.c_size_t, C.c_int, u8p, u8p, u8p]
+    L.oracle_cp_sweep.argtypes = [C.POINTER(C.c_uint64)] * 3
     return L
 
 

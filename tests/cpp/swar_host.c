@@ -202,3 +202,33 @@ void oracle_batch(const uint8_t* data, const uint64_t* off, size_t n_records, in
   }
   for (int t = 0; t < threads; ++t) pthread_join(tid[t], NULL);
 }
+
+/* Code-point sweep (proj/tests/test_oracle.cpp:106-121, acceptance.cpp:117-175)
+ * through the oracle restatement: every scalar accepted, every surrogate
+ * rejected as surrogate, every value above U+10FFFF (4-byte shape) rejected
+ * as too-large.  Also checks the SWAR lane formula on each encoding. */
+void oracle_cp_sweep(uint64_t* accepted, uint64_t* rejected, uint64_t* bad) {
+  uint64_t acc = 0, rej = 0, b = 0;
+  uint8_t e[4];
+  for (uint32_t cp = 0; cp <= 0x1FFFFF; ++cp) {
+    const int len = orc_encode(cp, e);
+    uint64_t off;
+    int kind;
+    const int ok = orc_validate(e, (size_t)len, &off, &kind);
+    const int swar = swar_validate(e, (size_t)len, cp & 3);
+    if (swar != ok) ++b;
+    if (cp > 0x10FFFF) {
+      if (ok || kind != ORC_TOO_LARGE || off != 0) ++b;
+      ++rej;
+    } else if (cp >= 0xD800 && cp <= 0xDFFF) {
+      if (ok || kind != ORC_SURROGATE || off != 0) ++b;
+      ++rej;
+    } else {
+      if (!ok) ++b;
+      ++acc;
+    }
+  }
+  *accepted = acc;
+  *rejected = rej;
+  *bad = b;
+}
