@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--config", default="c1", choices=["c0", "c1", "c3", "c4"])
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the C0/C2/C3/C4 side measurements")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     return ap.parse_args()
 
@@ -245,18 +246,18 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     seed = {"c0": 1, "c1": 2, "c4": 5}.get(args.config, 2)
     ascii_only = args.config == "c0"
     s, e = rank * per, (rank + 1) * per
-    halo = min(s, 16)
-    last = rank == world - 1
-    tail = 0 if last else 1  # the byte after the shard: lane e-1's lookahead
-    # The shard [s - halo, e + tail) of the global stream, generated in place
-    # (chunk seeds depend only on the chunk index: same bytes as generating
-    # the whole stream).
-    shard = torch.empty(e + tail - (s - halo), dtype=torch.uint8, device=dev)
-    _lib.check(lib.utf8v_gen_stream_range(shard.data_ptr(), n_total, s - halo, e + tail, seed, int(ascii_only),
+    from paper_2010_03090_b200 import sharding
+    sh = sharding.plan(n_total, world)[rank]
+    halo, last = sh.head, sh.last
+    # The shard [lo, hi) of the global stream (head + tail bytes included),
+    # generated in place: chunk seeds depend only on the chunk index, so the
+    # bytes equal those of the whole stream.
+    shard = torch.empty(sh.n_local, dtype=torch.uint8, device=dev)
+    _lib.check(lib.utf8v_gen_stream_range(shard.data_ptr(), n_total, sh.lo, sh.hi, seed, int(ascii_only),
                                           torch.cuda.current_stream().cuda_stream))
     torch.cuda.synchronize()
     n_local = shard.numel()
-    lane_lo, lane_hi = halo, (n_local + 3) if last else (halo + per)
+    lane_lo, lane_hi = sh.lanes
     flag = torch.zeros(1, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream()
     sp = stream.cuda_stream
@@ -330,29 +331,40 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                 "peak_source": peaks["source"], "kernel": "u8v::k_validate<false>",
                 "kernel_ms": kernel_ms, "algorithmic_bytes_per_launch": alg_bytes}
 
-    # ---- e2e through the public C-ABI with a pinned host buffer -----------
-    e2e = None
-    if rank == 0 or True:
-        host = torch.empty(per, dtype=torch.uint8, pin_memory=True)
-        host.copy_(shard[halo:halo + per])
+    # ---- e2e through the public API with pinned host buffers ---------------
+    es = max(1, args.e2e_steps)
+    if world == 1:
+        # The drop-in call: whole stream from pinned host memory.
+        host = torch.empty(n_local, dtype=torch.uint8, pin_memory=True)
+        host.copy_(shard)
         hp = host.data_ptr()
         ok = C.c_uint8(0)
-        _lib.check(lib.utf8v_cuda_validate(hp, per, 0, C.byref(ok)))  # warm + gate
-        assert ok.value == 1 or rank > 0  # shard alone may start/end mid-character
-        es = max(1, args.e2e_steps)
-        if world > 1:
-            dist.barrier()
+        _lib.check(lib.utf8v_cuda_validate(hp, n_local, 0, C.byref(ok)))  # warm + gate
+        assert ok.value == 1, "e2e verdict mismatch"
         t0 = time.perf_counter()
         for _ in range(es):
-            _lib.check(lib.utf8v_cuda_validate(hp, per, 0, C.byref(ok)))
+            _lib.check(lib.utf8v_cuda_validate(hp, n_local, 0, C.byref(ok)))
         et = time.perf_counter() - t0
-        tt = torch.tensor([et], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e = {"value": per * world * es / float(tt.item()) / 1e9, "unit": "GB/s",
-               "h2d_bytes_per_step": per * world, "d2h_bytes_per_step": 4 * world,
-               "path": "utf8v_cuda_validate(pinned host ptr): 32 MiB H2D pieces overlapped with K1"}
-        del host
+        path = "utf8v_cuda_validate(pinned host ptr): 32 MiB H2D pieces overlapped with K1"
+    else:
+        # Every rank: its pinned host shard -> utf8v_cuda_validate_lanes (H2D +
+        # K1) -> 4-byte NCCL allreduce(MAX) -> verdict (sharding.py).
+        host = torch.empty(n_local, dtype=torch.uint8, pin_memory=True)
+        host.copy_(shard)
+        hnp = host.numpy()
+        assert sharding.validate_sharded(hnp, sh, device=dev), "e2e verdict mismatch"
+        dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(es):
+            sharding.validate_sharded(hnp, sh, device=dev)
+        et = time.perf_counter() - t0
+        path = "sharding.validate_sharded(pinned host shard): utf8v_cuda_validate_lanes + NCCL allreduce(MAX)"
+    tt = torch.tensor([et], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    e2e = {"value": per * world * es / float(tt.item()) / 1e9, "unit": "GB/s",
+           "h2d_bytes_per_step": n_local * world, "d2h_bytes_per_step": 4 * world, "path": path}
+    del host
 
     # ---- CPU baseline (rank 0, N=1): the reference on a bounded sample ----
     cpu = None
@@ -369,6 +381,12 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                              f"validate_lookup (AVX2) split at character boundaries over {T} threads",
                    "single_thread_GBps": r1["best_GBps"], "cpu": cpu_model()}
 
+    extras = None
+    if rank == 0 and world == 1 and not args.no_extras:
+        del shard
+        torch.cuda.empty_cache()
+        extras = measure_extras(lib, dev, max(5, min(args.steps, 50)))
+
     if rank == 0:
         workload = {"c1": "C1: valid UTF-8, 0.4/0.2/0.3/0.1 length mix, seed 2, 1 GiB per GPU",
                     "c0": "C0: 64 MiB ASCII + 2% LF, seed 1, per GPU",
@@ -384,9 +402,80 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                                       + (" + 1-word NCCL allreduce(MAX) per step" if world > 1 else "")},
             "per_gpu_GBps": per_gpu, "verdict_valid": verdict_ok,
             "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks,
-            "gpu_launches": args.steps,
+            "gpu_launches": args.steps, "other_configs": extras,
         }
         print(json.dumps(out))
+
+
+def _time_device(fn, reps: int, stream) -> float:
+    """Mean ms of fn() over reps launches on `stream` (CUDA events)."""
+    import torch
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(reps):
+        fn()
+    b.record(stream)
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+def measure_extras(lib, dev, reps: int) -> dict:
+    """The other BASELINE configs at N=1 (not the headline): C0 GB/s, C2/C3
+    records/s through the batch kernel (K2), C4's 16 GiB stream through K1 and
+    its three variants' verdicts + first-error offsets (K3)."""
+    import torch
+
+    from paper_2010_03090_b200 import _lib, configs
+    import paper_2010_03090_b200 as u8
+
+    st = torch.cuda.current_stream()
+    sp = st.cuda_stream
+    out = {}
+    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+
+    d = configs.gen_c0()
+    n = d.numel()
+    ms = _time_device(lambda: _lib.check(lib.utf8v_cuda_validate_lanes_async(d.data_ptr(), n, 0, n + 3,
+                                                                             flag.data_ptr(), sp)), reps, st)
+    torch.cuda.synchronize()
+    out["c0"] = {"GBps": n / ms / 1e6, "ms": ms, "valid": int(flag.item()) == 0, "bytes": n}
+    del d
+
+    for name, gen in (("c2", configs.gen_c2), ("c3", configs.gen_c3)):
+        b = gen()
+        ver = torch.empty(b.n_records, dtype=torch.uint8, device=dev)
+        fn = lambda: _lib.check(lib.utf8v_cuda_validate_batch_async(  # noqa: E731
+            b.data.data_ptr(), b.nbytes, b.d_offsets.data_ptr(), b.n_records, ver.data_ptr(), None, sp))
+        ms = _time_device(fn, reps, st)
+        got = ver.cpu().numpy()
+        alg = b.nbytes + 8 * (b.n_records + 1) + b.n_records
+        out[name] = {"records_per_s": b.n_records / (ms / 1e3), "GBps": alg / ms / 1e6, "ms": ms,
+                     "records": b.n_records, "bytes": b.nbytes, "invalid_records": int((got == 0).sum()),
+                     "verdicts_match_expected": bool((got == b.expected).all())}
+        del b, ver
+        torch.cuda.empty_cache()
+
+    n4 = configs.C4["n"]
+    c4 = {}
+    for variant in (0, 1, 2):
+        d, err = configs.gen_c4(n4, variant=variant)
+        if variant == 0:
+            ms = _time_device(lambda: _lib.check(lib.utf8v_cuda_validate_lanes_async(
+                d.data_ptr(), n4, 0, n4 + 3, flag.data_ptr(), sp)), max(3, reps // 5), st)
+            c4["A_GBps"] = n4 / ms / 1e6
+            c4["A_ms"] = ms
+        v = u8.validate_lookup_verdict(d)
+        c4["ABC"[variant]] = {"valid": v.valid(), "offset": None if v.valid() else v.error.offset,
+                              "kind": None if v.valid() else str(v.error.kind), "expected_offset": err,
+                              "ok": (v.valid() if err is None else (not v.valid() and v.error.offset == err))}
+        del d
+        torch.cuda.empty_cache()
+    out["c4"] = c4
+    return out
 
 
 def main():

@@ -98,6 +98,13 @@ int utf8v_cuda_ops_self_test(uint64_t seed, int* out_ok);
 int utf8v_cuda_validate_lanes_async(const uint8_t* d_p, uint64_t n, uint64_t lane_lo,
                                     uint64_t lane_hi, uint32_t* d_flag, void* stream);
 
+/* Synchronous lane range over host or device bytes (the shard entry point of
+ * the multi-GPU layer, paper_2010_03090_b200/sharding.py): *out_flag = 0
+ * when lanes [lane_lo, lane_hi) hold no error, nonzero otherwise.  Same lane
+ * contract as utf8v_cuda_validate_lanes_async. */
+int utf8v_cuda_validate_lanes(const uint8_t* p, uint64_t n, uint64_t lane_lo, uint64_t lane_hi,
+                              int is_device, uint32_t* out_flag);
+
 /* Batch on device memory; d_verdicts is written fully (1/0 per record).
  * d_scratch: NULL or >= utf8v_cuda_batch_scratch_bytes(n) device bytes. */
 int utf8v_cuda_validate_batch_async(const uint8_t* d_data, uint64_t n, const uint64_t* d_offsets,

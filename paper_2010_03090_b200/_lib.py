@@ -38,6 +38,8 @@ SIGNATURES: dict[str, tuple] = {
     "utf8v_cuda_ops_self_test": (C.c_int, [C.c_uint64, C.POINTER(C.c_int)]),
     "utf8v_cuda_validate_lanes_async": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64,
                                                   C.c_void_p, C.c_void_p]),
+    "utf8v_cuda_validate_lanes": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int,
+                                            C.POINTER(C.c_uint32)]),
     "utf8v_cuda_validate_batch_async": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64,
                                                   C.c_void_p, C.c_void_p, C.c_void_p]),
     "utf8v_cuda_batch_scratch_bytes": (C.c_uint64, [C.c_uint64]),

@@ -275,6 +275,37 @@ int utf8v_cuda_validate_lanes_async(const uint8_t* d_p, uint64_t n, uint64_t lan
   return check_launch("validate kernel");
 }
 
+int utf8v_cuda_validate_lanes(const uint8_t* p, uint64_t n, uint64_t lane_lo, uint64_t lane_hi,
+                              int is_device, uint32_t* out_flag) {
+  t_launches = 0;
+  if (!out_flag) return fail(UTF8V_ERR_ARG, "out_flag is NULL");
+  if (lane_hi > n + 3 || lane_lo > lane_hi) return fail(UTF8V_ERR_ARG, "bad lane range");
+  *out_flag = 0;
+  if (lane_lo == lane_hi || n == 0) return UTF8V_OK;
+  if (!p) return fail(UTF8V_ERR_ARG, "NULL data");
+  Ctx* c;
+  int st = get_ctx(&c);
+  if (st) return st;
+  CK(cudaMemsetAsync(c->d_flag, 0, 4, c->s_comp));
+  if (is_device) {
+    u8v::launch_validate(u8v::make_desc(p, n, lane_lo, lane_hi), c->d_flag, c->s_comp);
+    ++t_launches;
+  } else {
+    // Copy everything, then one launch (a shard is one piece of work; the
+    // copy of the next rank's shard overlaps on its own GPU).
+    st = pipeline_h2d(*c, p, n, [](size_t, size_t, size_t) { return UTF8V_OK; });
+    if (st) return st;
+    u8v::launch_validate(u8v::make_desc(c->d_stage, n, lane_lo, lane_hi), c->d_flag, c->s_comp);
+    ++t_launches;
+  }
+  st = check_launch("validate kernel");
+  if (st) return st;
+  CK(cudaMemcpyAsync(c->h_res, c->d_flag, 4, cudaMemcpyDeviceToHost, c->s_comp));
+  CK(cudaStreamSynchronize(c->s_comp));
+  *out_flag = c->h_res[0];
+  return UTF8V_OK;
+}
+
 uint64_t utf8v_cuda_batch_scratch_bytes(uint64_t) { return 0; }
 
 int utf8v_cuda_validate_batch_async(const uint8_t* d_data, uint64_t n, const uint64_t* d_offsets,

@@ -104,6 +104,8 @@ def swar():
     L.exhaustive_inputs.argtypes = [C.c_int, u8p]
     L.oracle_batch.argtypes = [u8p, u8p, C.c_size_t, C.c_int, u8p, u8p, u8p]
     L.oracle_cp_sweep.argtypes = [C.POINTER(C.c_uint64)] * 3
+    L.swar_lanes.argtypes = [u8p, C.c_size_t, C.c_uint64, C.c_uint64]
+    L.swar_lanes.restype = C.c_int
     return L
 
 

@@ -1,0 +1,101 @@
+"""Multi-process (gloo, world_size 2 and 4) tests of the shard layer on the
+CPU: the shard plan, head/tail bytes and the allreduce(MAX) combine must
+reproduce the single-stream verdict for streams whose shard edges cut
+characters anywhere.  Each rank's lane-range flag comes from the device
+formula compiled for the CPU (tests/cpp/swar_host.c swar_lanes), so what is
+checked is exactly K1's lane contract."""
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+
+from paper_2010_03090_b200 import sharding
+from tests import _native as nat
+
+
+def cpu_shard_flag(local, shard):
+    a = np.ascontiguousarray(np.frombuffer(bytes(local), np.uint8))
+    lo, hi = shard.lanes
+    return int(nat.swar().swar_lanes(a.ctypes.data if a.size else None, a.size, lo, hi))
+
+
+def _streams():
+    rng = np.random.default_rng(8)
+    out = []
+    base = np.frombuffer(nat.generate_valid(15, 4099, 31), np.uint8).copy()
+    out.append(base)
+    for _ in range(40):
+        d = base.copy()
+        for _k in range(int(rng.integers(0, 2))):
+            d[int(rng.integers(0, d.size))] = int(rng.integers(0, 256))
+        out.append(d)
+    # errors planted right at the shard edges of a 2/4-way split
+    for world in (2, 4):
+        for sh in sharding.plan(base.size, world)[1:]:
+            for delta in (-3, -2, -1, 0, 1, 2):
+                d = base.copy()
+                d[sh.start + delta] = 0xC0
+                out.append(d)
+                e = base.copy()
+                e[sh.start + delta: sh.start + delta + 2] = [0xE0, 0x85]  # overlong pair
+                out.append(e)
+    out.append(np.concatenate([base, np.array([0xF0, 0x9F, 0x98], np.uint8)]))  # truncated end
+    return out
+
+
+def _worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        res = []
+        for d in _streams():
+            sh = sharding.plan(d.size, world)[rank]
+            local = d[sh.lo:sh.hi].tobytes()
+            res.append(sharding.validate_sharded(local, sh, shard_flag=cpu_shard_flag))
+        q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_verdict_equals_single_stream(world):
+    import multiprocessing as mp
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = [nat.oracle_verdict(d)[0] for d in _streams()]
+    for r in range(world):
+        assert results[r] == want
+
+
+def test_plan_covers_stream_and_lane_ranges():
+    for n in (0, 1, 17, 4096, 10 ** 6 + 3):
+        for world in (1, 2, 3, 8):
+            if n < 16 * world and world > 1:
+                continue
+            shards = sharding.plan(n, world)
+            assert shards[0].start == 0 and shards[-1].end == n
+            for a, b in zip(shards, shards[1:]):
+                assert a.end == b.start and b.head == min(b.start, sharding.HEAD) and a.tail == 1
+            covered = []
+            for sh in shards:
+                lo, hi = sh.lanes
+                covered.append((sh.lo + lo, sh.lo + hi))
+            assert covered[0][0] == 0 and covered[-1][1] == n + 3
+            for (a0, a1), (b0, b1) in zip(covered, covered[1:]):
+                assert a1 == b0
