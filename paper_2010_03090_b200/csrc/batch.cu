@@ -7,28 +7,38 @@
 //
 // B200 design: the records' bytes are contiguous in HBM with a CSR offsets
 // array, so the kernel ignores record sizes for load balance and sweeps the
-// byte array in the same 2 KiB warp steps as K1 (coalesced LDG.128, halo via
-// SHFL).  Record starts are turned into per-chunk boundary masks: each step
-// loads a window of 32 offsets (one coalesced load), every lane builds the
-// 20-bit mask of record starts over its chunk's [start-4, end) bytes, and
-// chunks with a start inside use u8v_word_errors_bounded, which drops
-// look-back sources from earlier records and emits the previous record's
-// end check.  Error attribution to records (a few offset reads) only runs
-// when a chunk actually holds an error.  Verdicts start at 1 (memset) and
-// invalid records get a plain 0 store (idempotent, no atomics).
+// byte array exactly like K1 (4 KiB warp steps, 32-byte chunks, one 256-bit
+// LDG each, halo and lookahead by SHFL).  Record starts only matter where
+// they fall inside a chunk's look-back window:
+//   * each step reads a window of 32 record starts (one coalesced load; more
+//     windows only if the step holds more than 31 starts);
+//   * a step with no start in it ("single") runs K1's chunk code unchanged;
+//   * otherwise the lanes holding a start OR a bit into a per-warp shared
+//     mask of the chunk it falls in (and the next chunk's look-back bits), and
+//     only chunks with a nonzero mask take the record-bounded word function
+//     (u8v_word_errors_bounded_lead), out of line so the hot loop stays small
+//     in the instruction cache.
+// Record attribution (a short scan of the offsets) runs only for chunks that
+// hold an error.  Verdicts start at 1 (memset by the caller) and invalid
+// records get a plain 0 store (idempotent, no atomics).
+//
+// The rare-pair check needs no record masking in the lead form: a flagged
+// pair (j, j+1) that crosses into the next record means byte j is a lead
+// ending its record, which is invalid anyway (utf8v_swar.h).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "chunk.cuh"
 #include "kernels.cuh"
 #include "utf8v_swar.h"
 
 namespace u8v {
 
 struct BatchDesc {
-  const uint8_t* base;   // 16-aligned; data byte i is base[off16 + i]
+  const uint8_t* base;   // 32-aligned; data byte i is base[off32 + i]
   const uint64_t* offsets;
   uint8_t* verdicts;
-  int64_t off16;
+  int64_t off32;
   int64_t lo, hi;        // bytes [lo, hi) (base coords) belong to some record
   int64_t c_begin, c_end;
   int64_t steps, steps_per_warp;
@@ -36,30 +46,11 @@ struct BatchDesc {
   u8v_consts k;  // runtime multipliers (FMA-pipe routing, utf8v_swar.h)
 };
 
-__device__ __forceinline__ uint4 ld_stream_b(const uint8_t* p) {
-  uint4 r;
-  asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-      : "l"(p));
-  return r;
-}
-
-__device__ __forceinline__ uint4 ld_chunk_masked_b(const uint8_t* base, int64_t c, int64_t lo,
-                                                   int64_t hi) {
-  const int64_t b0 = c * 16;
-  if (b0 >= lo && b0 + 16 <= hi) return ld_stream_b(base + b0);
-  uint32_t w[4] = {0, 0, 0, 0};
-#pragma unroll
-  for (int k = 0; k < 16; ++k) {
-    const int64_t q = b0 + k;
-    if (q >= lo && q < hi) w[k >> 2] |= (uint32_t)base[q] << (8 * (k & 3));
-  }
-  return make_uint4(w[0], w[1], w[2], w[3]);
-}
+constexpr int kWarpsPerCta = kThreads / 32;
 
 // Offset of record start r in base coordinates (r > n_records: +inf).
 __device__ __forceinline__ int64_t rec_start(const BatchDesc& d, int64_t r) {
-  return r <= d.n_records ? (int64_t)__ldg(d.offsets + r) + d.off16 : INT64_MAX;
+  return r <= d.n_records ? (int64_t)__ldg(d.offsets + r) + d.off32 : INT64_MAX;
 }
 
 // Warp-cooperative: the largest record r in [0, n_records-1] with
@@ -93,135 +84,145 @@ __device__ int64_t record_of(const BatchDesc& d, int64_t r, int64_t q) {
   return r < d.n_records ? r : d.n_records;
 }
 
-// Rare path: store 0 for the record of every flagged lane, and for the
-// record ending at every flagged record start (end check).
-__device__ void attribute(const BatchDesc& d, int64_t r_from, int64_t pos0, uint32_t err,
-                          uint32_t end_err) {
-  for (int j = 0; j < 4; ++j) {
-    const int64_t q = pos0 + j;
-    if ((err >> (8 * j + 7)) & 1) {
-      if (q >= rec_start(d, 0)) {
-        const int64_t r = record_of(d, r_from, q);
-        if (r < d.n_records) d.verdicts[r] = 0;
-      }
-    }
-    if ((end_err >> (8 * j + 7)) & 1) {
-      if (q - 1 >= rec_start(d, 0)) {
-        const int64_t r = record_of(d, r_from, q - 1);
-        if (r < d.n_records) d.verdicts[r] = 0;
-      }
+__device__ __forceinline__ void mark_invalid(const BatchDesc& d, int64_t r_from, int64_t q) {
+  if (q < rec_start(d, 0)) return;
+  const int64_t r = record_of(d, r_from, q);
+  if (r < d.n_records) d.verdicts[r] = 0;
+}
+
+// Out-of-line: the chunk evaluated with record bounds, and the records of
+// its flagged lanes (and of the records ending at flagged starts) marked
+// invalid.  mask bit j <-> a record starts at byte 32c - 4 + j, j < 36.
+// Runs for chunks holding a record start, and to attribute errors found by
+// the inline path (mask 0: the same flags as chunk_errors).
+__device__ __noinline__ void chunk_bounded(const BatchDesc& d, Chunk v, uint32_t prev,
+                                           uint32_t next, unsigned long long mask, int64_t c,
+                                           int64_t r_from) {
+  u8v_carry cr = u8v_carry_of(prev);
+#pragma unroll
+  for (int j = 0; j < kChunkWords; ++j) {
+    const uint32_t wn = j + 1 < kChunkWords ? v.w[j + 1] : next;
+    const uint32_t bm = u8v_spread4((uint32_t)(mask >> (4 + 4 * j)));
+    const uint32_t pbm = u8v_spread4((uint32_t)(mask >> (4 * j)));
+    uint32_t end_err;
+    const uint32_t e = u8v_word_errors_bounded_lead(v.w[j], wn, &cr, bm, pbm, &end_err, d.k);
+    if ((e | end_err) == 0) continue;
+    const int64_t q0 = c * kChunkBytes + 4 * j;
+    for (int b = 0; b < 4; ++b) {
+      if ((e >> (8 * b + 7)) & 1) mark_invalid(d, r_from, q0 + b);
+      if ((end_err >> (8 * b + 7)) & 1) mark_invalid(d, r_from, q0 + b - 1);
     }
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
+__global__ void __launch_bounds__(kThreads, 3) k_batch(BatchDesc d) {
+  __shared__ unsigned long long s_mask[kWarpsPerCta][kStepChunks];
   const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
   const int64_t warp = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
   int64_t step = warp * d.steps_per_warp;
   int64_t step_end = step + d.steps_per_warp;
   if (step_end > d.steps) step_end = d.steps;
   if (step >= step_end) return;
-
-  uint32_t carry_word = 0;
-  int64_t cstep = d.c_begin + step * kBStepChunks;
-  if (lane == 31 && cstep > 0) {
-    const int64_t pos = cstep * 16 - 4;
+  unsigned long long* m = s_mask[wib];
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
-      if (pos + k >= d.lo && pos + k < d.hi) carry_word |= (uint32_t)d.base[pos + k] << (8 * k);
-  }
-  int64_t r0 = find_record(d, cstep * 16 - 4);
+  for (int i = 0; i < kU; ++i) m[lane + 32 * i] = 0;
+
+  constexpr int64_t kStepBytes = (int64_t)kStepChunks * kChunkBytes;
+  int64_t cstep = d.c_begin + step * kStepChunks;
+  uint32_t carry_word = 0;
+  if (lane == 31 && cstep > 0)
+    carry_word = ld_word_masked(d.base, cstep * kChunkBytes - 4, d.lo, d.hi);
+  // r0: the record holding byte hs = step start - 2, the first byte whose
+  // record matters to the step (look-back of its first lanes).
+  int64_t r0 = find_record(d, cstep * kChunkBytes - 2);
 
   for (; step < step_end; ++step) {
-    cstep = d.c_begin + step * kBStepChunks;
-    const int64_t hs = cstep * 16 - 4;                  // first halo byte of the step
-    const int64_t se = (cstep + kBStepChunks) * 16;       // step end (exclusive)
-    // Window of record starts: O_k = start(r0 + k).
-    const int64_t ok = rec_start(d, r0 + lane);
-    const unsigned inside = __ballot_sync(0xFFFFFFFFu, ok < se);
-    const int nb = __popc(inside);  // starts before the step end (O_0 <= hs included)
-    const bool dense = nb == 32;    // window may not hold every start of the step
+    cstep = d.c_begin + step * kStepChunks;
+    const int64_t s0 = cstep * kChunkBytes;
+    const int64_t hs = s0 - 2;
+    const int64_t se = s0 + kStepBytes;
+    const int64_t nhs = se - 2;  // next step's hs
 
-    const bool interior = cstep * 16 >= d.lo && se <= d.hi;
-    uint4 v[kBU];
-    if (interior) {
+    const bool direct = s0 >= d.lo && se + 4 <= d.hi;
+    Chunk v[kU];
+    uint32_t nsw = 0;
+    if (direct) {
 #pragma unroll
-      for (int i = 0; i < kBU; ++i) v[i] = ld_stream_b(d.base + (cstep + lane + 32 * i) * 16);
+      for (int i = 0; i < kU; ++i) v[i] = ld_chunk(d.base + (cstep + lane + 32 * i) * kChunkBytes);
+      if (lane == 0) nsw = __ldg(reinterpret_cast<const uint32_t*>(d.base + se));
     } else {
 #pragma unroll
-      for (int i = 0; i < kBU; ++i) {
+      for (int i = 0; i < kU; ++i) {
         const int64_t c = cstep + lane + 32 * i;
-        v[i] = c < d.c_end ? ld_chunk_masked_b(d.base, c, d.lo, d.hi) : make_uint4(0, 0, 0, 0);
+        v[i] = c <= d.c_end ? ld_chunk_masked(d.base, c, d.lo, d.hi) : zero_chunk();
       }
+      if (lane == 0) nsw = ld_word_guarded(d.base, se, d.lo, d.hi);
     }
-    const bool single = !dense && nb == 1;  // the whole step lies in record r0
-    uint32_t hibits = 0;
-#pragma unroll
-    for (int i = 0; i < kBU; ++i) hibits |= v[i].x | v[i].y | v[i].z | v[i].w;
-    const bool all_ascii = single && __all_sync(0xFFFFFFFFu, (hibits & U8V_B7) == 0);
 
+    // Record starts in [hs, se): the window of the 32 records from r0.
+    int64_t ob = rec_start(d, r0 + lane);
+    unsigned below = __ballot_sync(0xFFFFFFFFu, ob < se);
+    const bool single = below == 1u && rec_start(d, r0) < hs;
+    int64_t r_next = r0;
+    if (!single) {
+      __syncwarp();  // the previous step's readers have cleared their masks
+      int64_t r = r0;
+      for (;;) {
+        if (ob >= hs && ob < se) {
+          const int64_t c = ob >> 5;  // chunk of the start (base coords)
+          const int li = (int)(c - cstep);
+          const int bit = (int)(ob & 31);
+          if (li >= 0) atomicOr(&m[li], 1ull << (bit + 4));
+          if (bit >= 30 && li + 1 < kStepChunks) atomicOr(&m[li + 1], 1ull << (bit - 28));
+        }
+        // The next step's r0: the last record starting at or before nhs.
+        const unsigned le = __ballot_sync(0xFFFFFFFFu, ob <= nhs);
+        if (le != 0u) r_next = r + (31 - __clz(le));
+        if (below != 0xFFFFFFFFu) break;
+        r += 32;  // more than 31 starts in this step: next window
+        ob = rec_start(d, r + lane);
+        below = __ballot_sync(0xFFFFFFFFu, ob < se);
+        if (below == 0u) break;
+      }
+      __syncwarp();
+    }
+
+    bool all_ascii = false;
+    if (single) {
+      uint32_t hibits = 0;
 #pragma unroll
-    for (int i = 0; i < kBU; ++i) {
-      const uint32_t supply = lane == 31 ? (i == 0 ? carry_word : v[i - 1].w) : v[i].w;
-      const uint32_t prev = __shfl_sync(0xFFFFFFFFu, supply, (lane + 31) & 31);
+      for (int i = 0; i < kU; ++i) hibits |= chunk_hibits(v[i]);
+      all_ascii = __all_sync(0xFFFFFFFFu, (hibits & U8V_B7) == 0);
+    }
+#pragma unroll
+    for (int i = 0; i < kU; ++i) {
+      const uint32_t up =
+          lane == 31 ? (i == 0 ? carry_word : v[i - 1].w[kChunkWords - 1]) : v[i].w[kChunkWords - 1];
+      const uint32_t prev = __shfl_sync(0xFFFFFFFFu, up, (lane + 31) & 31);
+      const uint32_t dn = lane == 0 ? (i + 1 < kU ? v[i + 1].w[0] : nsw) : v[i].w[0];
+      const uint32_t next = __shfl_sync(0xFFFFFFFFu, dn, (lane + 1) & 31);
       const int64_t c = cstep + lane + 32 * i;
-      const int64_t cb = c * 16 - 4;  // mask bit j <-> byte cb + j
-      // 20-bit mask of record starts over bytes [16c-4, 16c+16).
-      uint32_t mask = 0;
-      int64_t rc = r0;  // a record starting at or before cb (for attribution)
+      unsigned long long mask = 0;
       if (!single) {
-        if (!dense) {
-          for (int k = 0; k < nb; ++k) {
-            const int64_t b = __shfl_sync(0xFFFFFFFFu, ok, k);
-            if (b <= cb) rc = r0 + k;
-            if (b >= cb && b < cb + 20) mask |= 1u << (b - cb);
-          }
-        } else {
-          // Pathological density (> 31 records per 2 KiB): per-lane scan.
-          rc = record_of(d, r0, cb < 0 ? 0 : cb);
-          if (rc >= d.n_records) rc = d.n_records - 1;
-          for (int64_t r = rc; r <= d.n_records; ++r) {
-            const int64_t b = rec_start(d, r);
-            if (b >= cb + 20) break;
-            if (b >= cb) mask |= 1u << (b - cb);
-          }
-        }
+        mask = m[lane + 32 * i];
+        m[lane + 32 * i] = 0;
       }
-      if (c >= d.c_end) continue;  // after the warp-wide shuffles above
-      if (all_ascii) {
-        u8v_carry cr = u8v_carry_of(prev);
-        const uint32_t e = u8v_ascii_word_errors(v[i].x, &cr) & U8V_B7;
-        if (e) attribute(d, rc, c * 16, e, 0);
-      } else if ((mask >> 2) == 0) {
-        u8v_carry cr = u8v_carry_of(prev);
-        const uint32_t w4[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const uint32_t e = u8v_word_errors_k(w4[k], &cr, d.k) & U8V_B7;
-          if (e) attribute(d, rc, c * 16 + 4 * k, e, 0);
-        }
+      if (mask != 0) {
+        chunk_bounded(d, v[i], prev, next, mask, c, r0);
       } else {
-        u8v_carry cr = u8v_carry_of(prev);
-        const uint32_t w4[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const uint32_t bm = u8v_spread4(mask >> (4 + 4 * k));
-          const uint32_t pbm = u8v_spread4(mask >> (4 * k));
-          uint32_t end_err;
-          const uint32_t e = u8v_word_errors_bounded_k(w4[k], &cr, bm, pbm, &end_err, d.k);
-          if (e | end_err) attribute(d, rc, c * 16 + 4 * k, e, end_err);
+        uint32_t e;
+        if (all_ascii) {
+          u8v_carry cr = u8v_carry_of(prev);
+          e = u8v_ascii_word_errors(v[i].w[0], &cr) & U8V_B7;
+        } else {
+          e = chunk_errors<false>(v[i], prev, next, d.k, 0, 0, 0);
         }
+        if (e) chunk_bounded(d, v[i], prev, next, 0ull, c, r0);
       }
     }
-    if (lane == 31) carry_word = v[kBU - 1].w;
-    // Advance the record pointer to the record holding the next step's halo.
-    const int64_t nhs = hs + kBStepChunks * 16;
-    if (!dense) {
-      const unsigned le = __ballot_sync(0xFFFFFFFFu, ok <= nhs);
-      r0 += (31 - __clz(le));
-    } else {
-      r0 = find_record(d, nhs);
-    }
+    if (lane == 31) carry_word = v[kU - 1].w[kChunkWords - 1];
+    r0 = r_next;
   }
 }
 
@@ -235,19 +236,21 @@ void launch_batch_known(const uint8_t* data, const uint64_t* d_offsets, uint64_t
   if (n_records == 0) return;
   BatchDesc d;
   const uintptr_t up = (uintptr_t)data;
-  d.off16 = (int64_t)(up & 15u);
-  d.base = (const uint8_t*)(up - (uintptr_t)d.off16);
+  d.off32 = (int64_t)(up & (kChunkBytes - 1));
+  d.base = (const uint8_t*)(up - (uintptr_t)d.off32);
   d.offsets = d_offsets;
   d.verdicts = d_verdicts;
-  d.lo = d.off16 + (int64_t)first_off;
-  d.hi = d.off16 + (int64_t)last_off;
+  d.lo = d.off32 + (int64_t)first_off;
+  d.hi = d.off32 + (int64_t)last_off;
   d.n_records = (int64_t)n_records;
   d.k = u8v_make_consts();
   if (d.hi <= d.lo) return;  // every record empty: all valid
-  d.c_begin = d.lo / 16;
-  d.c_end = (d.hi + 3 + 15) / 16;
+  // Lanes [lo, hi]: lane hi carries the last record's end check; lanes past
+  // it read zeros behind a record start and cannot flag.
+  d.c_begin = d.lo / kChunkBytes;
+  d.c_end = d.hi / kChunkBytes + 1;
   const int64_t chunks = d.c_end - d.c_begin;
-  d.steps = (chunks + kBStepChunks - 1) / kBStepChunks;
+  d.steps = (chunks + kStepChunks - 1) / kStepChunks;
   int64_t warps = max_resident_warps();
   if (warps > d.steps) warps = d.steps;
   if (warps < 1) warps = 1;

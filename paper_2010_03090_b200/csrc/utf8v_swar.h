@@ -249,6 +249,36 @@ U8V_HD uint32_t u8v_word_errors_bounded(uint32_t w, u8v_carry* c, uint32_t bm, u
   return u8v_word_errors_bounded_k(w, c, bm, pbm, end_err, u8v_make_consts());
 }
 
+// Record-bounded, lead form (K2): S and the end checks exactly as
+// u8v_word_errors_bounded_k; the rare pair (j, j+1) is tested at lane j with
+// no boundary mask -- a flag on a pair that crosses into the next record
+// means byte j is a lead that ends its record, which is invalid anyway (its
+// end check fires too), and the flag sits on that record's lane.
+U8V_HD uint32_t u8v_word_errors_bounded_lead(uint32_t w, uint32_t wn, u8v_carry* c, uint32_t bm,
+                                             uint32_t pbm, uint32_t* end_err, u8v_consts k) {
+  const uint32_t s1 = w << 1, s2 = w << 2, s3 = w << 3;
+  const uint32_t f1 = w & s1;
+  const uint32_t f2 = f1 & s2;
+  const uint32_t f3 = f2 & s3;
+  const uint32_t e1 = u8v_fsl(c->f1, f1, 8);
+  const uint32_t e2 = u8v_fsl(c->f2, f2, 16);
+  const uint32_t e3 = u8v_fsl(c->f3, f3, 24);
+  const uint32_t b1 = u8v_fsl(pbm, bm, 8);   // a record starts at i-1
+  const uint32_t b2 = u8v_fsl(pbm, bm, 16);  // a record starts at i-2
+  const uint32_t m2 = bm | b1;
+  const uint32_t m3 = m2 | b2;
+  const uint32_t S = ((e1 & ~bm) | (e2 & ~m2) | (e3 & ~m3)) ^ (w & ~s1);
+  const uint32_t t = u8v_fsr(w, wn, 12);
+  const uint32_t zl = (s2 & 0x7C7C7C7Cu) | (t & 0x03030303u);
+  const uint32_t R = u8v_rare_key(s2, zl, f1, k);
+  *end_err = bm & (e1 | (e2 & ~b1) | (e3 & ~b1 & ~b2)) & U8V_B7;
+  c->p = w;
+  c->f1 = f1;
+  c->f2 = f2;
+  c->f3 = f3;
+  return (S | R) & U8V_B7;
+}
+
 // Spread 4 bits (bit k = byte k) to bit 7 of each byte.
 U8V_HD uint32_t u8v_spread4(uint32_t x) { return ((x & 0xFu) * 0x10204080u) & U8V_B7; }
 

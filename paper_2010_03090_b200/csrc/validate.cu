@@ -26,81 +26,11 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "chunk.cuh"
 #include "kernels.cuh"
 #include "utf8v_swar.h"
 
 namespace u8v {
-
-struct Chunk {
-  uint32_t w[kChunkWords];
-};
-
-__device__ __forceinline__ Chunk ld_chunk(const uint8_t* p) {
-  Chunk c;
-  asm("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-      : "=r"(c.w[0]), "=r"(c.w[1]), "=r"(c.w[2]), "=r"(c.w[3]), "=r"(c.w[4]), "=r"(c.w[5]),
-        "=r"(c.w[6]), "=r"(c.w[7])
-      : "l"(p));
-  return c;
-}
-
-// One chunk with every byte outside [lo, hi) replaced by zero; only bytes
-// inside the range are touched (edge chunks only).
-__device__ __forceinline__ Chunk ld_chunk_masked(const uint8_t* base, int64_t c, int64_t lo,
-                                                 int64_t hi) {
-  const int64_t b0 = c * kChunkBytes;
-  if (b0 >= lo && b0 + kChunkBytes <= hi) return ld_chunk(base + b0);
-  Chunk r;
-#pragma unroll
-  for (int j = 0; j < kChunkWords; ++j) r.w[j] = 0;
-  for (int k = 0; k < kChunkBytes; ++k) {
-    const int64_t q = b0 + k;
-    if (q >= lo && q < hi) r.w[k >> 2] |= (uint32_t)base[q] << (8 * (k & 3));
-  }
-  return r;
-}
-
-__device__ __forceinline__ uint32_t ld_word_masked(const uint8_t* base, int64_t pos, int64_t lo,
-                                                   int64_t hi) {
-  uint32_t w = 0;
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int64_t q = pos + k;
-    if (q >= lo && q < hi) w |= (uint32_t)base[q] << (8 * k);
-  }
-  return w;
-}
-
-// One 32-bit word, zero outside [lo, hi); a single LDG when fully inside.
-__device__ __forceinline__ uint32_t ld_word_guarded(const uint8_t* base, int64_t pos, int64_t lo,
-                                                    int64_t hi) {
-  if (pos >= lo && pos + 4 <= hi) return __ldg(reinterpret_cast<const uint32_t*>(base + pos));
-  return ld_word_masked(base, pos, lo, hi);
-}
-
-// Errors of one chunk given the word before it and the word after it (lead
-// form, utf8v_swar.h); kRanged drops lanes outside [L0, L1).
-template <bool kRanged>
-__device__ __forceinline__ uint32_t chunk_errors(const Chunk& v, uint32_t prev, uint32_t next,
-                                                 u8v_consts k, int64_t p0, int64_t L0, int64_t L1) {
-  u8v_carry c = u8v_carry_of(prev);
-  uint32_t e = 0;
-#pragma unroll
-  for (int j = 0; j < kChunkWords; ++j) {
-    const uint32_t wn = j + 1 < kChunkWords ? v.w[j + 1] : next;
-    uint32_t ej = u8v_word_errors_lead(v.w[j], wn, &c, k);
-    if (kRanged) ej = u8v_mask_word(ej, p0 + 4 * j, L0, L1);
-    e |= ej;
-  }
-  return e & U8V_B7;
-}
-
-__device__ __forceinline__ uint32_t chunk_hibits(const Chunk& v) {
-  uint32_t h = 0;
-#pragma unroll
-  for (int j = 0; j < kChunkWords; ++j) h |= v.w[j];
-  return h;
-}
 
 // Errors of one step's chunks v[i] (chunk cstep + lane + 32 i).  The word
 // before each chunk comes from lane L-1 (lane 0: lane 31's previous chunk,

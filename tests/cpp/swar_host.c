@@ -124,17 +124,19 @@ void swar_batch(const uint8_t* data, const uint64_t* offsets, size_t n_records, 
   u8v_carry c = u8v_carry_zero();
   uint32_t pbm = 0;
   size_t rcur = 0; /* record of the current lane */
+  const u8v_consts kc = u8v_make_consts();
   for (int64_t k = lo / 4; k < words; ++k) {
-    uint32_t w = 0, bm = 0;
+    uint32_t w = 0, wn = 0, bm = 0;
     for (int j = 0; j < 4; ++j) {
       const int64_t q = 4 * k + j;
       if (q >= lo && q < hi) w |= (uint32_t)data[q - (int64_t)off] << (8 * j);
+      if (q + 4 >= lo && q + 4 < hi) wn |= (uint32_t)data[q + 4 - (int64_t)off] << (8 * j);
       for (size_t r = 0; r <= n_records; ++r)
         if ((int64_t)offsets[r] + (int64_t)off == q) bm |= 0x80u << (8 * j);
     }
     if (k == lo / 4) c = u8v_carry_zero();
     uint32_t end_err = 0;
-    const uint32_t e = u8v_word_errors_bounded(w, &c, bm, pbm, &end_err);
+    const uint32_t e = u8v_word_errors_bounded_lead(w, wn, &c, bm, pbm, &end_err, kc);
     for (int j = 0; j < 4; ++j) {
       const int64_t q = 4 * k + j - (int64_t)off; /* data coords */
       /* record of lane q: largest r < n with offsets[r] <= q */
