@@ -4,9 +4,9 @@
  *
  * It replaces, for the Lookup path of the reference `utf8v` library, the
  * backend function-pointer table and its dispatch:
- *   struct lookup_backend          proj/include/utf8v/lookup.hpp:77-87
- *   lookup_backends / find_...     proj/include/utf8v/lookup.hpp:89-94, proj/src/lookup.cpp:16-37
- *   validate_lookup[_fallback]     proj/include/utf8v/lookup.hpp:96-100, proj/src/lookup.cpp:39-45
+ *   struct lookup_backend          proj/include/utf8v/lookup.hpp:18-28
+ *   lookup_backends / find_...     proj/include/utf8v/lookup.hpp:30-35, proj/src/lookup.cpp:16-37
+ *   validate_lookup[_fallback]     proj/include/utf8v/lookup.hpp:37-41, proj/src/lookup.cpp:39-45
  * and adds the position and record-batch variants the reference obtains by
  * re-running oracle_validate (proj/src/oracle.cpp:10-44; the CLI failure path
  * proj/tools/main.cpp:129-147) or by looping validate_lookup per record.
@@ -51,7 +51,7 @@ int utf8v_cuda_abi_version(void);
 /* Human-readable text of the last error on this thread ("" if none). */
 const char* utf8v_cuda_last_error(void);
 
-/* lookup_backend::validate (proj/include/utf8v/lookup.hpp:80) and
+/* lookup_backend::validate (proj/include/utf8v/lookup.hpp:21) and
  * validate_lookup (proj/src/lookup.cpp:39-41): *out_valid = 1 iff p[0..n)
  * is valid UTF-8.  Host input is streamed to the GPU in pieces, each piece
  * validated as soon as it lands (copy and compute overlap). */
@@ -73,13 +73,13 @@ int utf8v_cuda_validate_batch(const uint8_t* data, size_t n, const uint64_t* off
                               size_t n_records, int is_device, uint8_t* verdicts);
 
 /* Lane entry points over UTF8V_CUDA_WIDTH host bytes (lookup_backend
- * ::classify_lanes / length_error_lanes / incomplete_lanes, lookup.hpp:81-85;
+ * ::classify_lanes / length_error_lanes / incomplete_lanes, lookup.hpp:22-26;
  * proj/src/lookup_backend_detail.hpp:16-43), computed on the GPU. */
 int utf8v_cuda_classify_lanes(const uint8_t* input, const uint8_t* previous, uint8_t* out);
 int utf8v_cuda_length_error_lanes(const uint8_t* input, const uint8_t* previous, uint8_t* out);
 int utf8v_cuda_incomplete_lanes(const uint8_t* input, uint8_t* out);
 
-/* lookup_backend::ops_self_test (lookup.hpp:86; lookup_kernel.hpp:139-216):
+/* lookup_backend::ops_self_test (lookup.hpp:27; lookup_kernel.hpp:139-216):
  * *out_ok = 1 iff every SWAR vector operation matches plain arithmetic. */
 int utf8v_cuda_ops_self_test(uint64_t seed, int* out_ok);
 

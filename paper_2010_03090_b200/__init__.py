@@ -125,7 +125,7 @@ def _self_test(seed: int) -> bool:
 
 @dataclass(frozen=True)
 class LookupBackend:
-    """struct lookup_backend, proj/include/utf8v/lookup.hpp:77-87."""
+    """struct lookup_backend, proj/include/utf8v/lookup.hpp:18-28."""
     name: str
     width: int
     validate: Callable[[object], bool]

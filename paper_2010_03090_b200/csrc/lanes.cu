@@ -2,7 +2,7 @@
 //
 // The reference exposes, per backend, classify_lanes / length_error_lanes /
 // incomplete_lanes over exactly `width` bytes and a vector-operation self
-// test (proj/include/utf8v/lookup.hpp:77-87, proj/src/lookup_backend_detail.hpp
+// test (proj/include/utf8v/lookup.hpp:18-28, proj/src/lookup_backend_detail.hpp
 // :16-43, proj/include/utf8v/lookup_kernel.hpp:139-216) so tests can compare
 // backends lane by lane.  Here the "vector" is kLaneWidth = 64 bytes held as
 // 16 32-bit words, one word per thread, and the byte_vector operations are

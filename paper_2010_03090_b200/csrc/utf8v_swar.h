@@ -162,11 +162,19 @@ U8V_HD uint32_t u8v_fsr(uint32_t lo, uint32_t hi, unsigned s) {
 // error E (a bad pair at a character start is E itself; a lead inside
 // another character's continuation region also fails S there), so the first
 // flagged lane still satisfies E <= L <= E+3 (tests/test_swar.py).
+//
+// The lead flags are threshold adds on h = (w >> 1) & 0x7F..: bit 7 of
+// h + 0x20 / 0x10 / 0x08 is byte >= C0 / E0 / F0 (h < 0x80: no carry leaves a
+// lane).  One mask on the ALU pipe plus four IMADs replaces three LOP3s and
+// two shifts -- the loop is bound by the ALU pipe, so this is a measured
+// +4% (tools/kbench.cu, V6 vs V4).  Only bit 7 of f1/f2/f3 is meaningful,
+// as with the AND form.
 U8V_HD uint32_t u8v_word_errors_lead(uint32_t w, uint32_t wn, u8v_carry* c, u8v_consts k) {
-  const uint32_t s1 = w << 1, s2 = w << 2, s3 = w << 3;
-  const uint32_t f1 = w & s1;   // >= C0
-  const uint32_t f2 = f1 & s2;  // >= E0
-  const uint32_t f3 = f2 & s3;  // >= F0
+  const uint32_t s1 = w << 1, s2 = w << 2;
+  const uint32_t h = u8v_mulhi(w, 0x80000000u) & 0x7F7F7F7Fu;  // w >> 1, lanes kept apart
+  const uint32_t f1 = u8v_mad(h, k.one, 0x20202020u);            // >= C0
+  const uint32_t f2 = u8v_mad(h, k.one, 0x10101010u);            // >= E0
+  const uint32_t f3 = u8v_mad(h, k.one, 0x08080808u);            // >= F0
   const uint32_t e1 = u8v_fsl(c->f1, f1, 8);
   const uint32_t e2 = u8v_fsl(c->f2, f2, 16);
   const uint32_t e3 = u8v_fsl(c->f3, f3, 24);

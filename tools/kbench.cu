@@ -159,7 +159,44 @@ __device__ __forceinline__ uint32_t word5(uint32_t w, uint32_t wn, Carry& c, con
   return S | R;
 }
 
-template <int V, int U>
+// V6: V4 with the lead flags from threshold adds on the FMA pipe:
+// g1/g2/g3 = bit 7 of ((w >> 1) & 0x7F..) + 0x20/0x10/0x08 (a >= C0/E0/F0).
+__device__ __forceinline__ uint32_t word6(uint32_t w, uint32_t wn, Carry& c, const Cfg& k) {
+  const uint32_t s1 = mad(w, k.one, w), s2 = w << 2;
+  const uint32_t hm = mulhi(w, 0x80000000u) & 0x7F7F7F7Fu;
+  const uint32_t g1 = mad(hm, k.one, 0x20202020u);
+  const uint32_t g2 = mad(hm, k.one, 0x10101010u);
+  const uint32_t g3 = mad(hm, k.one, 0x08080808u);
+  const uint32_t e1 = __funnelshift_l(c.f1, g1, 8);
+  const uint32_t e2 = __funnelshift_l(c.f2, g2, 16);
+  const uint32_t e3 = __funnelshift_l(c.f3, g3, 24);
+  const uint32_t S = (e1 | e2 | e3) ^ (w & ~s1);
+  const uint32_t t = __funnelshift_r(w, wn, 12);
+  const uint32_t zl = (s2 & 0x7C7C7C7Cu) | (t & 0x03030303u);
+  const uint32_t R = rare(s2, zl, g1, k);
+  c.f1 = g1; c.f2 = g2; c.f3 = g3;
+  return S | R;
+}
+
+// V7: V6 with s2 from IMAD and the key mask as one bitselect + clear.
+__device__ __forceinline__ uint32_t word7(uint32_t w, uint32_t wn, Carry& c, const Cfg& k) {
+  const uint32_t s1 = mad(w, k.one, w), s2 = mad(w, 4u * k.one, 0u);
+  const uint32_t hm = mulhi(w, 0x80000000u) & 0x7F7F7F7Fu;
+  const uint32_t g1 = mad(hm, k.one, 0x20202020u);
+  const uint32_t g2 = mad(hm, k.one, 0x10101010u);
+  const uint32_t g3 = mad(hm, k.one, 0x08080808u);
+  const uint32_t e1 = __funnelshift_l(c.f1, g1, 8);
+  const uint32_t e2 = __funnelshift_l(c.f2, g2, 16);
+  const uint32_t e3 = __funnelshift_l(c.f3, g3, 24);
+  const uint32_t S = (e1 | e2 | e3) ^ (w & ~s1);
+  const uint32_t t = mad(wn, 1u << 20, mulhi(w, 1u << 20));
+  const uint32_t zl = (s2 & 0x7C7C7C7Cu) | (t & 0x03030303u);
+  const uint32_t R = rare(s2, zl, g1, k);
+  c.f1 = g1; c.f2 = g2; c.f3 = g3;
+  return S | R;
+}
+
+template <int V, int U, int PF = 0>
 __device__ __forceinline__ void body(const uint8_t* base, int64_t steps, int64_t spw, uint32_t* flag,
                                      const Cfg& k) {
   const int lane = threadIdx.x & 31;
@@ -171,6 +208,10 @@ __device__ __forceinline__ void body(const uint8_t* base, int64_t steps, int64_t
   uint32_t acc = 0;
   for (; step < se; ++step) {
     const uint8_t* sp = base + step * (int64_t)(U * 1024);
+    if (PF > 0 && lane == 0 && step + PF < se)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(sp + PF * (int64_t)(U * 1024)),
+                   "r"(U * 1024)
+                   : "memory");
     uint32_t v[U][8];
 #pragma unroll
     for (int i = 0; i < U; ++i)
@@ -192,6 +233,14 @@ __device__ __forceinline__ void body(const uint8_t* base, int64_t steps, int64_t
         const uint32_t nextw = __shfl_down_sync(0xFFFFFFFFu, v[i][0], 1);
 #pragma unroll
         for (int j = 0; j < 8; ++j) e |= word5(v[i][j], j < 7 ? v[i][j + 1] : nextw, c, k);
+      } else if (V == 6) {
+        const uint32_t nextw = __shfl_down_sync(0xFFFFFFFFu, v[i][0], 1);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) e |= word6(v[i][j], j < 7 ? v[i][j + 1] : nextw, c, k);
+      } else if (V == 7) {
+        const uint32_t nextw = __shfl_down_sync(0xFFFFFFFFu, v[i][0], 1);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) e |= word7(v[i][j], j < 7 ? v[i][j + 1] : nextw, c, k);
       } else {
 #pragma unroll
         for (int j = 0; j < 8; ++j) e |= word<V>(v[i][j], c, k);
@@ -203,6 +252,69 @@ __device__ __forceinline__ void body(const uint8_t* base, int64_t steps, int64_t
   const unsigned any = __reduce_or_sync(0xFFFFFFFFu, acc & 0x80808080u);
   if (lane == 0 && any) atomicOr(flag, 1u);
 }
+
+// Register double buffering: step s+1's chunks are loaded before step s is
+// evaluated (V6 word formula).
+template <int U>
+__device__ __forceinline__ void load_step(uint32_t (&v)[U][8], const uint8_t* sp, int lane) {
+#pragma unroll
+  for (int i = 0; i < U; ++i)
+    asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(v[i][0]), "=r"(v[i][1]), "=r"(v[i][2]), "=r"(v[i][3]), "=r"(v[i][4]),
+                   "=r"(v[i][5]), "=r"(v[i][6]), "=r"(v[i][7])
+                 : "l"(sp + (lane + 32 * i) * 32));
+}
+
+template <int U>
+__device__ __forceinline__ uint32_t eval_step(const uint32_t (&v)[U][8], uint32_t& carry_word, int lane,
+                                              const Cfg& k) {
+  uint32_t acc = 0;
+#pragma unroll
+  for (int i = 0; i < U; ++i) {
+    const uint32_t supply = lane == 31 ? (i == 0 ? carry_word : v[i - 1][7]) : v[i][7];
+    const uint32_t prev = __shfl_sync(0xFFFFFFFFu, supply, (lane + 31) & 31);
+    Carry c = carry_of(prev);
+    const uint32_t nextw = __shfl_down_sync(0xFFFFFFFFu, v[i][0], 1);
+    uint32_t e = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) e |= word6(v[i][j], j < 7 ? v[i][j + 1] : nextw, c, k);
+    acc |= e;
+  }
+  if (lane == 31) carry_word = v[U - 1][7];
+  return acc;
+}
+
+template <int U>
+__device__ __forceinline__ void body_db(const uint8_t* base, int64_t steps, int64_t spw, uint32_t* flag,
+                                        const Cfg& k) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int64_t step = warp * spw;
+  const int64_t se = step + spw < steps ? step + spw : steps;
+  if (step >= se) return;
+  uint32_t carry_word = 0, acc = 0;
+  uint32_t a[U][8], b[U][8];
+  load_step<U>(a, base + step * (int64_t)(U * 1024), lane);
+  for (; step + 1 < se; step += 2) {
+    load_step<U>(b, base + (step + 1) * (int64_t)(U * 1024), lane);
+    acc |= eval_step<U>(a, carry_word, lane, k);
+    if (step + 2 < se) load_step<U>(a, base + (step + 2) * (int64_t)(U * 1024), lane);
+    acc |= eval_step<U>(b, carry_word, lane, k);
+  }
+  if (step < se) acc |= eval_step<U>(a, carry_word, lane, k);
+  const unsigned any = __reduce_or_sync(0xFFFFFFFFu, acc & 0x80808080u);
+  if (lane == 0 && any) atomicOr(flag, 1u);
+}
+
+#define KB_KERNEL_DB(U, MINB)                                                                   \
+  __global__ void __launch_bounds__(256, MINB)                                                 \
+      k_db_u##U##_b##MINB(const uint8_t* base, int64_t steps, int64_t spw, uint32_t* flag, Cfg k) { \
+    body_db<U>(base, steps, spw, flag, k);                                                     \
+  }
+KB_KERNEL_DB(2, 3)
+KB_KERNEL_DB(1, 4)
+KB_KERNEL_DB(2, 2)
+KB_KERNEL_DB(4, 2)
 
 #define KB_KERNEL(V, U, MINB)                                                                  \
   __global__ void __launch_bounds__(256, MINB)                                                 \
@@ -225,6 +337,21 @@ KB_KERNEL(4, 4, 3)
 KB_KERNEL(4, 2, 5)
 KB_KERNEL(5, 2, 4)
 KB_KERNEL(5, 4, 3)
+KB_KERNEL(6, 4, 3)
+KB_KERNEL(6, 2, 4)
+KB_KERNEL(7, 4, 3)
+#define KB_KERNEL_PF(V, U, MINB, PF)                                                            \
+  __global__ void __launch_bounds__(256, MINB)                                                 \
+      k_v##V##_u##U##_b##MINB##_p##PF(const uint8_t* base, int64_t steps, int64_t spw,          \
+                                      uint32_t* flag, Cfg k) {                                 \
+    body<V, U, PF>(base, steps, spw, flag, k);                                                 \
+  }
+KB_KERNEL_PF(6, 4, 3, 1)
+KB_KERNEL_PF(6, 4, 3, 2)
+KB_KERNEL_PF(6, 4, 3, 4)
+KB_KERNEL_PF(6, 2, 4, 2)
+KB_KERNEL_PF(6, 2, 4, 4)
+KB_KERNEL_PF(4, 4, 3, 2)
 
 typedef void (*KFn)(const uint8_t*, int64_t, int64_t, uint32_t*, Cfg);
 struct Entry {
@@ -238,6 +365,10 @@ static const Entry kEntries[] = {
     {"v2_u2_b4", k_v2_u2_b4, 2}, {"v2_u1_b6", k_v2_u1_b6, 1}, {"v3_u2_b4", k_v3_u2_b4, 2},
     {"v4_u2_b4", k_v4_u2_b4, 2}, {"v0_u4_b3", k_v0_u4_b3, 4}, {"v4_u4_b3", k_v4_u4_b3, 4},
     {"v4_u2_b5", k_v4_u2_b5, 2}, {"v5_u2_b4", k_v5_u2_b4, 2}, {"v5_u4_b3", k_v5_u4_b3, 4},
+    {"v6_u4_b3", k_v6_u4_b3, 4}, {"v6_u2_b4", k_v6_u2_b4, 2}, {"v7_u4_b3", k_v7_u4_b3, 4},
+    {"db_u2_b3", k_db_u2_b3, 2}, {"db_u1_b4", k_db_u1_b4, 1}, {"db_u2_b2", k_db_u2_b2, 2}, {"db_u4_b2", k_db_u4_b2, 4},
+    {"v6_u4_b3_p1", k_v6_u4_b3_p1, 4}, {"v6_u4_b3_p2", k_v6_u4_b3_p2, 4}, {"v6_u4_b3_p4", k_v6_u4_b3_p4, 4},
+    {"v6_u2_b4_p2", k_v6_u2_b4_p2, 2}, {"v6_u2_b4_p4", k_v6_u2_b4_p4, 2}, {"v4_u4_b3_p2", k_v4_u4_b3_p2, 4},
 };
 
 }  // namespace kb
