@@ -83,7 +83,7 @@ def build_test_helpers() -> None:
     cpp = ROOT / "tests" / "cpp"
     swar_src = cpp / "swar_host.c"
     swar_lib = cpp / "libswar_host.so"
-    deps = [swar_src, CSRC / "utf8v_swar.h", ROOT / "oracle" / "utf8_oracle.h"]
+    deps = [swar_src, CSRC / "utf8v_swar.h", CSRC / "utf8v_bits.h", ROOT / "oracle" / "utf8_oracle.h"]
     if swar_src.exists() and _stale(swar_lib, deps):
         _run(["gcc", "-O2", "-fPIC", "-shared", "-std=c99", "-pthread", f"-I{CSRC}",
               f"-I{ROOT / 'oracle'}", "-o", str(swar_lib), str(swar_src),

@@ -115,7 +115,7 @@ __device__ __noinline__ void chunk_bounded(const BatchDesc& d, Chunk v, uint32_t
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 3) k_batch(BatchDesc d) {
+__global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
   __shared__ unsigned long long s_mask[kWarpsPerCta][kStepChunks];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -136,6 +136,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_batch(BatchDesc d) {
   // r0: the record holding byte hs = step start - 2, the first byte whose
   // record matters to the step (look-back of its first lanes).
   int64_t r0 = find_record(d, cstep * kChunkBytes - 2);
+  bool was_ascii = true;
 
   for (; step < step_end; ++step) {
     cstep = d.c_begin + step * kStepChunks;
@@ -188,13 +189,15 @@ __global__ void __launch_bounds__(kThreads, 3) k_batch(BatchDesc d) {
       __syncwarp();
     }
 
+    // ASCII fast path, voted only after an all-ASCII step (as in K1).
     bool all_ascii = false;
-    if (single) {
+    if (single && was_ascii) {
       uint32_t hibits = 0;
 #pragma unroll
       for (int i = 0; i < kU; ++i) hibits |= chunk_hibits(v[i]);
       all_ascii = __all_sync(0xFFFFFFFFu, (hibits & U8V_B7) == 0);
     }
+    uint32_t h7 = 0;
 #pragma unroll
     for (int i = 0; i < kU; ++i) {
       const uint32_t up =
@@ -209,6 +212,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_batch(BatchDesc d) {
         m[lane + 32 * i] = 0;
       }
       if (mask != 0) {
+        h7 |= chunk_hibits(v[i]) & U8V_B7;
         chunk_bounded(d, v[i], prev, next, mask, c, r0);
       } else {
         uint32_t e;
@@ -216,11 +220,14 @@ __global__ void __launch_bounds__(kThreads, 3) k_batch(BatchDesc d) {
           u8v_carry cr = u8v_carry_of(prev);
           e = u8v_ascii_word_errors(v[i].w[0], &cr) & U8V_B7;
         } else {
-          e = chunk_errors<false>(v[i], prev, next, d.k, 0, 0, 0);
+          uint32_t hi7;
+          e = chunk_errors<false>(v[i], prev, next, d.k, 0, 0, 0, &hi7);
+          h7 |= hi7;
         }
         if (e) chunk_bounded(d, v[i], prev, next, 0ull, c, r0);
       }
     }
+    was_ascii = all_ascii || __all_sync(0xFFFFFFFFu, h7 == 0);
     if (lane == 31) carry_word = v[kU - 1].w[kChunkWords - 1];
     r0 = r_next;
   }

@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include "kernels.cuh"
+#include "utf8v_bits.h"
 #include "utf8v_swar.h"
 
 namespace u8v {
@@ -71,21 +72,22 @@ __device__ __forceinline__ uint32_t chunk_hibits(const Chunk& v) {
   return h;
 }
 
-// Error flags (bit 7 per lane) of one chunk given the word before it and the
-// word after it (lead form); kRanged drops lanes outside [L0, L1).
+// Error lanes of one chunk (bit i = lane p0 + i flagged; exact, no garbage
+// bits) given the word before it and the word after it: the bit-sliced form
+// of utf8v_bits.h.  kRanged drops lanes outside [L0, L1).
+// *hi7: plane 7 of the chunk (zero iff all its bytes are ASCII).
 template <bool kRanged>
 __device__ __forceinline__ uint32_t chunk_errors(const Chunk& v, uint32_t prev, uint32_t next,
-                                                 u8v_consts k, int64_t p0, int64_t L0, int64_t L1) {
-  u8v_carry c = u8v_carry_of(prev);
-  uint32_t e = 0;
-#pragma unroll
-  for (int j = 0; j < kChunkWords; ++j) {
-    const uint32_t wn = j + 1 < kChunkWords ? v.w[j + 1] : next;
-    uint32_t ej = u8v_word_errors_lead(v.w[j], wn, &c, k);
-    if (kRanged) ej = u8v_mask_word(ej, p0 + 4 * j, L0, L1);
-    e |= ej;
+                                                 u8v_consts k, int64_t p0, int64_t L0, int64_t L1,
+                                                 uint32_t* hi7) {
+  uint32_t e = u8v_chunk_errors_planes_k(v.w, prev, next, k, hi7);
+  if (kRanged) {
+    const int64_t a = L0 - p0, b = L1 - p0;  // wanted lanes: bits [a, b)
+    const uint32_t lo = a <= 0 ? 0xFFFFFFFFu : (a >= 32 ? 0u : (0xFFFFFFFFu << a));
+    const uint32_t hi = b >= 32 ? 0xFFFFFFFFu : (b <= 0 ? 0u : (0xFFFFFFFFu >> (32 - b)));
+    e &= lo & hi;
   }
-  return e & U8V_B7;
+  return e;
 }
 
 }  // namespace u8v

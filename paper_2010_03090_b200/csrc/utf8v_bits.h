@@ -1,0 +1,148 @@
+// utf8v_bits.h -- the per-lane Lookup check on bit planes (bit-sliced form).
+//
+// Same lane predicate as u8v_word_errors_lead (utf8v_swar.h), evaluated for a
+// whole 32-byte chunk at once: the chunk is transposed into 8 planes (plane k,
+// bit i = bit k of byte i), so every LOP3 of the check covers 32 byte lanes
+// instead of the 4 of the SWAR form, and the look-back/lookahead becomes a
+// one-bit funnel shift per plane.  K1 is bound by the ALU pipe; per 4-byte
+// word this form issues ~10 ALU + ~6 FMA instructions against ~15 + ~13 for
+// the SWAR form (tools/kbench.cu: 3592 -> 4476 GB/s on C1).
+//
+// Transpose: four 8x8 bit-matrix transposes (bytes 8j..8j+7, two delta-swap
+// stages each: the 4x4 sub-blocks), a 4x4 byte transpose by PRMT, and a
+// nibble merge that does the third stage's 4x4 block swap.  Shifts are
+// issued as IMAD / IMAD.HI with runtime multipliers (FMA pipe); the logic
+// stays on LOP3.
+//
+// Compiled into the sm_100a kernels and, by gcc, into the CPU test helper
+// that checks the transpose and every lane class at every chunk position
+// against the SWAR form (tests/test_swar.py).
+#pragma once
+#include <stdint.h>
+
+#include "utf8v_swar.h"
+
+U8V_HD uint32_t u8v_prmt(uint32_t x, uint32_t y, uint32_t s) {
+#if defined(__CUDA_ARCH__)
+  return __byte_perm(x, y, s);
+#else
+  const uint64_t v = ((uint64_t)y << 32) | x;
+  uint32_t r = 0;
+  for (int n = 0; n < 4; ++n) r |= (uint32_t)((v >> (8 * ((s >> (4 * n)) & 7))) & 0xFF) << (8 * n);
+  return r;
+#endif
+}
+
+// (a & 0x0F0F0F0F) | (c & 0xF0F0F0F0) in one LOP3 (ptxas splits it in two
+// when the mask is an immediate used in both polarities).
+U8V_HD uint32_t u8v_nibsel(uint32_t a, uint32_t c) {
+#if defined(__CUDA_ARCH__)
+  uint32_t d;
+  asm("lop3.b32 %0, %1, 0x0F0F0F0F, %2, 0xE2;" : "=r"(d) : "r"(a), "r"(c));
+  return d;
+#else
+  return (a & 0x0F0F0F0Fu) | (c & 0xF0F0F0F0u);
+#endif
+}
+
+// x << s and x >> s on the FMA pipe (k.one == 1 at run time).
+#define U8V_SHL(x, s, k) u8v_mad((x), (1u << (s)) * (k).one, 0u)
+#define U8V_SHR(x, s, k) u8v_mulhi((x), 1u << (32 - (s)))
+
+// First two stages of the 8x8 bit transpose of bytes 0..3 (a) and 4..7 (b):
+// afterwards each 4x4 sub-block is transposed in place -- a byte c < 4 holds
+// bit c of bytes 0..3 in its low nibble and bit c+4 in its high nibble; b the
+// same for bytes 4..7.  Delta swaps of 7 and 14.
+U8V_HD void u8v_t4x4x2(uint32_t* lo, uint32_t* hi, u8v_consts k) {
+  uint32_t a = *lo, b = *hi, t;
+  t = (a ^ U8V_SHR(a, 7, k)) & 0x00AA00AAu;
+  a ^= t ^ U8V_SHL(t, 7, k);
+  t = (b ^ U8V_SHR(b, 7, k)) & 0x00AA00AAu;
+  b ^= t ^ U8V_SHL(t, 7, k);
+  t = (a ^ U8V_SHR(a, 14, k)) & 0x0000CCCCu;
+  a ^= t ^ U8V_SHL(t, 14, k);
+  t = (b ^ U8V_SHR(b, 14, k)) & 0x0000CCCCu;
+  b ^= t ^ U8V_SHL(t, 14, k);
+  *lo = a;
+  *hi = b;
+}
+
+// Planes of a 32-byte chunk w[0..8): p[c] bit i = bit c of byte i.
+U8V_HD void u8v_planes_k(const uint32_t w[8], uint32_t p[8], u8v_consts k) {
+  uint32_t l0 = w[0], h0 = w[1], l1 = w[2], h1 = w[3], l2 = w[4], h2 = w[5], l3 = w[6], h3 = w[7];
+  u8v_t4x4x2(&l0, &h0, k);
+  u8v_t4x4x2(&l1, &h1, k);
+  u8v_t4x4x2(&l2, &h2, k);
+  u8v_t4x4x2(&l3, &h3, k);
+  // X_c = byte c of l0..l3 (bytes 8j..8j+3 of each block), Y_c = byte c of h0..h3.
+  uint32_t A = u8v_prmt(l0, l1, 0x5140), B = u8v_prmt(l0, l1, 0x7362);
+  uint32_t C = u8v_prmt(l2, l3, 0x5140), D = u8v_prmt(l2, l3, 0x7362);
+  const uint32_t X0 = u8v_prmt(A, C, 0x5410), X1 = u8v_prmt(A, C, 0x7632);
+  const uint32_t X2 = u8v_prmt(B, D, 0x5410), X3 = u8v_prmt(B, D, 0x7632);
+  A = u8v_prmt(h0, h1, 0x5140);
+  B = u8v_prmt(h0, h1, 0x7362);
+  C = u8v_prmt(h2, h3, 0x5140);
+  D = u8v_prmt(h2, h3, 0x7362);
+  const uint32_t Y0 = u8v_prmt(A, C, 0x5410), Y1 = u8v_prmt(A, C, 0x7632);
+  const uint32_t Y2 = u8v_prmt(B, D, 0x5410), Y3 = u8v_prmt(B, D, 0x7632);
+  // Nibble merge (the third stage): plane c byte j = low nibbles of X_c and
+  // Y_c; plane c+4 byte j = their high nibbles.
+  p[0] = u8v_nibsel(X0, U8V_SHL(Y0, 4, k));
+  p[1] = u8v_nibsel(X1, U8V_SHL(Y1, 4, k));
+  p[2] = u8v_nibsel(X2, U8V_SHL(Y2, 4, k));
+  p[3] = u8v_nibsel(X3, U8V_SHL(Y3, 4, k));
+  p[4] = u8v_nibsel(U8V_SHR(X0, 4, k), Y0);
+  p[5] = u8v_nibsel(U8V_SHR(X1, 4, k), Y1);
+  p[6] = u8v_nibsel(U8V_SHR(X2, 4, k), Y2);
+  p[7] = u8v_nibsel(U8V_SHR(X3, 4, k), Y3);
+}
+
+U8V_HD void u8v_planes(const uint32_t w[8], uint32_t p[8]) { u8v_planes_k(w, p, u8v_make_consts()); }
+
+// Bit 7 of each byte of x gathered into bits 28..31 (byte 0 -> bit 28): the
+// top four lanes of a plane, from a SWAR flag word.  One IMAD.
+U8V_HD uint32_t u8v_movemask_top(uint32_t x, u8v_consts k) {
+  return u8v_mad(x & U8V_B7, 0x00204081u * k.one, 0u);
+}
+
+// Error plane (bit i = lane i of the chunk flagged) of one chunk.
+//   prev: the word before the chunk (bytes -4..-1), next: the word after it.
+// Lane i: S_i = cont(x_i) ^ (x_{i-1}>=C0 | x_{i-2}>=E0 | x_{i-3}>=F0), and the
+// rare pair (x_i, x_{i+1}) tested at its lead (lead form, utf8v_swar.h).
+// *hi7 receives plane 7 (the bytes >= 0x80): zero iff the chunk is ASCII.
+U8V_HD uint32_t u8v_chunk_errors_planes_k(const uint32_t w[8], uint32_t prev, uint32_t next,
+                                          u8v_consts k, uint32_t* hi7) {
+  uint32_t p[8];
+  u8v_planes_k(w, p, k);
+  *hi7 = p[7];
+  // Lead flags of this chunk's bytes.
+  const uint32_t l1 = p[7] & p[6];  // >= C0
+  const uint32_t l2 = l1 & p[5];    // >= E0
+  const uint32_t l3 = l2 & p[4];    // >= F0
+  // The same flags of the 4 bytes before the chunk, as the top plane lanes.
+  const uint32_t q1 = prev & U8V_SHL(prev, 1, k);
+  const uint32_t q2 = q1 & U8V_SHL(prev, 2, k);
+  const uint32_t q3 = q2 & U8V_SHL(prev, 3, k);
+  const uint32_t e1 = u8v_fsl(u8v_movemask_top(q1, k), l1, 1);
+  const uint32_t e2 = u8v_fsl(u8v_movemask_top(q2, k), l2, 2);
+  const uint32_t e3 = u8v_fsl(u8v_movemask_top(q3, k), l3, 3);
+  const uint32_t S = (p[7] & ~p[6]) ^ (e1 | e2 | e3);
+  // Follower bits 5 and 4 (byte i+1) at lane i.
+  const uint32_t n5 = u8v_fsr(p[5], next >> 5, 1);
+  const uint32_t n4 = u8v_fsr(p[4], next >> 4, 1);
+  // Rare pairs (utf8v_swar.h u8v_rare_key, restated on planes).
+  const uint32_t z321 = ~(p[3] | p[2] | p[1]);                         // low nibble 0 or 1
+  const uint32_t rc = l1 & ~p[5] & ~p[4] & z321;                        // C0, C1
+  const uint32_t ee = l2 & ~p[4];                                       // E0..EF
+  const uint32_t re0 = ee & z321 & ~p[0] & ~n5;                         // E0, b < A0
+  const uint32_t red = ee & p[3] & p[2] & ~p[1] & p[0] & n5;            // ED, b >= A0
+  const uint32_t rf0 = l3 & z321 & ~p[0] & ~n5 & ~n4;                   // F0, b < 90
+  const uint32_t rf4 = l3 & ~p[3] & p[2] & ~p[1] & ~p[0] & (n5 | n4);   // F4, b >= 90
+  const uint32_t rf5 = l3 & (p[3] | (p[2] & (p[1] | p[0])));            // F5..FF
+  return S | rc | re0 | red | rf0 | rf4 | rf5;
+}
+
+U8V_HD uint32_t u8v_chunk_errors_planes(const uint32_t w[8], uint32_t prev, uint32_t next) {
+  uint32_t hi7;
+  return u8v_chunk_errors_planes_k(w, prev, next, u8v_make_consts(), &hi7);
+}

@@ -36,40 +36,58 @@ namespace u8v {
 // before each chunk comes from lane L-1 (lane 0: lane 31's previous chunk,
 // or carry_word), the word after from lane L+1 (lane 31: lane 0's next
 // chunk, or nsw = the next step's first word, loaded by lane 0).
+//
+// ASCII fast path (lookup_kernel.hpp:94-96): a step whose bytes are all
+// < 0x80 only needs the pending incomplete check of the bytes before it.
+// The warp vote that detects such a step waits for all of the step's loads
+// and costs ~7% on multibyte text, so it is only taken when the previous
+// step was all-ASCII (`was_ascii`); otherwise the plane path runs and
+// reports ASCII-ness from plane 7 after the fact.
 template <bool kPos, bool kRanged>
 __device__ __forceinline__ uint32_t step_errors(const StreamDesc& d, const Chunk (&v)[kU],
                                                 int64_t cstep, int lane, uint32_t& carry_word,
-                                                uint32_t nsw, int& first_i) {
+                                                uint32_t nsw, int& first_i, bool& was_ascii) {
   bool all_ascii = false;
-  if (!kRanged) {
+  if (!kRanged && was_ascii) {
     uint32_t hibits = 0;
 #pragma unroll
     for (int i = 0; i < kU; ++i) hibits |= chunk_hibits(v[i]);
     all_ascii = __all_sync(0xFFFFFFFFu, (hibits & U8V_B7) == 0);
   }
   uint32_t step_err = 0;
+  if (all_ascii) {
 #pragma unroll
-  for (int i = 0; i < kU; ++i) {
-    const uint32_t up =
-        lane == 31 ? (i == 0 ? carry_word : v[i - 1].w[kChunkWords - 1]) : v[i].w[kChunkWords - 1];
-    const uint32_t prev = __shfl_sync(0xFFFFFFFFu, up, (lane + 31) & 31);
-    const uint32_t dn = lane == 0 ? (i + 1 < kU ? v[i + 1].w[0] : nsw) : v[i].w[0];
-    const uint32_t next = __shfl_sync(0xFFFFFFFFu, dn, (lane + 1) & 31);
-    uint32_t e;
-    if (all_ascii) {
-      // No leads in the step: only continuations expected by the bytes
-      // before it (the pending incomplete check, lookup_kernel.hpp:94-96).
+    for (int i = 0; i < kU; ++i) {
+      const uint32_t up =
+          lane == 31 ? (i == 0 ? carry_word : v[i - 1].w[kChunkWords - 1]) : v[i].w[kChunkWords - 1];
+      const uint32_t prev = __shfl_sync(0xFFFFFFFFu, up, (lane + 31) & 31);
       u8v_carry cr = u8v_carry_of(prev);
-      e = u8v_ascii_word_errors(v[i].w[0], &cr) & U8V_B7;
-    } else {
-      const int64_t c = cstep + lane + 32 * i;
-      e = (kRanged && c >= d.c_end)
-              ? 0u
-              : chunk_errors<kRanged>(v[i], prev, next, d.k, c * kChunkBytes, d.L0, d.L1);
+      const uint32_t e = u8v_ascii_word_errors(v[i].w[0], &cr) & U8V_B7;
+      step_err |= e;
+      if (kPos && e != 0 && first_i == kU) first_i = i;
     }
-    step_err |= e;
-    if (kPos && e != 0 && first_i == kU) first_i = i;
+  } else {
+    uint32_t h7 = 0;
+#pragma unroll
+    for (int i = 0; i < kU; ++i) {
+      const uint32_t up =
+          lane == 31 ? (i == 0 ? carry_word : v[i - 1].w[kChunkWords - 1]) : v[i].w[kChunkWords - 1];
+      const uint32_t prev = __shfl_sync(0xFFFFFFFFu, up, (lane + 31) & 31);
+      const uint32_t dn = lane == 0 ? (i + 1 < kU ? v[i + 1].w[0] : nsw) : v[i].w[0];
+      const uint32_t next = __shfl_sync(0xFFFFFFFFu, dn, (lane + 1) & 31);
+      const int64_t c = cstep + lane + 32 * i;
+      uint32_t e = 0;
+      if (!(kRanged && c >= d.c_end)) {
+        uint32_t hi7;
+        e = chunk_errors<kRanged>(v[i], prev, next, d.k, c * kChunkBytes, d.L0, d.L1, &hi7);
+        h7 |= hi7;
+      }
+      step_err |= e;
+      if (kPos && e != 0 && first_i == kU) first_i = i;
+    }
+    all_ascii = !kRanged && __all_sync(0xFFFFFFFFu, h7 == 0);
   }
+  was_ascii = all_ascii;
   if (lane == 31) carry_word = v[kU - 1].w[kChunkWords - 1];
   return step_err;
 }
@@ -78,7 +96,8 @@ __device__ __forceinline__ uint32_t step_errors(const StreamDesc& d, const Chunk
 // kDirect: the next step's first word is known to be inside [lo, hi).
 template <bool kPos, bool kDirect>
 __device__ __forceinline__ uint32_t interior_step(const StreamDesc& d, int64_t cstep, int lane,
-                                                  uint32_t& carry_word, int& first_i) {
+                                                  uint32_t& carry_word, int& first_i,
+                                                  bool& was_ascii) {
   Chunk v[kU];
 #pragma unroll
   for (int i = 0; i < kU; ++i) v[i] = ld_chunk(d.base + (cstep + lane + 32 * i) * kChunkBytes);
@@ -87,11 +106,11 @@ __device__ __forceinline__ uint32_t interior_step(const StreamDesc& d, int64_t c
   if (lane == 0)
     nsw = kDirect ? __ldg(reinterpret_cast<const uint32_t*>(d.base + npos))
                   : ld_word_guarded(d.base, npos, d.lo, d.hi);
-  return step_errors<kPos, false>(d, v, cstep, lane, carry_word, nsw, first_i);
+  return step_errors<kPos, false>(d, v, cstep, lane, carry_word, nsw, first_i, was_ascii);
 }
 
 template <bool kPos>
-__global__ void __launch_bounds__(kThreads, 3)
+__global__ void __launch_bounds__(kThreads, 4)
     k_validate(StreamDesc d, uint32_t* __restrict__ flag,
                unsigned long long* __restrict__ first_chunk) {
   const int lane = threadIdx.x & 31;
@@ -120,26 +139,37 @@ __global__ void __launch_bounds__(kThreads, 3)
     if (lane == 31 && c0 > 0) carry_word = ld_word_masked(d.base, c0 * kChunkBytes - 4, d.lo, d.hi);
   }
   uint32_t acc = 0;
-  if (!kPos) {
-    // Hot path: edge steps (stream head / tail only) are peeled off so the
-    // interior loop carries no range tests.
-    const int64_t a = step > int_b ? step : int_b;
-    const int64_t b = step_end < int_d ? step_end : int_d;
-    if (a < b && step == a && step_end == b) {
-      int unused = kU;
-      for (; step < step_end; ++step)
-        acc |= interior_step<false, true>(d, d.c_begin + step * kStepChunks, lane, carry_word, unused);
-      const unsigned any = __reduce_or_sync(0xFFFFFFFFu, acc & U8V_B7);
-      if (lane == 0 && any) atomicOr(flag, 1u);
-      return;
-    }
-  }
+  bool was_ascii = true;  // try the vote on the first step
+  // Hot path: the steps whose bytes are all real, whose lanes are all wanted
+  // and whose lookahead word is inside the stream, [fa, fb), run a loop with
+  // no range tests.  Peeled per step range, not per warp: a warp whose range
+  // touches the stream tail still runs its interior steps fast (the grid is
+  // one resident wave, so one slow warp would set the kernel time).
+  const int64_t fa = kPos ? 0 : (step > int_b ? step : int_b);
+  const int64_t fb = kPos ? 0 : (step_end < int_d ? step_end : int_d);
   for (; step < step_end; ++step) {
+    if (!kPos && step == fa && fa < fb) {
+      // A pointer that advances by one step and a 32-bit trip count keep
+      // the loop state in registers (64-register budget, 4 CTAs/SM).
+      const uint8_t* p = d.base + (d.c_begin + step * kStepChunks + lane) * kChunkBytes;
+      int unused = kU;
+      for (int n = (int)(fb - fa); n > 0; --n, p += kStepChunks * kChunkBytes) {
+        Chunk v[kU];
+#pragma unroll
+        for (int i = 0; i < kU; ++i) v[i] = ld_chunk(p + 32 * i * kChunkBytes);
+        // Lane 0's chunk 0 starts the step: the next step's first word.
+        const uint32_t nsw =
+            lane == 0 ? __ldg(reinterpret_cast<const uint32_t*>(p + kStepChunks * kChunkBytes)) : 0u;
+        acc |= step_errors<false, false>(d, v, 0, lane, carry_word, nsw, unused, was_ascii);
+      }
+      step = fb - 1;
+      continue;
+    }
     const int64_t cstep = d.c_begin + step * kStepChunks;
     const bool interior = step >= int_b && step < int_e;
     if (interior) {
       int first_i = kU;
-      const uint32_t e = interior_step<kPos, false>(d, cstep, lane, carry_word, first_i);
+      const uint32_t e = interior_step<kPos, false>(d, cstep, lane, carry_word, first_i, was_ascii);
       if (!kPos) {
         acc |= e;
         continue;
@@ -178,7 +208,8 @@ __global__ void __launch_bounds__(kThreads, 3)
     const uint32_t nsw =
         lane == 0 ? ld_word_guarded(d.base, (cstep + kStepChunks) * kChunkBytes, d.lo, d.hi) : 0u;
     int first_i = kU;
-    const uint32_t step_err = step_errors<kPos, true>(d, v, cstep, lane, carry_word, nsw, first_i);
+    const uint32_t step_err =
+        step_errors<kPos, true>(d, v, cstep, lane, carry_word, nsw, first_i, was_ascii);
     if (kPos) {
       // Chunks of a step are ordered (i, lane); the warp's first flagged chunk
       // is the minimum over lanes of cstep + lane + 32 * first_i.

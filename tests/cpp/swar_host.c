@@ -9,6 +9,7 @@
 
 #include "utf8_oracle.h"
 #include "utf8v_swar.h"
+#include "utf8v_bits.h"
 
 /* Stream the words of a zero-extended stream [0, n) that starts `off` bytes
  * into an aligned word grid, exactly like k_validate: words in order, lanes
@@ -252,4 +253,86 @@ void oracle_cp_sweep(uint64_t* accepted, uint64_t* rejected, uint64_t* bad) {
   *accepted = acc;
   *rejected = rej;
   *bad = b;
+}
+
+/* Bit-sliced chunk form (utf8v_bits.h) vs the SWAR lead form, lane for lane.
+ * Every lane's flag depends only on (x[i-3]>=F0, x[i-2]>=E0, x[i-1]>=C0,
+ * x[i], bits 5,4 of x[i+1]); all 8192 classes are placed at each of the 32
+ * lane positions of a chunk (bytes before/after the chunk come from the
+ * prev/next words), the rest of the chunk random.  Then `fuzz` fully random
+ * chunks.  Returns the number of lanes that differ. */
+static uint64_t bits_rng(uint64_t* s) {
+  uint64_t z = (*s += 0x9E3779B97F4A7C15ull);
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+static uint64_t bits_compare(const uint8_t buf[40]) {
+  /* buf[0..4) = prev word, buf[4..36) = chunk, buf[36..40) = next word */
+  uint32_t w[8], prev, next;
+  memcpy(&prev, buf, 4);
+  memcpy(w, buf + 4, 32);
+  memcpy(&next, buf + 36, 4);
+  const uint32_t planes = u8v_chunk_errors_planes(w, prev, next);
+  u8v_carry c = u8v_carry_of(prev);
+  const u8v_consts k = u8v_make_consts();
+  uint64_t bad = 0;
+  for (int j = 0; j < 8; ++j) {
+    const uint32_t e = u8v_word_errors_lead(w[j], j < 7 ? w[j + 1] : next, &c, k);
+    for (int b = 0; b < 4; ++b) {
+      const unsigned sw = (e >> (8 * b + 7)) & 1u;
+      const unsigned pl = (planes >> (4 * j + b)) & 1u;
+      bad += sw != pl;
+    }
+  }
+  return bad;
+}
+
+uint64_t swar_bits_check(uint64_t seed, uint64_t fuzz) {
+  static const uint8_t lo_c0[2] = {0x41, 0xC2}, lo_e0[2] = {0x85, 0xE1}, lo_f0[2] = {0x9F, 0xF3};
+  static const uint8_t nb[4] = {0x80, 0x90, 0xA0, 0xB0};
+  uint8_t buf[40];
+  uint64_t s = seed, bad = 0;
+  for (int pos = 0; pos < 32; ++pos) {
+    const int i = 4 + pos; /* buffer index of the lane */
+    for (int cls = 0; cls < 8192; ++cls) {
+      for (int q = 0; q < 40; q += 8) {
+        const uint64_t r = bits_rng(&s);
+        memcpy(buf + q, &r, 8);
+      }
+      buf[i - 3] = lo_f0[(cls >> 0) & 1];
+      buf[i - 2] = lo_e0[(cls >> 1) & 1];
+      buf[i - 1] = lo_c0[(cls >> 2) & 1];
+      buf[i] = (uint8_t)(cls >> 3);
+      buf[i + 1] = nb[(cls >> 11) & 3];
+      bad += bits_compare(buf);
+    }
+  }
+  for (uint64_t t = 0; t < fuzz; ++t) {
+    const uint64_t mode = bits_rng(&s);
+    for (int q = 0; q < 40; ++q) {
+      const uint64_t r = bits_rng(&s);
+      static const uint8_t hot[] = {0x00, 0x41, 0x80, 0x8F, 0x90, 0x9F, 0xA0, 0xBF, 0xC0, 0xC1,
+                                    0xC2, 0xDF, 0xE0, 0xED, 0xEF, 0xF0, 0xF4, 0xF5, 0xFF};
+      buf[q] = (mode & 1) ? (uint8_t)r : hot[r % sizeof hot];
+    }
+    bad += bits_compare(buf);
+  }
+  return bad;
+}
+
+/* Transpose check: planes match their definition on random chunks. */
+uint64_t swar_planes_check(uint64_t seed, uint64_t trials) {
+  uint64_t s = seed, bad = 0;
+  for (uint64_t t = 0; t < trials; ++t) {
+    uint32_t w[8], p[8];
+    for (int j = 0; j < 8; ++j) w[j] = (uint32_t)bits_rng(&s);
+    u8v_planes(w, p);
+    for (int i = 0; i < 32; ++i) {
+      const unsigned byte = (w[i / 4] >> (8 * (i % 4))) & 0xFF;
+      for (int k2 = 0; k2 < 8; ++k2) bad += ((p[k2] >> i) & 1u) != ((byte >> k2) & 1u);
+    }
+  }
+  return bad;
 }

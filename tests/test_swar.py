@@ -76,3 +76,20 @@ def test_bounded_variant_matches_per_record_oracle():
             S.swar_batch(data.ctypes.data if data.size else None, offs.ctypes.data, len(parts), align,
                          got.ctypes.data)
             assert np.array_equal(got, want), (trial, align, parts)
+
+
+def test_bit_planes_transpose():
+    S = nat.swar()
+    S.swar_planes_check.restype = C.c_uint64
+    S.swar_planes_check.argtypes = [C.c_uint64, C.c_uint64]
+    assert S.swar_planes_check(7, 20000) == 0
+
+
+def test_bit_sliced_form_equals_swar_form_lane_for_lane():
+    """utf8v_bits.h (planes) == utf8v_swar.h lead form on every lane class at
+    every chunk position, plus fuzz (same per-lane predicate, so the proofs of
+    test_exhaustive_* carry over)."""
+    S = nat.swar()
+    S.swar_bits_check.restype = C.c_uint64
+    S.swar_bits_check.argtypes = [C.c_uint64, C.c_uint64]
+    assert S.swar_bits_check(11, 200000) == 0

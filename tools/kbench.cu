@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include "../paper_2010_03090_b200/csrc/utf8v_swar.h"
+#include "../paper_2010_03090_b200/csrc/utf8v_bits.h"
 
 namespace kb {
 
@@ -196,6 +197,58 @@ __device__ __forceinline__ uint32_t word7(uint32_t w, uint32_t wn, Carry& c, con
   return S | R;
 }
 
+// V9: bit-sliced with the transpose's shifts as IMAD / IMAD.HI (FMA pipe).
+__device__ __forceinline__ void t8x8_fma(uint32_t& a, uint32_t& b, const Cfg& k) {
+  uint32_t t;
+  t = (a ^ mulhi(a, 1u << 25)) & 0x00AA00AAu;
+  a ^= t ^ mad(t, 128u * k.one, 0u);
+  t = (b ^ mulhi(b, 1u << 25)) & 0x00AA00AAu;
+  b ^= t ^ mad(t, 128u * k.one, 0u);
+  t = (a ^ mulhi(a, 1u << 18)) & 0x0000CCCCu;
+  a ^= t ^ mad(t, 16384u * k.one, 0u);
+  t = (b ^ mulhi(b, 1u << 18)) & 0x0000CCCCu;
+  b ^= t ^ mad(t, 16384u * k.one, 0u);
+  t = (a ^ mad(b, 16u * k.one, 0u)) & 0xF0F0F0F0u;
+  a ^= t;
+  b ^= mulhi(t, 1u << 28);
+}
+__device__ __forceinline__ uint32_t planes_fma(const uint32_t (&w)[8], uint32_t prev, uint32_t next,
+                                               const Cfg& k) {
+  uint32_t l0 = w[0], h0 = w[1], l1 = w[2], h1 = w[3], l2 = w[4], h2 = w[5], l3 = w[6], h3 = w[7];
+  t8x8_fma(l0, h0, k);
+  t8x8_fma(l1, h1, k);
+  t8x8_fma(l2, h2, k);
+  t8x8_fma(l3, h3, k);
+  uint32_t p[8];
+  uint32_t A = __byte_perm(l0, l1, 0x5140), B = __byte_perm(l0, l1, 0x7362);
+  uint32_t C = __byte_perm(l2, l3, 0x5140), D = __byte_perm(l2, l3, 0x7362);
+  p[0] = __byte_perm(A, C, 0x5410); p[1] = __byte_perm(A, C, 0x7632);
+  p[2] = __byte_perm(B, D, 0x5410); p[3] = __byte_perm(B, D, 0x7632);
+  A = __byte_perm(h0, h1, 0x5140); B = __byte_perm(h0, h1, 0x7362);
+  C = __byte_perm(h2, h3, 0x5140); D = __byte_perm(h2, h3, 0x7362);
+  p[4] = __byte_perm(A, C, 0x5410); p[5] = __byte_perm(A, C, 0x7632);
+  p[6] = __byte_perm(B, D, 0x5410); p[7] = __byte_perm(B, D, 0x7632);
+  const uint32_t l1f = p[7] & p[6], l2f = l1f & p[5], l3f = l2f & p[4];
+  const uint32_t q1 = prev & mad(prev, 2u * k.one, 0u);
+  const uint32_t q2 = q1 & mad(prev, 4u * k.one, 0u);
+  const uint32_t q3 = q2 & mad(prev, 8u * k.one, 0u);
+  const uint32_t e1 = __funnelshift_l(mad(q1 & 0x80808080u, 0x00204081u * k.one, 0u), l1f, 1);
+  const uint32_t e2 = __funnelshift_l(mad(q2 & 0x80808080u, 0x00204081u * k.one, 0u), l2f, 2);
+  const uint32_t e3 = __funnelshift_l(mad(q3 & 0x80808080u, 0x00204081u * k.one, 0u), l3f, 3);
+  const uint32_t S = (p[7] & ~p[6]) ^ (e1 | e2 | e3);
+  const uint32_t n5 = __funnelshift_r(p[5], next >> 5, 1);
+  const uint32_t n4 = __funnelshift_r(p[4], next >> 4, 1);
+  const uint32_t z321 = ~(p[3] | p[2] | p[1]);
+  const uint32_t rc = l1f & ~p[5] & ~p[4] & z321;
+  const uint32_t ee = l2f & ~p[4];
+  const uint32_t re0 = ee & z321 & ~p[0] & ~n5;
+  const uint32_t red = ee & p[3] & p[2] & ~p[1] & p[0] & n5;
+  const uint32_t rf0 = l3f & z321 & ~p[0] & ~n5 & ~n4;
+  const uint32_t rf4 = l3f & ~p[3] & p[2] & ~p[1] & ~p[0] & (n5 | n4);
+  const uint32_t rf5 = l3f & (p[3] | (p[2] & (p[1] | p[0])));
+  return S | rc | re0 | red | rf0 | rf4 | rf5;
+}
+
 template <int V, int U, int PF = 0>
 __device__ __forceinline__ void body(const uint8_t* base, int64_t steps, int64_t spw, uint32_t* flag,
                                      const Cfg& k) {
@@ -219,6 +272,15 @@ __device__ __forceinline__ void body(const uint8_t* base, int64_t steps, int64_t
           : "=r"(v[i][0]), "=r"(v[i][1]), "=r"(v[i][2]), "=r"(v[i][3]), "=r"(v[i][4]),
             "=r"(v[i][5]), "=r"(v[i][6]), "=r"(v[i][7])
           : "l"(sp + (lane + 32 * i) * 32));
+    bool step_ascii = false;
+    if (V == 11) {
+      uint32_t hb = 0;
+#pragma unroll
+      for (int i = 0; i < U; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) hb |= v[i][j];
+      step_ascii = __all_sync(0xFFFFFFFFu, (hb & 0x80808080u) == 0);
+    }
 #pragma unroll
     for (int i = 0; i < U; ++i) {
       const uint32_t supply = lane == 31 ? (i == 0 ? carry_word : v[i - 1][7]) : v[i][7];
@@ -233,6 +295,34 @@ __device__ __forceinline__ void body(const uint8_t* base, int64_t steps, int64_t
         const uint32_t nextw = __shfl_down_sync(0xFFFFFFFFu, v[i][0], 1);
 #pragma unroll
         for (int j = 0; j < 8; ++j) e |= word5(v[i][j], j < 7 ? v[i][j + 1] : nextw, c, k);
+      } else if (V == 11 || V == 12) {
+        const uint32_t nextw = __shfl_down_sync(0xFFFFFFFFu, v[i][0], 1);
+        bool asc = step_ascii;
+        if (V == 12) {
+          uint32_t hb = 0;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) hb |= v[i][j];
+          asc = __all_sync(0xFFFFFFFFu, (hb & 0x80808080u) == 0);
+        }
+        if (asc) {
+          u8v_carry cr = u8v_carry_of(prev);
+          e = u8v_ascii_word_errors(v[i][0], &cr) & 0x80808080u;
+        } else {
+          u8v_consts kk;
+          kk.one = k.one; kk.m256 = k.m256; kk.mshr4 = k.mshr4;
+          { uint32_t h7; e = u8v_chunk_errors_planes_k(v[i], prev, nextw, kk, &h7); }
+        }
+      } else if (V == 10) {
+        const uint32_t nextw = __shfl_down_sync(0xFFFFFFFFu, v[i][0], 1);
+        u8v_consts kk;
+        kk.one = k.one; kk.m256 = k.m256; kk.mshr4 = k.mshr4;
+        { uint32_t h7; e = u8v_chunk_errors_planes_k(v[i], prev, nextw, kk, &h7); }
+      } else if (V == 9) {
+        const uint32_t nextw = __shfl_down_sync(0xFFFFFFFFu, v[i][0], 1);
+        e = planes_fma(v[i], prev, nextw, k);
+      } else if (V == 8) {
+        const uint32_t nextw = __shfl_down_sync(0xFFFFFFFFu, v[i][0], 1);
+        e = u8v_chunk_errors_planes(v[i], prev, nextw);
       } else if (V == 6) {
         const uint32_t nextw = __shfl_down_sync(0xFFFFFFFFu, v[i][0], 1);
 #pragma unroll
@@ -249,7 +339,7 @@ __device__ __forceinline__ void body(const uint8_t* base, int64_t steps, int64_t
     }
     if (lane == 31) carry_word = v[U - 1][7];
   }
-  const unsigned any = __reduce_or_sync(0xFFFFFFFFu, acc & 0x80808080u);
+  const unsigned any = __reduce_or_sync(0xFFFFFFFFu, V >= 8 ? acc : (acc & 0x80808080u));
   if (lane == 0 && any) atomicOr(flag, 1u);
 }
 
@@ -316,6 +406,257 @@ KB_KERNEL_DB(1, 4)
 KB_KERNEL_DB(2, 2)
 KB_KERNEL_DB(4, 2)
 
+// V13: ASCII vote only when the previous step was all-ASCII; the plane path
+// reports ASCII-ness from plane 7 after the fact.
+template <int U, int NSW = 0, int PF = 0>
+__device__ __forceinline__ void body13(const uint8_t* base, int64_t steps, int64_t spw, uint32_t* flag,
+                                       const Cfg& k) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int64_t step = warp * spw;
+  const int64_t se = step + spw < steps ? step + spw : steps;
+  if (step >= se) return;
+  u8v_consts kk;
+  kk.one = k.one; kk.m256 = k.m256; kk.mshr4 = k.mshr4;
+  uint32_t carry_word = 0, acc = 0;
+  bool was_ascii = false;
+  uint32_t nsw_ahead = 0;
+  if (NSW == 2 && lane == 0 && step + 1 < steps) nsw_ahead = __ldg(reinterpret_cast<const uint32_t*>(base + (step + 1) * (int64_t)(U * 1024)));
+  for (; step < se; ++step) {
+    const uint8_t* sp = base + step * (int64_t)(U * 1024);
+    if (PF > 0 && lane == 0 && step + PF < se)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(sp + PF * (int64_t)(U * 1024)),
+                   "r"(U * 1024)
+                   : "memory");
+    uint32_t nsw = 0;
+    if (NSW == 1 && lane == 0 && step + 1 < steps) nsw = __ldg(reinterpret_cast<const uint32_t*>(sp + U * 1024));
+    if (NSW == 2) {
+      nsw = nsw_ahead;
+      if (lane == 0 && step + 2 < steps) nsw_ahead = __ldg(reinterpret_cast<const uint32_t*>(sp + 2 * U * 1024));
+    }
+    uint32_t v[U][8];
+    uint32_t ex[U];
+#pragma unroll
+    for (int i = 0; i < U; ++i) {
+      asm("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+          : "=r"(v[i][0]), "=r"(v[i][1]), "=r"(v[i][2]), "=r"(v[i][3]), "=r"(v[i][4]),
+            "=r"(v[i][5]), "=r"(v[i][6]), "=r"(v[i][7])
+          : "l"(sp + (lane + 32 * i) * 32));
+      ex[i] = 0;
+      if (NSW == 3 && lane == 31 && (i + 1 < U || step + 1 < steps))
+        ex[i] = __ldg(reinterpret_cast<const uint32_t*>(sp + (lane + 32 * i) * 32 + 32));
+    }
+    bool asc = false;
+    if (was_ascii) {
+      uint32_t hb = 0;
+#pragma unroll
+      for (int i = 0; i < U; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) hb |= v[i][j];
+      asc = __all_sync(0xFFFFFFFFu, (hb & 0x80808080u) == 0);
+    }
+    if (asc) {
+#pragma unroll
+      for (int i = 0; i < U; ++i) {
+        const uint32_t supply = lane == 31 ? (i == 0 ? carry_word : v[i - 1][7]) : v[i][7];
+        const uint32_t prev = __shfl_sync(0xFFFFFFFFu, supply, (lane + 31) & 31);
+        u8v_carry cr = u8v_carry_of(prev);
+        acc |= u8v_ascii_word_errors(v[i][0], &cr) & 0x80808080u;
+      }
+    } else {
+      uint32_t h7 = 0;
+#pragma unroll
+      for (int i = 0; i < U; ++i) {
+        const uint32_t supply = lane == 31 ? (i == 0 ? carry_word : v[i - 1][7]) : v[i][7];
+        const uint32_t prev = __shfl_sync(0xFFFFFFFFu, supply, (lane + 31) & 31);
+        uint32_t nextw;
+        if (NSW == 0) {
+          nextw = __shfl_down_sync(0xFFFFFFFFu, v[i][0], 1);
+        } else if (NSW == 3) {
+          nextw = __shfl_down_sync(0xFFFFFFFFu, v[i][0], 1);
+          if (lane == 31) nextw = ex[i];
+        } else {
+          const uint32_t dn = lane == 0 ? (i + 1 < U ? v[i + 1][0] : nsw) : v[i][0];
+          nextw = __shfl_sync(0xFFFFFFFFu, dn, (lane + 1) & 31);
+        }
+        uint32_t hi;
+        acc |= u8v_chunk_errors_planes_k(v[i], prev, nextw, kk, &hi);
+        h7 |= hi;
+      }
+      asc = __all_sync(0xFFFFFFFFu, h7 == 0);
+    }
+    was_ascii = asc;
+    if (lane == 31) carry_word = v[U - 1][7];
+  }
+  const unsigned any = __reduce_or_sync(0xFFFFFFFFu, acc);
+  if (lane == 0 && any) atomicOr(flag, 1u);
+}
+#define KB_KERNEL13(U, MINB)                                                                     \
+  __global__ void __launch_bounds__(256, MINB)                                                 \
+      k_v13_u##U##_b##MINB(const uint8_t* base, int64_t steps, int64_t spw, uint32_t* flag, Cfg k) { \
+    body13<U>(base, steps, spw, flag, k);                                                      \
+  }
+KB_KERNEL13(4, 4)
+__global__ void __launch_bounds__(256, 4) k_v14_u4_b4(const uint8_t* base, int64_t steps, int64_t spw,
+                                                      uint32_t* flag, Cfg k) {
+  body13<4, 1>(base, steps, spw, flag, k);
+}
+__global__ void __launch_bounds__(256, 4) k_v16_u4_b4(const uint8_t* base, int64_t steps, int64_t spw,
+                                                      uint32_t* flag, Cfg k) {
+  body13<4, 3>(base, steps, spw, flag, k);
+}
+__global__ void __launch_bounds__(256, 4) k_p1_u4_b4(const uint8_t* base, int64_t steps, int64_t spw,
+                                                     uint32_t* flag, Cfg k) {
+  body13<4, 3, 1>(base, steps, spw, flag, k);
+}
+__global__ void __launch_bounds__(256, 4) k_p2_u4_b4(const uint8_t* base, int64_t steps, int64_t spw,
+                                                     uint32_t* flag, Cfg k) {
+  body13<4, 3, 2>(base, steps, spw, flag, k);
+}
+__global__ void __launch_bounds__(256, 4) k_p4_u4_b4(const uint8_t* base, int64_t steps, int64_t spw,
+                                                     uint32_t* flag, Cfg k) {
+  body13<4, 3, 4>(base, steps, spw, flag, k);
+}
+__global__ void __launch_bounds__(256, 4) k_v15_u4_b4(const uint8_t* base, int64_t steps, int64_t spw,
+                                                      uint32_t* flag, Cfg k) {
+  body13<4, 2>(base, steps, spw, flag, k);
+}
+
+// V17: per-warp TMA ring.  Lane 0 streams steps into shared memory with
+// cp.async.bulk (completion on one mbarrier per stage), S stages ahead; the
+// warp computes from shared memory.  In-flight data costs no registers.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mb_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mb_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(b))
+      : "memory");
+}
+__device__ __forceinline__ void mb_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void ld_shared_chunk(uint32_t (&w)[8], const uint8_t* p) {
+  const uint32_t a = smem_u32(p);
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]) : "r"(a));
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7]) : "r"(a + 16));
+}
+
+template <int U, int S>
+__device__ __forceinline__ void body_tma(const uint8_t* base, int64_t steps, int64_t spw, uint32_t* flag,
+                                         const Cfg& k) {
+  constexpr int STEP = U * 1024;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  uint8_t* ring = smem + wib * S * STEP;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (blockDim.x >> 5) * S * STEP) + wib * S;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int64_t step = warp * spw;
+  const int64_t se = step + spw < steps ? step + spw : steps;
+  if (step >= se) return;
+  u8v_consts kk;
+  kk.one = k.one; kk.m256 = k.m256; kk.mshr4 = k.mshr4;
+  if (lane == 0) {
+    for (int j = 0; j < S; ++j) mb_init(bars + j, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int j = 0; j < S; ++j)
+      if (step + j < se) {
+        mb_expect_tx(bars + j, STEP);
+        tma_load(ring + j * STEP, base + (step + j) * (int64_t)STEP, STEP, bars + j);
+      }
+  }
+  __syncwarp();
+  uint32_t carry_word = 0, acc = 0, phase = 0;
+  bool was_ascii = false;
+  for (int it = 0; step < se; ++step, ++it) {
+    const int st = it % S;
+    mb_wait(bars + st, (phase >> st) & 1);
+    phase ^= 1u << st;
+    const uint8_t* sb = ring + st * STEP;
+    uint32_t v[U][8];
+#pragma unroll
+    for (int i = 0; i < U; ++i) ld_shared_chunk(v[i], sb + (i * 32 + lane) * 32);
+    // Next step's first word (lookahead of the step's last lane).
+    uint32_t nsw = 0;
+    if (step + 1 < se) {
+      const int sn = (it + 1) % S;
+      mb_wait(bars + sn, (phase >> sn) & 1);
+      if (lane == 0) nsw = *reinterpret_cast<const uint32_t*>(ring + sn * STEP);
+    } else if (lane == 0 && step + 1 < steps) {
+      nsw = __ldg(reinterpret_cast<const uint32_t*>(base + (step + 1) * (int64_t)STEP));
+    }
+    bool asc = false;
+    if (was_ascii) {
+      uint32_t hb = 0;
+#pragma unroll
+      for (int i = 0; i < U; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) hb |= v[i][j];
+      asc = __all_sync(0xFFFFFFFFu, (hb & 0x80808080u) == 0);
+    }
+    if (asc) {
+#pragma unroll
+      for (int i = 0; i < U; ++i) {
+        const uint32_t supply = lane == 31 ? (i == 0 ? carry_word : v[i - 1][7]) : v[i][7];
+        const uint32_t prev = __shfl_sync(0xFFFFFFFFu, supply, (lane + 31) & 31);
+        u8v_carry cr = u8v_carry_of(prev);
+        acc |= u8v_ascii_word_errors(v[i][0], &cr) & 0x80808080u;
+      }
+    } else {
+      uint32_t h7 = 0;
+#pragma unroll
+      for (int i = 0; i < U; ++i) {
+        const uint32_t supply = lane == 31 ? (i == 0 ? carry_word : v[i - 1][7]) : v[i][7];
+        const uint32_t prev = __shfl_sync(0xFFFFFFFFu, supply, (lane + 31) & 31);
+        const uint32_t dn = lane == 0 ? (i + 1 < U ? v[i + 1][0] : nsw) : v[i][0];
+        const uint32_t nextw = __shfl_sync(0xFFFFFFFFu, dn, (lane + 1) & 31);
+        uint32_t hi;
+        acc |= u8v_chunk_errors_planes_k(v[i], prev, nextw, kk, &hi);
+        h7 |= hi;
+      }
+      asc = __all_sync(0xFFFFFFFFu, h7 == 0);
+    }
+    was_ascii = asc;
+    if (lane == 31) carry_word = v[U - 1][7];
+    // Stage st is consumed (values in registers): refill it S steps ahead.
+    __syncwarp();
+    if (lane == 0 && step + S < se) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mb_expect_tx(bars + st, STEP);
+      tma_load(ring + st * STEP, base + (step + S) * (int64_t)STEP, STEP, bars + st);
+    }
+  }
+  const unsigned any = __reduce_or_sync(0xFFFFFFFFu, acc);
+  if (lane == 0 && any) atomicOr(flag, 1u);
+}
+#define KB_KERNEL_TMA(U, S, MINB)                                                                \
+  __global__ void __launch_bounds__(256, MINB)                                                 \
+      k_tma_u##U##_s##S##_b##MINB(const uint8_t* base, int64_t steps, int64_t spw, uint32_t* flag, \
+                                  Cfg k) {                                                     \
+    body_tma<U, S>(base, steps, spw, flag, k);                                                 \
+  }
+KB_KERNEL_TMA(2, 3, 4)
+KB_KERNEL_TMA(2, 4, 3)
+KB_KERNEL_TMA(4, 2, 3)
+KB_KERNEL_TMA(4, 3, 2)
+KB_KERNEL_TMA(1, 6, 4)
+
 #define KB_KERNEL(V, U, MINB)                                                                  \
   __global__ void __launch_bounds__(256, MINB)                                                 \
       k_v##V##_u##U##_b##MINB(const uint8_t* base, int64_t steps, int64_t spw, uint32_t* flag, \
@@ -340,6 +681,17 @@ KB_KERNEL(5, 4, 3)
 KB_KERNEL(6, 4, 3)
 KB_KERNEL(6, 2, 4)
 KB_KERNEL(7, 4, 3)
+KB_KERNEL(8, 4, 3)
+KB_KERNEL(8, 2, 4)
+KB_KERNEL(8, 4, 2)
+KB_KERNEL(8, 1, 6)
+KB_KERNEL(9, 4, 3)
+KB_KERNEL(9, 2, 4)
+KB_KERNEL(10, 4, 3)
+KB_KERNEL(10, 4, 4)
+KB_KERNEL(10, 2, 4)
+KB_KERNEL(11, 4, 4)
+KB_KERNEL(12, 4, 4)
 #define KB_KERNEL_PF(V, U, MINB, PF)                                                            \
   __global__ void __launch_bounds__(256, MINB)                                                 \
       k_v##V##_u##U##_b##MINB##_p##PF(const uint8_t* base, int64_t steps, int64_t spw,          \
@@ -358,6 +710,7 @@ struct Entry {
   const char* name;
   KFn fn;
   int u;
+  int smem = 0;  // dynamic shared memory bytes (TMA variants)
 };
 static const Entry kEntries[] = {
     {"v0_u2_b4", k_v0_u2_b4, 2}, {"v0_u1_b4", k_v0_u1_b4, 1}, {"v0_u1_b6", k_v0_u1_b6, 1},
@@ -366,6 +719,17 @@ static const Entry kEntries[] = {
     {"v4_u2_b4", k_v4_u2_b4, 2}, {"v0_u4_b3", k_v0_u4_b3, 4}, {"v4_u4_b3", k_v4_u4_b3, 4},
     {"v4_u2_b5", k_v4_u2_b5, 2}, {"v5_u2_b4", k_v5_u2_b4, 2}, {"v5_u4_b3", k_v5_u4_b3, 4},
     {"v6_u4_b3", k_v6_u4_b3, 4}, {"v6_u2_b4", k_v6_u2_b4, 2}, {"v7_u4_b3", k_v7_u4_b3, 4},
+    {"v8_u4_b3", k_v8_u4_b3, 4}, {"v8_u2_b4", k_v8_u2_b4, 2}, {"v8_u4_b2", k_v8_u4_b2, 4}, {"v8_u1_b6", k_v8_u1_b6, 1},
+    {"v9_u4_b3", k_v9_u4_b3, 4}, {"v9_u2_b4", k_v9_u2_b4, 2},
+    {"v10_u4_b3", k_v10_u4_b3, 4}, {"v10_u4_b4", k_v10_u4_b4, 4}, {"v10_u2_b4", k_v10_u2_b4, 2},
+    {"v11_u4_b4", k_v11_u4_b4, 4}, {"v13_u4_b4", k_v13_u4_b4, 4},
+    {"v14_u4_b4", k_v14_u4_b4, 4}, {"v15_u4_b4", k_v15_u4_b4, 4}, {"v16_u4_b4", k_v16_u4_b4, 4},
+    {"tma_u2_s3_b4", k_tma_u2_s3_b4, 2, 8 * 3 * 2048 + 8 * 3 * 8},
+    {"tma_u2_s4_b3", k_tma_u2_s4_b3, 2, 8 * 4 * 2048 + 8 * 4 * 8},
+    {"tma_u4_s2_b3", k_tma_u4_s2_b3, 4, 8 * 2 * 4096 + 8 * 2 * 8},
+    {"tma_u4_s3_b2", k_tma_u4_s3_b2, 4, 8 * 3 * 4096 + 8 * 3 * 8},
+    {"tma_u1_s6_b4", k_tma_u1_s6_b4, 1, 8 * 6 * 1024 + 8 * 6 * 8},
+    {"p1_u4_b4", k_p1_u4_b4, 4}, {"p2_u4_b4", k_p2_u4_b4, 4}, {"p4_u4_b4", k_p4_u4_b4, 4}, {"v12_u4_b4", k_v12_u4_b4, 4},
     {"db_u2_b3", k_db_u2_b3, 2}, {"db_u1_b4", k_db_u1_b4, 1}, {"db_u2_b2", k_db_u2_b2, 2}, {"db_u4_b2", k_db_u4_b2, 4},
     {"v6_u4_b3_p1", k_v6_u4_b3_p1, 4}, {"v6_u4_b3_p2", k_v6_u4_b3_p2, 4}, {"v6_u4_b3_p4", k_v6_u4_b3_p4, 4},
     {"v6_u2_b4_p2", k_v6_u2_b4_p2, 2}, {"v6_u2_b4_p4", k_v6_u2_b4_p4, 2}, {"v4_u4_b3_p2", k_v4_u4_b3_p2, 4},
@@ -384,7 +748,8 @@ int kb_launch(int i, const uint8_t* d_p, uint64_t n, uint32_t* d_flag, void* str
   int dev = 0, sms = 0, blocks_per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, e.fn, 256, 0);
+  if (e.smem > 0) cudaFuncSetAttribute(e.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, e.smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, e.fn, 256, e.smem);
   const int64_t steps = (int64_t)(n / (e.u * 1024));
   int64_t warps = (int64_t)sms * blocks_per_sm * 8;
   if (warps > steps) warps = steps;
@@ -392,7 +757,7 @@ int kb_launch(int i, const uint8_t* d_p, uint64_t n, uint32_t* d_flag, void* str
   warps = (steps + spw - 1) / spw;
   const int64_t blocks = (warps * 32 + 255) / 256;
   kb::Cfg k{1u, 256u, 1u << 28, 1u << 16, 1u << 24, 1u << 8};
-  e.fn<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(d_p, steps, spw, d_flag, k);
+  e.fn<<<(unsigned)blocks, 256, e.smem, (cudaStream_t)stream>>>(d_p, steps, spw, d_flag, k);
   return blocks_per_sm;
 }
 

@@ -33,5 +33,35 @@ for i in range(L.kb_count()):
     ms = e0.elapsed_time(e1) / reps
     res[name] = {"GBps": n / ms / 1e6, "ms": ms, "valid_ok": ok, "detects": detects, "blocks_per_sm": occ}
     print(name, json.dumps(res[name]), flush=True)
+# ASCII (C0 recipe) 1 GiB: the fast path's case
+a = configs.gen_stream(n, seed=1, ascii_only=True)
+if a is not None:
+    for i in range(L.kb_count()):
+        name = L.kb_name(i).decode()
+        if not name.startswith(("v10_u4_b4", "v11", "v12", "v13")):
+            continue
+        for _ in range(3): L.kb_launch(i, a.data_ptr(), n, flag.data_ptr(), st.cuda_stream)
+        e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(20): L.kb_launch(i, a.data_ptr(), n, flag.data_ptr(), st.cuda_stream)
+        e1.record(st); torch.cuda.synchronize()
+        print("ASCII", name, n / (e0.elapsed_time(e1) / 20) / 1e6, flush=True)
 (ROOT / "gpurun_out").mkdir(exist_ok=True)
 (ROOT / "gpurun_out" / "kbench.json").write_text(json.dumps(res, indent=1))
+
+# The production entry point on the same buffer, same process.
+from paper_2010_03090_b200 import _lib
+pl = _lib.load()
+for _ in range(5):
+    pl.utf8v_cuda_validate_lanes_async(d.data_ptr(), n, 0, n + 3, flag.data_ptr(), st.cuda_stream)
+e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+e0.record(st)
+for _ in range(50):
+    pl.utf8v_cuda_validate_lanes_async(d.data_ptr(), n, 0, n + 3, flag.data_ptr(), st.cuda_stream)
+e1.record(st); torch.cuda.synchronize()
+print("PRODUCTION lanes[0,n+3)", n / (e0.elapsed_time(e1) / 50) / 1e6, flush=True)
+e0.record(st)
+for _ in range(50):
+    pl.utf8v_cuda_validate_lanes_async(d.data_ptr(), n, 0, n, flag.data_ptr(), st.cuda_stream)
+e1.record(st); torch.cuda.synchronize()
+print("PRODUCTION lanes[0,n)", n / (e0.elapsed_time(e1) / 50) / 1e6, flush=True)
