@@ -657,6 +657,108 @@ KB_KERNEL_TMA(4, 2, 3)
 KB_KERNEL_TMA(4, 3, 2)
 KB_KERNEL_TMA(1, 6, 4)
 
+// V18: rolling reload.  Each chunk slot is refilled with the next step's
+// chunk right after it is consumed, so every load overlaps ~3/4 of a step of
+// compute, with no extra registers.
+__device__ __forceinline__ void ldg_chunk(uint32_t (&w)[8], const uint8_t* p) {
+  asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]),
+                 "=r"(w[7])
+               : "l"(p));
+}
+template <int U>
+__device__ __forceinline__ void body18(const uint8_t* base, int64_t steps, int64_t spw, uint32_t* flag,
+                                       const Cfg& k) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int64_t step = warp * spw;
+  const int64_t se = step + spw < steps ? step + spw : steps;
+  if (step >= se) return;
+  u8v_consts kk;
+  kk.one = k.one; kk.m256 = k.m256; kk.mshr4 = k.mshr4;
+  uint32_t v[U][8];
+  const uint8_t* p = base + step * (int64_t)(U * 1024) + lane * 32;
+#pragma unroll
+  for (int i = 0; i < U; ++i) ldg_chunk(v[i], p + i * 1024);
+  uint32_t carry_word = 0, acc = 0;
+  for (; step < se; ++step, p += U * 1024) {
+    const bool more = step + 1 < se;
+    uint32_t h7 = 0;
+#pragma unroll
+    for (int i = 0; i < U; ++i) {
+      const uint32_t supply = lane == 31 ? carry_word : v[i][7];
+      const uint32_t prev = __shfl_sync(0xFFFFFFFFu, supply, (lane + 31) & 31);
+      // Lane 0's next chunk (slot i+1 of this step, or slot 0 already holding
+      // the next step's first chunk).
+      const uint32_t dn = lane == 0 ? (i + 1 < U ? v[i + 1][0] : v[0][0]) : v[i][0];
+      const uint32_t nextw = __shfl_sync(0xFFFFFFFFu, dn, (lane + 1) & 31);
+      uint32_t hi;
+      acc |= u8v_chunk_errors_planes_k(v[i], prev, nextw, kk, &hi);
+      h7 |= hi;
+      carry_word = v[i][7];  // lane 31's value feeds lane 0 of the next chunk
+      if (more) ldg_chunk(v[i], p + U * 1024 + i * 1024);
+    }
+    (void)h7;
+  }
+  const unsigned any = __reduce_or_sync(0xFFFFFFFFu, acc);
+  if (lane == 0 && any) atomicOr(flag, 1u);
+}
+__global__ void __launch_bounds__(256, 4) k_v18_u4_b4(const uint8_t* base, int64_t steps, int64_t spw,
+                                                      uint32_t* flag, Cfg k) {
+  body18<4>(base, steps, spw, flag, k);
+}
+__global__ void __launch_bounds__(256, 3) k_v18_u4_b3(const uint8_t* base, int64_t steps, int64_t spw,
+                                                      uint32_t* flag, Cfg k) {
+  body18<4>(base, steps, spw, flag, k);
+}
+__global__ void __launch_bounds__(256, 4) k_v18_u2_b4(const uint8_t* base, int64_t steps, int64_t spw,
+                                                      uint32_t* flag, Cfg k) {
+  body18<2>(base, steps, spw, flag, k);
+}
+
+// V19: grid-stride step assignment (all warps sweep one moving window of
+// memory, for DRAM page locality); the halo word and the lookahead word are
+// loaded per step (their neighbours belong to other warps).
+template <int U>
+__device__ __forceinline__ void body19(const uint8_t* base, int64_t steps, uint32_t* flag, const Cfg& k) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  u8v_consts kk;
+  kk.one = k.one; kk.m256 = k.m256; kk.mshr4 = k.mshr4;
+  uint32_t acc = 0;
+  for (int64_t step = warp; step < steps; step += nwarps) {
+    const uint8_t* sp = base + step * (int64_t)(U * 1024);
+    uint32_t v[U][8];
+#pragma unroll
+    for (int i = 0; i < U; ++i) ldg_chunk(v[i], sp + (lane + 32 * i) * 32);
+    uint32_t carry_word = 0, nsw = 0;
+    if (lane == 31 && step > 0) carry_word = __ldg(reinterpret_cast<const uint32_t*>(sp - 4));
+    if (lane == 0 && step + 1 < steps) nsw = __ldg(reinterpret_cast<const uint32_t*>(sp + U * 1024));
+#pragma unroll
+    for (int i = 0; i < U; ++i) {
+      const uint32_t supply = lane == 31 ? (i == 0 ? carry_word : v[i - 1][7]) : v[i][7];
+      const uint32_t prev = __shfl_sync(0xFFFFFFFFu, supply, (lane + 31) & 31);
+      const uint32_t dn = lane == 0 ? (i + 1 < U ? v[i + 1][0] : nsw) : v[i][0];
+      const uint32_t nextw = __shfl_sync(0xFFFFFFFFu, dn, (lane + 1) & 31);
+      uint32_t hi;
+      acc |= u8v_chunk_errors_planes_k(v[i], prev, nextw, kk, &hi);
+    }
+  }
+  const unsigned any = __reduce_or_sync(0xFFFFFFFFu, acc);
+  if (lane == 0 && any) atomicOr(flag, 1u);
+}
+__global__ void __launch_bounds__(256, 4) k_v19_u4_b4(const uint8_t* base, int64_t steps, int64_t spw,
+                                                      uint32_t* flag, Cfg k) {
+  (void)spw;
+  body19<4>(base, steps, flag, k);
+}
+__global__ void __launch_bounds__(256, 4) k_v19_u2_b4(const uint8_t* base, int64_t steps, int64_t spw,
+                                                      uint32_t* flag, Cfg k) {
+  (void)spw;
+  body19<2>(base, steps, flag, k);
+}
+
 #define KB_KERNEL(V, U, MINB)                                                                  \
   __global__ void __launch_bounds__(256, MINB)                                                 \
       k_v##V##_u##U##_b##MINB(const uint8_t* base, int64_t steps, int64_t spw, uint32_t* flag, \
@@ -724,6 +826,8 @@ static const Entry kEntries[] = {
     {"v10_u4_b3", k_v10_u4_b3, 4}, {"v10_u4_b4", k_v10_u4_b4, 4}, {"v10_u2_b4", k_v10_u2_b4, 2},
     {"v11_u4_b4", k_v11_u4_b4, 4}, {"v13_u4_b4", k_v13_u4_b4, 4},
     {"v14_u4_b4", k_v14_u4_b4, 4}, {"v15_u4_b4", k_v15_u4_b4, 4}, {"v16_u4_b4", k_v16_u4_b4, 4},
+    {"v19_u4_b4", k_v19_u4_b4, 4}, {"v19_u2_b4", k_v19_u2_b4, 2},
+    {"v18_u4_b4", k_v18_u4_b4, 4}, {"v18_u4_b3", k_v18_u4_b3, 4}, {"v18_u2_b4", k_v18_u2_b4, 2},
     {"tma_u2_s3_b4", k_tma_u2_s3_b4, 2, 8 * 3 * 2048 + 8 * 3 * 8},
     {"tma_u2_s4_b3", k_tma_u2_s4_b3, 2, 8 * 4 * 2048 + 8 * 4 * 8},
     {"tma_u4_s2_b3", k_tma_u4_s2_b3, 4, 8 * 2 * 4096 + 8 * 2 * 8},
