@@ -106,6 +106,11 @@ int utf8v_cuda_validate_lanes(const uint8_t* p, uint64_t n, uint64_t lane_lo, ui
                               int is_device, uint32_t* out_flag);
 
 /* Batch on device memory; d_verdicts is written fully (1/0 per record).
+ * Fully asynchronous (no host round trip): the kernel reads d_offsets[0] and
+ * d_offsets[n_records] itself.  Offsets must be non-decreasing with
+ * d_offsets[n_records] <= n; malformed device offsets give unspecified
+ * verdicts but never an access outside d_data[0..n) (the synchronous host
+ * entry point, utf8v_cuda_validate_batch with is_device = 0, checks them).
  * d_scratch: NULL or >= utf8v_cuda_batch_scratch_bytes(n) device bytes. */
 int utf8v_cuda_validate_batch_async(const uint8_t* d_data, uint64_t n, const uint64_t* d_offsets,
                                     uint64_t n_records, uint8_t* d_verdicts, void* d_scratch,

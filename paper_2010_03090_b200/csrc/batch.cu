@@ -43,6 +43,7 @@ struct BatchDesc {
   int64_t c_begin, c_end;
   int64_t steps, steps_per_warp;
   int64_t n_records;
+  int64_t n_bytes;  // data size (clamp for malformed offsets)
   u8v_consts k;  // runtime multipliers (FMA-pipe routing, utf8v_swar.h)
 };
 
@@ -90,28 +91,21 @@ __device__ __forceinline__ void mark_invalid(const BatchDesc& d, int64_t r_from,
   if (r < d.n_records) d.verdicts[r] = 0;
 }
 
-// Out-of-line: the chunk evaluated with record bounds, and the records of
-// its flagged lanes (and of the records ending at flagged starts) marked
-// invalid.  mask bit j <-> a record starts at byte 32c - 4 + j, j < 36.
-// Runs for chunks holding a record start, and to attribute errors found by
-// the inline path (mask 0: the same flags as chunk_errors).
-__device__ __noinline__ void chunk_bounded(const BatchDesc& d, Chunk v, uint32_t prev,
-                                           uint32_t next, unsigned long long mask, int64_t c,
-                                           int64_t r_from) {
-  u8v_carry cr = u8v_carry_of(prev);
-#pragma unroll
-  for (int j = 0; j < kChunkWords; ++j) {
-    const uint32_t wn = j + 1 < kChunkWords ? v.w[j + 1] : next;
-    const uint32_t bm = u8v_spread4((uint32_t)(mask >> (4 + 4 * j)));
-    const uint32_t pbm = u8v_spread4((uint32_t)(mask >> (4 * j)));
-    uint32_t end_err;
-    const uint32_t e = u8v_word_errors_bounded_lead(v.w[j], wn, &cr, bm, pbm, &end_err, d.k);
-    if ((e | end_err) == 0) continue;
-    const int64_t q0 = c * kChunkBytes + 4 * j;
-    for (int b = 0; b < 4; ++b) {
-      if ((e >> (8 * b + 7)) & 1) mark_invalid(d, r_from, q0 + b);
-      if ((end_err >> (8 * b + 7)) & 1) mark_invalid(d, r_from, q0 + b - 1);
-    }
+// Out-of-line, only for chunks with a flagged lane: the record of every
+// flagged lane, and the record ending at every flagged record start (its end
+// check), is marked invalid.  err / end: lane bits of chunk c.
+__device__ __noinline__ void attribute_chunk(const BatchDesc& d, int64_t c, uint32_t err,
+                                             uint32_t end, int64_t r_from) {
+  const int64_t q0 = c * kChunkBytes;
+  while (err) {
+    const int i = __ffs(err) - 1;
+    err &= err - 1;
+    mark_invalid(d, r_from, q0 + i);
+  }
+  while (end) {
+    const int i = __ffs(end) - 1;
+    end &= end - 1;
+    mark_invalid(d, r_from, q0 + i - 1);
   }
 }
 
@@ -120,6 +114,21 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int64_t warp = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * kThreads) >> 5;
+  // The byte range comes from the offsets themselves (read here, so the
+  // launch needs no host round trip).  Malformed offsets are clamped to the
+  // data: the kernel never reads outside [0, n).
+  d.lo = d.off32 + (int64_t)__ldg(d.offsets);
+  d.hi = d.off32 + (int64_t)__ldg(d.offsets + d.n_records);
+  if (d.hi > d.off32 + d.n_bytes) d.hi = d.off32 + d.n_bytes;
+  if (d.lo > d.hi) d.lo = d.hi;
+  if (d.hi <= d.lo) return;  // every record empty: all valid
+  // Lanes [lo, hi]: lane hi carries the last record's end check; lanes past
+  // it read zeros behind a record start and cannot flag.
+  d.c_begin = d.lo / kChunkBytes;
+  d.c_end = d.hi / kChunkBytes + 1;
+  d.steps = (d.c_end - d.c_begin + kStepChunks - 1) / kStepChunks;
+  d.steps_per_warp = (d.steps + nwarps - 1) / nwarps;
   int64_t step = warp * d.steps_per_warp;
   int64_t step_end = step + d.steps_per_warp;
   if (step_end > d.steps) step_end = d.steps;
@@ -206,26 +215,22 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
       const uint32_t dn = lane == 0 ? (i + 1 < kU ? v[i + 1].w[0] : nsw) : v[i].w[0];
       const uint32_t next = __shfl_sync(0xFFFFFFFFu, dn, (lane + 1) & 31);
       const int64_t c = cstep + lane + 32 * i;
-      unsigned long long mask = 0;
-      if (!single) {
-        mask = m[lane + 32 * i];
-        m[lane + 32 * i] = 0;
-      }
-      if (mask != 0) {
-        h7 |= chunk_hibits(v[i]) & U8V_B7;
-        chunk_bounded(d, v[i], prev, next, mask, c, r0);
+      uint32_t err, end = 0, hi7 = 0;
+      if (all_ascii) {
+        u8v_carry cr = u8v_carry_of(prev);
+        err = u8v_ascii_word_errors(v[i].w[0], &cr) & U8V_B7;
+        if (err) err = u8v_chunk_errors_planes_k(v[i].w, prev, next, d.k, &hi7);  // exact lanes
+      } else if (single) {
+        err = u8v_chunk_errors_planes_k(v[i].w, prev, next, d.k, &hi7);
       } else {
-        uint32_t e;
-        if (all_ascii) {
-          u8v_carry cr = u8v_carry_of(prev);
-          e = u8v_ascii_word_errors(v[i].w[0], &cr) & U8V_B7;
-        } else {
-          uint32_t hi7;
-          e = chunk_errors<false>(v[i], prev, next, d.k, 0, 0, 0, &hi7);
-          h7 |= hi7;
-        }
-        if (e) chunk_bounded(d, v[i], prev, next, 0ull, c, r0);
+        // Every chunk of a step holding record starts takes the bounded form
+        // (uniform control flow; a zero mask gives the plain flags).
+        const unsigned long long mask = m[lane + 32 * i];
+        m[lane + 32 * i] = 0;
+        err = u8v_chunk_errors_planes_bounded_k(v[i].w, prev, next, d.k, mask, &end, &hi7);
       }
+      h7 |= hi7;
+      if (err | end) attribute_chunk(d, c, err, end, r0);
     }
     was_ascii = all_ascii || __all_sync(0xFFFFFFFFu, h7 == 0);
     if (lane == 31) carry_word = v[kU - 1].w[kChunkWords - 1];
@@ -235,34 +240,25 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
 
 }  // namespace u8v
 
-// Launcher used by capi.cu: needs the first and last offsets (host values).
+// Launcher used by capi.cu.  Fully asynchronous: the kernel reads the first
+// and last offsets itself; the grid is sized from the data size n.
 namespace u8v {
-void launch_batch_known(const uint8_t* data, const uint64_t* d_offsets, uint64_t n_records,
-                        uint64_t first_off, uint64_t last_off, uint8_t* d_verdicts,
-                        cudaStream_t st) {
-  if (n_records == 0) return;
+void launch_batch(const uint8_t* data, uint64_t n, const uint64_t* d_offsets, uint64_t n_records,
+                  uint8_t* d_verdicts, cudaStream_t st) {
+  if (n_records == 0 || n == 0) return;
   BatchDesc d;
   const uintptr_t up = (uintptr_t)data;
   d.off32 = (int64_t)(up & (kChunkBytes - 1));
   d.base = (const uint8_t*)(up - (uintptr_t)d.off32);
   d.offsets = d_offsets;
   d.verdicts = d_verdicts;
-  d.lo = d.off32 + (int64_t)first_off;
-  d.hi = d.off32 + (int64_t)last_off;
   d.n_records = (int64_t)n_records;
+  d.n_bytes = (int64_t)n;
   d.k = u8v_make_consts();
-  if (d.hi <= d.lo) return;  // every record empty: all valid
-  // Lanes [lo, hi]: lane hi carries the last record's end check; lanes past
-  // it read zeros behind a record start and cannot flag.
-  d.c_begin = d.lo / kChunkBytes;
-  d.c_end = d.hi / kChunkBytes + 1;
-  const int64_t chunks = d.c_end - d.c_begin;
-  d.steps = (chunks + kStepChunks - 1) / kStepChunks;
+  d.lo = d.hi = d.c_begin = d.c_end = d.steps = d.steps_per_warp = 0;  // set by the kernel
+  const int64_t max_steps = ((int64_t)n + d.off32 + 2 * kChunkBytes) / (kStepChunks * kChunkBytes) + 1;
   int64_t warps = max_resident_warps();
-  if (warps > d.steps) warps = d.steps;
-  if (warps < 1) warps = 1;
-  d.steps_per_warp = (d.steps + warps - 1) / warps;
-  warps = (d.steps + d.steps_per_warp - 1) / d.steps_per_warp;
+  if (warps > max_steps) warps = max_steps;
   const int64_t blocks = (warps * 32 + kThreads - 1) / kThreads;
   k_batch<<<(unsigned)blocks, kThreads, 0, st>>>(d);
 }

@@ -319,15 +319,10 @@ int utf8v_cuda_validate_batch_async(const uint8_t* d_data, uint64_t n, const uin
   int st = get_ctx(&c);
   if (st) return st;
   cudaStream_t s = (cudaStream_t)stream;
+  if (n > 0 && !d_data) return fail(UTF8V_ERR_ARG, "NULL data");
   CK(cudaMemsetAsync(d_verdicts, 1, n_records, s));
-  // First and last offsets decide the byte range; read them back (16 bytes).
-  uint64_t* h = reinterpret_cast<uint64_t*>(c->h_res + 8);
-  CK(cudaMemcpyAsync(h, d_offsets, 8, cudaMemcpyDeviceToHost, s));
-  CK(cudaMemcpyAsync(h + 1, d_offsets + n_records, 8, cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  if (h[1] < h[0] || h[1] > n) return fail(UTF8V_ERR_ARG, "offsets out of range");
-  if (h[1] > h[0] && !d_data) return fail(UTF8V_ERR_ARG, "NULL data");
-  u8v::launch_batch_known(d_data, d_offsets, n_records, h[0], h[1], d_verdicts, s);
+  // No host round trip: the kernel reads the first/last offsets itself.
+  u8v::launch_batch(d_data, n, d_offsets, n_records, d_verdicts, s);
   ++t_launches;
   return check_launch("batch kernel");
 }
@@ -363,8 +358,7 @@ int utf8v_cuda_validate_batch(const uint8_t* data, size_t n, const uint64_t* off
     if (st) return st;
   }
   CK(cudaMemsetAsync(d_ver, 1, n_records, c->s_comp));
-  u8v::launch_batch_known(n > 0 ? c->d_stage : nullptr, d_off, n_records, offsets[0],
-                          offsets[n_records], d_ver, c->s_comp);
+  u8v::launch_batch(n > 0 ? c->d_stage : nullptr, n, d_off, n_records, d_ver, c->s_comp);
   ++t_launches;
   st = check_launch("batch kernel");
   if (st) return st;

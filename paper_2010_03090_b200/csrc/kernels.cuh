@@ -39,11 +39,10 @@ void launch_first_error(const StreamDesc& d, uint64_t n, uint32_t* flag,
                         int* out_kind, cudaStream_t st);
 
 // batch.cu
-// Caller sets d_verdicts[] = 1 first; first_off/last_off = offsets[0] and
-// offsets[n_records] (host values).
-void launch_batch_known(const uint8_t* data, const uint64_t* d_offsets, uint64_t n_records,
-                        uint64_t first_off, uint64_t last_off, uint8_t* d_verdicts,
-                        cudaStream_t st);
+// Caller sets d_verdicts[] = 1 first.  Asynchronous: the kernel reads
+// offsets[0] and offsets[n_records] itself (clamped to the n data bytes).
+void launch_batch(const uint8_t* data, uint64_t n, const uint64_t* d_offsets, uint64_t n_records,
+                  uint8_t* d_verdicts, cudaStream_t st);
 
 // lanes.cu (lane entry points of the lookup_backend table, width kLaneWidth)
 constexpr int kLaneWidth = 64;

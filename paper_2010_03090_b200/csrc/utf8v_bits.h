@@ -146,3 +146,45 @@ U8V_HD uint32_t u8v_chunk_errors_planes(const uint32_t w[8], uint32_t prev, uint
   uint32_t hi7;
   return u8v_chunk_errors_planes_k(w, prev, next, u8v_make_consts(), &hi7);
 }
+
+// Record-bounded form (K2): as u8v_chunk_errors_planes_k, for a chunk of a
+// record batch.  bnd bit j <-> a record starts at byte j - 4 of the chunk
+// (j < 36: bytes -4..31).  Look-back sources from an earlier record are
+// dropped (each record starts with a zero prev vector); *end_err gets, at
+// each record start i, the end check of the record before it (its lanes
+// i-3..i-1 expected continuations: u8v_word_errors_bounded_lead).  The rare
+// pair needs no mask in the lead form (utf8v_swar.h).
+U8V_HD uint32_t u8v_chunk_errors_planes_bounded_k(const uint32_t w[8], uint32_t prev, uint32_t next,
+                                                  u8v_consts k, uint64_t bnd, uint32_t* end_err,
+                                                  uint32_t* hi7) {
+  uint32_t p[8];
+  u8v_planes_k(w, p, k);
+  *hi7 = p[7];
+  const uint32_t l1 = p[7] & p[6];
+  const uint32_t l2 = l1 & p[5];
+  const uint32_t l3 = l2 & p[4];
+  const uint32_t q1 = prev & U8V_SHL(prev, 1, k);
+  const uint32_t q2 = q1 & U8V_SHL(prev, 2, k);
+  const uint32_t q3 = q2 & U8V_SHL(prev, 3, k);
+  const uint32_t e1 = u8v_fsl(u8v_movemask_top(q1, k), l1, 1);
+  const uint32_t e2 = u8v_fsl(u8v_movemask_top(q2, k), l2, 2);
+  const uint32_t e3 = u8v_fsl(u8v_movemask_top(q3, k), l3, 3);
+  const uint32_t B = (uint32_t)(bnd >> 4);           // a record starts at lane i
+  const uint32_t pre = (uint32_t)bnd << 28;          // bits 30, 31: starts at -2, -1
+  const uint32_t B1 = u8v_fsl(pre, B, 1);            // ... at i-1
+  const uint32_t B2 = u8v_fsl(pre, B, 2);            // ... at i-2
+  const uint32_t m2 = B | B1, m3 = m2 | B2;
+  const uint32_t S = (p[7] & ~p[6]) ^ ((e1 & ~B) | (e2 & ~m2) | (e3 & ~m3));
+  *end_err = B & (e1 | (e2 & ~B1) | (e3 & ~B1 & ~B2));
+  const uint32_t n5 = u8v_fsr(p[5], next >> 5, 1);
+  const uint32_t n4 = u8v_fsr(p[4], next >> 4, 1);
+  const uint32_t z321 = ~(p[3] | p[2] | p[1]);
+  const uint32_t rc = l1 & ~p[5] & ~p[4] & z321;
+  const uint32_t ee = l2 & ~p[4];
+  const uint32_t re0 = ee & z321 & ~p[0] & ~n5;
+  const uint32_t red = ee & p[3] & p[2] & ~p[1] & p[0] & n5;
+  const uint32_t rf0 = l3 & z321 & ~p[0] & ~n5 & ~n4;
+  const uint32_t rf4 = l3 & ~p[3] & p[2] & ~p[1] & ~p[0] & (n5 | n4);
+  const uint32_t rf5 = l3 & (p[3] | (p[2] & (p[1] | p[0])));
+  return S | rc | re0 | red | rf0 | rf4 | rf5;
+}

@@ -336,3 +336,41 @@ uint64_t swar_planes_check(uint64_t seed, uint64_t trials) {
   }
   return bad;
 }
+
+/* Record-bounded plane form vs the SWAR bounded lead form, lane for lane, on
+ * random chunks with random record-start masks (bits for bytes -4..31). */
+uint64_t swar_bits_bounded_check(uint64_t seed, uint64_t trials) {
+  uint64_t s = seed, bad = 0;
+  const u8v_consts k = u8v_make_consts();
+  static const uint8_t hot[] = {0x00, 0x41, 0x80, 0x8F, 0x90, 0x9F, 0xA0, 0xBF, 0xC0, 0xC1,
+                                0xC2, 0xDF, 0xE0, 0xED, 0xEF, 0xF0, 0xF4, 0xF5, 0xFF};
+  for (uint64_t t = 0; t < trials; ++t) {
+    uint8_t buf[40];
+    const uint64_t mode = bits_rng(&s);
+    for (int q = 0; q < 40; ++q) {
+      const uint64_t r = bits_rng(&s);
+      buf[q] = (mode & 1) ? (uint8_t)r : hot[r % sizeof hot];
+    }
+    uint64_t bnd = bits_rng(&s) & bits_rng(&s) & ((1ull << 36) - 1); /* ~25% density */
+    if (mode & 2) bnd &= bits_rng(&s);                                /* sparser */
+    uint32_t w[8], prev, next;
+    memcpy(&prev, buf, 4);
+    memcpy(w, buf + 4, 32);
+    memcpy(&next, buf + 36, 4);
+    uint32_t end_pl = 0, hi7 = 0;
+    const uint32_t err_pl = u8v_chunk_errors_planes_bounded_k(w, prev, next, k, bnd, &end_pl, &hi7);
+    u8v_carry c = u8v_carry_of(prev);
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t bm = u8v_spread4((uint32_t)(bnd >> (4 + 4 * j)));
+      const uint32_t pbm = u8v_spread4((uint32_t)(bnd >> (4 * j)));
+      uint32_t end_sw = 0;
+      const uint32_t e = u8v_word_errors_bounded_lead(w[j], j < 7 ? w[j + 1] : next, &c, bm, pbm,
+                                                      &end_sw, k);
+      for (int b = 0; b < 4; ++b) {
+        bad += ((e >> (8 * b + 7)) & 1u) != ((err_pl >> (4 * j + b)) & 1u);
+        bad += ((end_sw >> (8 * b + 7)) & 1u) != ((end_pl >> (4 * j + b)) & 1u);
+      }
+    }
+  }
+  return bad;
+}

@@ -93,3 +93,12 @@ def test_bit_sliced_form_equals_swar_form_lane_for_lane():
     S.swar_bits_check.restype = C.c_uint64
     S.swar_bits_check.argtypes = [C.c_uint64, C.c_uint64]
     assert S.swar_bits_check(11, 200000) == 0
+
+
+def test_bit_sliced_bounded_form_equals_swar_bounded_form():
+    """K2's record-bounded plane form == u8v_word_errors_bounded_lead lane for
+    lane (errors and end-of-record checks) under random record-start masks."""
+    S = nat.swar()
+    S.swar_bits_bounded_check.restype = C.c_uint64
+    S.swar_bits_bounded_check.argtypes = [C.c_uint64, C.c_uint64]
+    assert S.swar_bits_bounded_check(5, 300000) == 0

@@ -759,6 +759,57 @@ __global__ void __launch_bounds__(256, 4) k_v19_u2_b4(const uint8_t* base, int64
   body19<2>(base, steps, flag, k);
 }
 
+// V20: V19 (grid-stride) with lane 31's follower words (the first word of
+// lane 0's next chunk, and of the next step) and its halo word fetched one
+// step ahead, so no chunk waits on another chunk's load.
+template <int U>
+__device__ __forceinline__ void body20(const uint8_t* base, int64_t steps, uint32_t* flag, const Cfg& k) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  u8v_consts kk;
+  kk.one = k.one; kk.m256 = k.m256; kk.mshr4 = k.mshr4;
+  uint32_t acc = 0;
+  uint32_t fw[U], hw = 0;  // follower words and halo word of the current step (lane 31)
+  auto fetch = [&](int64_t st, uint32_t (&f)[U], uint32_t& h) {
+    const uint8_t* sp = base + st * (int64_t)(U * 1024);
+#pragma unroll
+    for (int i = 0; i < U; ++i)
+      f[i] = (i + 1 < U || st + 1 < steps) ? __ldg(reinterpret_cast<const uint32_t*>(sp + (i + 1) * 1024)) : 0u;
+    h = st > 0 ? __ldg(reinterpret_cast<const uint32_t*>(sp - 4)) : 0u;
+  };
+  if (lane == 31 && warp < steps) fetch(warp, fw, hw);
+  for (int64_t step = warp; step < steps; step += nwarps) {
+    const uint8_t* sp = base + step * (int64_t)(U * 1024);
+    uint32_t v[U][8];
+#pragma unroll
+    for (int i = 0; i < U; ++i) ldg_chunk(v[i], sp + (lane + 32 * i) * 32);
+    uint32_t nf[U], nh = 0;
+    if (lane == 31 && step + nwarps < steps) fetch(step + nwarps, nf, nh);
+#pragma unroll
+    for (int i = 0; i < U; ++i) {
+      const uint32_t supply = lane == 31 ? (i == 0 ? hw : v[i - 1][7]) : v[i][7];
+      const uint32_t prev = __shfl_sync(0xFFFFFFFFu, supply, (lane + 31) & 31);
+      uint32_t nextw = __shfl_down_sync(0xFFFFFFFFu, v[i][0], 1);
+      if (lane == 31) nextw = fw[i];
+      uint32_t hi;
+      acc |= u8v_chunk_errors_planes_k(v[i], prev, nextw, kk, &hi);
+    }
+    if (lane == 31) {
+#pragma unroll
+      for (int i = 0; i < U; ++i) fw[i] = nf[i];
+      hw = nh;
+    }
+  }
+  const unsigned any = __reduce_or_sync(0xFFFFFFFFu, acc);
+  if (lane == 0 && any) atomicOr(flag, 1u);
+}
+__global__ void __launch_bounds__(256, 4) k_v20_u4_b4(const uint8_t* base, int64_t steps, int64_t spw,
+                                                      uint32_t* flag, Cfg k) {
+  (void)spw;
+  body20<4>(base, steps, flag, k);
+}
+
 #define KB_KERNEL(V, U, MINB)                                                                  \
   __global__ void __launch_bounds__(256, MINB)                                                 \
       k_v##V##_u##U##_b##MINB(const uint8_t* base, int64_t steps, int64_t spw, uint32_t* flag, \
@@ -826,7 +877,7 @@ static const Entry kEntries[] = {
     {"v10_u4_b3", k_v10_u4_b3, 4}, {"v10_u4_b4", k_v10_u4_b4, 4}, {"v10_u2_b4", k_v10_u2_b4, 2},
     {"v11_u4_b4", k_v11_u4_b4, 4}, {"v13_u4_b4", k_v13_u4_b4, 4},
     {"v14_u4_b4", k_v14_u4_b4, 4}, {"v15_u4_b4", k_v15_u4_b4, 4}, {"v16_u4_b4", k_v16_u4_b4, 4},
-    {"v19_u4_b4", k_v19_u4_b4, 4}, {"v19_u2_b4", k_v19_u2_b4, 2},
+    {"v20_u4_b4", k_v20_u4_b4, 4}, {"v19_u4_b4", k_v19_u4_b4, 4}, {"v19_u2_b4", k_v19_u2_b4, 2},
     {"v18_u4_b4", k_v18_u4_b4, 4}, {"v18_u4_b3", k_v18_u4_b3, 4}, {"v18_u2_b4", k_v18_u2_b4, 2},
     {"tma_u2_s3_b4", k_tma_u2_s3_b4, 2, 8 * 3 * 2048 + 8 * 3 * 8},
     {"tma_u2_s4_b3", k_tma_u2_s4_b3, 2, 8 * 4 * 2048 + 8 * 4 * 8},
