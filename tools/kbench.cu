@@ -810,6 +810,38 @@ __global__ void __launch_bounds__(256, 4) k_v20_u4_b4(const uint8_t* base, int64
   body20<4>(base, steps, flag, k);
 }
 
+// V21: load-only ceiling of the access pattern (grid-stride 4 KiB steps,
+// 256-bit loads, OR-reduce; no validation).
+template <int U>
+__device__ __forceinline__ void body21(const uint8_t* base, int64_t steps, uint32_t* flag) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  uint32_t acc = 0;
+  for (int64_t step = warp; step < steps; step += nwarps) {
+    const uint8_t* sp = base + step * (int64_t)(U * 1024);
+    uint32_t v[U][8];
+#pragma unroll
+    for (int i = 0; i < U; ++i) ldg_chunk(v[i], sp + (lane + 32 * i) * 32);
+#pragma unroll
+    for (int i = 0; i < U; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc ^= v[i][j];
+  }
+  const unsigned any = __reduce_or_sync(0xFFFFFFFFu, acc == 0x12345678u);
+  if (lane == 0 && any) atomicOr(flag, 1u);
+}
+__global__ void __launch_bounds__(256, 4) k_v21_u4_b4(const uint8_t* base, int64_t steps, int64_t spw,
+                                                      uint32_t* flag, Cfg k) {
+  (void)spw; (void)k;
+  body21<4>(base, steps, flag);
+}
+__global__ void __launch_bounds__(256, 8) k_v21_u4_b8(const uint8_t* base, int64_t steps, int64_t spw,
+                                                      uint32_t* flag, Cfg k) {
+  (void)spw; (void)k;
+  body21<4>(base, steps, flag);
+}
+
 #define KB_KERNEL(V, U, MINB)                                                                  \
   __global__ void __launch_bounds__(256, MINB)                                                 \
       k_v##V##_u##U##_b##MINB(const uint8_t* base, int64_t steps, int64_t spw, uint32_t* flag, \
@@ -877,6 +909,7 @@ static const Entry kEntries[] = {
     {"v10_u4_b3", k_v10_u4_b3, 4}, {"v10_u4_b4", k_v10_u4_b4, 4}, {"v10_u2_b4", k_v10_u2_b4, 2},
     {"v11_u4_b4", k_v11_u4_b4, 4}, {"v13_u4_b4", k_v13_u4_b4, 4},
     {"v14_u4_b4", k_v14_u4_b4, 4}, {"v15_u4_b4", k_v15_u4_b4, 4}, {"v16_u4_b4", k_v16_u4_b4, 4},
+    {"v21_u4_b4", k_v21_u4_b4, 4}, {"v21_u4_b8", k_v21_u4_b8, 4},
     {"v20_u4_b4", k_v20_u4_b4, 4}, {"v19_u4_b4", k_v19_u4_b4, 4}, {"v19_u2_b4", k_v19_u2_b4, 2},
     {"v18_u4_b4", k_v18_u4_b4, 4}, {"v18_u4_b3", k_v18_u4_b3, 4}, {"v18_u2_b4", k_v18_u2_b4, 2},
     {"tma_u2_s3_b4", k_tma_u2_s3_b4, 2, 8 * 3 * 2048 + 8 * 3 * 8},
