@@ -59,4 +59,22 @@ verdict validate_lookup_verdict(bytes_view input);
 std::vector<std::uint8_t> validate_lookup_batch(bytes_view data,
                                                 std::span<const std::uint64_t> offsets);
 
+// One stream validated in pieces (the Lookup counterpart of threading
+// fsm_state through validate_fsm, proj/include/utf8v/fsm.hpp:15-20):
+// feed() host pieces in order, finish() gives the verdict of their
+// concatenation and resets the stream.
+class lookup_stream {
+ public:
+  lookup_stream();
+  ~lookup_stream();
+  lookup_stream(const lookup_stream&) = delete;
+  lookup_stream& operator=(const lookup_stream&) = delete;
+  void feed(bytes_view piece);
+  bool finish();
+  std::uint64_t bytes_fed() const;
+
+ private:
+  void* handle_ = nullptr;
+};
+
 }  // namespace utf8v

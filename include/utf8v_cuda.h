@@ -117,6 +117,24 @@ int utf8v_cuda_validate_batch_async(const uint8_t* d_data, uint64_t n, const uin
                                     void* stream);
 uint64_t utf8v_cuda_batch_scratch_bytes(uint64_t n);
 
+/* ---- streaming: one stream validated in pieces -------------------------
+ * The device-side restatement of threading fsm_state through
+ * validate_fsm(piece, state) (proj/include/utf8v/fsm.hpp:15-20; the
+ * streaming non-goal of SPEC.md:312): feed pieces in order, finish() gives
+ * the verdict of their concatenation.  The session carries 4 bytes and an
+ * error flag on the device; every piece is validated in place (device
+ * pieces are not copied), only the <= 4 lanes straddling a piece boundary run
+ * in a one-thread kernel (csrc/utf8v_stream.h).  Pieces may have any length,
+ * including 0.  Device pieces must stay valid until the next call on the
+ * session (the work is asynchronous on the session's own stream); host
+ * pieces are consumed before feed returns.  finish() resets the session. */
+typedef struct utf8v_cuda_stream utf8v_cuda_stream;
+int utf8v_cuda_stream_create(utf8v_cuda_stream** out);
+int utf8v_cuda_stream_feed(utf8v_cuda_stream* s, const uint8_t* p, size_t n, int is_device);
+int utf8v_cuda_stream_finish(utf8v_cuda_stream* s, uint8_t* out_valid);
+uint64_t utf8v_cuda_stream_bytes(const utf8v_cuda_stream* s);
+void utf8v_cuda_stream_destroy(utf8v_cuda_stream* s);
+
 /* Number of kernel launches the last call on this thread enqueued. */
 int utf8v_cuda_last_launch_count(void);
 

@@ -9,6 +9,7 @@ Python face of libutf8v_cuda.so, mirroring the reference's Lookup API
     validate_lookup_fallback(d)  same device path (no CPU fallback exists)
     validate_lookup_verdict(d)   Verdict, bit-exact with oracle_validate
     validate_lookup_batch(d, offsets)  one verdict per CSR record
+    LookupStream()               one stream validated in pieces (feed / finish)
 
 `data` is host bytes (bytes / bytearray / memoryview / numpy uint8) or a CUDA
 torch.uint8 tensor (device-resident, validated in place).  All compute runs on
@@ -28,6 +29,7 @@ from . import _lib
 __all__ = [
     "ErrorKind", "Utf8Error", "Verdict", "LookupBackend", "lookup_backends", "find_lookup_backend",
     "validate_lookup", "validate_lookup_fallback", "validate_lookup_verdict", "validate_lookup_batch",
+    "LookupStream",
     "validate_lanes_async", "validate_batch_async", "WIDTH",
 ]
 
@@ -209,3 +211,52 @@ def validate_lanes_async(d_ptr: int, n: int, lane_lo: int, lane_hi: int, d_flag_
 
 def validate_batch_async(d_data: int, n: int, d_offsets: int, n_records: int, d_verdicts: int, stream: int = 0) -> None:
     _lib.check(_lib.load().utf8v_cuda_validate_batch_async(d_data, n, d_offsets, n_records, d_verdicts, None, stream))
+
+
+class LookupStream:
+    """One stream validated in pieces: feed() pieces in order, finish() returns
+    the verdict of their concatenation (the device restatement of threading
+    fsm_state through validate_fsm, proj/include/utf8v/fsm.hpp:15-20).
+    Pieces are host bytes or CUDA uint8 tensors (validated in place; the
+    session keeps a reference to the last device piece until the next call).
+    finish() resets the session for the next stream."""
+
+    def __init__(self):
+        self._lib = _lib.load()
+        h = C.c_void_p()
+        _lib.check(self._lib.utf8v_cuda_stream_create(C.byref(h)))
+        self._h = h
+        self._keep = None
+
+    def feed(self, data) -> "LookupStream":
+        ptr, n, dev, keep = _input(data)
+        _lib.check(self._lib.utf8v_cuda_stream_feed(self._h, ptr, n, dev))
+        self._keep = keep if dev else None
+        return self
+
+    def finish(self) -> bool:
+        ok = C.c_uint8(0)
+        _lib.check(self._lib.utf8v_cuda_stream_finish(self._h, C.byref(ok)))
+        self._keep = None
+        return bool(ok.value)
+
+    @property
+    def bytes_fed(self) -> int:
+        return int(self._lib.utf8v_cuda_stream_bytes(self._h))
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) and self._h.value:
+            self._lib.utf8v_cuda_stream_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __enter__(self) -> "LookupStream":
+        return self
+
+    def __exit__(self, *exc) -> None:
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

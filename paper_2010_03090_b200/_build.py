@@ -25,7 +25,7 @@ LIB = PKG / "libutf8v_cuda.so"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC,-O3",
                      f"-I{ROOT / 'include'}", "--expt-relaxed-constexpr"]
-CU_SOURCES = ["validate.cu", "batch.cu", "lanes.cu", "gen.cu", "capi.cu"]
+CU_SOURCES = ["validate.cu", "batch.cu", "lanes.cu", "gen.cu", "stream.cu", "capi.cu"]
 CXX_SOURCES = ["lookup.cpp"]
 
 
@@ -83,7 +83,8 @@ def build_test_helpers() -> None:
     cpp = ROOT / "tests" / "cpp"
     swar_src = cpp / "swar_host.c"
     swar_lib = cpp / "libswar_host.so"
-    deps = [swar_src, CSRC / "utf8v_swar.h", CSRC / "utf8v_bits.h", ROOT / "oracle" / "utf8_oracle.h"]
+    deps = [swar_src, CSRC / "utf8v_swar.h", CSRC / "utf8v_bits.h", CSRC / "utf8v_stream.h",
+            ROOT / "oracle" / "utf8_oracle.h"]
     if swar_src.exists() and _stale(swar_lib, deps):
         _run(["gcc", "-O2", "-fPIC", "-shared", "-std=c99", "-pthread", f"-I{CSRC}",
               f"-I{ROOT / 'oracle'}", "-o", str(swar_lib), str(swar_src),

@@ -416,4 +416,94 @@ int utf8v_cuda_ops_self_test(uint64_t seed, int* out_ok) {
   return UTF8V_OK;
 }
 
+// ---- streaming session (utf8v_stream.h) ------------------------------------
+struct utf8v_cuda_stream {
+  int dev = 0;
+  cudaStream_t s = nullptr;
+  uint32_t* d_state = nullptr;  // [0] carry, [1] error flag
+  uint32_t* h_res = nullptr;    // pinned
+  uint8_t* d_buf = nullptr;     // staging for host pieces
+  size_t cap = 0;
+  uint64_t total = 0;
+};
+
+int utf8v_cuda_stream_create(utf8v_cuda_stream** out) {
+  if (!out) return fail(UTF8V_ERR_ARG, "NULL out");
+  *out = nullptr;
+  Ctx* c;
+  int st = get_ctx(&c);
+  if (st) return st;
+  utf8v_cuda_stream* s = new utf8v_cuda_stream();
+  cudaGetDevice(&s->dev);
+  if (cudaStreamCreateWithFlags(&s->s, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaMalloc(&s->d_state, 64) != cudaSuccess || cudaMallocHost(&s->h_res, 64) != cudaSuccess ||
+      cudaMemsetAsync(s->d_state, 0, 64, s->s) != cudaSuccess) {
+    const cudaError_t e = cudaGetLastError();
+    utf8v_cuda_stream_destroy(s);
+    return fail(UTF8V_ERR_CUDA, "stream session allocation", e);
+  }
+  *out = s;
+  return UTF8V_OK;
+}
+
+int utf8v_cuda_stream_feed(utf8v_cuda_stream* s, const uint8_t* p, size_t n, int is_device) {
+  t_launches = 0;
+  if (!s) return fail(UTF8V_ERR_ARG, "NULL session");
+  if (n == 0) return UTF8V_OK;
+  if (!p) return fail(UTF8V_ERR_ARG, "NULL piece");
+  CK(cudaSetDevice(s->dev));
+  const uint8_t* d = p;
+  if (!is_device) {
+    if (s->cap < n) {
+      if (s->d_buf) {
+        CK(cudaStreamSynchronize(s->s));
+        cudaFree(s->d_buf);
+      }
+      s->d_buf = nullptr;
+      s->cap = 0;
+      const size_t cap = (n + 0xFFFFF) & ~size_t(0xFFFFF);
+      CK(cudaMalloc(&s->d_buf, cap));
+      s->cap = cap;
+    }
+    CK(cudaMemcpyAsync(s->d_buf, p, n, cudaMemcpyHostToDevice, s->s));
+    d = s->d_buf;
+  }
+  // Lanes straddling the previous piece, then the piece's own lanes in place.
+  u8v::launch_stream_edge(s->d_state, d, n, 0, s->s);
+  ++t_launches;
+  if (n > 4) {
+    u8v::launch_validate(u8v::make_desc(d, n, 3, n - 1), s->d_state + 1, s->s);
+    ++t_launches;
+  }
+  s->total += n;
+  if (!is_device) CK(cudaStreamSynchronize(s->s));  // the caller may reuse its buffer
+  return check_launch("stream feed");
+}
+
+int utf8v_cuda_stream_finish(utf8v_cuda_stream* s, uint8_t* out_valid) {
+  t_launches = 0;
+  if (!s || !out_valid) return fail(UTF8V_ERR_ARG, "NULL session/out_valid");
+  CK(cudaSetDevice(s->dev));
+  u8v::launch_stream_edge(s->d_state, nullptr, 0, 1, s->s);
+  ++t_launches;
+  CK(cudaMemcpyAsync(s->h_res, s->d_state + 1, 4, cudaMemcpyDeviceToHost, s->s));
+  CK(cudaMemsetAsync(s->d_state, 0, 8, s->s));  // ready for the next stream
+  CK(cudaStreamSynchronize(s->s));
+  *out_valid = s->h_res[0] == 0 ? 1 : 0;
+  s->total = 0;
+  return check_launch("stream finish");
+}
+
+uint64_t utf8v_cuda_stream_bytes(const utf8v_cuda_stream* s) { return s ? s->total : 0; }
+
+void utf8v_cuda_stream_destroy(utf8v_cuda_stream* s) {
+  if (!s) return;
+  if (s->s) cudaStreamSynchronize(s->s);
+  if (s->d_buf) cudaFree(s->d_buf);
+  if (s->d_state) cudaFree(s->d_state);
+  if (s->h_res) cudaFreeHost(s->h_res);
+  if (s->s) cudaStreamDestroy(s->s);
+  delete s;
+}
+
 }  // extern "C"

@@ -44,6 +44,10 @@ void launch_first_error(const StreamDesc& d, uint64_t n, uint32_t* flag,
 void launch_batch(const uint8_t* data, uint64_t n, const uint64_t* d_offsets, uint64_t n_records,
                   uint8_t* d_verdicts, cudaStream_t st);
 
+// stream.cu: d_state[0] = carry, d_state[1] = error flag (utf8v_stream.h).
+void launch_stream_edge(uint32_t* d_state, const uint8_t* d_piece, uint64_t n, int finish,
+                        cudaStream_t st);
+
 // lanes.cu (lane entry points of the lookup_backend table, width kLaneWidth)
 constexpr int kLaneWidth = 64;
 void set_tables(const uint8_t t1[16], const uint8_t t2[16], const uint8_t t3[16]);

@@ -88,4 +88,30 @@ std::vector<std::uint8_t> validate_lookup_batch(bytes_view data,
   return out;
 }
 
+lookup_stream::lookup_stream() {
+  utf8v_cuda_stream* s = nullptr;
+  const int st = utf8v_cuda_stream_create(&s);
+  if (st != UTF8V_OK) raise(st);
+  handle_ = s;
+}
+
+lookup_stream::~lookup_stream() { utf8v_cuda_stream_destroy(static_cast<utf8v_cuda_stream*>(handle_)); }
+
+void lookup_stream::feed(bytes_view piece) {
+  const int st =
+      utf8v_cuda_stream_feed(static_cast<utf8v_cuda_stream*>(handle_), piece.data(), piece.size(), 0);
+  if (st != UTF8V_OK) raise(st);
+}
+
+bool lookup_stream::finish() {
+  std::uint8_t ok = 0;
+  const int st = utf8v_cuda_stream_finish(static_cast<utf8v_cuda_stream*>(handle_), &ok);
+  if (st != UTF8V_OK) raise(st);
+  return ok != 0;
+}
+
+std::uint64_t lookup_stream::bytes_fed() const {
+  return utf8v_cuda_stream_bytes(static_cast<const utf8v_cuda_stream*>(handle_));
+}
+
 }  // namespace utf8v

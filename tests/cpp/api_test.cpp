@@ -7,6 +7,7 @@
 // box: tests/cpp/api_test  (exit 0 = every case passed).
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
 #include <cstring>
 #include <functional>
 #include <string>
@@ -268,6 +269,29 @@ TEST(batch, "record batches: empty, ragged, every error class") {
     want.push_back(oracle_ok(rec) ? 1 : 0);
   }
   CHECK(utf8v::validate_lookup_batch(data, offs) == want);
+}
+
+TEST(stream, "a stream fed in pieces gives the verdict of the whole (fsm.hpp:15-20)") {
+  bytes buf(1 << 14);
+  std::uint64_t s = 7;
+  utf8v::lookup_stream ls;
+  CHECK(ls.finish());
+  for (std::uint64_t seed = 1; seed <= 40; ++seed) {
+    for (int strategy = -1; strategy < 7; ++strategy) {
+      const std::size_t n = strategy < 0 ? orc_generate_valid(0xF, 3000, seed, buf.data(), buf.size())
+                                         : orc_generate_invalid(0xF, 3000, seed, strategy, buf.data(), buf.size());
+      if (n == static_cast<std::size_t>(-1)) continue;
+      const bytes b(buf.begin(), buf.begin() + static_cast<std::ptrdiff_t>(n));
+      std::size_t at = 0;
+      while (at < n) {
+        const std::size_t len = std::min<std::size_t>(n - at, xorshift(s) % 9 == 0 ? 0 : 1 + xorshift(s) % 700);
+        ls.feed(utf8v::bytes_view(b.data() + at, len));
+        at += len;
+      }
+      CHECK(ls.bytes_fed() == n);
+      CHECK(ls.finish() == oracle_ok(b));
+    }
+  }
 }
 
 TEST(threads, "validators are callable concurrently (bench.cpp:112-118)") {

@@ -10,6 +10,7 @@
 #include "utf8_oracle.h"
 #include "utf8v_swar.h"
 #include "utf8v_bits.h"
+#include "utf8v_stream.h"
 
 /* Stream the words of a zero-extended stream [0, n) that starts `off` bytes
  * into an aligned word grid, exactly like k_validate: words in order, lanes
@@ -373,4 +374,33 @@ uint64_t swar_bits_bounded_check(uint64_t seed, uint64_t trials) {
     }
   }
   return bad;
+}
+
+/* A stream fed in pieces (cut at `cuts`, n_cuts ascending inside [0, n]),
+ * stitched with utf8v_stream.h exactly as the device session does it (edge
+ * lanes from the carry, the rest in place over each piece); returns 1 when
+ * the stitched verdict is "valid". */
+int swar_stream_split(const uint8_t* p, size_t n, const uint64_t* cuts, size_t n_cuts) {
+  uint32_t carry = 0, err = 0;
+  uint64_t start = 0;
+  for (size_t c = 0; c <= n_cuts; ++c) {
+    const uint64_t end = c < n_cuts ? cuts[c] : n;
+    const uint8_t* q = p + start;
+    const uint64_t m = end - start;
+    uint8_t h[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (uint64_t i = 0; i < m && i < 8; ++i) h[i] = q[i];
+    uint32_t h0, h1, tail = 0;
+    memcpy(&h0, h, 4);
+    memcpy(&h1, h + 4, 4);
+    err |= u8v_stream_edge(carry, h0, h1, m, 0);
+    if (m > 4) err |= (uint32_t)swar_lanes(q, (size_t)m, 3, m - 1);
+    for (uint64_t i = 0; i < 4 && i < m; ++i) {
+      const uint64_t src = m >= 4 ? m - 4 + i : i;
+      tail |= (uint32_t)q[src] << (8 * i);
+    }
+    carry = u8v_stream_carry(carry, tail, m);
+    start = end;
+  }
+  err |= u8v_stream_edge(carry, 0, 0, 0, 1);
+  return err == 0;
 }

@@ -102,3 +102,42 @@ def test_bit_sliced_bounded_form_equals_swar_bounded_form():
     S.swar_bits_bounded_check.restype = C.c_uint64
     S.swar_bits_bounded_check.argtypes = [C.c_uint64, C.c_uint64]
     assert S.swar_bits_bounded_check(5, 300000) == 0
+
+
+def test_stream_stitching_equals_whole_stream():
+    """utf8v_stream.h: any split of a stream into pieces (empty, 1..8-byte,
+    large), stitched through the carry, gives the whole stream's verdict --
+    on generated valid/invalid corpora and on all short inputs around a cut."""
+    S = nat.swar()
+    S.swar_stream_split.restype = C.c_int
+    S.swar_stream_split.argtypes = [C.c_void_p, C.c_size_t, C.c_void_p, C.c_size_t]
+    rng = np.random.default_rng(3)
+    checked = 0
+    for seed in range(1, 120):
+        for strategy in (None, 0, 1, 2, 3, 4, 5, 6):
+            data = nat.generate_valid(0xF, 200 + seed * 7, seed) if strategy is None else \
+                nat.generate_invalid(0xF, 200 + seed * 7, seed, strategy)
+            if data is None:
+                continue
+            buf = np.frombuffer(data, dtype=np.uint8).copy()
+            want = nat.oracle_verdict(bytes(buf))[0]
+            for _ in range(6):
+                k = int(rng.integers(0, 12))
+                cuts = np.sort(rng.integers(0, len(buf) + 1, size=k)).astype(np.uint64)
+                got = S.swar_stream_split(buf.ctypes.data, len(buf), cuts.ctypes.data, len(cuts))
+                assert bool(got) == bool(want), (seed, strategy, cuts.tolist())
+                checked += 1
+    # Every 4-byte window of "interesting" bytes, cut at every position.
+    hot = [0x41, 0x80, 0xA0, 0xBF, 0xC2, 0xE0, 0xED, 0xF0, 0xF4]
+    for a in hot:
+        for b in hot:
+            for c in hot:
+                for d in hot:
+                    buf = np.array([0x41, a, b, c, d, 0x41, 0x41, 0x41, 0x41], dtype=np.uint8)
+                    want = nat.oracle_verdict(bytes(buf))[0]
+                    for cut in range(len(buf) + 1):
+                        cuts = np.array([cut], dtype=np.uint64)
+                        got = S.swar_stream_split(buf.ctypes.data, len(buf), cuts.ctypes.data, 1)
+                        assert bool(got) == bool(want), (buf.tolist(), cut)
+                        checked += 1
+    assert checked > 5000
