@@ -71,6 +71,22 @@ def build_cuda(force: bool = False, verbose: bool = False) -> Path:
     return LIB
 
 
+CLI = PKG / "bin" / "utf8v-cuda"
+
+
+def build_cli() -> Path:
+    """tools/utf8v_cuda_cli.cpp -> paper_2010_03090_b200/bin/utf8v-cuda (the
+    reference CLI's validate/bench on the C++ API)."""
+    src = ROOT / "tools" / "utf8v_cuda_cli.cpp"
+    if src.exists() and _stale(CLI, [src, LIB, ROOT / "include" / "utf8v" / "lookup.hpp"]):
+        CLI.parent.mkdir(exist_ok=True)
+        cuda = Path(_nvcc()).resolve().parents[1]
+        _run(["g++", "-O2", "-std=c++20", f"-I{ROOT / 'include'}", f"-I{cuda / 'include'}", "-o", str(CLI),
+              str(src), f"-L{PKG}", "-lutf8v_cuda", f"-L{cuda / 'lib64'}", "-lcudart",
+              f"-Wl,-rpath,{PKG}", "-Wl,-rpath,$ORIGIN/.."])
+    return CLI
+
+
 def build_oracle() -> None:
     """oracle/ checkers (test infrastructure). `make ref` is a no-op without
     the reference checkout (the GPU box uses the prebuilt oracle/_ref)."""
@@ -100,6 +116,7 @@ def build_test_helpers() -> None:
 
 def build_all(force: bool = False, verbose: bool = False) -> None:
     build_cuda(force=force, verbose=verbose)
+    build_cli()
     build_oracle()
     build_test_helpers()
 

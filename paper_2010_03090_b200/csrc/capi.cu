@@ -6,8 +6,13 @@
 #include <stdint.h>
 #include <string.h>
 
+#include <algorithm>
+#include <atomic>
+#include <condition_variable>
+#include <functional>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/utf8v_cuda.h"
@@ -83,7 +88,12 @@ struct Ctx {
   uint8_t* d_stage = nullptr;
   size_t stage_cap = 0;
   std::vector<cudaEvent_t> events;
+  // Pageable host input: pinned staging ring (kSlots x kPiece) and the event
+  // of the DMA that last read each slot.
+  uint8_t* h_ring = nullptr;
+  cudaEvent_t slot_done[4] = {nullptr, nullptr, nullptr, nullptr};
 };
+constexpr int kSlots = 4;
 thread_local Ctx t_ctx[kMaxDevices];
 
 int get_ctx(Ctx** out) {
@@ -141,19 +151,146 @@ int check_launch(const char* what) {
   return UTF8V_OK;
 }
 
+// Host copy pool for pageable inputs: a pageable cudaMemcpyAsync is staged by
+// the driver at ~11 GB/s on the GPU box (one CPU thread); copying each piece
+// into a pinned slot with several threads and then DMA-ing the slot runs the
+// PCIe link at its rate.  Workers are persistent (created once per process).
+class CopyPool {
+ public:
+  static CopyPool& get() {
+    static CopyPool* pool = new CopyPool();  // never destroyed: workers outlive exit
+    return *pool;
+  }
+  // dst[0..n) = src[0..n), split over the workers and the calling thread.
+  // Concurrent callers (the API is re-entrant) take turns.
+  void copy(uint8_t* dst, const uint8_t* src, size_t n) {
+    const size_t parts = workers_.size() + 1;
+    if (n < (4u << 20) || parts == 1) {
+      memcpy(dst, src, n);
+      return;
+    }
+    std::lock_guard<std::mutex> turn(call_m_);
+    const size_t seg = ((n + parts - 1) / parts + 4095) & ~size_t(4095);
+    {
+      std::lock_guard<std::mutex> g(m_);
+      dst_ = dst;
+      src_ = src;
+      n_ = n;
+      seg_ = seg;
+      next_.store(1);
+      pending_ = parts - 1;
+      ++gen_;
+    }
+    cv_.notify_all();
+    run_segment(0);
+    for (;;) {
+      const size_t k = next_.fetch_add(1);
+      if (k >= parts) break;
+      run_segment(k);
+      std::lock_guard<std::mutex> g(m_);
+      --pending_;
+    }
+    std::unique_lock<std::mutex> lk(m_);
+    done_cv_.wait(lk, [&] { return pending_ == 0; });
+  }
+
+ private:
+  CopyPool() {
+    const unsigned hw = std::thread::hardware_concurrency();
+    const unsigned n = hw > 2 ? std::min(hw - 1, 11u) : 0u;
+    for (unsigned i = 0; i < n; ++i) workers_.emplace_back([this] { loop(); });
+    for (auto& t : workers_) t.detach();
+  }
+  void run_segment(size_t k) {
+    const size_t a = k * seg_;
+    if (a >= n_) return;
+    const size_t len = std::min(seg_, n_ - a);
+    memcpy(dst_ + a, src_ + a, len);
+  }
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> lk(m_);
+        cv_.wait(lk, [&] { return gen_ != seen; });
+        seen = gen_;
+      }
+      for (;;) {
+        const size_t k = next_.fetch_add(1);
+        if (k >= workers_.size() + 1) break;
+        run_segment(k);
+        std::lock_guard<std::mutex> g(m_);
+        if (--pending_ == 0) done_cv_.notify_all();
+      }
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex call_m_, m_;
+  std::condition_variable cv_, done_cv_;
+  uint64_t gen_ = 0;
+  std::atomic<size_t> next_{0};
+  size_t pending_ = 0;
+  uint8_t* dst_ = nullptr;
+  const uint8_t* src_ = nullptr;
+  size_t n_ = 0, seg_ = 0;
+};
+
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeDevice ||
+         a.type == cudaMemoryTypeManaged;
+}
+
+int ensure_ring(Ctx& c) {
+  if (c.h_ring) return UTF8V_OK;
+  CK(cudaMallocHost(&c.h_ring, kSlots * kPiece));
+  for (int i = 0; i < kSlots; ++i) CK(cudaEventCreateWithFlags(&c.slot_done[i], cudaEventDisableTiming));
+  return UTF8V_OK;
+}
+
 // Copy host bytes into the stage in pieces on s_copy; `each(k, off, len)`
 // runs on s_comp after piece k has landed.
+// Piece size: about n/8 (so small inputs still pipeline), 2..32 MiB, a
+// multiple of 1 MiB.
+size_t piece_size(size_t n) {
+  size_t p = ((n / 8) + 0xFFFFF) & ~size_t(0xFFFFF);
+  if (p < (2u << 20)) p = 2u << 20;
+  if (p > kPiece) p = kPiece;
+  return p;
+}
+
 template <class F>
 int pipeline_h2d(Ctx& c, const uint8_t* p, size_t n, F each) {
   int st = ensure_stage(c, n);
   if (st) return st;
-  const size_t pieces = (n + kPiece - 1) / kPiece;
+  const size_t piece = piece_size(n);
+  const size_t pieces = (n + piece - 1) / piece;
   st = ensure_events(c, pieces);
   if (st) return st;
+  const bool pageable = !is_pinned(p);
+  if (pageable) {
+    st = ensure_ring(c);
+    if (st) return st;
+  }
   for (size_t k = 0; k < pieces; ++k) {
-    const size_t off = k * kPiece;
-    const size_t len = n - off < kPiece ? n - off : kPiece;
-    CK(cudaMemcpyAsync(c.d_stage + off, p + off, len, cudaMemcpyHostToDevice, c.s_copy));
+    const size_t off = k * piece;
+    const size_t len = n - off < piece ? n - off : piece;
+    if (pageable) {
+      // Slot k % kSlots is free once the DMA that last read it has finished;
+      // the parallel host copy of this piece overlaps the DMA of the last.
+      const int slot = (int)(k % kSlots);
+      uint8_t* h = c.h_ring + (size_t)slot * kPiece;
+      if (k >= (size_t)kSlots) CK(cudaEventSynchronize(c.slot_done[slot]));
+      CopyPool::get().copy(h, p + off, len);
+      CK(cudaMemcpyAsync(c.d_stage + off, h, len, cudaMemcpyHostToDevice, c.s_copy));
+      CK(cudaEventRecord(c.slot_done[slot], c.s_copy));
+    } else {
+      CK(cudaMemcpyAsync(c.d_stage + off, p + off, len, cudaMemcpyHostToDevice, c.s_copy));
+    }
     CK(cudaEventRecord(c.events[k], c.s_copy));
     CK(cudaStreamWaitEvent(c.s_comp, c.events[k], 0));
     st = each(k, off, len);
