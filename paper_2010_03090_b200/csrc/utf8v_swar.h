@@ -136,14 +136,6 @@ U8V_HD uint32_t u8v_rare_key(uint32_t a4, uint32_t zl, uint32_t e1, u8v_consts k
   return e1 & ((a4 & bad_ef) | (~a4 & ~ge08));
 }
 
-// Lag form: the pair ending at each lane of w (a = previous byte), flags at b.
-U8V_HD uint32_t u8v_rare_pairs(uint32_t w, uint32_t ph, uint32_t e1, u8v_consts k) {
-  const uint32_t a = u8v_mad(w, k.m256, ph);
-  const uint32_t a4 = a << 2;  // bits 7..2 = a5..a0
-  const uint32_t zl = (a4 & 0x7C7C7C7Cu) | (u8v_mulhi(w, k.mshr4) & 0x03030303u);
-  return u8v_rare_key(a4, zl, e1, k);
-}
-
 // Upper 32 bits of ((hi:lo) >> s), 0 < s < 32.  SHF.R.W on sm_100a.
 U8V_HD uint32_t u8v_fsr(uint32_t lo, uint32_t hi, unsigned s) {
 #if defined(__CUDA_ARCH__)
@@ -189,79 +181,19 @@ U8V_HD uint32_t u8v_word_errors_lead(uint32_t w, uint32_t wn, u8v_carry* c, u8v_
   return S | R;
 }
 
-// Error flags (bit 7 of each byte lane, other bits garbage -- mask with U8V_B7
-// or test via u8v_any) for the four lanes of word w, given the previous word.
-// Advances the carry to w.
-U8V_HD uint32_t u8v_word_errors_k(uint32_t w, u8v_carry* c, u8v_consts k) {
-  // --- S: structure (cont XOR expected-continuation) ---------------------
-  const uint32_t s1 = w << 1, s2 = w << 2, s3 = w << 3;
-  const uint32_t f1 = w & s1;   // >= C0
-  const uint32_t f2 = f1 & s2;  // >= E0
-  const uint32_t f3 = f2 & s3;  // >= F0
-  const uint32_t e1 = u8v_fsl(c->f1, f1, 8);   // x[i-1] >= C0
-  const uint32_t e2 = u8v_fsl(c->f2, f2, 16);  // x[i-2] >= E0
-  const uint32_t e3 = u8v_fsl(c->f3, f3, 24);  // x[i-3] >= F0
-  const uint32_t cont = w & ~s1;               // 10xxxxxx
-  const uint32_t S = (e1 | e2 | e3) ^ cont;
-  const uint32_t R = u8v_rare_pairs(w, c->ph, e1, k);
-  c->p = w;
-  c->f1 = f1;
-  c->f2 = f2;
-  c->f3 = f3;
-  c->ph = u8v_mulhi(w, k.m256);
-  return S | R;
-}
-
-U8V_HD uint32_t u8v_word_errors(uint32_t w, u8v_carry* c) {
-  return u8v_word_errors_k(w, c, u8v_make_consts());
-}
-
-// Record-bounded variant for the batch kernel: each record is its own
-// zero-extended stream.  bm / pbm carry, in bit 7 of byte k, "a record
-// starts at byte k" of this / the previous word.  Lane i drops every
+// Record-bounded lead form (K2's reference in SWAR; the kernel runs the plane
+// form of utf8v_bits.h, proven equal to this one lane for lane): each record
+// is its own zero-extended stream.  bm / pbm carry, in bit 7 of byte k, "a
+// record starts at byte k" of this / the previous word.  Lane i drops every
 // look-back source that lies in an earlier record (i-1 if a record starts at
-// i; i-2 if one starts at i or i-1; i-3 if at i, i-1 or i-2), which is the
+// i; i-2 if one starts at i or i-1; i-3 if at i, i-1 or i-2) -- the
 // reference's zero prev vector at a record start (lookup_kernel.hpp:115).
 // *end_err receives, at each record start b, the previous record's
 // end-of-stream check (lookup_kernel.hpp:48-68, :111) restricted to that
-// record's own bytes; the returned flags belong to the record of their lane.
-U8V_HD uint32_t u8v_word_errors_bounded_k(uint32_t w, u8v_carry* c, uint32_t bm, uint32_t pbm,
-                                          uint32_t* end_err, u8v_consts k) {
-  const uint32_t s1 = w << 1, s2 = w << 2, s3 = w << 3;
-  const uint32_t f1 = w & s1;
-  const uint32_t f2 = f1 & s2;
-  const uint32_t f3 = f2 & s3;
-  const uint32_t e1 = u8v_fsl(c->f1, f1, 8);
-  const uint32_t e2 = u8v_fsl(c->f2, f2, 16);
-  const uint32_t e3 = u8v_fsl(c->f3, f3, 24);
-  const uint32_t b1 = u8v_fsl(pbm, bm, 8);   // a record starts at i-1
-  const uint32_t b2 = u8v_fsl(pbm, bm, 16);  // a record starts at i-2
-  const uint32_t m2 = bm | b1;
-  const uint32_t m3 = m2 | b2;
-  const uint32_t cont = w & ~s1;
-  const uint32_t S = ((e1 & ~bm) | (e2 & ~m2) | (e3 & ~m3)) ^ cont;
-
-  const uint32_t R = u8v_rare_pairs(w, c->ph, e1, k) & ~bm;
-
-  *end_err = bm & (e1 | (e2 & ~b1) | (e3 & ~b1 & ~b2)) & U8V_B7;
-  c->p = w;
-  c->f1 = f1;
-  c->f2 = f2;
-  c->f3 = f3;
-  c->ph = u8v_mulhi(w, k.m256);
-  return (S | R) & U8V_B7;
-}
-
-U8V_HD uint32_t u8v_word_errors_bounded(uint32_t w, u8v_carry* c, uint32_t bm, uint32_t pbm,
-                                        uint32_t* end_err) {
-  return u8v_word_errors_bounded_k(w, c, bm, pbm, end_err, u8v_make_consts());
-}
-
-// Record-bounded, lead form (K2): S and the end checks exactly as
-// u8v_word_errors_bounded_k; the rare pair (j, j+1) is tested at lane j with
-// no boundary mask -- a flag on a pair that crosses into the next record
-// means byte j is a lead that ends its record, which is invalid anyway (its
-// end check fires too), and the flag sits on that record's lane.
+// record's own bytes.  The rare pair (j, j+1) is tested at lane j with no
+// boundary mask: a flag on a pair that crosses into the next record means
+// byte j is a lead that ends its record, which is invalid anyway (its end
+// check fires too), and the flag sits on that record's lane.
 U8V_HD uint32_t u8v_word_errors_bounded_lead(uint32_t w, uint32_t wn, u8v_carry* c, uint32_t bm,
                                              uint32_t pbm, uint32_t* end_err, u8v_consts k) {
   const uint32_t s1 = w << 1, s2 = w << 2, s3 = w << 3;
@@ -302,14 +234,6 @@ U8V_HD uint32_t u8v_ascii_word_errors(uint32_t w, u8v_carry* c) {
   c->ph = w >> 24;
   return e;
 }
-
-// End-of-stream lanes n, n+1, n+2: check_incomplete of the last three bytes
-// (lookup_kernel.hpp:48-68, :111).  Equivalent to u8v_word_errors(0, c).
-U8V_HD uint32_t u8v_end_errors(const u8v_carry* c) {
-  return u8v_fsl(c->f1, 0, 8) | u8v_fsl(c->f2, 0, 16) | u8v_fsl(c->f3, 0, 24);
-}
-
-U8V_HD int u8v_any(uint32_t err) { return (err & U8V_B7) != 0; }
 
 // Bytes outside [lo, hi) of word at byte position `pos` replaced by zero --
 // the zero-extended stream the reference builds with its zeroed tail block

@@ -112,7 +112,8 @@ uint64_t swar_pairs(size_t offset, unsigned align) {
   return mm;
 }
 
-/* Batch semantics through u8v_word_errors_bounded, as k_batch drives it:
+/* Batch semantics through u8v_word_errors_bounded_lead (the SWAR statement of
+ * K2), with the record-start masks built per word:
  * records [offsets[r], offsets[r+1]) of one contiguous buffer starting `off`
  * bytes into the word grid.  verdicts[r] = 1 / 0. */
 void swar_batch(const uint8_t* data, const uint64_t* offsets, size_t n_records, unsigned off,

@@ -10,6 +10,25 @@
 
 namespace kb {
 
+// Historical lag form (round-1 v0..v3; removed from utf8v_swar.h): the rare
+// pair ending at each lane is tested at the follower's lane.
+__device__ __forceinline__ uint32_t lag_rare_pairs(uint32_t w, uint32_t ph, uint32_t e1, u8v_consts k) {
+  const uint32_t a = u8v_mad(w, k.m256, ph);
+  const uint32_t a4 = a << 2;
+  const uint32_t zl = (a4 & 0x7C7C7C7Cu) | (u8v_mulhi(w, k.mshr4) & 0x03030303u);
+  return u8v_rare_key(a4, zl, e1, k);
+}
+__device__ __forceinline__ uint32_t u8v_word_errors_k(uint32_t w, u8v_carry* c, u8v_consts k) {
+  const uint32_t s1 = w << 1, s2 = w << 2, s3 = w << 3;
+  const uint32_t f1 = w & s1, f2 = f1 & s2, f3 = f2 & s3;
+  const uint32_t e1 = u8v_fsl(c->f1, f1, 8), e2 = u8v_fsl(c->f2, f2, 16), e3 = u8v_fsl(c->f3, f3, 24);
+  const uint32_t S = (e1 | e2 | e3) ^ (w & ~s1);
+  const uint32_t R = lag_rare_pairs(w, c->ph, e1, k);
+  c->p = w; c->f1 = f1; c->f2 = f2; c->f3 = f3; c->ph = u8v_mulhi(w, k.m256);
+  return S | R;
+}
+
+
 struct Cfg {
   uint32_t one, m256, mshr4, m2_16, m2_24, m2_8;
 };
@@ -842,6 +861,61 @@ __global__ void __launch_bounds__(256, 8) k_v21_u4_b8(const uint8_t* base, int64
   body21<4>(base, steps, flag);
 }
 
+// V22: V19 with other load flavours: LF = 1 adds the L2::256B prefetch-size
+// hint, LF = 2 is a plain ld.global.v8 (L1-allocating).
+template <int LF>
+__device__ __forceinline__ void ldg_chunk_lf(uint32_t (&w)[8], const uint8_t* p) {
+  if (LF == 1)
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]),
+                   "=r"(w[7])
+                 : "l"(p));
+  else
+    asm volatile("ld.global.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]),
+                   "=r"(w[7])
+                 : "l"(p));
+}
+template <int U, int LF>
+__device__ __forceinline__ void body22(const uint8_t* base, int64_t steps, uint32_t* flag, const Cfg& k) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  u8v_consts kk;
+  kk.one = k.one; kk.m256 = k.m256; kk.mshr4 = k.mshr4;
+  uint32_t acc = 0;
+  for (int64_t step = warp; step < steps; step += nwarps) {
+    const uint8_t* sp = base + step * (int64_t)(U * 1024);
+    uint32_t v[U][8];
+#pragma unroll
+    for (int i = 0; i < U; ++i) ldg_chunk_lf<LF>(v[i], sp + (lane + 32 * i) * 32);
+    uint32_t carry_word = 0, nsw = 0;
+    if (lane == 31 && step > 0) carry_word = __ldg(reinterpret_cast<const uint32_t*>(sp - 4));
+    if (lane == 0 && step + 1 < steps) nsw = __ldg(reinterpret_cast<const uint32_t*>(sp + U * 1024));
+#pragma unroll
+    for (int i = 0; i < U; ++i) {
+      const uint32_t supply = lane == 31 ? (i == 0 ? carry_word : v[i - 1][7]) : v[i][7];
+      const uint32_t prev = __shfl_sync(0xFFFFFFFFu, supply, (lane + 31) & 31);
+      const uint32_t dn = lane == 0 ? (i + 1 < U ? v[i + 1][0] : nsw) : v[i][0];
+      const uint32_t nextw = __shfl_sync(0xFFFFFFFFu, dn, (lane + 1) & 31);
+      uint32_t hi;
+      acc |= u8v_chunk_errors_planes_k(v[i], prev, nextw, kk, &hi);
+    }
+  }
+  const unsigned any = __reduce_or_sync(0xFFFFFFFFu, acc);
+  if (lane == 0 && any) atomicOr(flag, 1u);
+}
+__global__ void __launch_bounds__(256, 4) k_v22a_u4_b4(const uint8_t* base, int64_t steps, int64_t spw,
+                                                       uint32_t* flag, Cfg k) {
+  (void)spw;
+  body22<4, 1>(base, steps, flag, k);
+}
+__global__ void __launch_bounds__(256, 4) k_v22b_u4_b4(const uint8_t* base, int64_t steps, int64_t spw,
+                                                       uint32_t* flag, Cfg k) {
+  (void)spw;
+  body22<4, 2>(base, steps, flag, k);
+}
+
 #define KB_KERNEL(V, U, MINB)                                                                  \
   __global__ void __launch_bounds__(256, MINB)                                                 \
       k_v##V##_u##U##_b##MINB(const uint8_t* base, int64_t steps, int64_t spw, uint32_t* flag, \
@@ -909,6 +983,7 @@ static const Entry kEntries[] = {
     {"v10_u4_b3", k_v10_u4_b3, 4}, {"v10_u4_b4", k_v10_u4_b4, 4}, {"v10_u2_b4", k_v10_u2_b4, 2},
     {"v11_u4_b4", k_v11_u4_b4, 4}, {"v13_u4_b4", k_v13_u4_b4, 4},
     {"v14_u4_b4", k_v14_u4_b4, 4}, {"v15_u4_b4", k_v15_u4_b4, 4}, {"v16_u4_b4", k_v16_u4_b4, 4},
+    {"v22a_u4_b4", k_v22a_u4_b4, 4}, {"v22b_u4_b4", k_v22b_u4_b4, 4},
     {"v21_u4_b4", k_v21_u4_b4, 4}, {"v21_u4_b8", k_v21_u4_b8, 4},
     {"v20_u4_b4", k_v20_u4_b4, 4}, {"v19_u4_b4", k_v19_u4_b4, 4}, {"v19_u2_b4", k_v19_u2_b4, 2},
     {"v18_u4_b4", k_v18_u4_b4, 4}, {"v18_u4_b3", k_v18_u4_b3, 4}, {"v18_u2_b4", k_v18_u2_b4, 2},
