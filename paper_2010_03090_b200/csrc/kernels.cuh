@@ -8,22 +8,20 @@
 namespace u8v {
 
 constexpr int kThreads = 256;              // 8 warps per CTA
-// K1/K3 (validate.cu): 32-byte lane chunks, one 256-bit LDG each.
+// K1/K3 (validate.cu) and K2 (batch.cu): 32-byte lane chunks, one 256-bit
+// LDG each; a warp step is 4 chunks per lane.
 constexpr int kChunkBytes = 32;
 constexpr int kChunkWords = kChunkBytes / 4;
 constexpr int kU = 4;                      // chunks per lane per step
 constexpr int kStepChunks = 32 * kU;       // 128 chunks = 4 KiB per warp step
-// K2 (batch.cu): 16-byte lane chunks.
-constexpr int kBU = 4;
-constexpr int kBStepChunks = 32 * kBU;     // 128 chunks = 2 KiB per warp step
 
 // error_kind numbering of proj/include/utf8v/verdict.hpp:20-27.
 enum { kHeaderBits = 0, kTooShort = 1, kTooLong = 2, kOverlong = 3, kTooLarge = 4, kSurrogate = 5 };
 
 struct StreamDesc {
-  const uint8_t* base;     // 16-byte aligned view of the stream
+  const uint8_t* base;     // 32-byte aligned view of the stream
   int64_t lo, hi;          // valid bytes [lo, hi) relative to base; others read 0
-  int64_t off16;           // stream byte 0 is base[off16]
+  int64_t off32;           // stream byte 0 is base[off32]
   int64_t L0, L1;          // lanes evaluated: [L0, L1) relative to base
   int64_t c_begin, c_end;  // chunks evaluated: [c_begin, c_end)
   int64_t steps;           // ceil((c_end - c_begin) / kStepChunks)

@@ -275,7 +275,7 @@ StreamDesc make_desc(const uint8_t* p, uint64_t n, uint64_t lane_lo, uint64_t la
   d.base = (const uint8_t*)(up - (uintptr_t)off);
   d.lo = off;
   d.hi = off + (int64_t)n;
-  d.off16 = off;
+  d.off32 = off;
   d.k = u8v_make_consts();
   d.L0 = off + (int64_t)lane_lo;
   d.L1 = off + (int64_t)lane_hi;
@@ -305,7 +305,7 @@ void launch_first_error(const StreamDesc& d, uint64_t n, uint32_t* flag,
     const int64_t blocks = (warps * 32 + kThreads - 1) / kThreads;
     k_validate<true><<<(unsigned)blocks, kThreads, 0, st>>>(d, flag, first_chunk);
   }
-  k_locate<<<1, 32, 0, st>>>(d.base + d.off16, n, d.off16, first_chunk, out_offset, out_kind);
+  k_locate<<<1, 32, 0, st>>>(d.base + d.off32, n, d.off32, first_chunk, out_offset, out_kind);
 }
 
 }  // namespace u8v

@@ -916,6 +916,27 @@ __global__ void __launch_bounds__(256, 4) k_v22b_u4_b4(const uint8_t* base, int6
   body22<4, 2>(base, steps, flag, k);
 }
 
+__global__ void __launch_bounds__(256, 2) k_v19_u8_b2(const uint8_t* base, int64_t steps, int64_t spw,
+                                                      uint32_t* flag, Cfg k) {
+  (void)spw;
+  body19<8>(base, steps, flag, k);
+}
+__global__ void __launch_bounds__(256, 6) k_v19_u2_b6(const uint8_t* base, int64_t steps, int64_t spw,
+                                                      uint32_t* flag, Cfg k) {
+  (void)spw;
+  body19<2>(base, steps, flag, k);
+}
+__global__ void __launch_bounds__(256, 5) k_v19_u2_b5(const uint8_t* base, int64_t steps, int64_t spw,
+                                                      uint32_t* flag, Cfg k) {
+  (void)spw;
+  body19<2>(base, steps, flag, k);
+}
+__global__ void __launch_bounds__(256, 3) k_v19_u4_b3(const uint8_t* base, int64_t steps, int64_t spw,
+                                                      uint32_t* flag, Cfg k) {
+  (void)spw;
+  body19<4>(base, steps, flag, k);
+}
+
 #define KB_KERNEL(V, U, MINB)                                                                  \
   __global__ void __launch_bounds__(256, MINB)                                                 \
       k_v##V##_u##U##_b##MINB(const uint8_t* base, int64_t steps, int64_t spw, uint32_t* flag, \
@@ -983,6 +1004,8 @@ static const Entry kEntries[] = {
     {"v10_u4_b3", k_v10_u4_b3, 4}, {"v10_u4_b4", k_v10_u4_b4, 4}, {"v10_u2_b4", k_v10_u2_b4, 2},
     {"v11_u4_b4", k_v11_u4_b4, 4}, {"v13_u4_b4", k_v13_u4_b4, 4},
     {"v14_u4_b4", k_v14_u4_b4, 4}, {"v15_u4_b4", k_v15_u4_b4, 4}, {"v16_u4_b4", k_v16_u4_b4, 4},
+    {"v19_u8_b2", k_v19_u8_b2, 8}, {"v19_u2_b6", k_v19_u2_b6, 2}, {"v19_u2_b5", k_v19_u2_b5, 2},
+    {"v19_u4_b3", k_v19_u4_b3, 4},
     {"v22a_u4_b4", k_v22a_u4_b4, 4}, {"v22b_u4_b4", k_v22b_u4_b4, 4},
     {"v21_u4_b4", k_v21_u4_b4, 4}, {"v21_u4_b8", k_v21_u4_b8, 4},
     {"v20_u4_b4", k_v20_u4_b4, 4}, {"v19_u4_b4", k_v19_u4_b4, 4}, {"v19_u2_b4", k_v19_u2_b4, 2},
