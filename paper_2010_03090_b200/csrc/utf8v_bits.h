@@ -8,11 +8,11 @@
 // word this form issues ~10 ALU + ~6 FMA instructions against ~15 + ~13 for
 // the SWAR form (tools/kbench.cu: 3592 -> 4476 GB/s on C1).
 //
-// Transpose: four 8x8 bit-matrix transposes (bytes 8j..8j+7, two delta-swap
-// stages each: the 4x4 sub-blocks), a 4x4 byte transpose by PRMT, and a
-// nibble merge that does the third stage's 4x4 block swap.  Shifts are
-// issued as IMAD / IMAD.HI with runtime multipliers (FMA pipe); the logic
-// stays on LOP3.
+// Transpose: a 4x4 byte transpose by PRMT lines up row q of the four 8x8 bit
+// blocks in one register, then three cross-register stages transpose all four
+// blocks at once (2 shifts + 2 LOP3 per register pair and stage: 16 PRMT +
+// 24 LOP3 + 24 IMAD per chunk).  Shifts are issued as IMAD / IMAD.HI with
+// runtime multipliers (FMA pipe); the logic stays on LOP3.
 //
 // Compiled into the sm_100a kernels and, by gcc, into the CPU test helper
 // that checks the transpose and every lane class at every chunk position
@@ -33,68 +33,71 @@ U8V_HD uint32_t u8v_prmt(uint32_t x, uint32_t y, uint32_t s) {
 #endif
 }
 
-// (a & 0x0F0F0F0F) | (c & 0xF0F0F0F0) in one LOP3 (ptxas splits it in two
-// when the mask is an immediate used in both polarities).
-U8V_HD uint32_t u8v_nibsel(uint32_t a, uint32_t c) {
-#if defined(__CUDA_ARCH__)
-  uint32_t d;
-  asm("lop3.b32 %0, %1, 0x0F0F0F0F, %2, 0xE2;" : "=r"(d) : "r"(a), "r"(c));
-  return d;
-#else
-  return (a & 0x0F0F0F0Fu) | (c & 0xF0F0F0F0u);
-#endif
-}
-
 // x << s and x >> s on the FMA pipe (k.one == 1 at run time).
 #define U8V_SHL(x, s, k) u8v_mad((x), (1u << (s)) * (k).one, 0u)
 #define U8V_SHR(x, s, k) u8v_mulhi((x), 1u << (32 - (s)))
 
-// First two stages of the 8x8 bit transpose of bytes 0..3 (a) and 4..7 (b):
-// afterwards each 4x4 sub-block is transposed in place -- a byte c < 4 holds
-// bit c of bytes 0..3 in its low nibble and bit c+4 in its high nibble; b the
-// same for bytes 4..7.  Delta swaps of 7 and 14.
-U8V_HD void u8v_t4x4x2(uint32_t* lo, uint32_t* hi, u8v_consts k) {
-  uint32_t a = *lo, b = *hi, t;
-  t = (a ^ U8V_SHR(a, 7, k)) & 0x00AA00AAu;
-  a ^= t ^ U8V_SHL(t, 7, k);
-  t = (b ^ U8V_SHR(b, 7, k)) & 0x00AA00AAu;
-  b ^= t ^ U8V_SHL(t, 7, k);
-  t = (a ^ U8V_SHR(a, 14, k)) & 0x0000CCCCu;
-  a ^= t ^ U8V_SHL(t, 14, k);
-  t = (b ^ U8V_SHR(b, 14, k)) & 0x0000CCCCu;
-  b ^= t ^ U8V_SHL(t, 14, k);
-  *lo = a;
-  *hi = b;
-}
+// (x & m) | (y & ~m) in one LOP3 with m an immediate (ptxas splits the
+// expression in two when m appears in both polarities).
+#if defined(__CUDA_ARCH__)
+#define U8V_BITSEL(m, x, y)                                                        \
+  ([](uint32_t xx, uint32_t yy) {                                                  \
+    uint32_t d;                                                                    \
+    asm("lop3.b32 %0, %1, " #m ", %2, 0xE2;" : "=r"(d) : "r"(xx), "r"(yy));        \
+    return d;                                                                      \
+  }((x), (y)))
+#else
+#define U8V_BITSEL(m, x, y) ((((uint32_t)(x)) & (uint32_t)(m)) | (((uint32_t)(y)) & ~(uint32_t)(m)))
+#endif
+
+// One stage of the 8x8 bit transpose across a register pair (x = row a,
+// y = row a + s, per byte lane): the bits of x at columns with bit log2(s)
+// set trade places with the bits of y s columns lower.  Two shifts (FMA
+// pipe) and two LOP3 per pair.
+#define U8V_XSTAGE(x, y, s, mhi, mlo, k)                                  \
+  do {                                                                    \
+    const uint32_t _x = (x), _y = (y);                                    \
+    (x) = U8V_BITSEL(mhi, U8V_SHL(_y, s, k), _x);                          \
+    (y) = U8V_BITSEL(mlo, U8V_SHR(_x, s, k), _y);                          \
+  } while (0)
 
 // Planes of a 32-byte chunk w[0..8): p[c] bit i = bit c of byte i.
+// 1. Two 4x4 byte transposes (PRMT) make r[q] = byte q of each 8-byte block
+//    (r[q] byte j = byte 8j+q): row q of the four 8x8 bit blocks, side by side.
+// 2. Three cross-register stages (s = 1, 2, 4) transpose every 8x8 block at
+//    once: afterwards r[c] byte j bit q = bit c of byte 8j+q, i.e. plane c.
 U8V_HD void u8v_planes_k(const uint32_t w[8], uint32_t p[8], u8v_consts k) {
-  uint32_t l0 = w[0], h0 = w[1], l1 = w[2], h1 = w[3], l2 = w[4], h2 = w[5], l3 = w[6], h3 = w[7];
-  u8v_t4x4x2(&l0, &h0, k);
-  u8v_t4x4x2(&l1, &h1, k);
-  u8v_t4x4x2(&l2, &h2, k);
-  u8v_t4x4x2(&l3, &h3, k);
-  // X_c = byte c of l0..l3 (bytes 8j..8j+3 of each block), Y_c = byte c of h0..h3.
-  uint32_t A = u8v_prmt(l0, l1, 0x5140), B = u8v_prmt(l0, l1, 0x7362);
-  uint32_t C = u8v_prmt(l2, l3, 0x5140), D = u8v_prmt(l2, l3, 0x7362);
-  const uint32_t X0 = u8v_prmt(A, C, 0x5410), X1 = u8v_prmt(A, C, 0x7632);
-  const uint32_t X2 = u8v_prmt(B, D, 0x5410), X3 = u8v_prmt(B, D, 0x7632);
-  A = u8v_prmt(h0, h1, 0x5140);
-  B = u8v_prmt(h0, h1, 0x7362);
-  C = u8v_prmt(h2, h3, 0x5140);
-  D = u8v_prmt(h2, h3, 0x7362);
-  const uint32_t Y0 = u8v_prmt(A, C, 0x5410), Y1 = u8v_prmt(A, C, 0x7632);
-  const uint32_t Y2 = u8v_prmt(B, D, 0x5410), Y3 = u8v_prmt(B, D, 0x7632);
-  // Nibble merge (the third stage): plane c byte j = low nibbles of X_c and
-  // Y_c; plane c+4 byte j = their high nibbles.
-  p[0] = u8v_nibsel(X0, U8V_SHL(Y0, 4, k));
-  p[1] = u8v_nibsel(X1, U8V_SHL(Y1, 4, k));
-  p[2] = u8v_nibsel(X2, U8V_SHL(Y2, 4, k));
-  p[3] = u8v_nibsel(X3, U8V_SHL(Y3, 4, k));
-  p[4] = u8v_nibsel(U8V_SHR(X0, 4, k), Y0);
-  p[5] = u8v_nibsel(U8V_SHR(X1, 4, k), Y1);
-  p[6] = u8v_nibsel(U8V_SHR(X2, 4, k), Y2);
-  p[7] = u8v_nibsel(U8V_SHR(X3, 4, k), Y3);
+  // rows 0..3 come from the even words (bytes 8j..8j+3), rows 4..7 from the odd.
+  uint32_t A = u8v_prmt(w[0], w[2], 0x5140), B = u8v_prmt(w[0], w[2], 0x7362);
+  uint32_t C = u8v_prmt(w[4], w[6], 0x5140), D = u8v_prmt(w[4], w[6], 0x7362);
+  uint32_t r0 = u8v_prmt(A, C, 0x5410), r1 = u8v_prmt(A, C, 0x7632);
+  uint32_t r2 = u8v_prmt(B, D, 0x5410), r3 = u8v_prmt(B, D, 0x7632);
+  A = u8v_prmt(w[1], w[3], 0x5140);
+  B = u8v_prmt(w[1], w[3], 0x7362);
+  C = u8v_prmt(w[5], w[7], 0x5140);
+  D = u8v_prmt(w[5], w[7], 0x7362);
+  uint32_t r4 = u8v_prmt(A, C, 0x5410), r5 = u8v_prmt(A, C, 0x7632);
+  uint32_t r6 = u8v_prmt(B, D, 0x5410), r7 = u8v_prmt(B, D, 0x7632);
+  U8V_XSTAGE(r0, r1, 1, 0xAAAAAAAA, 0x55555555, k);
+  U8V_XSTAGE(r2, r3, 1, 0xAAAAAAAA, 0x55555555, k);
+  U8V_XSTAGE(r4, r5, 1, 0xAAAAAAAA, 0x55555555, k);
+  U8V_XSTAGE(r6, r7, 1, 0xAAAAAAAA, 0x55555555, k);
+  U8V_XSTAGE(r0, r2, 2, 0xCCCCCCCC, 0x33333333, k);
+  U8V_XSTAGE(r1, r3, 2, 0xCCCCCCCC, 0x33333333, k);
+  U8V_XSTAGE(r4, r6, 2, 0xCCCCCCCC, 0x33333333, k);
+  U8V_XSTAGE(r5, r7, 2, 0xCCCCCCCC, 0x33333333, k);
+  U8V_XSTAGE(r0, r4, 4, 0xF0F0F0F0, 0x0F0F0F0F, k);
+  U8V_XSTAGE(r1, r5, 4, 0xF0F0F0F0, 0x0F0F0F0F, k);
+  U8V_XSTAGE(r2, r6, 4, 0xF0F0F0F0, 0x0F0F0F0F, k);
+  U8V_XSTAGE(r3, r7, 4, 0xF0F0F0F0, 0x0F0F0F0F, k);
+  p[0] = r0;
+  p[1] = r1;
+  p[2] = r2;
+  p[3] = r3;
+  p[4] = r4;
+  p[5] = r5;
+  p[6] = r6;
+  p[7] = r7;
 }
 
 U8V_HD void u8v_planes(const uint32_t w[8], uint32_t p[8]) { u8v_planes_k(w, p, u8v_make_consts()); }
