@@ -72,22 +72,22 @@ __device__ __forceinline__ uint32_t chunk_hibits(const Chunk& v) {
   return h;
 }
 
-// Error lanes of one chunk (bit i = lane p0 + i flagged; exact, no garbage
-// bits) given the word before it and the word after it: the bit-sliced form
-// of utf8v_bits.h.  kRanged drops lanes outside [L0, L1).
+// Error lanes of one chunk given the word before it and the word after it:
+// the bit-sliced form of utf8v_bits.h.  Unranged (K1/K3 interior): the
+// permuted-order form -- the result is nonzero iff some lane of the chunk is
+// flagged, bit pos(i) = lane p0 + i.  kRanged (edge steps): natural order,
+// bit i = lane p0 + i, lanes outside [L0, L1) dropped.
 // *hi7: plane 7 of the chunk (zero iff all its bytes are ASCII).
 template <bool kRanged>
 __device__ __forceinline__ uint32_t chunk_errors(const Chunk& v, uint32_t prev, uint32_t next,
                                                  u8v_consts k, int64_t p0, int64_t L0, int64_t L1,
                                                  uint32_t* hi7) {
+  if (!kRanged) return u8v_chunk_errors_planes_perm_k(v.w, prev, next, k, hi7);
   uint32_t e = u8v_chunk_errors_planes_k(v.w, prev, next, k, hi7);
-  if (kRanged) {
-    const int64_t a = L0 - p0, b = L1 - p0;  // wanted lanes: bits [a, b)
-    const uint32_t lo = a <= 0 ? 0xFFFFFFFFu : (a >= 32 ? 0u : (0xFFFFFFFFu << a));
-    const uint32_t hi = b >= 32 ? 0xFFFFFFFFu : (b <= 0 ? 0u : (0xFFFFFFFFu >> (32 - b)));
-    e &= lo & hi;
-  }
-  return e;
+  const int64_t a = L0 - p0, b = L1 - p0;  // wanted lanes: bits [a, b)
+  const uint32_t lo = a <= 0 ? 0xFFFFFFFFu : (a >= 32 ? 0u : (0xFFFFFFFFu << a));
+  const uint32_t hi = b >= 32 ? 0xFFFFFFFFu : (b <= 0 ? 0u : (0xFFFFFFFFu >> (32 - b)));
+  return e & lo & hi;
 }
 
 }  // namespace u8v

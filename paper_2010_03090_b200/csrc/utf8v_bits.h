@@ -191,3 +191,70 @@ U8V_HD uint32_t u8v_chunk_errors_planes_bounded_k(const uint32_t w[8], uint32_t 
   const uint32_t rf5 = l3 & (p[3] | (p[2] & (p[1] | p[0])));
   return S | rc | re0 | red | rf0 | rf4 | rf5;
 }
+
+// ---- permuted-order form (K1, K3) -----------------------------------------
+// Without the PRMT row gather the eight words of a chunk already are the
+// rows of four 8x8 bit blocks -- block b = bytes {b, b+4, ..., b+28} -- so the
+// three cross-register stages alone give the planes, in the order
+//   pos(i) = 8 * (i mod 4) + (i div 4)       (byte i = 4q + b  ->  bit 8b + q).
+// K1/K3 only need "some lane of the chunk is flagged", so only the shifted
+// planes must follow the permutation:
+//   look-back by k (k = 1..3):  byte i-k is at pos(i) - 8k when b >= k, else at
+//     pos(i) + 31 - 8k (word q-1), or in the previous chunk when q = 0:
+//     lag_k(P) = (P << 8k) + ((P >> (31-8k)) & M_k | carry_k),
+//     M_k = bits [0, 8k) without {0, 8, 16}, carry_k = the flags of the
+//     previous word's bytes 4-k..3 landing on bits 0, 8, 16: one IMAD.HI of
+//     the bit-7 flag word, (f >> (39 - 8k)).
+//   lookahead (byte i+1): pos(i) + 8 when b <= 2, else pos(i) - 23 (word
+//     q+1), or the next chunk's byte 0 for i = 31: a funnel shift by 8 of
+//     ((P >> 1) & 0x7F | next-byte bit << 7 : P).
+// 16 PRMT fewer per chunk than u8v_chunk_errors_planes_k; same lane flags
+// (tests/test_swar.py maps the bits back and compares).
+U8V_HD uint32_t u8v_perm_pos(unsigned i) { return 8u * (i & 3u) + (i >> 2); }
+
+U8V_HD uint32_t u8v_chunk_errors_planes_perm_k(const uint32_t w[8], uint32_t prev, uint32_t next,
+                                               u8v_consts k, uint32_t* hi7) {
+  uint32_t r0 = w[0], r1 = w[1], r2 = w[2], r3 = w[3], r4 = w[4], r5 = w[5], r6 = w[6], r7 = w[7];
+  U8V_XSTAGE(r0, r1, 1, 0xAAAAAAAA, 0x55555555, k);
+  U8V_XSTAGE(r2, r3, 1, 0xAAAAAAAA, 0x55555555, k);
+  U8V_XSTAGE(r4, r5, 1, 0xAAAAAAAA, 0x55555555, k);
+  U8V_XSTAGE(r6, r7, 1, 0xAAAAAAAA, 0x55555555, k);
+  U8V_XSTAGE(r0, r2, 2, 0xCCCCCCCC, 0x33333333, k);
+  U8V_XSTAGE(r1, r3, 2, 0xCCCCCCCC, 0x33333333, k);
+  U8V_XSTAGE(r4, r6, 2, 0xCCCCCCCC, 0x33333333, k);
+  U8V_XSTAGE(r5, r7, 2, 0xCCCCCCCC, 0x33333333, k);
+  U8V_XSTAGE(r0, r4, 4, 0xF0F0F0F0, 0x0F0F0F0F, k);
+  U8V_XSTAGE(r1, r5, 4, 0xF0F0F0F0, 0x0F0F0F0F, k);
+  U8V_XSTAGE(r2, r6, 4, 0xF0F0F0F0, 0x0F0F0F0F, k);
+  U8V_XSTAGE(r3, r7, 4, 0xF0F0F0F0, 0x0F0F0F0F, k);
+  const uint32_t p0 = r0, p1 = r1, p2 = r2, p3 = r3, p4 = r4, p5 = r5, p6 = r6, p7 = r7;
+  *hi7 = p7;
+  const uint32_t l1 = p7 & p6;  // >= C0
+  const uint32_t l2 = l1 & p5;  // >= E0
+  const uint32_t l3 = l2 & p4;  // >= F0
+  // Bit-7 flags of the previous word's bytes.
+  const uint32_t q1 = prev & U8V_SHL(prev, 1, k) & U8V_B7;
+  const uint32_t q2 = q1 & U8V_SHL(prev, 2, k);
+  const uint32_t q3 = q2 & U8V_SHL(prev, 3, k);
+  const uint32_t t1 = U8V_BITSEL(0x000000FE, U8V_SHR(l1, 23, k), U8V_SHR(q1, 31, k));
+  const uint32_t t2 = U8V_BITSEL(0x0000FEFE, U8V_SHR(l2, 15, k), U8V_SHR(q2, 23, k));
+  const uint32_t t3 = U8V_BITSEL(0x00FEFEFE, U8V_SHR(l3, 7, k), U8V_SHR(q3, 15, k));
+  const uint32_t e1 = u8v_mad(l1, 0x100u * k.one, t1);
+  const uint32_t e2 = u8v_mad(l2, 0x10000u * k.one, t2);
+  const uint32_t e3 = u8v_mad(l3, 0x1000000u * k.one, t3);
+  const uint32_t S = (p7 & ~p6) ^ (e1 | e2 | e3);
+  // Follower bits 5 and 4 at the lead's position.
+  const uint32_t nx5 = U8V_SHL(next, 2, k);  // bit 7 = next byte 0's bit 5
+  const uint32_t nx4 = U8V_SHL(next, 3, k);  // bit 7 = next byte 0's bit 4
+  const uint32_t n5 = u8v_fsr(p5, U8V_BITSEL(0x7F, U8V_SHR(p5, 1, k), nx5), 8);
+  const uint32_t n4 = u8v_fsr(p4, U8V_BITSEL(0x7F, U8V_SHR(p4, 1, k), nx4), 8);
+  const uint32_t z321 = ~(p3 | p2 | p1);
+  const uint32_t rc = l1 & ~p5 & ~p4 & z321;
+  const uint32_t ee = l2 & ~p4;
+  const uint32_t re0 = ee & z321 & ~p0 & ~n5;
+  const uint32_t red = ee & p3 & p2 & ~p1 & p0 & n5;
+  const uint32_t rf0 = l3 & z321 & ~p0 & ~n5 & ~n4;
+  const uint32_t rf4 = l3 & ~p3 & p2 & ~p1 & ~p0 & (n5 | n4);
+  const uint32_t rf5 = l3 & (p3 | (p2 & (p1 | p0)));
+  return S | rc | re0 | red | rf0 | rf4 | rf5;
+}

@@ -405,3 +405,54 @@ int swar_stream_split(const uint8_t* p, size_t n, const uint64_t* cuts, size_t n
   err |= u8v_stream_edge(carry, 0, 0, 0, 1);
   return err == 0;
 }
+
+/* Permuted-order plane form: error bit pos(i) == natural form's bit i, on
+ * random chunks and on every lane class at every position. */
+static uint64_t perm_compare(const uint8_t buf[40]) {
+  uint32_t w[8], prev, next, h7a, h7b;
+  memcpy(&prev, buf, 4);
+  memcpy(w, buf + 4, 32);
+  memcpy(&next, buf + 36, 4);
+  const u8v_consts k = u8v_make_consts();
+  const uint32_t nat = u8v_chunk_errors_planes_k(w, prev, next, k, &h7a);
+  const uint32_t per = u8v_chunk_errors_planes_perm_k(w, prev, next, k, &h7b);
+  uint64_t bad = 0;
+  for (unsigned i = 0; i < 32; ++i) {
+    bad += ((nat >> i) & 1u) != ((per >> u8v_perm_pos(i)) & 1u);
+    bad += ((h7a >> i) & 1u) != ((h7b >> u8v_perm_pos(i)) & 1u);
+  }
+  return bad;
+}
+
+uint64_t swar_bits_perm_check(uint64_t seed, uint64_t fuzz) {
+  static const uint8_t lo_c0[2] = {0x41, 0xC2}, lo_e0[2] = {0x85, 0xE1}, lo_f0[2] = {0x9F, 0xF3};
+  static const uint8_t nb[4] = {0x80, 0x90, 0xA0, 0xB0};
+  uint8_t buf[40];
+  uint64_t s = seed, bad = 0;
+  for (int pos = 0; pos < 32; ++pos) {
+    const int i = 4 + pos;
+    for (int cls = 0; cls < 8192; ++cls) {
+      for (int q = 0; q < 40; q += 8) {
+        const uint64_t r = bits_rng(&s);
+        memcpy(buf + q, &r, 8);
+      }
+      buf[i - 3] = lo_f0[(cls >> 0) & 1];
+      buf[i - 2] = lo_e0[(cls >> 1) & 1];
+      buf[i - 1] = lo_c0[(cls >> 2) & 1];
+      buf[i] = (uint8_t)(cls >> 3);
+      buf[i + 1] = nb[(cls >> 11) & 3];
+      bad += perm_compare(buf);
+    }
+  }
+  static const uint8_t hot[] = {0x00, 0x41, 0x80, 0x8F, 0x90, 0x9F, 0xA0, 0xBF, 0xC0, 0xC1,
+                                0xC2, 0xDF, 0xE0, 0xED, 0xEF, 0xF0, 0xF4, 0xF5, 0xFF};
+  for (uint64_t t = 0; t < fuzz; ++t) {
+    const uint64_t mode = bits_rng(&s);
+    for (int q = 0; q < 40; ++q) {
+      const uint64_t r = bits_rng(&s);
+      buf[q] = (mode & 1) ? (uint8_t)r : hot[r % sizeof hot];
+    }
+    bad += perm_compare(buf);
+  }
+  return bad;
+}

@@ -141,3 +141,13 @@ def test_stream_stitching_equals_whole_stream():
                         assert bool(got) == bool(want), (buf.tolist(), cut)
                         checked += 1
     assert checked > 5000
+
+
+def test_bit_sliced_permuted_form_equals_natural_form():
+    """K1's permuted-order plane form (no PRMT gather) flags exactly the lanes
+    of the natural-order form, bit pos(i) <-> lane i, on every lane class at
+    every chunk position plus fuzz."""
+    S = nat.swar()
+    S.swar_bits_perm_check.restype = C.c_uint64
+    S.swar_bits_perm_check.argtypes = [C.c_uint64, C.c_uint64]
+    assert S.swar_bits_perm_check(13, 300000) == 0
