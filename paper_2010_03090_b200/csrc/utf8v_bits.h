@@ -108,6 +108,29 @@ U8V_HD uint32_t u8v_movemask_top(uint32_t x, u8v_consts k) {
   return u8v_mad(x & U8V_B7, 0x00204081u * k.one, 0u);
 }
 
+// The rare lead pairs on planes (utf8v_swar.h u8v_rare_key restated), lead
+// lanes l1/l2/l3 (>= C0/E0/F0), the lead's low bits p5..p0, the follower's
+// bits 5 and 4 (n5, n4; meaningful when the follower is a continuation, else
+// S fires anyway).  Factored so every line is one 3-input LOP3:
+//   C0/C1  l1 & ~p5 & ~p4 & lo=0|1               (z = ~(p3|p2|p1))
+//   E0/F0  z & ~p0 & ~n5 & l2 & ~(p4 & n4)       (E0: b<A0; F0: b<90)
+//   ED     l2 & ~p4 & (p3 & p2 & ~p1) & p0 & n5  (b >= A0)
+//   F4     l3 & (~p3 & p2 & ~p1) & ~p0 & (n5|n4) (b >= 90)
+//   F5..FF l3 & (p3 | p2 & (p1 | p0))
+U8V_HD uint32_t u8v_rare_planes(uint32_t l1, uint32_t l2, uint32_t l3, uint32_t p5, uint32_t p4,
+                                uint32_t p3, uint32_t p2, uint32_t p1, uint32_t p0, uint32_t n5,
+                                uint32_t n4) {
+  const uint32_t z = ~(p3 | p2 | p1);
+  const uint32_t rc = (l1 & ~p5 & ~p4) & z;
+  const uint32_t x = z & ~p0 & ~n5;
+  const uint32_t y = l2 & ~(p4 & n4);
+  const uint32_t ed = (p3 & p2 & ~p1) & (p0 & n5);
+  const uint32_t red = (l2 & ~p4) & ed;
+  const uint32_t f4 = (~p3 & p2 & ~p1) & (~p0 & (n5 | n4));
+  const uint32_t rf5 = l3 & (p3 | (p2 & (p1 | p0)));
+  return rc | (x & y) | red | (l3 & f4) | rf5;
+}
+
 // Error plane (bit i = lane i of the chunk flagged) of one chunk.
 //   prev: the word before the chunk (bytes -4..-1), next: the word after it.
 // Lane i: S_i = cont(x_i) ^ (x_{i-1}>=C0 | x_{i-2}>=E0 | x_{i-3}>=F0), and the
@@ -134,15 +157,7 @@ U8V_HD uint32_t u8v_chunk_errors_planes_k(const uint32_t w[8], uint32_t prev, ui
   const uint32_t n5 = u8v_fsr(p[5], next >> 5, 1);
   const uint32_t n4 = u8v_fsr(p[4], next >> 4, 1);
   // Rare pairs (utf8v_swar.h u8v_rare_key, restated on planes).
-  const uint32_t z321 = ~(p[3] | p[2] | p[1]);                         // low nibble 0 or 1
-  const uint32_t rc = l1 & ~p[5] & ~p[4] & z321;                        // C0, C1
-  const uint32_t ee = l2 & ~p[4];                                       // E0..EF
-  const uint32_t re0 = ee & z321 & ~p[0] & ~n5;                         // E0, b < A0
-  const uint32_t red = ee & p[3] & p[2] & ~p[1] & p[0] & n5;            // ED, b >= A0
-  const uint32_t rf0 = l3 & z321 & ~p[0] & ~n5 & ~n4;                   // F0, b < 90
-  const uint32_t rf4 = l3 & ~p[3] & p[2] & ~p[1] & ~p[0] & (n5 | n4);   // F4, b >= 90
-  const uint32_t rf5 = l3 & (p[3] | (p[2] & (p[1] | p[0])));            // F5..FF
-  return S | rc | re0 | red | rf0 | rf4 | rf5;
+  return S | u8v_rare_planes(l1, l2, l3, p[5], p[4], p[3], p[2], p[1], p[0], n5, n4);
 }
 
 U8V_HD uint32_t u8v_chunk_errors_planes(const uint32_t w[8], uint32_t prev, uint32_t next) {
@@ -181,15 +196,7 @@ U8V_HD uint32_t u8v_chunk_errors_planes_bounded_k(const uint32_t w[8], uint32_t 
   *end_err = B & (e1 | (e2 & ~B1) | (e3 & ~B1 & ~B2));
   const uint32_t n5 = u8v_fsr(p[5], next >> 5, 1);
   const uint32_t n4 = u8v_fsr(p[4], next >> 4, 1);
-  const uint32_t z321 = ~(p[3] | p[2] | p[1]);
-  const uint32_t rc = l1 & ~p[5] & ~p[4] & z321;
-  const uint32_t ee = l2 & ~p[4];
-  const uint32_t re0 = ee & z321 & ~p[0] & ~n5;
-  const uint32_t red = ee & p[3] & p[2] & ~p[1] & p[0] & n5;
-  const uint32_t rf0 = l3 & z321 & ~p[0] & ~n5 & ~n4;
-  const uint32_t rf4 = l3 & ~p[3] & p[2] & ~p[1] & ~p[0] & (n5 | n4);
-  const uint32_t rf5 = l3 & (p[3] | (p[2] & (p[1] | p[0])));
-  return S | rc | re0 | red | rf0 | rf4 | rf5;
+  return S | u8v_rare_planes(l1, l2, l3, p[5], p[4], p[3], p[2], p[1], p[0], n5, n4);
 }
 
 // ---- permuted-order form (K1, K3) -----------------------------------------
@@ -248,13 +255,5 @@ U8V_HD uint32_t u8v_chunk_errors_planes_perm_k(const uint32_t w[8], uint32_t pre
   const uint32_t nx4 = U8V_SHL(next, 3, k);  // bit 7 = next byte 0's bit 4
   const uint32_t n5 = u8v_fsr(p5, U8V_BITSEL(0x7F, U8V_SHR(p5, 1, k), nx5), 8);
   const uint32_t n4 = u8v_fsr(p4, U8V_BITSEL(0x7F, U8V_SHR(p4, 1, k), nx4), 8);
-  const uint32_t z321 = ~(p3 | p2 | p1);
-  const uint32_t rc = l1 & ~p5 & ~p4 & z321;
-  const uint32_t ee = l2 & ~p4;
-  const uint32_t re0 = ee & z321 & ~p0 & ~n5;
-  const uint32_t red = ee & p3 & p2 & ~p1 & p0 & n5;
-  const uint32_t rf0 = l3 & z321 & ~p0 & ~n5 & ~n4;
-  const uint32_t rf4 = l3 & ~p3 & p2 & ~p1 & ~p0 & (n5 | n4);
-  const uint32_t rf5 = l3 & (p3 | (p2 & (p1 | p0)));
-  return S | rc | re0 | red | rf0 | rf4 | rf5;
+  return S | u8v_rare_planes(l1, l2, l3, p5, p4, p3, p2, p1, p0, n5, n4);
 }

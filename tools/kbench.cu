@@ -937,6 +937,50 @@ __global__ void __launch_bounds__(256, 3) k_v19_u4_b3(const uint8_t* base, int64
   body19<4>(base, steps, flag, k);
 }
 
+// V23: V19 (grid-stride, correct halo/lookahead) with the permuted-order
+// planes (production K1's chunk form), for occupancy / unroll sweeps.
+template <int U>
+__device__ __forceinline__ void body23(const uint8_t* base, int64_t steps, uint32_t* flag, const Cfg& k) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  u8v_consts kk;
+  kk.one = k.one; kk.m256 = k.m256; kk.mshr4 = k.mshr4;
+  uint32_t acc = 0;
+  for (int64_t step = warp; step < steps; step += nwarps) {
+    const uint8_t* sp = base + step * (int64_t)(U * 1024);
+    uint32_t v[U][8];
+#pragma unroll
+    for (int i = 0; i < U; ++i) ldg_chunk(v[i], sp + (lane + 32 * i) * 32);
+    uint32_t carry_word = 0, nsw = 0;
+    if (lane == 31 && step > 0) carry_word = __ldg(reinterpret_cast<const uint32_t*>(sp - 4));
+    if (lane == 0 && step + 1 < steps) nsw = __ldg(reinterpret_cast<const uint32_t*>(sp + U * 1024));
+#pragma unroll
+    for (int i = 0; i < U; ++i) {
+      const uint32_t supply = lane == 31 ? (i == 0 ? carry_word : v[i - 1][7]) : v[i][7];
+      const uint32_t prev = __shfl_sync(0xFFFFFFFFu, supply, (lane + 31) & 31);
+      const uint32_t dn = lane == 0 ? (i + 1 < U ? v[i + 1][0] : nsw) : v[i][0];
+      const uint32_t nextw = __shfl_sync(0xFFFFFFFFu, dn, (lane + 1) & 31);
+      uint32_t hi;
+      acc |= u8v_chunk_errors_planes_perm_k(v[i], prev, nextw, kk, &hi);
+    }
+  }
+  const unsigned any = __reduce_or_sync(0xFFFFFFFFu, acc);
+  if (lane == 0 && any) atomicOr(flag, 1u);
+}
+#define KB_KERNEL23(U, MINB)                                                                     \
+  __global__ void __launch_bounds__(256, MINB)                                                 \
+      k_v23_u##U##_b##MINB(const uint8_t* base, int64_t steps, int64_t spw, uint32_t* flag, Cfg k) { \
+    (void)spw;                                                                                 \
+    body23<U>(base, steps, flag, k);                                                           \
+  }
+KB_KERNEL23(4, 4)
+KB_KERNEL23(4, 3)
+KB_KERNEL23(8, 2)
+KB_KERNEL23(2, 5)
+KB_KERNEL23(2, 4)
+KB_KERNEL23(4, 5)
+
 #define KB_KERNEL(V, U, MINB)                                                                  \
   __global__ void __launch_bounds__(256, MINB)                                                 \
       k_v##V##_u##U##_b##MINB(const uint8_t* base, int64_t steps, int64_t spw, uint32_t* flag, \
@@ -1004,6 +1048,8 @@ static const Entry kEntries[] = {
     {"v10_u4_b3", k_v10_u4_b3, 4}, {"v10_u4_b4", k_v10_u4_b4, 4}, {"v10_u2_b4", k_v10_u2_b4, 2},
     {"v11_u4_b4", k_v11_u4_b4, 4}, {"v13_u4_b4", k_v13_u4_b4, 4},
     {"v14_u4_b4", k_v14_u4_b4, 4}, {"v15_u4_b4", k_v15_u4_b4, 4}, {"v16_u4_b4", k_v16_u4_b4, 4},
+    {"v23_u4_b4", k_v23_u4_b4, 4}, {"v23_u4_b3", k_v23_u4_b3, 4}, {"v23_u8_b2", k_v23_u8_b2, 8},
+    {"v23_u2_b5", k_v23_u2_b5, 2}, {"v23_u2_b4", k_v23_u2_b4, 2}, {"v23_u4_b5", k_v23_u4_b5, 4},
     {"v19_u8_b2", k_v19_u8_b2, 8}, {"v19_u2_b6", k_v19_u2_b6, 2}, {"v19_u2_b5", k_v19_u2_b5, 2},
     {"v19_u4_b3", k_v19_u4_b3, 4},
     {"v22a_u4_b4", k_v22a_u4_b4, 4}, {"v22b_u4_b4", k_v22b_u4_b4, 4},
