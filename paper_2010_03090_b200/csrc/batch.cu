@@ -93,19 +93,20 @@ __device__ __forceinline__ void mark_invalid(const BatchDesc& d, int64_t r_from,
 
 // Out-of-line, only for chunks with a flagged lane: the record of every
 // flagged lane, and the record ending at every flagged record start (its end
-// check), is marked invalid.  err / end: lane bits of chunk c.
+// check), is marked invalid.  err / end: lane bits of chunk c in the permuted
+// plane order of utf8v_bits.h (bit pos(i) = byte i).
 __device__ __noinline__ void attribute_chunk(const BatchDesc& d, int64_t c, uint32_t err,
                                              uint32_t end, int64_t r_from) {
   const int64_t q0 = c * kChunkBytes;
   while (err) {
     const int i = __ffs(err) - 1;
     err &= err - 1;
-    mark_invalid(d, r_from, q0 + i);
+    mark_invalid(d, r_from, q0 + u8v_perm_byte((unsigned)i));
   }
   while (end) {
     const int i = __ffs(end) - 1;
     end &= end - 1;
-    mark_invalid(d, r_from, q0 + i - 1);
+    mark_invalid(d, r_from, q0 + u8v_perm_byte((unsigned)i) - 1);
   }
 }
 
@@ -183,8 +184,11 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
           const int64_t c = ob >> 5;  // chunk of the start (base coords)
           const int li = (int)(c - cstep);
           const int bit = (int)(ob & 31);
-          if (li >= 0) atomicOr(&m[li], 1ull << (bit + 4));
-          if (bit >= 30 && li + 1 < kStepChunks) atomicOr(&m[li + 1], 1ull << (bit - 28));
+          // Low word: the chunk's record-start plane in permuted order; high
+          // word of the next chunk: starts at its bytes -1 / -2 (bits 31 / 23).
+          if (li >= 0) atomicOr(&m[li], 1ull << u8v_perm_pos((unsigned)bit));
+          if (bit >= 30 && li + 1 < kStepChunks)
+            atomicOr(&m[li + 1], 1ull << (bit == 31 ? 63 : 55));
         }
         // The next step's r0: the last record starting at or before nhs.
         const unsigned le = __ballot_sync(0xFFFFFFFFu, ob <= nhs);
@@ -219,15 +223,16 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
       if (all_ascii) {
         u8v_carry cr = u8v_carry_of(prev);
         err = u8v_ascii_word_errors(v[i].w[0], &cr) & U8V_B7;
-        if (err) err = u8v_chunk_errors_planes_k(v[i].w, prev, next, d.k, &hi7);  // exact lanes
+        if (err) err = u8v_chunk_errors_planes_perm_k(v[i].w, prev, next, d.k, &hi7);  // exact lanes
       } else if (single) {
-        err = u8v_chunk_errors_planes_k(v[i].w, prev, next, d.k, &hi7);
+        err = u8v_chunk_errors_planes_perm_k(v[i].w, prev, next, d.k, &hi7);
       } else {
         // Every chunk of a step holding record starts takes the bounded form
         // (uniform control flow; a zero mask gives the plain flags).
         const unsigned long long mask = m[lane + 32 * i];
         m[lane + 32 * i] = 0;
-        err = u8v_chunk_errors_planes_bounded_k(v[i].w, prev, next, d.k, mask, &end, &hi7);
+        err = u8v_chunk_errors_planes_perm_bounded_k(v[i].w, prev, next, d.k, (uint32_t)mask,
+                                                     (uint32_t)(mask >> 32), &end, &hi7);
       }
       h7 |= hi7;
       if (err | end) attribute_chunk(d, c, err, end, r0);

@@ -456,3 +456,38 @@ uint64_t swar_bits_perm_check(uint64_t seed, uint64_t fuzz) {
   }
   return bad;
 }
+
+/* Permuted bounded form vs natural bounded form (errors and end checks),
+ * random chunks and random record-start masks. */
+uint64_t swar_bits_perm_bounded_check(uint64_t seed, uint64_t trials) {
+  uint64_t s = seed, bad = 0;
+  const u8v_consts k = u8v_make_consts();
+  static const uint8_t hot[] = {0x00, 0x41, 0x80, 0x8F, 0x90, 0x9F, 0xA0, 0xBF, 0xC0, 0xC1,
+                                0xC2, 0xDF, 0xE0, 0xED, 0xEF, 0xF0, 0xF4, 0xF5, 0xFF};
+  for (uint64_t t = 0; t < trials; ++t) {
+    uint8_t buf[40];
+    const uint64_t mode = bits_rng(&s);
+    for (int q = 0; q < 40; ++q) {
+      const uint64_t r = bits_rng(&s);
+      buf[q] = (mode & 1) ? (uint8_t)r : hot[r % sizeof hot];
+    }
+    uint64_t bnd = bits_rng(&s) & bits_rng(&s) & ((1ull << 36) - 1);
+    if (mode & 2) bnd &= bits_rng(&s);
+    uint32_t w[8], prev, next, e_nat, e_per, h7a, h7b;
+    memcpy(&prev, buf, 4);
+    memcpy(w, buf + 4, 32);
+    memcpy(&next, buf + 36, 4);
+    const uint32_t err_nat = u8v_chunk_errors_planes_bounded_k(w, prev, next, k, bnd, &e_nat, &h7a);
+    uint32_t B = 0;
+    for (unsigned i = 0; i < 32; ++i)
+      if ((bnd >> (i + 4)) & 1) B |= 1u << u8v_perm_pos(i);
+    /* starts at bytes -1 / -2 (natural mask bits 3 / 2) -> pre bits 31 / 23 */
+    const uint32_t pre2 = (uint32_t)((bnd >> 3) & 1) << 31 | (uint32_t)((bnd >> 2) & 1) << 23;
+    const uint32_t err_per = u8v_chunk_errors_planes_perm_bounded_k(w, prev, next, k, B, pre2, &e_per, &h7b);
+    for (unsigned i = 0; i < 32; ++i) {
+      bad += ((err_nat >> i) & 1u) != ((err_per >> u8v_perm_pos(i)) & 1u);
+      bad += ((e_nat >> i) & 1u) != ((e_per >> u8v_perm_pos(i)) & 1u);
+    }
+  }
+  return bad;
+}

@@ -151,3 +151,13 @@ def test_bit_sliced_permuted_form_equals_natural_form():
     S.swar_bits_perm_check.restype = C.c_uint64
     S.swar_bits_perm_check.argtypes = [C.c_uint64, C.c_uint64]
     assert S.swar_bits_perm_check(13, 300000) == 0
+
+
+def test_bit_sliced_permuted_bounded_form_equals_natural_bounded_form():
+    """K2's permuted record-bounded plane form (record-start plane and the
+    starts just before the chunk in permuted layout) flags the same lanes and
+    end checks as the natural bounded form."""
+    S = nat.swar()
+    S.swar_bits_perm_bounded_check.restype = C.c_uint64
+    S.swar_bits_perm_bounded_check.argtypes = [C.c_uint64, C.c_uint64]
+    assert S.swar_bits_perm_bounded_check(17, 300000) == 0
