@@ -49,14 +49,24 @@ struct BatchDesc {
 
 constexpr int kWarpsPerCta = kThreads / 32;
 
+// What the record lookups need, passed by value: the out-of-line
+// attribution taking the whole descriptor by reference would pin it in local
+// memory and turn every offset lookup of the hot window loop into an LDL.
+struct RecView {
+  const uint64_t* offsets;
+  uint8_t* verdicts;
+  int64_t off32;
+  int64_t n_records;
+};
+
 // Offset of record start r in base coordinates (r > n_records: +inf).
-__device__ __forceinline__ int64_t rec_start(const BatchDesc& d, int64_t r) {
+__device__ __forceinline__ int64_t rec_start(const RecView& d, int64_t r) {
   return r <= d.n_records ? (int64_t)__ldg(d.offsets + r) + d.off32 : INT64_MAX;
 }
 
 // Warp-cooperative: the largest record r in [0, n_records-1] with
 // start(r) <= pos (0 when pos precedes every record).  32-ary search.
-__device__ int64_t find_record(const BatchDesc& d, int64_t pos) {
+__device__ int64_t find_record(const RecView& d, int64_t pos) {
   const int lane = threadIdx.x & 31;
   int64_t a = 0, b = d.n_records;  // answer index in [a, b], start(a) <= pos
   if (rec_start(d, 0) > pos) return 0;
@@ -80,12 +90,12 @@ __device__ int64_t find_record(const BatchDesc& d, int64_t pos) {
 
 // Record holding byte q (base coords), scanning forward from record r
 // (start(r) <= q).  n_records when q is past the last record.
-__device__ int64_t record_of(const BatchDesc& d, int64_t r, int64_t q) {
+__device__ int64_t record_of(const RecView& d, int64_t r, int64_t q) {
   while (r < d.n_records && rec_start(d, r + 1) <= q) ++r;
   return r < d.n_records ? r : d.n_records;
 }
 
-__device__ __forceinline__ void mark_invalid(const BatchDesc& d, int64_t r_from, int64_t q) {
+__device__ __forceinline__ void mark_invalid(const RecView& d, int64_t r_from, int64_t q) {
   if (q < rec_start(d, 0)) return;
   const int64_t r = record_of(d, r_from, q);
   if (r < d.n_records) d.verdicts[r] = 0;
@@ -95,8 +105,8 @@ __device__ __forceinline__ void mark_invalid(const BatchDesc& d, int64_t r_from,
 // flagged lane, and the record ending at every flagged record start (its end
 // check), is marked invalid.  err / end: lane bits of chunk c in the permuted
 // plane order of utf8v_bits.h (bit pos(i) = byte i).
-__device__ __noinline__ void attribute_chunk(const BatchDesc& d, int64_t c, uint32_t err,
-                                             uint32_t end, int64_t r_from) {
+__device__ __noinline__ void attribute_chunk(RecView d, int64_t c, uint32_t err, uint32_t end,
+                                             int64_t r_from) {
   const int64_t q0 = c * kChunkBytes;
   while (err) {
     const int i = __ffs(err) - 1;
@@ -119,6 +129,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
   // The byte range comes from the offsets themselves (read here, so the
   // launch needs no host round trip).  Malformed offsets are clamped to the
   // data: the kernel never reads outside [0, n).
+  const RecView rv{d.offsets, d.verdicts, d.off32, d.n_records};
   d.lo = d.off32 + (int64_t)__ldg(d.offsets);
   d.hi = d.off32 + (int64_t)__ldg(d.offsets + d.n_records);
   if (d.hi > d.off32 + d.n_bytes) d.hi = d.off32 + d.n_bytes;
@@ -145,7 +156,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
     carry_word = ld_word_masked(d.base, cstep * kChunkBytes - 4, d.lo, d.hi);
   // r0: the record holding byte hs = step start - 2, the first byte whose
   // record matters to the step (look-back of its first lanes).
-  int64_t r0 = find_record(d, cstep * kChunkBytes - 2);
+  int64_t r0 = find_record(rv, cstep * kChunkBytes - 2);
   bool was_ascii = true;
 
   for (; step < step_end; ++step) {
@@ -172,9 +183,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
     }
 
     // Record starts in [hs, se): the window of the 32 records from r0.
-    int64_t ob = rec_start(d, r0 + lane);
+    int64_t ob = rec_start(rv, r0 + lane);
     unsigned below = __ballot_sync(0xFFFFFFFFu, ob < se);
-    const bool single = below == 1u && rec_start(d, r0) < hs;
+    const bool single = below == 1u && rec_start(rv, r0) < hs;
     int64_t r_next = r0;
     if (!single) {
       __syncwarp();  // the previous step's readers have cleared their masks
@@ -195,7 +206,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
         if (le != 0u) r_next = r + (31 - __clz(le));
         if (below != 0xFFFFFFFFu) break;
         r += 32;  // more than 31 starts in this step: next window
-        ob = rec_start(d, r + lane);
+        ob = rec_start(rv, r + lane);
         below = __ballot_sync(0xFFFFFFFFu, ob < se);
         if (below == 0u) break;
       }
@@ -235,7 +246,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
                                                      (uint32_t)(mask >> 32), &end, &hi7);
       }
       h7 |= hi7;
-      if (err | end) attribute_chunk(d, c, err, end, r0);
+      if (err | end) attribute_chunk(rv, c, err, end, r0);
     }
     was_ascii = all_ascii || __all_sync(0xFFFFFFFFu, h7 == 0);
     if (lane == 31) carry_word = v[kU - 1].w[kChunkWords - 1];
