@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
     // Record starts in [hs, se): the window of the 32 records from r0.
     int64_t ob = rec_start(rv, r0 + lane);
     unsigned below = __ballot_sync(0xFFFFFFFFu, ob < se);
-    const bool single = below == 1u && rec_start(rv, r0) < hs;
+    const bool single = below == 1u && __shfl_sync(0xFFFFFFFFu, ob, 0) < hs;  // ob(0) = start(r0)
     int64_t r_next = r0;
     if (!single) {
       __syncwarp();  // the previous step's readers have cleared their masks
