@@ -11,7 +11,7 @@ every rank validates 1 GiB per step; `value` is the box aggregate.
 
 `e2e` repeats the metric through the public C-ABI with a HOST (pinned)
 buffer: utf8v_cuda_validate(host_ptr, n, 0, &ok), which streams the bytes
-over PCIe in 32 MiB pieces and validates each as it lands; every step
+over PCIe in pieces (n/8, 2..32 MiB) and validates each as it lands; every step
 includes the 1 GiB H2D copy and the 4-byte verdict read back.
 
 `--impl reference` times the unmodified reference CPU implementation
@@ -345,7 +345,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         for _ in range(es):
             _lib.check(lib.utf8v_cuda_validate(hp, n_local, 0, C.byref(ok)))
         et = time.perf_counter() - t0
-        path = "utf8v_cuda_validate(pinned host ptr): 32 MiB H2D pieces overlapped with K1"
+        path = "utf8v_cuda_validate(pinned host ptr): H2D pieces (32 MiB at 1 GiB) overlapped with K1"
     else:
         # Every rank: its pinned host shard -> utf8v_cuda_validate_lanes (H2D +
         # K1) -> 4-byte NCCL allreduce(MAX) -> verdict (sharding.py).
@@ -398,7 +398,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             "data": "synthetic (seeded splitmix64 generator, DESIGN.md 'Synthetic inputs')",
             "config": {"workload": workload, "bytes_per_gpu": per, "bytes_total": per * world,
                        "l2": "input (>=1 GiB) larger than the 126 MB L2; no flush needed",
-                       "parallelism": f"dp{world}: byte-range shards with 3-byte halo"
+                       "parallelism": f"dp{world}: byte-range shards (<=16-byte look-back head, 1-byte tail)"
                                       + (" + 1-word NCCL allreduce(MAX) per step" if world > 1 else "")},
             "per_gpu_GBps": per_gpu, "verdict_valid": verdict_ok,
             "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks,

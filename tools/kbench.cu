@@ -981,6 +981,70 @@ KB_KERNEL23(2, 5)
 KB_KERNEL23(2, 4)
 KB_KERNEL23(4, 5)
 
+// V24: V23 (grid-stride, permuted planes) with rolling reload: each chunk
+// slot is refilled with the same chunk of this warp's next step as soon as
+// it is consumed; lane 31's last word is kept for the next chunk's halo.
+template <int U>
+__device__ __forceinline__ void body24(const uint8_t* base, int64_t steps, uint32_t* flag, const Cfg& k) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  u8v_consts kk;
+  kk.one = k.one; kk.m256 = k.m256; kk.mshr4 = k.mshr4;
+  uint32_t acc = 0;
+  int64_t step = warp;
+  if (step >= steps) return;
+  const int64_t stride = nwarps * (int64_t)(U * 1024);
+  const uint8_t* sp = base + step * (int64_t)(U * 1024);
+  uint32_t v[U][8];
+#pragma unroll
+  for (int i = 0; i < U; ++i) ldg_chunk(v[i], sp + (lane + 32 * i) * 32);
+  uint32_t carry_word = 0, nsw = 0;
+  if (lane == 31 && step > 0) carry_word = __ldg(reinterpret_cast<const uint32_t*>(sp - 4));
+  if (lane == 0 && step + 1 < steps) nsw = __ldg(reinterpret_cast<const uint32_t*>(sp + U * 1024));
+  for (; step < steps; step += nwarps, sp += stride) {
+    const bool more = step + nwarps < steps;
+    const uint8_t* np = sp + stride;
+    // Next step's halo / lookahead words, early.
+    uint32_t ncarry = 0, nnsw = 0;
+    if (more) {
+      if (lane == 31) ncarry = __ldg(reinterpret_cast<const uint32_t*>(np - 4));
+      if (lane == 0 && step + nwarps + 1 < steps) nnsw = __ldg(reinterpret_cast<const uint32_t*>(np + U * 1024));
+    }
+    uint32_t last = carry_word;  // lane 31: the word before the chunk being processed
+#pragma unroll
+    for (int i = 0; i < U; ++i) {
+      const uint32_t supply = lane == 31 ? last : v[i][7];
+      const uint32_t prev = __shfl_sync(0xFFFFFFFFu, supply, (lane + 31) & 31);
+      const uint32_t dn = lane == 0 ? (i + 1 < U ? v[i + 1][0] : nsw) : v[i][0];
+      const uint32_t nextw = __shfl_sync(0xFFFFFFFFu, dn, (lane + 1) & 31);
+      uint32_t hi;
+      acc |= u8v_chunk_errors_planes_perm_k(v[i], prev, nextw, kk, &hi);
+      last = v[i][7];
+      if (more) ldg_chunk(v[i], np + (lane + 32 * i) * 32);
+    }
+    carry_word = ncarry;
+    nsw = nnsw;
+  }
+  const unsigned any = __reduce_or_sync(0xFFFFFFFFu, acc);
+  if (lane == 0 && any) atomicOr(flag, 1u);
+}
+__global__ void __launch_bounds__(256, 4) k_v24_u4_b4(const uint8_t* base, int64_t steps, int64_t spw,
+                                                      uint32_t* flag, Cfg k) {
+  (void)spw;
+  body24<4>(base, steps, flag, k);
+}
+__global__ void __launch_bounds__(256, 3) k_v24_u4_b3(const uint8_t* base, int64_t steps, int64_t spw,
+                                                      uint32_t* flag, Cfg k) {
+  (void)spw;
+  body24<4>(base, steps, flag, k);
+}
+__global__ void __launch_bounds__(256, 4) k_v24_u2_b4(const uint8_t* base, int64_t steps, int64_t spw,
+                                                      uint32_t* flag, Cfg k) {
+  (void)spw;
+  body24<2>(base, steps, flag, k);
+}
+
 #define KB_KERNEL(V, U, MINB)                                                                  \
   __global__ void __launch_bounds__(256, MINB)                                                 \
       k_v##V##_u##U##_b##MINB(const uint8_t* base, int64_t steps, int64_t spw, uint32_t* flag, \
@@ -1048,6 +1112,7 @@ static const Entry kEntries[] = {
     {"v10_u4_b3", k_v10_u4_b3, 4}, {"v10_u4_b4", k_v10_u4_b4, 4}, {"v10_u2_b4", k_v10_u2_b4, 2},
     {"v11_u4_b4", k_v11_u4_b4, 4}, {"v13_u4_b4", k_v13_u4_b4, 4},
     {"v14_u4_b4", k_v14_u4_b4, 4}, {"v15_u4_b4", k_v15_u4_b4, 4}, {"v16_u4_b4", k_v16_u4_b4, 4},
+    {"v24_u4_b4", k_v24_u4_b4, 4}, {"v24_u4_b3", k_v24_u4_b3, 4}, {"v24_u2_b4", k_v24_u2_b4, 2},
     {"v23_u4_b4", k_v23_u4_b4, 4}, {"v23_u4_b3", k_v23_u4_b3, 4}, {"v23_u8_b2", k_v23_u8_b2, 8},
     {"v23_u2_b5", k_v23_u2_b5, 2}, {"v23_u2_b4", k_v23_u2_b4, 2}, {"v23_u4_b5", k_v23_u4_b5, 4},
     {"v19_u8_b2", k_v19_u8_b2, 8}, {"v19_u2_b6", k_v19_u2_b6, 2}, {"v19_u2_b5", k_v19_u2_b5, 2},
