@@ -367,11 +367,40 @@ int utf8v_cuda_validate_verdict(const uint8_t* p, size_t n, int is_device, uint8
   Ctx* c;
   int st = get_ctx(&c);
   if (st) return st;
+  // Valid text (the common case) costs one K1 pass: K1 runs first (for host
+  // input piece by piece as the bytes land, as in utf8v_cuda_validate), and
+  // only a flagged input is rescanned by K3 + the window decode.
   const uint8_t* d = p;
-  if (!is_device) {
-    st = pipeline_h2d(*c, p, n, [](size_t, size_t, size_t) { return UTF8V_OK; });
+  CK(cudaMemsetAsync(c->d_flag, 0, 4, c->s_comp));
+  if (is_device) {
+    u8v::launch_validate(u8v::make_desc(p, n, 0, n + 3), c->d_flag, c->s_comp);
+    ++t_launches;
+  } else {
+    size_t prev_off = 0, prev_len = 0;
+    bool have_prev = false;
+    st = pipeline_h2d(*c, p, n, [&](size_t, size_t off, size_t len) {
+      if (have_prev) {
+        u8v::launch_validate(u8v::make_desc(c->d_stage, n, prev_off, prev_off + prev_len),
+                             c->d_flag, c->s_comp);
+        ++t_launches;
+      }
+      prev_off = off;
+      prev_len = len;
+      have_prev = true;
+      return check_launch("validate kernel");
+    });
     if (st) return st;
+    u8v::launch_validate(u8v::make_desc(c->d_stage, n, prev_off, n + 3), c->d_flag, c->s_comp);
+    ++t_launches;
     d = c->d_stage;
+  }
+  st = check_launch("validate kernel");
+  if (st) return st;
+  CK(cudaMemcpyAsync(c->h_res, c->d_flag, 4, cudaMemcpyDeviceToHost, c->s_comp));
+  CK(cudaStreamSynchronize(c->s_comp));
+  if (c->h_res[0] == 0) {
+    *out_valid = 1;
+    return UTF8V_OK;
   }
   CK(cudaMemsetAsync(c->d_flag, 0, 4, c->s_comp));
   CK(cudaMemsetAsync(c->d_pos, 0xFF, 16, c->s_comp));
