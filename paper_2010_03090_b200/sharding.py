@@ -112,3 +112,126 @@ def validate_sharded(local, shard: Shard, group=None, device=None,
     verdict of the whole stream."""
     flag = (shard_flag or shard_error_flag)(local, shard)
     return combine(flag, group=group, device=device)
+
+
+# ---- record batches (C2, C3) over G GPUs (SURVEY §8(e)) ---------------------
+# Contiguous record ranges balanced by bytes; every record is validated whole
+# by one rank, so the verdict slices are disjoint and there is no reduction:
+# each rank writes (and reads back) the verdicts of its own records.
+
+@dataclass(frozen=True)
+class RecordShard:
+    index: int
+    count: int
+    r_begin: int    # first record of the shard
+    r_end: int      # one past the last record
+    b_begin: int    # offsets[r_begin]: first byte of the shard in the data
+    b_end: int      # offsets[r_end]
+
+    @property
+    def n_records(self) -> int:
+        return self.r_end - self.r_begin
+
+    @property
+    def n_bytes(self) -> int:
+        return self.b_end - self.b_begin
+
+
+def plan_records(offsets, world: int) -> list[RecordShard]:
+    """Split records [0, N) into `world` contiguous ranges with about equal
+    bytes: shard k starts at the first record whose start is >= k*total/world
+    (records are never cut).  `offsets`: N+1 non-decreasing uint64 (CSR)."""
+    import numpy as np
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    offs = np.asarray(offsets, dtype=np.uint64)
+    if offs.ndim != 1 or offs.size < 1:
+        raise ValueError("offsets must hold N+1 entries")
+    n = offs.size - 1
+    first, total = int(offs[0]), int(offs[-1]) - int(offs[0])
+    cuts = [0]
+    for k in range(1, world):
+        target = first + (k * total) // world
+        cuts.append(max(cuts[-1], int(np.searchsorted(offs[:n], np.uint64(target), side="left"))))
+    cuts.append(n)
+    return [RecordShard(k, world, cuts[k], cuts[k + 1], int(offs[cuts[k]]), int(offs[cuts[k + 1]]))
+            for k in range(world)]
+
+
+def local_records(data, offsets, shard: RecordShard):
+    """The shard's bytes and its offsets rebased to them (offsets[r] -
+    offsets[r_begin] for r in [r_begin, r_end]) -- the arguments of the batch
+    entry point on this rank."""
+    import numpy as np
+    offs = np.asarray(offsets, dtype=np.uint64)
+    local_offs = offs[shard.r_begin:shard.r_end + 1] - np.uint64(shard.b_begin)
+    return data[shard.b_begin:shard.b_end], local_offs
+
+
+def validate_batch_sharded(data, offsets, shard: RecordShard,
+                           batch_fn: Optional[Callable[[object, object], object]] = None):
+    """This rank's verdicts (uint8, one per record of the shard).  `data` /
+    `offsets` are the whole batch (host arrays or the rank's copy); only the
+    shard's slice is validated.  batch_fn defaults to the GPU batch entry
+    point (validate_lookup_batch); the CPU tests inject the checker."""
+    local, local_offs = local_records(data, offsets, shard)
+    if batch_fn is None:
+        from . import validate_lookup_batch as batch_fn  # noqa: N813
+    return batch_fn(local, local_offs)
+
+
+def gather_verdicts(local, shards: list[RecordShard], group=None):
+    """All ranks' verdict slices concatenated in record order (optional: the
+    batch needs no reduction; this is for callers that want every verdict on
+    every rank).  Uses all_gather_object, so it works with gloo and NCCL."""
+    import numpy as np
+    import torch.distributed as dist
+    parts = [None] * len(shards)
+    dist.all_gather_object(parts, np.asarray(local, dtype=np.uint8), group=group)
+    return np.concatenate(parts) if parts else np.zeros(0, np.uint8)
+
+
+# ---- overlapping the verdict allreduce with the next step ---------------------
+
+class PipelinedFlags:
+    """Per-step error flags whose allreduce(MAX) overlaps the next step's
+    kernel (bench.py's multi-GPU loop).  Flags rotate over `depth` buffers: a
+    buffer is reused only after the allreduce that last read it finished
+    (Work.wait(): a stream wait under NCCL, a host wait under gloo), so a
+    kernel never ORs into a flag a collective is still reducing.  drain()
+    waits for everything and returns the max over all steps and ranks."""
+
+    def __init__(self, make_flag: Callable[[], object], depth: int = 2, group=None):
+        if depth < 1:
+            raise ValueError("depth must be >= 1")
+        self.flags = [make_flag() for _ in range(depth)]
+        self.works: list = [None] * depth
+        self.group = group
+        self.i = 0
+
+    def acquire(self):
+        """The flag this step's kernel ORs into (zeroed by the caller or not:
+        MAX of accumulated flags is still the OR of all verdicts)."""
+        k = self.i % len(self.flags)
+        if self.works[k] is not None:
+            self.works[k].wait()
+            self.works[k] = None
+        return self.flags[k]
+
+    def submit(self, flag) -> None:
+        import torch.distributed as dist
+        k = self.i % len(self.flags)
+        if dist.is_available() and dist.is_initialized():
+            self.works[k] = dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=self.group, async_op=True)
+        self.i += 1
+
+    def wait_all(self) -> None:
+        """Every submitted allreduce is complete (for the current stream)."""
+        for k, w in enumerate(self.works):
+            if w is not None:
+                w.wait()
+                self.works[k] = None
+
+    def drain(self) -> int:
+        self.wait_all()
+        return max(int(f.max().item()) for f in self.flags)

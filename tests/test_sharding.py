@@ -99,3 +99,124 @@ def test_plan_covers_stream_and_lane_ranges():
             assert covered[0][0] == 0 and covered[-1][1] == n + 3
             for (a0, a1), (b0, b1) in zip(covered, covered[1:]):
                 assert a1 == b0
+
+
+# ---- record batches -----------------------------------------------------------
+
+def _batch(seed=5, n_records=300):
+    rng = np.random.default_rng(seed)
+    parts = []
+    for r in range(n_records):
+        size = int(rng.integers(0, 900))
+        if r % 5 == 0:
+            parts.append(np.frombuffer(nat.generate_invalid(15, max(size, 4), seed + r, r % 7), np.uint8))
+        elif r % 11 == 0:
+            parts.append(np.zeros(0, np.uint8))
+        else:
+            parts.append(np.frombuffer(nat.generate_valid(15, size, seed + r), np.uint8))
+    offs = np.zeros(n_records + 1, np.uint64)
+    offs[1:] = np.cumsum([p.size for p in parts])
+    return np.concatenate(parts), offs, parts
+
+
+def test_plan_records_covers_and_balances():
+    data, offs, parts = _batch()
+    for world in (1, 2, 3, 4, 8):
+        shards = sharding.plan_records(offs, world)
+        assert shards[0].r_begin == 0 and shards[-1].r_end == len(parts)
+        for a, b in zip(shards, shards[1:]):
+            assert a.r_end == b.r_begin and a.b_end == b.b_begin
+        total = int(offs[-1])
+        biggest = max(p.size for p in parts)
+        for sh in shards:
+            assert abs(sh.n_bytes - total / world) <= biggest + 1
+            local, local_offs = sharding.local_records(data, offs, sh)
+            assert local_offs[0] == 0 and int(local_offs[-1]) == local.size == sh.n_bytes
+
+
+def cpu_batch(local, local_offs):
+    a = np.ascontiguousarray(local)
+    out = np.ones(len(local_offs) - 1, np.uint8)
+    for r in range(len(local_offs) - 1):
+        out[r] = nat.oracle_verdict(a[int(local_offs[r]):int(local_offs[r + 1])].tobytes())[0]
+    return out
+
+
+def _batch_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        data, offs, _ = _batch()
+        shards = sharding.plan_records(offs, world)
+        mine = sharding.validate_batch_sharded(data, offs, shards[rank], batch_fn=cpu_batch)
+        q.put((rank, sharding.gather_verdicts(mine, shards).tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_batch_sharded_verdicts_equal_per_record_oracle():
+    import multiprocessing as mp
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_batch_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    _, _, parts = _batch()
+    want = [int(nat.oracle_verdict(p.tobytes())[0]) for p in parts]
+    for r in range(world):
+        assert results[r] == want
+
+
+def _pipelined_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        out = []
+        for pattern in ([], [(5, 1)], [(0, 0), (7, 1)], [(19, 1)]):
+            pf = sharding.PipelinedFlags(lambda: torch.zeros(1, dtype=torch.int32), depth=2)
+            for step in range(20):
+                f = pf.acquire()
+                for (s, r) in pattern:          # rank r's kernel flags an error at step s
+                    if s == step and r == rank:
+                        f.fill_(1)
+                pf.submit(f)
+            out.append(pf.drain())
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_pipelined_flags_reduce_every_step():
+    import multiprocessing as mp
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_pipelined_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in range(world):
+        assert results[r] == [0, 1, 1, 1]
