@@ -105,6 +105,18 @@ int utf8v_cuda_validate_lanes_async(const uint8_t* d_p, uint64_t n, uint64_t lan
 int utf8v_cuda_validate_lanes(const uint8_t* p, uint64_t n, uint64_t lane_lo, uint64_t lane_hi,
                               int is_device, uint32_t* out_flag);
 
+/* One process, several GPUs (C4): host input p[0..n) is cut
+ * into n_gpus byte-range shards (as paper_2010_03090_b200/sharding.py: a
+ * look-back head of up to 16 bytes and a 1-byte lookahead tail per shard),
+ * each copied over its GPU's own PCIe link and validated there by one host
+ * thread per GPU; the 4-byte flags are combined on the host (no collective
+ * is needed inside one process).  Shard g runs on visible device g % count
+ * (n_gpus may exceed the device count: shards then share devices).  Device
+ * input (is_device != 0) and shards under 1 MiB are validated on the
+ * current GPU. */
+int utf8v_cuda_validate_sharded(const uint8_t* p, size_t n, int n_gpus, int is_device,
+                                uint8_t* out_valid);
+
 /* Batch on device memory; d_verdicts is written fully (1/0 per record).
  * Fully asynchronous (no host round trip): the kernel reads d_offsets[0] and
  * d_offsets[n_records] itself.  Offsets must be non-decreasing with

@@ -43,6 +43,7 @@ SIGNATURES: dict[str, tuple] = {
     "utf8v_cuda_validate_batch_async": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64,
                                                   C.c_void_p, C.c_void_p, C.c_void_p]),
     "utf8v_cuda_batch_scratch_bytes": (C.c_uint64, [C.c_uint64]),
+    "utf8v_cuda_validate_sharded": (C.c_int, [C.c_void_p, C.c_size_t, C.c_int, C.c_int, _u8p]),
     "utf8v_cuda_stream_create": (C.c_int, [C.POINTER(C.c_void_p)]),
     "utf8v_cuda_stream_feed": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int]),
     "utf8v_cuda_stream_finish": (C.c_int, [C.c_void_p, _u8p]),

@@ -299,6 +299,31 @@ int pipeline_h2d(Ctx& c, const uint8_t* p, size_t n, F each) {
   return UTF8V_OK;
 }
 
+// Lanes [lane_lo, lane_hi) of the host stream p[0..n) on this thread's
+// device: pieces are copied on s_copy and piece k-1's lanes are validated on
+// s_comp once piece k has landed (lane j reads byte j+1).  ORs into c.d_flag.
+int validate_host_lanes(Ctx& c, const uint8_t* p, size_t n, uint64_t lane_lo, uint64_t lane_hi) {
+  size_t prev_off = 0, prev_len = 0;
+  bool have_prev = false;
+  auto launch = [&](uint64_t a, uint64_t b) {
+    const uint64_t lo = a > lane_lo ? a : lane_lo, hi = b < lane_hi ? b : lane_hi;
+    if (lo < hi) {
+      u8v::launch_validate(u8v::make_desc(c.d_stage, n, lo, hi), c.d_flag, c.s_comp);
+      ++t_launches;
+    }
+  };
+  int st = pipeline_h2d(c, p, n, [&](size_t, size_t off, size_t len) {
+    if (have_prev) launch(prev_off, prev_off + prev_len);
+    prev_off = off;
+    prev_len = len;
+    have_prev = true;
+    return check_launch("validate kernel");
+  });
+  if (st) return st;
+  launch(prev_off, n + 3);
+  return check_launch("validate kernel");
+}
+
 }  // namespace
 
 extern "C" {
@@ -326,24 +351,9 @@ int utf8v_cuda_validate(const uint8_t* p, size_t n, int is_device, uint8_t* out_
     ++t_launches;
   } else {
     // Piece k's lanes read one byte of piece k+1 (a rare pair is tested at
-    // its lead's lane), so piece k is validated once piece k+1 has landed:
-    // the callback for piece k launches piece k-1; the last piece follows.
-    size_t prev_off = 0, prev_len = 0;
-    bool have_prev = false;
-    st = pipeline_h2d(*c, p, n, [&](size_t, size_t off, size_t len) {
-      if (have_prev) {
-        u8v::launch_validate(u8v::make_desc(c->d_stage, n, prev_off, prev_off + prev_len),
-                             c->d_flag, c->s_comp);
-        ++t_launches;
-      }
-      prev_off = off;
-      prev_len = len;
-      have_prev = true;
-      return check_launch("validate kernel");
-    });
+    // its lead's lane), so piece k is validated once piece k+1 has landed.
+    st = validate_host_lanes(*c, p, n, 0, n + 3);
     if (st) return st;
-    u8v::launch_validate(u8v::make_desc(c->d_stage, n, prev_off, n + 3), c->d_flag, c->s_comp);
-    ++t_launches;
   }
   st = check_launch("validate kernel");
   if (st) return st;
@@ -376,22 +386,8 @@ int utf8v_cuda_validate_verdict(const uint8_t* p, size_t n, int is_device, uint8
     u8v::launch_validate(u8v::make_desc(p, n, 0, n + 3), c->d_flag, c->s_comp);
     ++t_launches;
   } else {
-    size_t prev_off = 0, prev_len = 0;
-    bool have_prev = false;
-    st = pipeline_h2d(*c, p, n, [&](size_t, size_t off, size_t len) {
-      if (have_prev) {
-        u8v::launch_validate(u8v::make_desc(c->d_stage, n, prev_off, prev_off + prev_len),
-                             c->d_flag, c->s_comp);
-        ++t_launches;
-      }
-      prev_off = off;
-      prev_len = len;
-      have_prev = true;
-      return check_launch("validate kernel");
-    });
+    st = validate_host_lanes(*c, p, n, 0, n + 3);
     if (st) return st;
-    u8v::launch_validate(u8v::make_desc(c->d_stage, n, prev_off, n + 3), c->d_flag, c->s_comp);
-    ++t_launches;
     d = c->d_stage;
   }
   st = check_launch("validate kernel");
@@ -457,12 +453,8 @@ int utf8v_cuda_validate_lanes(const uint8_t* p, uint64_t n, uint64_t lane_lo, ui
     u8v::launch_validate(u8v::make_desc(p, n, lane_lo, lane_hi), c->d_flag, c->s_comp);
     ++t_launches;
   } else {
-    // Copy everything, then one launch (a shard is one piece of work; the
-    // copy of the next rank's shard overlaps on its own GPU).
-    st = pipeline_h2d(*c, p, n, [](size_t, size_t, size_t) { return UTF8V_OK; });
+    st = validate_host_lanes(*c, p, n, lane_lo, lane_hi);
     if (st) return st;
-    u8v::launch_validate(u8v::make_desc(c->d_stage, n, lane_lo, lane_hi), c->d_flag, c->s_comp);
-    ++t_launches;
   }
   st = check_launch("validate kernel");
   if (st) return st;
@@ -579,6 +571,63 @@ int utf8v_cuda_ops_self_test(uint64_t seed, int* out_ok) {
   CK(cudaMemcpyAsync(c->h_res, c->d_ok, 4, cudaMemcpyDeviceToHost, c->s_comp));
   CK(cudaStreamSynchronize(c->s_comp));
   *out_ok = (int)c->h_res[0];
+  return UTF8V_OK;
+}
+
+// ---- one process, several GPUs ----
+int utf8v_cuda_validate_sharded(const uint8_t* p, size_t n, int n_gpus, int is_device,
+                                uint8_t* out_valid) {
+  t_launches = 0;
+  if (!out_valid) return fail(UTF8V_ERR_ARG, "out_valid is NULL");
+  if (n_gpus < 1) return fail(UTF8V_ERR_ARG, "n_gpus must be >= 1");
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    return fail(UTF8V_ERR_NO_DEVICE, "no CUDA device");
+  }
+  // Device input lives on one GPU: validated there.  Shards under 1 MiB: one GPU.
+  if (is_device || n_gpus == 1 || n < (size_t)n_gpus * (1u << 20))
+    return utf8v_cuda_validate(p, n, is_device, out_valid);
+  if (!p) return fail(UTF8V_ERR_ARG, "NULL data with n > 0");
+  // Shards as sharding.plan: cuts at floor(k n / G) rounded down to 16 bytes,
+  // a look-back head of up to 16 bytes, a 1-byte lookahead tail (not on the
+  // last shard, which also evaluates the end-of-input lanes n..n+2).
+  std::vector<uint64_t> cut(n_gpus + 1);
+  for (int k = 0; k <= n_gpus; ++k)
+    cut[k] = k == n_gpus ? n : ((uint64_t)k * n / (uint64_t)n_gpus) & ~uint64_t(15);
+  std::vector<uint32_t> flags(n_gpus, 0);
+  std::vector<int> status(n_gpus, UTF8V_OK);
+  std::vector<std::string> errs(n_gpus);
+  std::vector<int> launches(n_gpus, 0);
+  int caller_dev = 0;
+  cudaGetDevice(&caller_dev);
+  std::vector<std::thread> th;
+  for (int g = 0; g < n_gpus; ++g)
+    th.emplace_back([&, g] {
+      // Shards go round-robin over the visible devices.
+      if (cudaSetDevice(g % count) != cudaSuccess) {
+        status[g] = fail(UTF8V_ERR_CUDA, "cudaSetDevice", cudaGetLastError());
+        errs[g] = t_err;
+        return;
+      }
+      const uint64_t s = cut[g], e = cut[g + 1];
+      const uint64_t head = s < 16 ? s : 16;
+      const bool last = g == n_gpus - 1;
+      const uint64_t lo = s - head, hi = last ? e : e + 1;
+      const uint64_t lane_hi = last ? (hi - lo) + 3 : head + (e - s);
+      status[g] = utf8v_cuda_validate_lanes(p + lo, hi - lo, head, lane_hi, 0, &flags[g]);
+      launches[g] = t_launches;
+      if (status[g]) errs[g] = t_err;
+    });
+  for (auto& t : th) t.join();
+  cudaSetDevice(caller_dev);
+  uint32_t any = 0;
+  for (int g = 0; g < n_gpus; ++g) {
+    if (status[g]) return fail(status[g], "GPU " + std::to_string(g) + ": " + errs[g]);
+    any |= flags[g];
+    t_launches += launches[g];
+  }
+  *out_valid = any == 0 ? 1 : 0;
   return UTF8V_OK;
 }
 

@@ -19,3 +19,32 @@ def test_record_shards_on_gpu_match_whole_batch():
         shards = sharding.plan_records(offs, world)
         parts = [sharding.validate_batch_sharded(data, offs, sh) for sh in shards]
         assert (np.concatenate(parts) == whole).all(), world
+
+
+def test_single_process_sharded_entry_point():
+    """utf8v_cuda_validate_sharded: host input cut into n_gpus shards (one
+    host thread each, round-robin over the visible devices), errors planted
+    around every shard edge; verdict equals the whole-stream oracle."""
+    import ctypes as C
+    from paper_2010_03090_b200 import _lib, configs
+    from tests import _native as nat
+    lib = _lib.load()
+    base = configs.gen_c1(8 << 20, seed=4).cpu().numpy()
+    ok = C.c_uint8()
+    for g in (1, 2, 3, 4, 8):
+        _lib.check(lib.utf8v_cuda_validate_sharded(base.ctypes.data, base.size, g, 0, C.byref(ok)))
+        assert ok.value == 1, g
+        cuts = [((k * base.size) // g) & ~15 for k in range(1, g)]
+        for cut in cuts[:3]:
+            for delta in (-3, -1, 0, 1, 2):
+                for seq in (b"\xc0", b"\xe0\x80", b"\xed\xa0", b"\x80"):
+                    d = base.copy()
+                    d[cut + delta:cut + delta + len(seq)] = np.frombuffer(seq, np.uint8)
+                    want = nat.oracle_verdict(d.tobytes())[0]
+                    _lib.check(lib.utf8v_cuda_validate_sharded(d.ctypes.data, d.size, g, 0, C.byref(ok)))
+                    assert ok.value == int(want), (g, cut, delta, seq)
+        t = base.copy()
+        t[-2:] = [0xF0, 0x9F]  # truncated at the very end (last shard's end check)
+        _lib.check(lib.utf8v_cuda_validate_sharded(t.ctypes.data, t.size, g, 0, C.byref(ok)))
+        assert ok.value == 0
+    assert lib.utf8v_cuda_validate_sharded(base.ctypes.data, base.size, 0, 0, C.byref(ok)) == _lib.UTF8V_ERR_ARG
