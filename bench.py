@@ -436,7 +436,8 @@ def _time_device(fn, reps: int, stream) -> float:
 
 def _time_device_flushed(fn, reps: int, stream, dev) -> float:
     """Mean ms of fn() timed launch by launch, with the 126 MB L2 flushed
-    (a 512 MiB scratch write) before each one -- for inputs that fit in L2."""
+    (a 512 MiB scratch write, then a read of it) before each one -- for inputs
+    that fit in L2."""
     import torch
     scratch = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     for _ in range(3):
@@ -445,7 +446,11 @@ def _time_device_flushed(fn, reps: int, stream, dev) -> float:
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
     with torch.cuda.stream(stream):
         for a, b in ev:
+            # Flush: write then read 512 MiB (> the 126 MB L2), so L2 holds
+            # clean unrelated lines -- no pending write-backs compete with the
+            # timed kernel.
             scratch.fill_(1)
+            scratch.view(torch.int64).sum()
             a.record(stream)
             fn()
             b.record(stream)

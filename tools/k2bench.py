@@ -30,7 +30,8 @@ for name, gen in (("c2", configs.gen_c2), ("c3", configs.gen_c3)):
     torch.cuda.synchronize()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
     for a, z in ev:
-        scratch.fill_(1)  # flush L2
+        scratch.fill_(1)  # flush L2 (write, then read: no dirty lines left)
+        scratch.view(torch.int64).sum()
         a.record(st)
         run()
         z.record(st)
