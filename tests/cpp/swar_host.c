@@ -491,3 +491,25 @@ uint64_t swar_bits_perm_bounded_check(uint64_t seed, uint64_t trials) {
   }
   return bad;
 }
+
+/* The acceptance gate's mutation corpus (proj/tests/acceptance.cpp:263-272):
+ * for every seed in [seed_lo, seed_hi), optionally the valid buffer, then one
+ * buffer per mutation strategy (kinds {1,2,3,4}, `target` bytes), all
+ * concatenated into out (capacity cap) with CSR offsets offs[0..count].
+ * Returns the number of buffers, or (size_t)-1 when cap is too small. */
+size_t mutation_corpus(uint64_t seed_lo, uint64_t seed_hi, size_t target, int with_valid, uint8_t* out,
+                       size_t cap, uint64_t* offs) {
+  size_t count = 0, at = 0;
+  offs[0] = 0;
+  for (uint64_t seed = seed_lo; seed < seed_hi; ++seed) {
+    for (int strat = with_valid ? -1 : 0; strat < 6; ++strat) {
+      if (cap - at < target + 64) return (size_t)-1;
+      const size_t n = strat < 0 ? orc_generate_valid(0xF, target, seed, out + at, cap - at)
+                                 : orc_generate_invalid(0xF, target, seed, strat, out + at, cap - at);
+      if (n == (size_t)-1) return (size_t)-1;
+      at += n;
+      offs[++count] = at;
+    }
+  }
+  return count;
+}

@@ -241,13 +241,25 @@ def test_generated_corpora_verdicts_and_positions():
 
 
 def test_mutation_fuzz_batch(torch):
-    # acceptance.cpp:263-272 -- seeds x 6 strategies (subset), batched.
-    items = _mutation_corpora(range(1, 20001))
-    data, offs = _batch_of(items)
+    # acceptance.cpp:263-272 -- all 125,000 seeds x 6 strategies (750k mutated
+    # 64-byte buffers) plus each seed's valid buffer, as one batch: every
+    # verdict equals the oracle's and every mutation is invalid.
+    import ctypes as C
+    S = nat.swar()
+    S.mutation_corpus.restype = C.c_size_t
+    S.mutation_corpus.argtypes = [C.c_uint64, C.c_uint64, C.c_size_t, C.c_int, C.c_void_p, C.c_size_t, C.c_void_p]
+    seeds = 125000
+    cap = seeds * 7 * (64 + 64)
+    data = np.empty(cap, np.uint8)
+    offs = np.zeros(seeds * 7 + 1, np.uint64)
+    count = S.mutation_corpus(1, seeds + 1, 64, 1, data.ctypes.data, cap, offs.ctypes.data)
+    assert count == seeds * 7
+    data = data[: int(offs[-1])]
     want = nat.oracle_batch(data, offs)
     got = u8.validate_lookup_batch(torch.from_numpy(data.copy()).cuda(), torch.from_numpy(offs.view(np.int64)).cuda())
     assert np.array_equal(got, want)
-    assert (want == 0).sum() == 6 * 20000
+    assert (want.reshape(seeds, 7)[:, 1:] == 0).all()          # every mutation invalid
+    assert (want.reshape(seeds, 7)[:, 0] == 1).all()           # every generated buffer valid
 
 
 def test_pinned_offset_fuzz_positions():
