@@ -471,3 +471,55 @@ def test_stream_range_generator_matches_full_stream(torch):
         out = torch.empty(max(hi - lo, 1), dtype=torch.uint8, device="cuda")
         _lib.check(lib.utf8v_gen_stream_range(out.data_ptr(), n, lo, hi, 9, 0, torch.cuda.current_stream().cuda_stream))
         assert torch.equal(out[: hi - lo], full[lo:hi]), (lo, hi)
+
+
+def test_k1_structural_boundaries():
+    """Errors placed at (and -3..+3 around) every boundary K1's plumbing
+    handles -- 32-byte chunks, lanes, 1 KiB load instructions, 4 KiB warp
+    steps, the grid-stride wrap (resident warps x 4 KiB) -- including
+    sequences that straddle the boundary (lead before, follower after).
+    Verdict (K1) and first-error offset/kind (K3) equal the windowed oracle,
+    for device and host input."""
+    d = configs.gen_c1(64 << 20, seed=7)
+    h = d.cpu().numpy()
+    n = d.numel()
+    resident = 148 * 4 * 8 * 4096  # warps x step bytes on a B200 (upper bound of the wrap)
+    bounds = [32, 64, 31 * 32, 1024, 2048, 3072, 4096, 8192, 4096 * 37, resident // 2, resident,
+              resident + 4096, 2 * resident, n - 4096, n - 32]
+    seqs = [b"\x80", b"\xc3", b"\xe0\x9f\xbf", b"\xed\xa0\x80", b"\xf4\x90\x80\x80", b"\xf0\x9f\x98",
+            b"\xc0\x80", b"\xff"]
+    checked = 0
+    for b in bounds:
+        for delta in range(-3, 4):
+            for seq in seqs:
+                pos = b + delta
+                if pos < 0 or pos + len(seq) > n:
+                    continue
+                lo = max(0, pos - 16)
+                while lo > 0 and (h[lo] & 0xC0) == 0x80:
+                    lo -= 1
+                hi = min(n, pos + len(seq) + 16)
+                while hi < n and (h[hi] & 0xC0) == 0x80:
+                    hi += 1
+                win = h[lo:hi].copy()
+                win[pos - lo:pos - lo + len(seq)] = np.frombuffer(seq, np.uint8)
+                exp = nat.oracle_verdict(win)
+                old = d[pos:pos + len(seq)].clone()
+                d[pos:pos + len(seq)] = torch_from(seq)
+                assert u8.validate_lookup(d) is exp[0], (b, delta, seq)
+                v = u8.validate_lookup_verdict(d)
+                if exp[0]:
+                    assert v.valid()
+                else:
+                    assert (v.error.offset, int(v.error.kind)) == (exp[1] + lo, exp[2]), (b, delta, seq)
+                if checked % 17 == 0:  # the host (pipelined H2D) path on a subset
+                    assert u8.validate_lookup(d.cpu().numpy().tobytes()) is exp[0]
+                d[pos:pos + len(seq)] = old
+                checked += 1
+    assert checked > 700
+    assert u8.validate_lookup(d) is True
+
+
+def torch_from(seq):
+    import torch
+    return torch.tensor(list(seq), dtype=torch.uint8, device="cuda")
