@@ -10,6 +10,7 @@ Python face of libutf8v_cuda.so, mirroring the reference's Lookup API
     validate_lookup_verdict(d)   Verdict, bit-exact with oracle_validate
     validate_lookup_batch(d, offsets)  one verdict per CSR record
     LookupStream()               one stream validated in pieces (feed / finish)
+    validate_lookup_sharded(d, g)  host input over g GPUs in this process
 
 `data` is host bytes (bytes / bytearray / memoryview / numpy uint8) or a CUDA
 torch.uint8 tensor (device-resident, validated in place).  All compute runs on
@@ -29,7 +30,7 @@ from . import _lib
 __all__ = [
     "ErrorKind", "Utf8Error", "Verdict", "LookupBackend", "lookup_backends", "find_lookup_backend",
     "validate_lookup", "validate_lookup_fallback", "validate_lookup_verdict", "validate_lookup_batch",
-    "LookupStream",
+    "LookupStream", "validate_lookup_sharded",
     "validate_lanes_async", "validate_batch_async", "WIDTH",
 ]
 
@@ -178,6 +179,17 @@ def validate_lookup_verdict(data) -> Verdict:
     if ok.value:
         return Verdict.ok()
     return Verdict.fail(off.value, ErrorKind(kind.value))
+
+
+def validate_lookup_sharded(data, n_gpus: int) -> bool:
+    """Host bytes validated over `n_gpus` GPUs of this process
+    (utf8v_cuda_validate_sharded: one host thread and one PCIe link per
+    shard, flags combined on the host).  Device tensors are validated on
+    their own GPU."""
+    ptr, n, dev, _keep = _input(data)
+    ok = C.c_uint8(0)
+    _lib.check(_lib.load().utf8v_cuda_validate_sharded(ptr, n, int(n_gpus), dev, C.byref(ok)))
+    return bool(ok.value)
 
 
 def validate_lookup_batch(data, offsets) -> np.ndarray:

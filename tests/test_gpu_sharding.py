@@ -77,3 +77,16 @@ def test_malformed_device_offsets_stay_in_bounds():
         assert int(buf[-1].item()) == 0xAB, mutate
     # the library still validates correctly afterwards
     assert (np.asarray(u8.validate_lookup_batch(b.data, b.d_offsets)) == b.expected).all()
+
+
+def test_python_sharded_wrapper():
+    import paper_2010_03090_b200 as u8
+    from paper_2010_03090_b200 import configs
+    d = configs.gen_c1(6 << 20, seed=3)
+    h = d.cpu().numpy()
+    for g in (1, 2, 5):
+        assert u8.validate_lookup_sharded(h.tobytes(), g) is True
+        bad = h.copy()
+        bad[(3 << 20) + 1] = 0xFF
+        assert u8.validate_lookup_sharded(bad, g) is False
+    assert u8.validate_lookup_sharded(d, 4) is True  # device input: its own GPU
