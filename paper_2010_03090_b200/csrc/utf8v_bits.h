@@ -33,9 +33,29 @@ U8V_HD uint32_t u8v_prmt(uint32_t x, uint32_t y, uint32_t s) {
 #endif
 }
 
-// x << s and x >> s on the FMA pipe (k.one == 1 at run time).
-#define U8V_SHL(x, s, k) u8v_mad((x), (1u << (s)) * (k).one, 0u)
-#define U8V_SHR(x, s, k) u8v_mulhi((x), 1u << (32 - (s)))
+// x << s and x >> s on the FMA pipe: a multiply by an immediate power of two
+// (IMAD.SHL) and a multiply-high (IMAD.HI).  Inline PTX keeps ptxas from
+// turning them into SHF/LEA on the ALU pipe, and immediates need no
+// registers (no per-chunk rematerialisation under register pressure).
+#if defined(__CUDA_ARCH__)
+template <unsigned kMul>
+__device__ __forceinline__ uint32_t u8v_mul_imm(uint32_t x) {
+  uint32_t d;
+  asm("mul.lo.u32 %0, %1, %2;" : "=r"(d) : "r"(x), "n"(kMul));
+  return d;
+}
+template <unsigned kMul>
+__device__ __forceinline__ uint32_t u8v_mulhi_imm(uint32_t x) {
+  uint32_t d;
+  asm("mul.hi.u32 %0, %1, %2;" : "=r"(d) : "r"(x), "n"(kMul));
+  return d;
+}
+#define U8V_SHL(x, s, k) u8v_mul_imm<(1u << (s))>(x)
+#define U8V_SHR(x, s, k) u8v_mulhi_imm<(1u << (32 - (s)))>(x)
+#else
+#define U8V_SHL(x, s, k) ((uint32_t)(x) << (s))
+#define U8V_SHR(x, s, k) ((uint32_t)(x) >> (s))
+#endif
 
 // (x & m) | (y & ~m) in one LOP3 with m an immediate (ptxas splits the
 // expression in two when m appears in both polarities).
