@@ -50,9 +50,18 @@ __device__ __forceinline__ uint32_t u8v_mulhi_imm(uint32_t x) {
   asm("mul.hi.u32 %0, %1, %2;" : "=r"(d) : "r"(x), "n"(kMul));
   return d;
 }
+// x * kMul + y (kMul an immediate; IMAD).
+template <unsigned kMul>
+__device__ __forceinline__ uint32_t u8v_mad_imm(uint32_t x, uint32_t y) {
+  uint32_t d;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(x), "n"(kMul), "r"(y));
+  return d;
+}
 #define U8V_SHL(x, s, k) u8v_mul_imm<(1u << (s))>(x)
 #define U8V_SHR(x, s, k) u8v_mulhi_imm<(1u << (32 - (s)))>(x)
+#define U8V_SHLADD(x, s, y, k) u8v_mad_imm<(1u << (s))>((x), (y))
 #else
+#define U8V_SHLADD(x, s, y, k) ((((uint32_t)(x)) << (s)) + (uint32_t)(y))
 #define U8V_SHL(x, s, k) ((uint32_t)(x) << (s))
 #define U8V_SHR(x, s, k) ((uint32_t)(x) >> (s))
 #endif
@@ -125,7 +134,12 @@ U8V_HD void u8v_planes(const uint32_t w[8], uint32_t p[8]) { u8v_planes_k(w, p, 
 // Bit 7 of each byte of x gathered into bits 28..31 (byte 0 -> bit 28): the
 // top four lanes of a plane, from a SWAR flag word.  One IMAD.
 U8V_HD uint32_t u8v_movemask_top(uint32_t x, u8v_consts k) {
-  return u8v_mad(x & U8V_B7, 0x00204081u * k.one, 0u);
+  (void)k;
+#if defined(__CUDA_ARCH__)
+  return u8v_mul_imm<0x00204081u>(x & U8V_B7);
+#else
+  return (x & U8V_B7) * 0x00204081u;
+#endif
 }
 
 // The rare lead pairs on planes (utf8v_swar.h u8v_rare_key restated), lead
@@ -266,9 +280,9 @@ U8V_HD uint32_t u8v_chunk_errors_planes_perm_k(const uint32_t w[8], uint32_t pre
   const uint32_t t1 = U8V_BITSEL(0x000000FE, U8V_SHR(l1, 23, k), U8V_SHR(q1, 31, k));
   const uint32_t t2 = U8V_BITSEL(0x0000FEFE, U8V_SHR(l2, 15, k), U8V_SHR(q2, 23, k));
   const uint32_t t3 = U8V_BITSEL(0x00FEFEFE, U8V_SHR(l3, 7, k), U8V_SHR(q3, 15, k));
-  const uint32_t e1 = u8v_mad(l1, 0x100u * k.one, t1);
-  const uint32_t e2 = u8v_mad(l2, 0x10000u * k.one, t2);
-  const uint32_t e3 = u8v_mad(l3, 0x1000000u * k.one, t3);
+  const uint32_t e1 = U8V_SHLADD(l1, 8, t1, k);
+  const uint32_t e2 = U8V_SHLADD(l2, 16, t2, k);
+  const uint32_t e3 = U8V_SHLADD(l3, 24, t3, k);
   const uint32_t S = (p7 & ~p6) ^ (e1 | e2 | e3);
   // Follower bits 5 and 4 at the lead's position.
   const uint32_t nx5 = U8V_SHL(next, 2, k);  // bit 7 = next byte 0's bit 5
@@ -310,17 +324,17 @@ U8V_HD uint32_t u8v_chunk_errors_planes_perm_bounded_k(const uint32_t w[8], uint
   const uint32_t q1 = prev & U8V_SHL(prev, 1, k) & U8V_B7;
   const uint32_t q2 = q1 & U8V_SHL(prev, 2, k);
   const uint32_t q3 = q2 & U8V_SHL(prev, 3, k);
-  const uint32_t e1 = u8v_mad(l1, 0x100u * k.one,
-                              U8V_BITSEL(0x000000FE, U8V_SHR(l1, 23, k), U8V_SHR(q1, 31, k)));
-  const uint32_t e2 = u8v_mad(l2, 0x10000u * k.one,
-                              U8V_BITSEL(0x0000FEFE, U8V_SHR(l2, 15, k), U8V_SHR(q2, 23, k)));
-  const uint32_t e3 = u8v_mad(l3, 0x1000000u * k.one,
-                              U8V_BITSEL(0x00FEFEFE, U8V_SHR(l3, 7, k), U8V_SHR(q3, 15, k)));
+  const uint32_t e1 =
+      U8V_SHLADD(l1, 8, U8V_BITSEL(0x000000FE, U8V_SHR(l1, 23, k), U8V_SHR(q1, 31, k)), k);
+  const uint32_t e2 =
+      U8V_SHLADD(l2, 16, U8V_BITSEL(0x0000FEFE, U8V_SHR(l2, 15, k), U8V_SHR(q2, 23, k)), k);
+  const uint32_t e3 =
+      U8V_SHLADD(l3, 24, U8V_BITSEL(0x00FEFEFE, U8V_SHR(l3, 7, k), U8V_SHR(q3, 15, k)), k);
   // Record starts one / two bytes back, in permuted order (lags of B).
-  const uint32_t B1 = u8v_mad(B, 0x100u * k.one,
-                              U8V_BITSEL(0x000000FE, U8V_SHR(B, 23, k), U8V_SHR(pre, 31, k)));
-  const uint32_t B2 = u8v_mad(B, 0x10000u * k.one,
-                              U8V_BITSEL(0x0000FEFE, U8V_SHR(B, 15, k), U8V_SHR(pre, 23, k)));
+  const uint32_t B1 =
+      U8V_SHLADD(B, 8, U8V_BITSEL(0x000000FE, U8V_SHR(B, 23, k), U8V_SHR(pre, 31, k)), k);
+  const uint32_t B2 =
+      U8V_SHLADD(B, 16, U8V_BITSEL(0x0000FEFE, U8V_SHR(B, 15, k), U8V_SHR(pre, 23, k)), k);
   const uint32_t m2 = B | B1, m3 = m2 | B2;
   const uint32_t S = (p7 & ~p6) ^ ((e1 & ~B) | (e2 & ~m2) | (e3 & ~m3));
   *end_err = B & (e1 | (e2 & ~B1) | (e3 & ~B1 & ~B2));
