@@ -45,7 +45,10 @@ extern "C" {
  * >= 32 so the roster stays widest-first, proj/tests/test_lookup.cpp:41-42). */
 #define UTF8V_CUDA_WIDTH 64
 
-/* ABI version (bumped on any signature change). */
+/* ABI version (bumped on any signature or contract change).
+ *   1  first round-1 interface
+ *   2  streaming session, utf8v_cuda_validate_sharded; the async batch entry
+ *      point reads its first/last offsets on the device (no host sync) */
 int utf8v_cuda_abi_version(void);
 
 /* Human-readable text of the last error on this thread ("" if none). */

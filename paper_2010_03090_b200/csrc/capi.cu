@@ -328,7 +328,7 @@ int validate_host_lanes(Ctx& c, const uint8_t* p, size_t n, uint64_t lane_lo, ui
 
 extern "C" {
 
-int utf8v_cuda_abi_version(void) { return 1; }
+int utf8v_cuda_abi_version(void) { return 2; }
 
 const char* utf8v_cuda_last_error(void) { return t_err.c_str(); }
 
