@@ -53,3 +53,15 @@ def test_bench_report_schema(device):
                            "best_throughput", "mean_throughput", "compensated"}
     assert rep[0]["input_bytes"] == 1 << 22 and rep[0]["repeats"] == 3
     assert rep[0]["best_throughput"] >= rep[0]["mean_throughput"] > 0
+
+
+@pytest.mark.gpu
+def test_bench_compensate(tmp_path):
+    r = run("bench", "--size", 1 << 22, "--repeats", 3, "--compensate", "--json")
+    assert r.returncode == 0, r.stderr
+    rep = json.loads(r.stdout)[0]
+    assert rep["compensated"] is True and rep["mean_seconds"] >= rep["best_seconds"] >= 0
+    bad = tmp_path / "bad.bin"
+    bad.write_bytes(b"ok\xc0\x80")
+    r = run("bench", "--file", bad, "--compensate")   # compensation needs well-formed input
+    assert r.returncode == 2

@@ -3,7 +3,7 @@
 //
 //   utf8v-cuda validate [--algo cuda] [--json] [FILE]     (stdin when omitted)
 //   utf8v-cuda bench [--algo cuda] [--file F | --size N --seed S]
-//                    [--repeats R] [--device] [--json]
+//                    [--repeats R] [--device] [--compensate] [--json]
 //
 // Exit codes as proj/tools/main.cpp:28-31: 0 valid / success, 1 malformed
 // input, 2 usage or I/O error, 3 internal inconsistency.  `validate` prints
@@ -13,7 +13,10 @@
 // A missing device or CUDA failure exits 2 (environment error).
 // `bench` reports with the schema of proj/src/bench.cpp:127-139.  Host input
 // is timed end to end (host buffer in, verdict out, PCIe included), --device
-// times the device-resident path.
+// times the device-resident path.  --compensate times the input and the
+// input doubled and reports the difference (bench.cpp:70-78,92-99: fixed
+// per-call overhead cancels; well-formed input only).
+#include <algorithm>
 #include <chrono>
 #include <cstdint>
 #include <cstdio>
@@ -42,7 +45,7 @@ int usage(const char* why) {
   if (why) std::cerr << "error: " << why << "\n";
   std::cerr << "usage: utf8v-cuda validate [--algo cuda] [--json] [FILE]\n"
                "       utf8v-cuda bench [--algo cuda] [--file F | --size N --seed S] [--repeats R]"
-               " [--device] [--json]\n";
+               " [--device] [--compensate] [--json]\n";
   return k_exit_usage;
 }
 
@@ -96,8 +99,12 @@ int run_validate(const std::string& path, bool as_json) {
   }
 }
 
+struct timing {
+  double best, mean;
+};
+
 int run_bench(const std::string& file, std::uint64_t size, std::uint64_t seed, int repeats,
-              bool device, bool as_json) {
+              bool device, bool compensate, bool as_json) {
   std::vector<std::uint8_t> bytes;
   std::string input_name;
   bool expect_valid = true;
@@ -113,52 +120,84 @@ int run_bench(const std::string& file, std::uint64_t size, std::uint64_t seed, i
     }
     input_name = "c1-mix seed=" + std::to_string(seed);
   }
-  const std::uint8_t* p = bytes.data();
-  std::uint8_t* d = nullptr;
-  if (device) {
-    if (cudaMalloc(&d, bytes.size() ? bytes.size() : 1) != cudaSuccess ||
-        cudaMemcpy(d, bytes.data(), bytes.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
-      std::cerr << "error: device buffer\n";
-      return k_exit_inconsistent;
-    }
-    p = d;
+  if (compensate && !expect_valid) {
+    std::cerr << "error: compensated timing needs well-formed input\n";
+    return k_exit_usage;
   }
-  auto once = [&]() -> int {
+  // Host or device copies of the input (and of the input doubled).
+  std::vector<std::uint8_t> doubled;
+  if (compensate) {
+    doubled.reserve(bytes.size() * 2);
+    doubled.insert(doubled.end(), bytes.begin(), bytes.end());
+    doubled.insert(doubled.end(), bytes.begin(), bytes.end());
+  }
+  std::vector<std::uint8_t*> dev_bufs;
+  auto place = [&](const std::vector<std::uint8_t>& b) -> const std::uint8_t* {
+    if (!device) return b.data();
+    std::uint8_t* d = nullptr;
+    if (cudaMalloc(&d, b.size() ? b.size() : 1) != cudaSuccess ||
+        cudaMemcpy(d, b.data(), b.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+      return nullptr;
+    dev_bufs.push_back(d);
+    return d;
+  };
+  const std::uint8_t* p1 = place(bytes);
+  const std::uint8_t* p2 = compensate ? place(doubled) : nullptr;
+  if (!p1 || (compensate && !p2)) {
+    std::cerr << "error: device buffer\n";
+    return k_exit_inconsistent;
+  }
+  auto once = [&](const std::uint8_t* p, std::size_t n) -> int {
     std::uint8_t ok = 0;
-    if (utf8v_cuda_validate(p, bytes.size(), device ? 1 : 0, &ok) != UTF8V_OK) return -1;
+    if (utf8v_cuda_validate(p, n, device ? 1 : 0, &ok) != UTF8V_OK) return -1;
     return ok;
   };
   // Correctness gate before timing (proj/src/bench.cpp:80-86).
-  const int gate = once();
+  int gate = once(p1, bytes.size());
+  if (gate >= 0 && compensate) gate = once(p2, doubled.size()) == 1 && gate == 1 ? 1 : -1;
   if (gate < 0 || (gate == 1) != expect_valid) {
     std::cerr << "error: validator_mismatch on '" << input_name << "'\n";
     return k_exit_inconsistent;
   }
-  double best = std::numeric_limits<double>::infinity(), sum = 0.0;
-  for (int r = 0; r < repeats; ++r) {
-    const auto t0 = std::chrono::steady_clock::now();
-    if (once() < 0) return k_exit_inconsistent;
-    const double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-    best = s < best ? s : best;
-    sum += s;
+  auto passes = [&](const std::uint8_t* p, std::size_t n, timing& t) -> bool {
+    t.best = std::numeric_limits<double>::infinity();
+    double sum = 0.0;
+    for (int r = 0; r < repeats; ++r) {
+      const auto t0 = std::chrono::steady_clock::now();
+      if (once(p, n) < 0) return false;
+      const double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      t.best = s < t.best ? s : t.best;
+      sum += s;
+    }
+    t.mean = sum / repeats;
+    return true;
+  };
+  timing t{};
+  if (!passes(p1, bytes.size(), t)) return k_exit_inconsistent;
+  if (compensate) {
+    timing td{};
+    if (!passes(p2, doubled.size(), td)) return k_exit_inconsistent;
+    // Difference of the two runs, clamped to 0 <= best <= mean (bench.cpp:92-99).
+    t.best = std::max(td.best - t.best, 0.0);
+    t.mean = std::max(td.mean - t.mean, t.best);
   }
-  const double mean = sum / repeats;
+  for (std::uint8_t* d : dev_bufs) cudaFree(d);
+  const double best = t.best, mean = t.mean;
   const double n = (double)bytes.size();
   const std::string name = device ? "cuda-device" : "cuda";
   std::cerr << "lookup backend: cuda (" << UTF8V_CUDA_WIDTH << "-byte lanes, sm_100a)\n";
   if (as_json) {
     std::printf(
-        "[\n  {\n    \"best_seconds\": %.9g,\n    \"best_throughput\": %.9g,\n    \"compensated\": false,\n"
+        "[\n  {\n    \"best_seconds\": %.9g,\n    \"best_throughput\": %.9g,\n    \"compensated\": %s,\n"
         "    \"input_bytes\": %zu,\n    \"input_name\": \"%s\",\n    \"mean_seconds\": %.9g,\n"
         "    \"mean_throughput\": %.9g,\n    \"repeats\": %d,\n    \"validator\": \"%s\"\n  }\n]\n",
-        best, n / best, bytes.size(), json_escape(input_name).c_str(), mean, n / mean, repeats,
-        name.c_str());
+        best, n / best, compensate ? "true" : "false", bytes.size(), json_escape(input_name).c_str(), mean,
+        n / mean, repeats, name.c_str());
   } else {
     std::printf("%-13s%-22s%12s%12s%12s\n", "validator", "input", "bytes", "best GB/s", "mean GB/s");
     std::printf("%-13s%-22s%12zu%12.3f%12.3f\n", name.c_str(), input_name.c_str(), bytes.size(),
                 n / best / 1e9, n / mean / 1e9);
   }
-  if (d) cudaFree(d);
   return k_exit_ok;
 }
 
@@ -172,7 +211,7 @@ int main(int argc, char** argv) {
     return k_exit_ok;
   }
   std::string file, algo = "cuda";
-  bool as_json = false, device = false;
+  bool as_json = false, device = false, compensate = false;
   std::uint64_t size = 1ull << 26, seed = 2;
   int repeats = 20;
   for (int i = 2; i < argc; ++i) {
@@ -186,6 +225,8 @@ int main(int argc, char** argv) {
       as_json = true;
     } else if (a == "--device") {
       device = true;
+    } else if (a == "--compensate") {
+      compensate = true;
     } else if (a == "--algo" || a.rfind("--algo=", 0) == 0) {
       const char* v = a == "--algo" ? value("--algo") : a.c_str() + 7;
       if (!v) return usage("--algo needs a value");
@@ -213,7 +254,7 @@ int main(int argc, char** argv) {
   if (cmd == "validate") return run_validate(file, as_json);
   if (cmd == "bench") {
     if (repeats < 1) return usage("--repeats must be >= 1");
-    return run_bench(file, size, seed, repeats, device, as_json);
+    return run_bench(file, size, seed, repeats, device, compensate, as_json);
   }
   return usage(("unknown command " + cmd).c_str());
 }
