@@ -497,6 +497,42 @@ def measure_extras(lib, dev, reps: int) -> dict:
         del b, ver
         torch.cuda.empty_cache()
 
+    # The user-facing entry points on C1 (1 GiB): the verdict API on valid and
+    # on invalid input (K1, then K3 + window decode), the streaming session
+    # over device pieces, and host input from pageable memory.
+    d = configs.gen_c1()
+    n = d.numel()
+    api = {}
+    ms = _time_device(lambda: u8.validate_lookup_verdict(d), 5, st)
+    api["verdict_valid_GBps"] = n / ms / 1e6
+    orig = int(d[n // 2].item())
+    d[n // 2] = 0xC0
+    v = u8.validate_lookup_verdict(d)
+    ms = _time_device(lambda: u8.validate_lookup_verdict(d), 5, st)
+    api["verdict_invalid_GBps"] = n / ms / 1e6
+    api["verdict_invalid_offset"] = v.error.offset if not v.valid() else None
+    d[n // 2] = orig
+    def stream_once(piece):
+        with u8.LookupStream() as sess:
+            for a in range(0, n, piece):
+                sess.feed(d[a:a + piece])
+            return sess.finish()
+    for mib in (64, 256):
+        ms = _time_device(lambda: stream_once(mib << 20), 5, st)
+        api[f"stream_{mib}MiB_pieces_GBps"] = n / ms / 1e6
+    host = d.cpu().numpy()
+    ok = C.c_uint8()
+    _lib.check(lib.utf8v_cuda_validate(host.ctypes.data, n, 0, C.byref(ok)))  # warm: pinned ring
+    t0 = time.perf_counter()
+    for _ in range(3):
+        _lib.check(lib.utf8v_cuda_validate(host.ctypes.data, n, 0, C.byref(ok)))
+    api["pageable_host_GBps"] = 3 * n / (time.perf_counter() - t0) / 1e9
+    api["note"] = ("device-timed (verdict, stream) / wall-clock (pageable host, PCIe included); the C1 byte at n/2 "
+                   "is set to 0xC0 for the invalid case and restored afterwards")
+    out["c1_api"] = api
+    del d, host
+    torch.cuda.empty_cache()
+
     n4 = configs.C4["n"]
     c4 = {}
     for variant in (0, 1, 2):

@@ -80,7 +80,7 @@ struct Ctx {
   bool ready = false;
   cudaStream_t s_comp = nullptr, s_copy = nullptr;
   uint32_t* d_flag = nullptr;               // [0] verdict flag
-  unsigned long long* d_pos = nullptr;      // [0] first chunk, [1] offset
+  unsigned long long* d_pos = nullptr;      // [0] first chunk, [1] offset, [2] K3 round
   int* d_kind = nullptr;
   uint8_t* d_lanes = nullptr;               // 3 x UTF8V_CUDA_WIDTH
   int* d_ok = nullptr;
@@ -400,8 +400,8 @@ int utf8v_cuda_validate_verdict(const uint8_t* p, size_t n, int is_device, uint8
   }
   CK(cudaMemsetAsync(c->d_flag, 0, 4, c->s_comp));
   CK(cudaMemsetAsync(c->d_pos, 0xFF, 16, c->s_comp));
-  u8v::launch_first_error(u8v::make_desc(d, n, 0, n + 3), n, c->d_flag, c->d_pos, c->d_pos + 1,
-                          c->d_kind, c->s_comp);
+  u8v::launch_first_error(u8v::make_desc(d, n, 0, n + 3), n, c->d_flag, c->d_pos, c->d_pos + 2,
+                          c->d_pos + 1, c->d_kind, c->s_comp);
   t_launches += 2;
   st = check_launch("first_error kernel");
   if (st) return st;

@@ -32,9 +32,9 @@ struct StreamDesc {
 int max_resident_warps();
 StreamDesc make_desc(const uint8_t* p, uint64_t n, uint64_t lane_lo, uint64_t lane_hi);
 void launch_validate(const StreamDesc& d, uint32_t* flag, cudaStream_t st);
-void launch_first_error(const StreamDesc& d, uint64_t n, uint32_t* flag,
-                        unsigned long long* first_chunk, unsigned long long* out_offset,
-                        int* out_kind, cudaStream_t st);
+void launch_first_error(const StreamDesc& d, uint64_t n, uint32_t* flag, unsigned long long* first_chunk,
+                        unsigned long long* next_round, unsigned long long* out_offset, int* out_kind,
+                        cudaStream_t st);
 
 // batch.cu
 // Caller sets d_verdicts[] = 1 first.  Asynchronous: the kernel reads

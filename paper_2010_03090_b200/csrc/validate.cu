@@ -1,10 +1,11 @@
 // validate.cu -- sm_100a kernels for single-stream Lookup validation.
 //
-//   k_validate<false>   K1: OR of the per-lane error flags of one stream (or
+//   k_validate          K1: OR of the per-lane error flags of one stream (or
 //                       of one lane range of it: a pipeline piece, a shard),
 //                       reduced with REDUX + one atomicOr per warp.
-//   k_validate<true>    K3: the same scan, recording the first 32-byte chunk
-//                       that holds a flagged lane (atomicMin per warp).
+//   k_first_error       K3: the same per-step scan over steps claimed in
+//                       order, recording the first 32-byte chunk that holds a
+//                       flagged lane (atomicMin); stops past that chunk.
 //   k_locate            K3b: one thread decodes the <= 42-byte window around
 //                       that chunk and writes the reference's (offset, kind).
 //
@@ -92,40 +93,76 @@ __device__ __forceinline__ uint32_t step_errors(const StreamDesc& d, const Chunk
   return step_err;
 }
 
-// Steps are dealt to warps round-robin (step = warp + j * nwarps): at any
-// moment all warps sweep one window of ~nwarps * 4 KiB, which keeps DRAM
+// Interior steps (all bytes real, all lanes wanted, lookahead word in range)
+// form one contiguous run [*int_b, *int_d) of step indices; only the
+// head/tail steps take masked loads.
+__device__ __forceinline__ void interior_steps(const StreamDesc& d, int64_t* int_b, int64_t* int_d) {
+  const int64_t in_lo = d.lo > d.L0 ? d.lo : d.L0;
+  const int64_t in_hi = d.hi < d.L1 ? d.hi : d.L1;
+  const int64_t sb = kStepChunks * (int64_t)kChunkBytes;
+  int64_t b = (in_lo - d.c_begin * kChunkBytes + sb - 1) / sb;
+  if (b < 0) b = 0;
+  int64_t e = (in_hi - d.c_begin * kChunkBytes) / sb;
+  const int64_t h = (d.hi - 4 - d.c_begin * kChunkBytes) / sb;
+  if (e > h) e = h;
+  if (e < b) e = b;
+  *int_b = b;
+  *int_d = e;
+}
+
+// Errors of step `step` (any step: interior steps take the plain loads, edge
+// steps the masked ones and lane ranges).  The chunk after the last evaluated
+// one is loaded too: its first byte is the lookahead of the last evaluated
+// lane (lead form).
+template <bool kPos>
+__device__ __forceinline__ uint32_t any_step_errors(const StreamDesc& d, int64_t step, bool interior, int lane,
+                                                    int& first_i, bool& was_ascii) {
+  const int64_t sb = kStepChunks * (int64_t)kChunkBytes;
+  const int64_t cstep = d.c_begin + step * kStepChunks;
+  const int64_t s0 = cstep * kChunkBytes;
+  Chunk v[kU];
+  uint32_t carry_word = 0, nsw = 0;
+  if (interior) {
+    const uint8_t* p = d.base + s0 + lane * kChunkBytes;
+#pragma unroll
+    for (int i = 0; i < kU; ++i) v[i] = ld_chunk(p + 32 * i * kChunkBytes);
+    if (lane == 31) carry_word = ld_word_guarded(d.base, s0 - 4, d.lo, d.hi);
+    if (lane == 0) nsw = __ldg(reinterpret_cast<const uint32_t*>(d.base + s0 + sb));
+    return step_errors<kPos, false>(d, v, cstep, lane, carry_word, nsw, first_i, was_ascii);
+  }
+#pragma unroll
+  for (int i = 0; i < kU; ++i) {
+    const int64_t c = cstep + lane + 32 * i;
+    v[i] = c <= d.c_end ? ld_chunk_masked(d.base, c, d.lo, d.hi) : zero_chunk();
+  }
+  if (lane == 31) carry_word = ld_word_guarded(d.base, s0 - 4, d.lo, d.hi);
+  if (lane == 0) nsw = ld_word_guarded(d.base, s0 + sb, d.lo, d.hi);
+  return step_errors<kPos, true>(d, v, cstep, lane, carry_word, nsw, first_i, was_ascii);
+}
+
+// K1.  Steps are dealt to warps round-robin (step = warp + j * nwarps): at
+// any moment all warps sweep one window of ~nwarps * 4 KiB, which keeps DRAM
 // pages open (+2.5% over contiguous per-warp ranges, tools/kbench.cu V19).
 // Steps are therefore independent: each loads its own halo word (lane 31,
 // the word before the step) and lookahead word (lane 0, the word after).
-template <bool kPos>
-__global__ void __launch_bounds__(kThreads, 4)
-    k_validate(StreamDesc d, uint32_t* __restrict__ flag,
-               unsigned long long* __restrict__ first_chunk) {
+__global__ void __launch_bounds__(kThreads, 4) k_validate(StreamDesc d, uint32_t* __restrict__ flag) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * kThreads) >> 5;
-  const int64_t in_lo = d.lo > d.L0 ? d.lo : d.L0;  // interior: all bytes real,
-  const int64_t in_hi = d.hi < d.L1 ? d.hi : d.L1;  // all lanes wanted
-  // Interior steps with an in-range lookahead word form one contiguous run
-  // [int_b, int_d) of step indices; only the head/tail steps take masked loads.
   const int64_t sb = kStepChunks * (int64_t)kChunkBytes;
-  int64_t int_b = (in_lo - d.c_begin * kChunkBytes + sb - 1) / sb;
-  if (int_b < 0) int_b = 0;
-  int64_t int_d = (in_hi - d.c_begin * kChunkBytes) / sb;
-  const int64_t int_h = (d.hi - 4 - d.c_begin * kChunkBytes) / sb;
-  if (int_d > int_h) int_d = int_h;
-  if (int_d < int_b) int_d = int_b;
+  int64_t int_b, int_d;
+  interior_steps(d, &int_b, &int_d);
 
   uint32_t acc = 0;
   bool was_ascii = true;  // try the vote on the first step
+  int unused = kU;
   for (int64_t step = warp; step < d.steps; step += nwarps) {
-    if (!kPos && step >= int_b && step < int_d) {
+    if (step >= int_b && step < int_d) {
       // Hot loop over this warp's interior steps: a pointer advanced by
       // nwarps steps and a 32-bit trip count keep the state in registers.
       const int n = (int)((int_d - 1 - step) / nwarps) + 1;
       const int64_t stride = nwarps * sb;
       const uint8_t* p = d.base + (d.c_begin + step * kStepChunks) * kChunkBytes;
-      int unused = kU;
       for (int j = 0; j < n; ++j, p += stride) {
         Chunk v[kU];
 #pragma unroll
@@ -138,40 +175,46 @@ __global__ void __launch_bounds__(kThreads, 4)
       step += (int64_t)(n - 1) * nwarps;
       continue;
     }
-    const int64_t cstep = d.c_begin + step * kStepChunks;
-    const int64_t s0 = cstep * kChunkBytes;
-    Chunk v[kU];
-    uint32_t carry_word = 0, nsw = 0;
-    uint32_t step_err;
+    acc |= any_step_errors<false>(d, step, false, lane, unused, was_ascii);
+  }
+  const unsigned any = __reduce_or_sync(0xFFFFFFFFu, acc);
+  if (lane == 0 && any) atomicOr(flag, 1u);
+}
+
+// K3: the first 32-byte chunk that holds a flagged lane.  Steps are claimed
+// in order, one round of kThreads/32 consecutive steps per CTA and atomicAdd,
+// together with the earliest flagged chunk recorded so far: a round that
+// starts after it cannot hold an earlier one, and every later round starts
+// later still, so the CTA stops.  K3 therefore scans about the prefix up to
+// the first error (plus the rounds in flight, <= one per resident CTA).
+// Chunks of a step are ordered (i, lane): the warp's first flagged chunk is
+// the minimum over lanes of cstep + lane + 32 * first_i.
+__global__ void __launch_bounds__(kThreads, 4)
+    k_first_error(StreamDesc d, uint32_t* __restrict__ flag, unsigned long long* __restrict__ first_chunk,
+                  unsigned long long* __restrict__ next_round) {
+  constexpr int kWarps = kThreads / 32;
+  __shared__ unsigned long long s_round, s_seen;
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  int64_t int_b, int_d;
+  interior_steps(d, &int_b, &int_d);
+  bool was_ascii = true;
+  for (;;) {
+    if (threadIdx.x == 0) {
+      s_round = atomicAdd(next_round, 1ull);
+      s_seen = *reinterpret_cast<volatile const unsigned long long*>(first_chunk);
+    }
+    __syncthreads();
+    const int64_t step0 = (int64_t)s_round * kWarps;
+    const unsigned long long seen = s_seen;
+    __syncthreads();
+    if (step0 >= d.steps || (unsigned long long)(d.c_begin + step0 * kStepChunks) > seen) break;
+    const int64_t step = step0 + wib;
+    if (step >= d.steps) continue;
     int first_i = kU;
-    if (step >= int_b && step < int_d) {
-      const uint8_t* p = d.base + s0 + lane * kChunkBytes;
-#pragma unroll
-      for (int i = 0; i < kU; ++i) v[i] = ld_chunk(p + 32 * i * kChunkBytes);
-      if (lane == 31) carry_word = ld_word_guarded(d.base, s0 - 4, d.lo, d.hi);
-      if (lane == 0) nsw = __ldg(reinterpret_cast<const uint32_t*>(d.base + s0 + sb));
-      step_err = step_errors<kPos, false>(d, v, cstep, lane, carry_word, nsw, first_i, was_ascii);
-    } else {
-      // Edge step (stream head or tail): masked loads and lane ranges.  The
-      // chunk after the last evaluated one is loaded too: its first byte is
-      // the lookahead of the last evaluated lane (lead form).
-#pragma unroll
-      for (int i = 0; i < kU; ++i) {
-        const int64_t c = cstep + lane + 32 * i;
-        v[i] = c <= d.c_end ? ld_chunk_masked(d.base, c, d.lo, d.hi) : zero_chunk();
-      }
-      if (lane == 31) carry_word = ld_word_guarded(d.base, s0 - 4, d.lo, d.hi);
-      if (lane == 0) nsw = ld_word_guarded(d.base, s0 + sb, d.lo, d.hi);
-      step_err = step_errors<kPos, true>(d, v, cstep, lane, carry_word, nsw, first_i, was_ascii);
-    }
-    if (!kPos) {
-      acc |= step_err;
-      continue;
-    }
-    // K3: chunks of a step are ordered (i, lane); the warp's first flagged
-    // chunk is the minimum over lanes of cstep + lane + 32 * first_i, and the
-    // warp's later steps cannot hold an earlier one.
+    any_step_errors<true>(d, step, step >= int_b && step < int_d, lane, first_i, was_ascii);
     if (__any_sync(0xFFFFFFFFu, first_i < kU)) {
+      const int64_t cstep = d.c_begin + step * kStepChunks;
       unsigned long long m = first_i < kU ? (unsigned long long)(cstep + lane + 32 * first_i) : ~0ull;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
@@ -182,12 +225,7 @@ __global__ void __launch_bounds__(kThreads, 4)
         atomicMin(first_chunk, m);
         atomicOr(flag, 1u);
       }
-      return;
     }
-  }
-  if (!kPos) {
-    const unsigned any = __reduce_or_sync(0xFFFFFFFFu, acc);
-    if (lane == 0 && any) atomicOr(flag, 1u);
   }
 }
 
@@ -258,7 +296,7 @@ int max_resident_warps() {
     int dev = 0, sms = 0, blocks = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_validate<false>, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_validate, kThreads, 0);
     if (blocks < 1) blocks = 1;
     warps = sms * blocks * (kThreads / 32);
   }
@@ -294,16 +332,20 @@ void launch_validate(const StreamDesc& d, uint32_t* flag, cudaStream_t st) {
   if (d.steps <= 0) return;
   const int64_t warps = (d.steps + d.steps_per_warp - 1) / d.steps_per_warp;
   const int64_t blocks = (warps * 32 + kThreads - 1) / kThreads;
-  k_validate<false><<<(unsigned)blocks, kThreads, 0, st>>>(d, flag, nullptr);
+  k_validate<<<(unsigned)blocks, kThreads, 0, st>>>(d, flag);
 }
 
-void launch_first_error(const StreamDesc& d, uint64_t n, uint32_t* flag,
-                        unsigned long long* first_chunk, unsigned long long* out_offset,
-                        int* out_kind, cudaStream_t st) {
+void launch_first_error(const StreamDesc& d, uint64_t n, uint32_t* flag, unsigned long long* first_chunk,
+                        unsigned long long* next_round, unsigned long long* out_offset, int* out_kind,
+                        cudaStream_t st) {
   if (d.steps > 0) {
-    const int64_t warps = (d.steps + d.steps_per_warp - 1) / d.steps_per_warp;
-    const int64_t blocks = (warps * 32 + kThreads - 1) / kThreads;
-    k_validate<true><<<(unsigned)blocks, kThreads, 0, st>>>(d, flag, first_chunk);
+    // Enough CTAs to fill the GPU; each claims rounds until the stream (or
+    // the prefix before the first error) is exhausted.
+    const int64_t rounds = (d.steps + kThreads / 32 - 1) / (kThreads / 32);
+    const int64_t resident = max_resident_warps() / (kThreads / 32);
+    const int64_t blocks = rounds < resident ? rounds : resident;
+    cudaMemsetAsync(next_round, 0, sizeof(*next_round), st);
+    k_first_error<<<(unsigned)blocks, kThreads, 0, st>>>(d, flag, first_chunk, next_round);
   }
   k_locate<<<1, 32, 0, st>>>(d.base + d.off32, n, d.off32, first_chunk, out_offset, out_kind);
 }

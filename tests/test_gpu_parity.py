@@ -328,6 +328,35 @@ def test_lane_ranges_compose(torch):
         assert int(flag.item()) != 0
 
 
+def test_first_error_ordered_claims(torch):
+    """K3 claims 32 KiB rounds (8 warp steps) in order and stops past the
+    earliest flagged chunk recorded so far: with several errors, at round
+    and step boundaries, the reported one is always the first."""
+    d = configs.gen_c1(64 << 20, seed=21)
+    h = d.cpu().numpy()
+    n = h.size
+    rng = np.random.default_rng(8)
+    rnd = 8 * 4096
+    cands = [0, 1, rnd - 1, rnd, rnd + 1, 4096 - 2, 7 * rnd + 4095, n // 2, n // 2 + rnd, n - 2, n - 1]
+    cands += [int(x) for x in rng.integers(0, n, 12)]
+    for trial in range(12):
+        k = int(rng.integers(1, 5))
+        picks = sorted(set(int(cands[i]) for i in rng.integers(0, len(cands), k)))
+        bad = h.copy()
+        for p in picks:
+            bad[p] = 0xFF if trial % 3 else 0x80
+        exp = nat.oracle_verdict(bad, threads=16)
+        v = u8.validate_lookup_verdict(torch.from_numpy(bad).cuda())
+        if exp[0]:  # 0x80 over a continuation byte can stay valid
+            assert v.valid()
+            continue
+        assert (v.error.offset, int(v.error.kind)) == (exp[1], exp[2]), (picks, trial)
+    # garbage everywhere: every round flags, the answer is the first byte's
+    g = torch.from_numpy(np.full(n, 0xFF, np.uint8)).cuda()
+    v = u8.validate_lookup_verdict(g)
+    assert (v.error.offset, int(v.error.kind)) == (0, int(u8.ErrorKind.HEADER_BITS))
+
+
 # ---- configs -----------------------------------------------------------------
 def test_c0_full_size():
     d = configs.gen_c0()
