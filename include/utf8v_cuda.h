@@ -48,7 +48,12 @@ extern "C" {
 /* ABI version (bumped on any signature or contract change).
  *   1  first round-1 interface
  *   2  streaming session, utf8v_cuda_validate_sharded; the async batch entry
- *      point reads its first/last offsets on the device (no host sync) */
+ *      point reads its first/last offsets on the device (no host sync)
+ *   3  device input to the synchronous entry points (is_device = 1) and to
+ *      utf8v_cuda_stream_feed is ordered after all work issued before the
+ *      call to the legacy default stream, like a synchronous cudaMemcpy;
+ *      writes made on a non-blocking stream must be synchronised by the
+ *      caller */
 int utf8v_cuda_abi_version(void);
 
 /* Human-readable text of the last error on this thread ("" if none). */

@@ -87,11 +87,22 @@ def _host_view(data):
     return ptr, int(a.size), a
 
 
+def _after_current_stream(t) -> None:
+    """The C-ABI orders device input after the legacy default stream (torch's
+    default stream); bytes written on another current torch stream are
+    waited for here."""
+    import torch
+    cur = torch.cuda.current_stream(t.device)
+    if cur.cuda_stream != 0:
+        cur.synchronize()
+
+
 def _input(data):
     """(pointer, size, is_device, keepalive)."""
     if _is_cuda_tensor(data):
         if data.dtype.itemsize != 1 or not data.is_contiguous():
             raise ValueError("device input must be a contiguous 1-byte tensor")
+        _after_current_stream(data)
         return (data.data_ptr() if data.numel() else None), int(data.numel()), 1, data
     ptr, n, keep = _host_view(data)
     return ptr, n, 0, keep

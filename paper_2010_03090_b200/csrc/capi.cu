@@ -92,6 +92,7 @@ struct Ctx {
   // of the DMA that last read each slot.
   uint8_t* h_ring = nullptr;
   cudaEvent_t slot_done[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t ev_legacy = nullptr;          // see after_legacy()
 };
 constexpr int kSlots = 4;
 thread_local Ctx t_ctx[kMaxDevices];
@@ -119,9 +120,20 @@ int get_ctx(Ctx** out) {
     CK(cudaMalloc(&c.d_lanes, 4 * UTF8V_CUDA_WIDTH));
     CK(cudaMalloc(&c.d_ok, 64));
     CK(cudaMallocHost(&c.h_res, 256));
+    CK(cudaEventCreateWithFlags(&c.ev_legacy, cudaEventDisableTiming));
     c.ready = true;
   }
   *out = &c;
+  return UTF8V_OK;
+}
+
+// Device input to the synchronous entry points is ordered like a
+// synchronous cudaMemcpy: after all work issued before the call to the legacy
+// default stream (and, through it, to every blocking stream).  The library
+// streams are non-blocking, so the order is made explicit with one event.
+int after_legacy(cudaStream_t s, cudaEvent_t ev) {
+  CK(cudaEventRecord(ev, cudaStreamLegacy));
+  CK(cudaStreamWaitEvent(s, ev, 0));
   return UTF8V_OK;
 }
 
@@ -328,7 +340,7 @@ int validate_host_lanes(Ctx& c, const uint8_t* p, size_t n, uint64_t lane_lo, ui
 
 extern "C" {
 
-int utf8v_cuda_abi_version(void) { return 2; }
+int utf8v_cuda_abi_version(void) { return 3; }
 
 const char* utf8v_cuda_last_error(void) { return t_err.c_str(); }
 
@@ -347,6 +359,8 @@ int utf8v_cuda_validate(const uint8_t* p, size_t n, int is_device, uint8_t* out_
   if (st) return st;
   CK(cudaMemsetAsync(c->d_flag, 0, 4, c->s_comp));
   if (is_device) {
+    st = after_legacy(c->s_comp, c->ev_legacy);
+    if (st) return st;
     u8v::launch_validate(u8v::make_desc(p, n, 0, n + 3), c->d_flag, c->s_comp);
     ++t_launches;
   } else {
@@ -383,6 +397,8 @@ int utf8v_cuda_validate_verdict(const uint8_t* p, size_t n, int is_device, uint8
   const uint8_t* d = p;
   CK(cudaMemsetAsync(c->d_flag, 0, 4, c->s_comp));
   if (is_device) {
+    st = after_legacy(c->s_comp, c->ev_legacy);
+    if (st) return st;
     u8v::launch_validate(u8v::make_desc(p, n, 0, n + 3), c->d_flag, c->s_comp);
     ++t_launches;
   } else {
@@ -450,6 +466,8 @@ int utf8v_cuda_validate_lanes(const uint8_t* p, uint64_t n, uint64_t lane_lo, ui
   if (st) return st;
   CK(cudaMemsetAsync(c->d_flag, 0, 4, c->s_comp));
   if (is_device) {
+    st = after_legacy(c->s_comp, c->ev_legacy);
+    if (st) return st;
     u8v::launch_validate(u8v::make_desc(p, n, lane_lo, lane_hi), c->d_flag, c->s_comp);
     ++t_launches;
   } else {
@@ -493,6 +511,8 @@ int utf8v_cuda_validate_batch(const uint8_t* data, size_t n, const uint64_t* off
   if (is_device) {
     Ctx* c;
     int st = get_ctx(&c);
+    if (st) return st;
+    st = after_legacy(c->s_comp, c->ev_legacy);
     if (st) return st;
     st = utf8v_cuda_validate_batch_async(data, n, offsets, n_records, verdicts, nullptr, c->s_comp);
     if (st) return st;
@@ -640,6 +660,7 @@ struct utf8v_cuda_stream {
   uint8_t* d_buf = nullptr;     // staging for host pieces
   size_t cap = 0;
   uint64_t total = 0;
+  cudaEvent_t ev_legacy = nullptr;  // see after_legacy()
 };
 
 int utf8v_cuda_stream_create(utf8v_cuda_stream** out) {
@@ -652,6 +673,7 @@ int utf8v_cuda_stream_create(utf8v_cuda_stream** out) {
   cudaGetDevice(&s->dev);
   if (cudaStreamCreateWithFlags(&s->s, cudaStreamNonBlocking) != cudaSuccess ||
       cudaMalloc(&s->d_state, 64) != cudaSuccess || cudaMallocHost(&s->h_res, 64) != cudaSuccess ||
+      cudaEventCreateWithFlags(&s->ev_legacy, cudaEventDisableTiming) != cudaSuccess ||
       cudaMemsetAsync(s->d_state, 0, 64, s->s) != cudaSuccess) {
     const cudaError_t e = cudaGetLastError();
     utf8v_cuda_stream_destroy(s);
@@ -668,7 +690,10 @@ int utf8v_cuda_stream_feed(utf8v_cuda_stream* s, const uint8_t* p, size_t n, int
   if (!p) return fail(UTF8V_ERR_ARG, "NULL piece");
   CK(cudaSetDevice(s->dev));
   const uint8_t* d = p;
-  if (!is_device) {
+  if (is_device) {
+    const int st = after_legacy(s->s, s->ev_legacy);
+    if (st) return st;
+  } else {
     if (s->cap < n) {
       if (s->d_buf) {
         CK(cudaStreamSynchronize(s->s));
@@ -717,6 +742,7 @@ void utf8v_cuda_stream_destroy(utf8v_cuda_stream* s) {
   if (s->d_buf) cudaFree(s->d_buf);
   if (s->d_state) cudaFree(s->d_state);
   if (s->h_res) cudaFreeHost(s->h_res);
+  if (s->ev_legacy) cudaEventDestroy(s->ev_legacy);
   if (s->s) cudaStreamDestroy(s->s);
   delete s;
 }

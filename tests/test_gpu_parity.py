@@ -357,6 +357,33 @@ def test_first_error_ordered_claims(torch):
     assert (v.error.offset, int(v.error.kind)) == (0, int(u8.ErrorKind.HEADER_BITS))
 
 
+def test_device_input_ordered_after_torch_work(torch):
+    """Device input written asynchronously (a 256 MiB copy/fill still in
+    flight) is seen by the synchronous calls and the stream session: the
+    C-ABI orders after the legacy default stream (ABI 3), the Python mirror
+    after torch's current stream."""
+    d = configs.gen_c1(256 << 20, seed=31)
+    x = torch.empty_like(d)
+    for trial in range(3):
+        x.fill_(0xFF)
+        x.copy_(d)                      # in flight on the default stream
+        assert u8.validate_lookup(x) is True
+        x.fill_(0xFF)
+        assert u8.validate_lookup_verdict(x).error.offset == 0
+        x.copy_(d)
+        with u8.LookupStream() as sess:
+            sess.feed(x[: 100 << 20]).feed(x[100 << 20:])
+            assert sess.finish() is True
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            x.fill_(0xC0)               # in flight on a non-default stream
+            assert u8.validate_lookup(x) is False
+            x.copy_(d)
+            assert u8.validate_lookup(x) is True
+        torch.cuda.current_stream().wait_stream(side)
+
+
 # ---- configs -----------------------------------------------------------------
 def test_c0_full_size():
     d = configs.gen_c0()
