@@ -143,8 +143,8 @@ uint64_t utf8v_cuda_batch_scratch_bytes(uint64_t n);
  * streaming non-goal of SPEC.md:312): feed pieces in order, finish() gives
  * the verdict of their concatenation.  The session carries 4 bytes and an
  * error flag on the device; every piece is validated in place (device
- * pieces are not copied), only the <= 4 lanes straddling a piece boundary run
- * in a one-thread kernel (csrc/utf8v_stream.h).  Pieces may have any length,
+ * pieces are not copied) by one K1 launch whose first thread also evaluates
+ * the <= 4 lanes straddling the previous piece (csrc/stream_edge.cuh).  Pieces may have any length,
  * including 0.  Device pieces must stay valid until the next call on the
  * session (the work is asynchronous on the session's own stream); host
  * pieces are consumed before feed returns.  finish() resets the session. */

@@ -708,13 +708,17 @@ int utf8v_cuda_stream_feed(utf8v_cuda_stream* s, const uint8_t* p, size_t n, int
     CK(cudaMemcpyAsync(s->d_buf, p, n, cudaMemcpyHostToDevice, s->s));
     d = s->d_buf;
   }
-  // Lanes straddling the previous piece, then the piece's own lanes in place.
-  u8v::launch_stream_edge(s->d_state, d, n, 0, s->s);
-  ++t_launches;
-  if (n > 4) {
-    u8v::launch_validate(u8v::make_desc(d, n, 3, n - 1), s->d_state + 1, s->s);
-    ++t_launches;
+  // The piece's own lanes in place; K1's first thread also runs the lanes
+  // straddling the previous piece (a piece too short for K1 lanes runs them
+  // in the one-thread edge kernel).
+  u8v::StreamDesc desc = u8v::make_desc(d, n, 3, n > 4 ? n - 1 : 3);
+  if (desc.steps > 0) {
+    desc.session = s->d_state;
+    u8v::launch_validate(desc, s->d_state + 1, s->s);
+  } else {
+    u8v::launch_stream_edge(s->d_state, d, n, 0, s->s);
   }
+  ++t_launches;
   s->total += n;
   if (!is_device) CK(cudaStreamSynchronize(s->s));  // the caller may reuse its buffer
   return check_launch("stream feed");

@@ -27,6 +27,8 @@ struct StreamDesc {
   int64_t steps;           // ceil((c_end - c_begin) / kStepChunks)
   int64_t steps_per_warp;
   u8v_consts k;  // runtime multipliers (FMA-pipe routing, utf8v_swar.h)
+  uint32_t* session;  // non-null: K1's first thread also runs the stream-session
+                      // edge of this piece (stream_edge.cuh) on session[0..1]
 };
 
 int max_resident_warps();

@@ -29,6 +29,7 @@
 
 #include "chunk.cuh"
 #include "kernels.cuh"
+#include "stream_edge.cuh"
 #include "utf8v_swar.h"
 
 namespace u8v {
@@ -146,6 +147,8 @@ __device__ __forceinline__ uint32_t any_step_errors(const StreamDesc& d, int64_t
 // Steps are therefore independent: each loads its own halo word (lane 31,
 // the word before the step) and lookahead word (lane 0, the word after).
 __global__ void __launch_bounds__(kThreads, 4) k_validate(StreamDesc d, uint32_t* __restrict__ flag) {
+  if (d.session != nullptr && blockIdx.x == 0 && threadIdx.x == 0)
+    stream_edge_piece(d.session, d.base + d.off32, (uint64_t)(d.hi - d.lo), 0);
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * kThreads) >> 5;
@@ -325,6 +328,7 @@ StreamDesc make_desc(const uint8_t* p, uint64_t n, uint64_t lane_lo, uint64_t la
   if (warps > d.steps) warps = d.steps;
   if (warps < 1) warps = 1;
   d.steps_per_warp = (d.steps + warps - 1) / warps;
+  d.session = nullptr;
   return d;
 }
 

@@ -93,7 +93,7 @@ def test_large_device_stream_and_launch_count():
         for c in cuts + [d.numel()]:
             s.feed(d[prev:c])
             n = c - prev
-            assert lib.utf8v_cuda_last_launch_count() == (0 if n == 0 else (1 if n <= 4 else 2))
+            assert lib.utf8v_cuda_last_launch_count() == (0 if n == 0 else 1)  # K1 runs the edge too
             prev = c
         assert s.bytes_fed == d.numel()
         assert s.finish() is True
