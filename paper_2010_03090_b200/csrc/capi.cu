@@ -714,7 +714,12 @@ int utf8v_cuda_stream_feed(utf8v_cuda_stream* s, const uint8_t* p, size_t n, int
   u8v::StreamDesc desc = u8v::make_desc(d, n, 3, n > 4 ? n - 1 : 3);
   if (desc.steps > 0) {
     desc.session = s->d_state;
-    u8v::launch_validate(desc, s->d_state + 1, s->s);
+    // Device pieces overlap the previous feed's K1 (the only other work on
+    // the session stream); a host piece's K1 follows its own H2D copy.
+    if (is_device)
+      u8v::launch_validate_piece(desc, s->d_state + 1, s->s);
+    else
+      u8v::launch_validate(desc, s->d_state + 1, s->s);
   } else {
     u8v::launch_stream_edge(s->d_state, d, n, 0, s->s);
   }

@@ -34,6 +34,10 @@ struct StreamDesc {
 int max_resident_warps();
 StreamDesc make_desc(const uint8_t* p, uint64_t n, uint64_t lane_lo, uint64_t lane_hi);
 void launch_validate(const StreamDesc& d, uint32_t* flag, cudaStream_t st);
+// A stream-session piece (d.session set, d.steps > 0) on the session's own
+// stream: K1 launched with programmatic stream serialization, so consecutive
+// feeds overlap; the edge thread waits for the previous feed (validate.cu).
+void launch_validate_piece(const StreamDesc& d, uint32_t* flag, cudaStream_t st);
 void launch_first_error(const StreamDesc& d, uint64_t n, uint32_t* flag, unsigned long long* first_chunk,
                         unsigned long long* next_round, unsigned long long* out_offset, int* out_kind,
                         cudaStream_t st);

@@ -147,8 +147,17 @@ __device__ __forceinline__ uint32_t any_step_errors(const StreamDesc& d, int64_t
 // Steps are therefore independent: each loads its own halo word (lane 31,
 // the word before the step) and lookahead word (lane 0, the word after).
 __global__ void __launch_bounds__(kThreads, 4) k_validate(StreamDesc d, uint32_t* __restrict__ flag) {
-  if (d.session != nullptr && blockIdx.x == 0 && threadIdx.x == 0)
-    stream_edge_piece(d.session, d.base + d.off32, (uint64_t)(d.hi - d.lo), 0);
+  if (d.session != nullptr) {
+    // Session feeds are launched with programmatic stream serialization
+    // (launch_validate_piece): the next piece's grid may start as soon as
+    // every block of this one has started, and only the edge thread, which
+    // reads the carry the previous feed wrote, waits for that feed.
+    asm volatile("griddepcontrol.launch_dependents;");
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      stream_edge_piece(d.session, d.base + d.off32, (uint64_t)(d.hi - d.lo), 0);
+    }
+  }
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * kThreads) >> 5;
@@ -337,6 +346,20 @@ void launch_validate(const StreamDesc& d, uint32_t* flag, cudaStream_t st) {
   const int64_t warps = (d.steps + d.steps_per_warp - 1) / d.steps_per_warp;
   const int64_t blocks = (warps * 32 + kThreads - 1) / kThreads;
   k_validate<<<(unsigned)blocks, kThreads, 0, st>>>(d, flag);
+}
+
+void launch_validate_piece(const StreamDesc& d, uint32_t* flag, cudaStream_t st) {
+  const int64_t warps = (d.steps + d.steps_per_warp - 1) / d.steps_per_warp;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)((warps * 32 + kThreads - 1) / kThreads));
+  cfg.blockDim = dim3(kThreads);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_validate, d, flag);
 }
 
 void launch_first_error(const StreamDesc& d, uint64_t n, uint32_t* flag, unsigned long long* first_chunk,
