@@ -8,23 +8,21 @@
 // B200 design: the records' bytes are contiguous in HBM with a CSR offsets
 // array, so the kernel ignores record sizes for load balance and sweeps the
 // byte array exactly like K1 (4 KiB warp steps, 32-byte chunks, one 256-bit
-// LDG each, halo and lookahead by SHFL).  Record starts only matter where
-// they fall inside a chunk's look-back window:
-//   * each step reads a window of 32 record starts (one coalesced load; more
-//     windows only if the step holds more than 31 starts);
-//   * a step with no start in it ("single") runs K1's chunk code unchanged;
-//   * otherwise the lanes holding a start OR a bit into a per-warp shared
-//     mask of the chunk it falls in (and the next chunk's look-back bits), and
-//     only chunks with a nonzero mask take the record-bounded word function
-//     (u8v_word_errors_bounded_lead), out of line so the hot loop stays small
-//     in the instruction cache.
-// Record attribution (a short scan of the offsets) runs only for chunks that
-// hold an error.  Verdicts start at 1 (memset by the caller) and invalid
-// records get a plain 0 store (idempotent, no atomics).
-//
-// The rare-pair check needs no record masking in the lead form: a flagged
-// pair (j, j+1) that crosses into the next record means byte j is a lead
-// ending its record, which is invalid anyway (utf8v_swar.h).
+// LDG each, halo and lookahead by SHFL, the same unbounded permuted plane
+// form).  A lane's record-bounded flag can differ from its unbounded one
+// only for the first three lanes of a record (their look-back crosses the
+// start) and for the previous record's end-of-stream lanes, so:
+//   * a flagged lane (rare) is attributed, out of line, to its record unless
+//     it is one of that record's first three lanes;
+//   * every record start is checked on its own: the window lane that holds
+//     it reads the 8 bytes around it (L2-hot: the sweep just streamed them)
+//     and runs u8v_boundary_errors (utf8v_swar.h) for the record ending there
+//     and the record starting there.
+// The decomposition is proven against per-record validation on the CPU
+// (tests/test_swar.py::test_k2_boundary_decomposition_adversarial).  Each
+// step reads a window of 32 record starts (one coalesced load) only when
+// the next start falls inside it.  Verdicts start at 1 (memset by the
+// caller) and invalid records get a plain 0 store (idempotent, no atomics).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -46,8 +44,6 @@ struct BatchDesc {
   int64_t n_bytes;  // data size (clamp for malformed offsets)
   u8v_consts k;  // runtime multipliers (FMA-pipe routing, utf8v_swar.h)
 };
-
-constexpr int kWarpsPerCta = kThreads / 32;
 
 // What the record lookups need, passed by value: the out-of-line
 // attribution taking the whole descriptor by reference would pin it in local
@@ -88,42 +84,111 @@ __device__ int64_t find_record(const RecView& d, int64_t pos) {
   return r < d.n_records ? r : d.n_records - 1;
 }
 
-// Record holding byte q (base coords), scanning forward from record r
-// (start(r) <= q).  n_records when q is past the last record.
-__device__ int64_t record_of(const RecView& d, int64_t r, int64_t q) {
-  while (r < d.n_records && rec_start(d, r + 1) <= q) ++r;
-  return r < d.n_records ? r : d.n_records;
+// Window positions are 32-bit offsets from the step start, clamped far out
+// of the step on either side (compares and shuffles stay 32-bit).
+constexpr int kFar = 1 << 30;
+__device__ __forceinline__ int rel32(int64_t pos, int64_t s0) {
+  const int64_t r = pos - s0;
+  return r > kFar ? kFar : (r < -kFar ? -kFar : (int)r);
 }
 
-__device__ __forceinline__ void mark_invalid(const RecView& d, int64_t r_from, int64_t q) {
-  if (q < rec_start(d, 0)) return;
-  const int64_t r = record_of(d, r_from, q);
-  if (r < d.n_records) d.verdicts[r] = 0;
+// Out of line, for steps with a flagged lane: each flagged lane q goes to
+// its record -- the last window start at or before q, found by a 5-step
+// shuffle search over the window (lane L holds start(r0 + L) - s0), or r0
+// when the step holds no start -- unless q is one of that record's first
+// three lanes or lies past the data (those lanes are settled by
+// fix_boundary).  err[i]: lane bits of chunk (lane + 32 i) of the step in
+// the permuted plane order of utf8v_bits.h (bit pos(i) = byte i).
+__device__ __noinline__ void attribute_step(RecView d, int64_t s0, int64_t hi, const uint32_t* err_in,
+                                            int o, bool window, int64_t r0, int base_rel) {
+  const int lane = threadIdx.x & 31;
+  const bool full = window && __all_sync(0xFFFFFFFFu, o < kStepChunks * kChunkBytes);
+  const int hi_rel = rel32(hi, s0);
+#pragma unroll 1
+  for (int i = 0; i < kU; ++i) {
+    uint32_t e = err_in[i];
+    while (__any_sync(0xFFFFFFFFu, e != 0u)) {
+      int q = -1;
+      if (e) {
+        const int bit = __ffs(e) - 1;
+        e &= e - 1;
+        q = (lane + 32 * i) * kChunkBytes + (int)u8v_perm_byte((unsigned)bit);
+      }
+      int L = 0;
+      if (window) {
+#pragma unroll
+        for (int st = 16; st > 0; st >>= 1) {
+          const int cand = L + st;
+          const int t = __shfl_sync(0xFFFFFFFFu, o, cand & 31);
+          if (cand <= 31 && t <= q) L = cand;
+        }
+      }
+      const int start = window ? __shfl_sync(0xFFFFFFFFu, o, L) : base_rel;
+      if (q >= 0 && q < hi_rel && q >= start) {
+        int64_t r = r0 + L;
+        int64_t st_abs = s0 + start;
+        if (full && L == 31) {  // more starts than one window holds: walk on
+          const int64_t qa = s0 + q;
+          while (r < d.n_records && rec_start(d, r + 1) <= qa) ++r;
+          st_abs = rec_start(d, r);
+        }
+        if (r < d.n_records && s0 + q - st_abs >= 3) d.verdicts[r] = 0;
+      }
+    }
+  }
 }
 
-// Out-of-line, only for chunks with a flagged lane: the record of every
-// flagged lane, and the record ending at every flagged record start (its end
-// check), is marked invalid.  err / end: lane bits of chunk c in the permuted
-// plane order of utf8v_bits.h (bit pos(i) = byte i).
-__device__ __noinline__ void attribute_chunk(RecView d, int64_t c, uint32_t err, uint32_t end,
-                                             int64_t r_from) {
-  const int64_t q0 = c * kChunkBytes;
-  while (err) {
-    const int i = __ffs(err) - 1;
-    err &= err - 1;
-    mark_invalid(d, r_from, q0 + u8v_perm_byte((unsigned)i));
+// Bytes s-4 .. s+3 (base coords) as one little-endian word: two aligned
+// 8-byte loads when they lie in chunks the sweep reads anyway, else byte by
+// byte inside [lo, hi).  Bytes outside the two records are masked later.
+__device__ __forceinline__ uint64_t bytes_around(const uint8_t* base, int64_t s, int64_t lo, int64_t hi) {
+  const int64_t a0 = (s - 4) & ~(int64_t)7;
+  if (a0 >= (lo & ~(int64_t)31) && a0 + 16 <= ((hi + 31) & ~(int64_t)31)) {
+    const uint64_t w0 = __ldg(reinterpret_cast<const unsigned long long*>(base + a0));
+    const uint64_t w1 = __ldg(reinterpret_cast<const unsigned long long*>(base + a0 + 8));
+    const unsigned sh = (unsigned)(s - 4 - a0) * 8u;
+    return sh ? (w0 >> sh) | (w1 << (64u - sh)) : w0;
   }
-  while (end) {
-    const int i = __ffs(end) - 1;
-    end &= end - 1;
-    mark_invalid(d, r_from, q0 + u8v_perm_byte((unsigned)i) - 1);
+  uint64_t w = 0;
+  for (int k = 0; k < 8; ++k) {
+    const int64_t q = s - 4 + k;
+    if (q >= lo && q < hi) w |= (uint64_t)base[q] << (8 * k);
   }
+  return w;
+}
+
+// The record boundary at s: record rr-1 = [a, s) ends there, record rr =
+// [s, b) starts there (either may be empty or absent).
+__device__ __forceinline__ void fix_boundary(const RecView& rv, const uint8_t* base, int64_t lo, int64_t hi,
+                                             int64_t s, int64_t a, int64_t b, int64_t rr, u8v_consts k) {
+  const uint64_t w8 = bytes_around(base, s, lo, hi);
+  int64_t ka = a - (s - 4), kb = b - (s - 4);
+  ka = ka < 0 ? 0 : (ka > 4 ? 4 : ka);
+  kb = kb < 4 ? 4 : (kb > 8 ? 8 : kb);
+  const uint32_t f = u8v_boundary_errors(w8, (unsigned)ka, (unsigned)kb, k);
+  if ((f & 1u) && rr > 0) rv.verdicts[rr - 1] = 0;
+  if ((f & 2u) && rr < rv.n_records) rv.verdicts[rr] = 0;
+}
+
+// One batch of record boundaries: lane L takes start(r_f + L) when it lies in
+// the warp's byte range [range_lo, range_hi).  f_prev = start(r_f - 1).
+// Returns start(r_f + 31), the next batch's f_prev.
+__device__ __noinline__ int64_t fix_batch(RecView rv, const uint8_t* base, int64_t lo, int64_t hi, int64_t r_f,
+                                          int64_t f_prev, int64_t range_lo, int64_t range_hi, u8v_consts k) {
+  const int lane = threadIdx.x & 31;
+  const int64_t o = rec_start(rv, r_f + lane);
+  int64_t a = __shfl_up_sync(0xFFFFFFFFu, o, 1);
+  if (lane == 0) a = f_prev;
+  int64_t b = __shfl_down_sync(0xFFFFFFFFu, o, 1);
+  if (lane == 31) b = rec_start(rv, r_f + 32);
+  const int64_t rr = r_f + lane;
+  if (o >= range_lo && o < range_hi)
+    fix_boundary(rv, base, lo, hi, o, rr > 0 ? a : o, rr < rv.n_records ? b : o, rr, k);
+  return __shfl_sync(0xFFFFFFFFu, o, 31);
 }
 
 __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
-  __shared__ unsigned long long s_mask[kWarpsPerCta][kStepChunks];
   const int lane = threadIdx.x & 31;
-  const int wib = threadIdx.x >> 5;
   const int64_t warp = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * kThreads) >> 5;
   // The byte range comes from the offsets themselves (read here, so the
@@ -135,8 +200,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
   if (d.hi > d.off32 + d.n_bytes) d.hi = d.off32 + d.n_bytes;
   if (d.lo > d.hi) d.lo = d.hi;
   if (d.hi <= d.lo) return;  // every record empty: all valid
-  // Lanes [lo, hi]: lane hi carries the last record's end check; lanes past
-  // it read zeros behind a record start and cannot flag.
+  // Lanes [lo, hi]: the chunk holding byte hi is swept too; the last
+  // record's end is settled by the boundary at hi.
   d.c_begin = d.lo / kChunkBytes;
   d.c_end = d.hi / kChunkBytes + 1;
   d.steps = (d.c_end - d.c_begin + kStepChunks - 1) / kStepChunks;
@@ -145,27 +210,29 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
   int64_t step_end = step + d.steps_per_warp;
   if (step_end > d.steps) step_end = d.steps;
   if (step >= step_end) return;
-  unsigned long long* m = s_mask[wib];
-#pragma unroll
-  for (int i = 0; i < kU; ++i) m[lane + 32 * i] = 0;
 
   constexpr int64_t kStepBytes = (int64_t)kStepChunks * kChunkBytes;
   int64_t cstep = d.c_begin + step * kStepChunks;
   uint32_t carry_word = 0;
   if (lane == 31 && cstep > 0)
     carry_word = ld_word_masked(d.base, cstep * kChunkBytes - 4, d.lo, d.hi);
-  // r0: the record holding byte hs = step start - 2, the first byte whose
-  // record matters to the step (look-back of its first lanes).
-  int64_t r0 = find_record(rv, cstep * kChunkBytes - 2);
+  const int64_t range_lo = cstep * kChunkBytes;
+  const int64_t range_hi = (d.c_begin + step_end * kStepChunks) * kChunkBytes;
+  // Boundary cursor: batches of 32 record starts from r_f, the first start
+  // in the warp's range; a batch runs once the sweep has passed its last
+  // start (f_last), so its bytes are still L2-hot.
+  const int64_t r_in = find_record(rv, range_lo - 1);  // last start before the range (or 0)
+  int64_t r_f = rec_start(rv, r_in) < range_lo ? r_in + 1 : r_in;
+  int64_t f_prev = r_f > 0 ? rec_start(rv, r_f - 1) : 0;
+  int64_t f_last = rec_start(rv, r_f + 31);
+  // Attribution cursor (advanced lazily, on steps with a flagged lane).
+  int64_t r_att = r_in;
   bool was_ascii = true;
 
   for (; step < step_end; ++step) {
     cstep = d.c_begin + step * kStepChunks;
     const int64_t s0 = cstep * kChunkBytes;
-    const int64_t hs = s0 - 2;
     const int64_t se = s0 + kStepBytes;
-    const int64_t nhs = se - 2;  // next step's hs
-
     const bool direct = s0 >= d.lo && se + 4 <= d.hi;
     Chunk v[kU];
     uint32_t nsw = 0;
@@ -182,46 +249,16 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
       if (lane == 0) nsw = ld_word_guarded(d.base, se, d.lo, d.hi);
     }
 
-    // Record starts in [hs, se): the window of the 32 records from r0.
-    int64_t ob = rec_start(rv, r0 + lane);
-    unsigned below = __ballot_sync(0xFFFFFFFFu, ob < se);
-    const bool single = below == 1u && __shfl_sync(0xFFFFFFFFu, ob, 0) < hs;  // ob(0) = start(r0)
-    int64_t r_next = r0;
-    if (!single) {
-      __syncwarp();  // the previous step's readers have cleared their masks
-      int64_t r = r0;
-      for (;;) {
-        if (ob >= hs && ob < se) {
-          const int64_t c = ob >> 5;  // chunk of the start (base coords)
-          const int li = (int)(c - cstep);
-          const int bit = (int)(ob & 31);
-          // Low word: the chunk's record-start plane in permuted order; high
-          // word of the next chunk: starts at its bytes -1 / -2 (bits 31 / 23).
-          if (li >= 0) atomicOr(&m[li], 1ull << u8v_perm_pos((unsigned)bit));
-          if (bit >= 30 && li + 1 < kStepChunks)
-            atomicOr(&m[li + 1], 1ull << (bit == 31 ? 63 : 55));
-        }
-        // The next step's r0: the last record starting at or before nhs.
-        const unsigned le = __ballot_sync(0xFFFFFFFFu, ob <= nhs);
-        if (le != 0u) r_next = r + (31 - __clz(le));
-        if (below != 0xFFFFFFFFu) break;
-        r += 32;  // more than 31 starts in this step: next window
-        ob = rec_start(rv, r + lane);
-        below = __ballot_sync(0xFFFFFFFFu, ob < se);
-        if (below == 0u) break;
-      }
-      __syncwarp();
-    }
-
-    // ASCII fast path, voted only after an all-ASCII step (as in K1).
+    // Unbounded lane flags (K1's chunk form); ASCII fast path voted only
+    // after an all-ASCII step.
     bool all_ascii = false;
-    if (single && was_ascii) {
+    if (was_ascii) {
       uint32_t hibits = 0;
 #pragma unroll
       for (int i = 0; i < kU; ++i) hibits |= chunk_hibits(v[i]);
       all_ascii = __all_sync(0xFFFFFFFFu, (hibits & U8V_B7) == 0);
     }
-    uint32_t h7 = 0;
+    uint32_t h7 = 0, err[kU], any = 0;
 #pragma unroll
     for (int i = 0; i < kU; ++i) {
       const uint32_t up =
@@ -229,28 +266,47 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
       const uint32_t prev = __shfl_sync(0xFFFFFFFFu, up, (lane + 31) & 31);
       const uint32_t dn = lane == 0 ? (i + 1 < kU ? v[i + 1].w[0] : nsw) : v[i].w[0];
       const uint32_t next = __shfl_sync(0xFFFFFFFFu, dn, (lane + 1) & 31);
-      const int64_t c = cstep + lane + 32 * i;
-      uint32_t err, end = 0, hi7 = 0;
+      uint32_t hi7 = 0;
       if (all_ascii) {
         u8v_carry cr = u8v_carry_of(prev);
-        err = u8v_ascii_word_errors(v[i].w[0], &cr) & U8V_B7;
-        if (err) err = u8v_chunk_errors_planes_perm_k(v[i].w, prev, next, d.k, &hi7);  // exact lanes
-      } else if (single) {
-        err = u8v_chunk_errors_planes_perm_k(v[i].w, prev, next, d.k, &hi7);
+        err[i] = u8v_ascii_word_errors(v[i].w[0], &cr) & U8V_B7;
+        if (err[i]) err[i] = u8v_chunk_errors_planes_perm_k(v[i].w, prev, next, d.k, &hi7);  // exact lanes
       } else {
-        // Every chunk of a step holding record starts takes the bounded form
-        // (uniform control flow; a zero mask gives the plain flags).
-        const unsigned long long mask = m[lane + 32 * i];
-        m[lane + 32 * i] = 0;
-        err = u8v_chunk_errors_planes_perm_bounded_k(v[i].w, prev, next, d.k, (uint32_t)mask,
-                                                     (uint32_t)(mask >> 32), &end, &hi7);
+        err[i] = u8v_chunk_errors_planes_perm_k(v[i].w, prev, next, d.k, &hi7);
       }
       h7 |= hi7;
-      if (err | end) attribute_chunk(rv, c, err, end, r0);
+      any |= err[i];
     }
     was_ascii = all_ascii || __all_sync(0xFFFFFFFFu, h7 == 0);
     if (lane == 31) carry_word = v[kU - 1].w[kChunkWords - 1];
-    r0 = r_next;
+
+    if (__any_sync(0xFFFFFFFFu, any != 0u)) {
+      // The window of the step: lane L holds start(r_att + L) - s0, with
+      // r_att moved up to the last record starting at or before s0.
+      int o;
+      for (;;) {
+        o = rel32(rec_start(rv, r_att + lane), s0);
+        const unsigned le = __ballot_sync(0xFFFFFFFFu, o <= 0);
+        if (le == 0xFFFFFFFFu) {
+          r_att += 31;
+          continue;
+        }
+        const int top = le ? 31 - __clz(le) : 0;
+        if (top == 0) break;
+        r_att += top;
+      }
+      attribute_step(rv, s0, d.hi, err, o, true, r_att, __shfl_sync(0xFFFFFFFFu, o, 0));
+    }
+    while (f_last < se) {
+      f_prev = fix_batch(rv, d.base, d.lo, d.hi, r_f, f_prev, range_lo, range_hi, d.k);
+      r_f += 32;
+      f_last = rec_start(rv, r_f + 31);
+    }
+  }
+  // The range's remaining boundaries.
+  while (rec_start(rv, r_f) < range_hi) {
+    f_prev = fix_batch(rv, d.base, d.lo, d.hi, r_f, f_prev, range_lo, range_hi, d.k);
+    r_f += 32;
   }
 }
 

@@ -219,6 +219,34 @@ U8V_HD uint32_t u8v_word_errors_bounded_lead(uint32_t w, uint32_t wn, u8v_carry*
   return (S | R) & U8V_B7;
 }
 
+// A record boundary at byte s, for K2's unbounded sweep (batch.cu).  w8
+// holds bytes s-4 .. s+3 (byte k of w8 = byte s-4+k).  A = the record ending
+// at s owns bytes k in [ka, 4), B = the record starting at s owns bytes k in
+// [4, kb) (ka = 4: no A bytes, kb = 4: no B bytes); every other byte is
+// dropped, so each record is its own zero-extended stream.  Returns bit 0 if
+// A's end-of-stream lanes (n_A .. n_A+2, lookup_kernel.hpp:48-68, :111)
+// flag, bit 1 if one of B's first three lanes (look-back within B only,
+// from the zero prev vector of lookup_kernel.hpp:115) flags.  These are the
+// only lanes whose record-bounded flag can differ from the unbounded one
+// (the rare pair needs no bound: see u8v_word_errors_bounded_lead).
+U8V_HD uint32_t u8v_boundary_errors(uint64_t w8, unsigned ka, unsigned kb, u8v_consts k) {
+  const uint64_t keep_a = ka >= 4 ? 0ull : (0xFFFFFFFFull & ~((1ull << (8 * ka)) - 1ull));
+  const uint64_t keep_b = kb <= 4 ? 0ull : ((kb >= 8 ? ~0ull : (1ull << (8 * kb)) - 1ull) & ~0xFFFFFFFFull);
+  const uint32_t xa = (uint32_t)(w8 & keep_a);
+  const uint32_t xb = (uint32_t)((w8 & keep_b) >> 32);
+  // A's lanes n_A .. n_A+2 read zeros from n_A on: they flag iff a lead in
+  // A's last three bytes wants more bytes than A has (byte 3 of xa >= C0,
+  // byte 2 >= E0, byte 1 >= F0) -- bit 7 of each byte of t1/t2/t3 is
+  // "byte >= C0/E0/F0".
+  const uint32_t t1 = xa & (xa << 1);
+  const uint32_t t2 = t1 & (xa << 2);
+  const uint32_t t3 = t2 & (xa << 3);
+  const uint32_t ea = (t1 & 0x80000000u) | (t2 & 0x00800000u) | (t3 & 0x00008000u);
+  u8v_carry z = u8v_carry_zero();
+  const uint32_t eb = u8v_word_errors_lead(xb, 0, &z, k) & 0x00808080u;  // B's lanes 0 .. 2
+  return (ea ? 1u : 0u) | (eb ? 2u : 0u);
+}
+
 // Spread 4 bits (bit k = byte k) to bit 7 of each byte.
 U8V_HD uint32_t u8v_spread4(uint32_t x) { return ((x & 0xFu) * 0x10204080u) & U8V_B7; }
 

@@ -165,6 +165,57 @@ void swar_batch(const uint8_t* data, const uint64_t* offsets, size_t n_records, 
   }
 }
 
+/* K2's decomposition (batch.cu): the UNBOUNDED lane flags of the whole
+ * buffer, attributed to the record of each flagged lane except the first
+ * three lanes of a record, plus u8v_boundary_errors at every record start
+ * (and at the end of the last record).  Must equal per-record validation. */
+void swar_batch_decomp(const uint8_t* data, const uint64_t* offsets, size_t n_records, unsigned off,
+                       uint8_t* verdicts) {
+  if (n_records == 0) return;
+  for (size_t r = 0; r < n_records; ++r) verdicts[r] = 1;
+  const int64_t lo = (int64_t)off + (int64_t)offsets[0];
+  const int64_t hi = (int64_t)off + (int64_t)offsets[n_records];
+  if (hi <= lo) return;
+  const u8v_consts kc = u8v_make_consts();
+  /* 1. unbounded flags over the zero-extended [lo, hi), lanes up to hi+3 */
+  const int64_t words = (hi + 3 + 3) / 4;
+  u8v_carry c = u8v_carry_zero();
+  const uint8_t* p0 = data + offsets[0]; /* word_at indexes from byte lo */
+  uint32_t w = word_at(p0, 0, lo, hi);
+  for (int64_t k = 0; k < words; ++k) {
+    const uint32_t wn = word_at(p0, k + 1, lo, hi);
+    const uint32_t e = u8v_word_errors_lead(w, wn, &c, kc) & U8V_B7;
+    w = wn;
+    for (int j = 0; j < 4; ++j) {
+      if (!((e >> (8 * j + 7)) & 1)) continue;
+      const int64_t q = 4 * k + j - (int64_t)off; /* data coords */
+      if (q < (int64_t)offsets[0] || q >= (int64_t)offsets[n_records]) continue;
+      size_t r = 0;
+      while (r + 1 < n_records && (int64_t)offsets[r + 1] <= q) ++r;
+      if (q - (int64_t)offsets[r] >= 3) verdicts[r] = 0; /* boundary lanes: step 2 */
+    }
+  }
+  /* 2. every boundary */
+  for (size_t rr = 0; rr <= n_records; ++rr) {
+    const int64_t s0 = (int64_t)offsets[rr];
+    int64_t a = rr > 0 ? (int64_t)offsets[rr - 1] : s0;
+    int64_t b = rr < n_records ? (int64_t)offsets[rr + 1] : s0;
+    if (a > s0) a = s0;
+    if (b < s0) b = s0;
+    uint64_t w8 = 0;
+    for (int k = 0; k < 8; ++k) {
+      const int64_t q = s0 - 4 + k;
+      if (q >= (int64_t)offsets[0] && q < (int64_t)offsets[n_records]) w8 |= (uint64_t)data[q] << (8 * k);
+    }
+    int64_t ka = a - (s0 - 4), kb = b - (s0 - 4);
+    ka = ka < 0 ? 0 : ka > 4 ? 4 : ka;
+    kb = kb < 4 ? 4 : kb > 8 ? 8 : kb;
+    const uint32_t f = u8v_boundary_errors(w8, (unsigned)ka, (unsigned)kb, kc);
+    if ((f & 1u) && rr > 0) verdicts[rr - 1] = 0;
+    if ((f & 2u) && rr < n_records) verdicts[rr] = 0;
+  }
+}
+
 /* Oracle verdicts for every input of exactly `len` bytes (len <= 3), in the
  * order v = 0 .. 256^len - 1 with byte i = (v >> 8i) & 0xFF. */
 void oracle_exhaustive_verdicts(int len, uint8_t* out) {

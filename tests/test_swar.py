@@ -76,6 +76,9 @@ def test_bounded_variant_matches_per_record_oracle():
             S.swar_batch(data.ctypes.data if data.size else None, offs.ctypes.data, len(parts), align,
                          got.ctypes.data)
             assert np.array_equal(got, want), (trial, align, parts)
+            S.swar_batch_decomp(data.ctypes.data if data.size else None, offs.ctypes.data, len(parts), align,
+                                got.ctypes.data)
+            assert np.array_equal(got, want), ("decomp", trial, align, parts)
 
 
 def test_bit_planes_transpose():
@@ -161,3 +164,47 @@ def test_bit_sliced_permuted_bounded_form_equals_natural_bounded_form():
     S.swar_bits_perm_bounded_check.restype = C.c_uint64
     S.swar_bits_perm_bounded_check.argtypes = [C.c_uint64, C.c_uint64]
     assert S.swar_bits_perm_bounded_check(17, 300000) == 0
+
+
+def test_k2_boundary_decomposition_adversarial():
+    """K2 = unbounded lane flags (boundary lanes skipped) + u8v_boundary_errors
+    at every record start: equal to per-record validation on records of 0..6
+    bytes drawn from the bytes that matter at a boundary (continuations of
+    each range, every rare lead, ASCII), at every word alignment."""
+    rng = np.random.default_rng(29)
+    S = nat.swar()
+    alphabet = np.array([0x41, 0x80, 0x8F, 0x90, 0x9F, 0xA0, 0xBF, 0xC0, 0xC1, 0xC2, 0xDF, 0xE0,
+                         0xE1, 0xED, 0xEF, 0xF0, 0xF1, 0xF4, 0xF5, 0xFF], np.uint8)
+    for trial in range(2000):
+        parts = [bytes(rng.choice(alphabet, int(rng.integers(0, 7)))) for _ in range(int(rng.integers(1, 12)))]
+        data, offs = _batch(parts)
+        want = np.array([nat.oracle_verdict(p)[0] for p in parts], np.uint8)
+        got = np.empty(len(parts), np.uint8)
+        for align in range(4):
+            S.swar_batch_decomp(data.ctypes.data if data.size else None, offs.ctypes.data, len(parts), align,
+                                got.ctypes.data)
+            assert np.array_equal(got, want), (trial, align, parts)
+    # whole characters at the edges of the ranges and their prefixes: records
+    # that are valid, truncated at either end, or split across a boundary
+    chars = [b"A", b"\xC2\x80", b"\xDF\xBF", b"\xE0\xA0\x80", b"\xED\x9F\xBF", b"\xEF\xBF\xBF",
+             b"\xF0\x90\x80\x80", b"\xF4\x8F\xBF\xBF"]
+    n_valid = 0
+    for trial in range(2000):
+        parts = []
+        for _ in range(int(rng.integers(1, 10))):
+            rec = b"".join(chars[int(i)] for i in rng.integers(0, len(chars), int(rng.integers(0, 3))))
+            cut = int(rng.integers(0, 3))
+            if cut == 1 and rec:
+                rec = rec[int(rng.integers(1, len(rec) + 1)):]     # starts mid-character
+            elif cut == 2 and rec:
+                rec = rec[: int(rng.integers(0, len(rec)))]        # ends mid-character
+            parts.append(rec)
+        data, offs = _batch(parts)
+        want = np.array([nat.oracle_verdict(p)[0] for p in parts], np.uint8)
+        n_valid += int(want.sum())
+        got = np.empty(len(parts), np.uint8)
+        for align in range(4):
+            S.swar_batch_decomp(data.ctypes.data if data.size else None, offs.ctypes.data, len(parts), align,
+                                got.ctypes.data)
+            assert np.array_equal(got, want), (trial, align, parts)
+    assert n_valid > 2000  # both kinds well represented
