@@ -97,11 +97,13 @@ __device__ __forceinline__ int rel32(int64_t pos, int64_t s0) {
 // shuffle search over the window (lane L holds start(r0 + L) - s0), or r0
 // when the step holds no start -- unless q is one of that record's first
 // three lanes or lies past the data (those lanes are settled by
-// fix_boundary).  err[i]: lane bits of chunk (lane + 32 i) of the step in
+// fix_boundary).  e0..e3: lane bits of chunk (lane + 32 i) of the step in
 // the permuted plane order of utf8v_bits.h (bit pos(i) = byte i).
-__device__ __noinline__ void attribute_step(RecView d, int64_t s0, int64_t hi, const uint32_t* err_in,
-                                            int o, bool window, int64_t r0, int base_rel) {
+__device__ __noinline__ void attribute_step(RecView d, int64_t s0, int64_t hi, uint32_t e0, uint32_t e1,
+                                            uint32_t e2, uint32_t e3, int o, bool window, int64_t r0,
+                                            int base_rel) {
   const int lane = threadIdx.x & 31;
+  const uint32_t err_in[kU] = {e0, e1, e2, e3};
   const bool full = window && __all_sync(0xFFFFFFFFu, o < kStepChunks * kChunkBytes);
   const int hi_rel = rel32(hi, s0);
 #pragma unroll 1
@@ -171,20 +173,18 @@ __device__ __forceinline__ void fix_boundary(const RecView& rv, const uint8_t* b
 }
 
 // One batch of record boundaries: lane L takes start(r_f + L) when it lies in
-// the warp's byte range [range_lo, range_hi).  f_prev = start(r_f - 1).
-// Returns start(r_f + 31), the next batch's f_prev.
-__device__ __noinline__ int64_t fix_batch(RecView rv, const uint8_t* base, int64_t lo, int64_t hi, int64_t r_f,
-                                          int64_t f_prev, int64_t range_lo, int64_t range_hi, u8v_consts k) {
+// the warp's byte range [range_lo, range_hi).
+__device__ __noinline__ void fix_batch(RecView rv, const uint8_t* base, int64_t lo, int64_t hi, int64_t r_f,
+                                       int64_t range_lo, int64_t range_hi, u8v_consts k) {
   const int lane = threadIdx.x & 31;
   const int64_t o = rec_start(rv, r_f + lane);
   int64_t a = __shfl_up_sync(0xFFFFFFFFu, o, 1);
-  if (lane == 0) a = f_prev;
+  if (lane == 0) a = r_f > 0 ? rec_start(rv, r_f - 1) : o;
   int64_t b = __shfl_down_sync(0xFFFFFFFFu, o, 1);
   if (lane == 31) b = rec_start(rv, r_f + 32);
   const int64_t rr = r_f + lane;
   if (o >= range_lo && o < range_hi)
     fix_boundary(rv, base, lo, hi, o, rr > 0 ? a : o, rr < rv.n_records ? b : o, rr, k);
-  return __shfl_sync(0xFFFFFFFFu, o, 31);
 }
 
 __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
@@ -206,33 +206,34 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
   d.c_end = d.hi / kChunkBytes + 1;
   d.steps = (d.c_end - d.c_begin + kStepChunks - 1) / kStepChunks;
   d.steps_per_warp = (d.steps + nwarps - 1) / nwarps;
-  int64_t step = warp * d.steps_per_warp;
-  int64_t step_end = step + d.steps_per_warp;
+  const int64_t step0 = warp * d.steps_per_warp;
+  int64_t step_end = step0 + d.steps_per_warp;
   if (step_end > d.steps) step_end = d.steps;
-  if (step >= step_end) return;
+  if (step0 >= step_end) return;
+  const int nsteps = (int)(step_end - step0);
 
-  constexpr int64_t kStepBytes = (int64_t)kStepChunks * kChunkBytes;
-  int64_t cstep = d.c_begin + step * kStepChunks;
+  constexpr int kStepBytes = kStepChunks * kChunkBytes;
+  // Loop state is kept 32-bit and relative (positions to range_lo, records
+  // to r_in) so it stays in registers across the chunk math.
+  const int64_t range_lo = (d.c_begin + step0 * kStepChunks) * kChunkBytes;
+  const int64_t range_hi = range_lo + (int64_t)nsteps * kStepBytes;
   uint32_t carry_word = 0;
-  if (lane == 31 && cstep > 0)
-    carry_word = ld_word_masked(d.base, cstep * kChunkBytes - 4, d.lo, d.hi);
-  const int64_t range_lo = cstep * kChunkBytes;
-  const int64_t range_hi = (d.c_begin + step_end * kStepChunks) * kChunkBytes;
-  // Boundary cursor: batches of 32 record starts from r_f, the first start
-  // in the warp's range; a batch runs once the sweep has passed its last
-  // start (f_last), so its bytes are still L2-hot.
+  if (lane == 31 && range_lo > 0) carry_word = ld_word_masked(d.base, range_lo - 4, d.lo, d.hi);
+  // Boundary cursor: batches of 32 record starts from r_in + rf, the first
+  // start in the warp's range; a batch runs once the sweep has passed its
+  // last start (f_last, clamped: a batch is correct whenever it runs), so
+  // its bytes are still L2-hot.
   const int64_t r_in = find_record(rv, range_lo - 1);  // last start before the range (or 0)
-  int64_t r_f = rec_start(rv, r_in) < range_lo ? r_in + 1 : r_in;
-  int64_t f_prev = r_f > 0 ? rec_start(rv, r_f - 1) : 0;
-  int64_t f_last = rec_start(rv, r_f + 31);
+  int rf = rec_start(rv, r_in) < range_lo ? 1 : 0;
+  int f_last = rel32(rec_start(rv, r_in + rf + 31), range_lo);
   // Attribution cursor (advanced lazily, on steps with a flagged lane).
-  int64_t r_att = r_in;
+  int ratt = 0;
   bool was_ascii = true;
 
-  for (; step < step_end; ++step) {
-    cstep = d.c_begin + step * kStepChunks;
-    const int64_t s0 = cstep * kChunkBytes;
+  for (int j = 0; j < nsteps; ++j) {
+    const int64_t s0 = range_lo + (int64_t)j * kStepBytes;
     const int64_t se = s0 + kStepBytes;
+    const int64_t cstep = s0 / kChunkBytes;
     const bool direct = s0 >= d.lo && se + 4 <= d.hi;
     Chunk v[kU];
     uint32_t nsw = 0;
@@ -285,28 +286,29 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
       // r_att moved up to the last record starting at or before s0.
       int o;
       for (;;) {
-        o = rel32(rec_start(rv, r_att + lane), s0);
+        o = rel32(rec_start(rv, r_in + ratt + lane), s0);
         const unsigned le = __ballot_sync(0xFFFFFFFFu, o <= 0);
         if (le == 0xFFFFFFFFu) {
-          r_att += 31;
+          ratt += 31;
           continue;
         }
         const int top = le ? 31 - __clz(le) : 0;
         if (top == 0) break;
-        r_att += top;
+        ratt += top;
       }
-      attribute_step(rv, s0, d.hi, err, o, true, r_att, __shfl_sync(0xFFFFFFFFu, o, 0));
+      attribute_step(rv, s0, d.hi, err[0], err[1], err[2], err[3], o, true, r_in + ratt,
+                     __shfl_sync(0xFFFFFFFFu, o, 0));
     }
-    while (f_last < se) {
-      f_prev = fix_batch(rv, d.base, d.lo, d.hi, r_f, f_prev, range_lo, range_hi, d.k);
-      r_f += 32;
-      f_last = rec_start(rv, r_f + 31);
+    while (f_last < (j + 1) * kStepBytes) {
+      fix_batch(rv, d.base, d.lo, d.hi, r_in + rf, range_lo, range_hi, d.k);
+      rf += 32;
+      f_last = rel32(rec_start(rv, r_in + rf + 31), range_lo);
     }
   }
   // The range's remaining boundaries.
-  while (rec_start(rv, r_f) < range_hi) {
-    f_prev = fix_batch(rv, d.base, d.lo, d.hi, r_f, f_prev, range_lo, range_hi, d.k);
-    r_f += 32;
+  while (rec_start(rv, r_in + rf) < range_hi) {
+    fix_batch(rv, d.base, d.lo, d.hi, r_in + rf, range_lo, range_hi, d.k);
+    rf += 32;
   }
 }
 
