@@ -103,39 +103,49 @@ __device__ __noinline__ void attribute_step(RecView d, int64_t s0, int64_t hi, u
                                             uint32_t e2, uint32_t e3, int o, bool window, int64_t r0,
                                             int base_rel) {
   const int lane = threadIdx.x & 31;
-  const uint32_t err_in[kU] = {e0, e1, e2, e3};
   const bool full = window && __all_sync(0xFFFFFFFFu, o < kStepChunks * kChunkBytes);
   const int hi_rel = rel32(hi, s0);
-#pragma unroll 1
-  for (int i = 0; i < kU; ++i) {
-    uint32_t e = err_in[i];
-    while (__any_sync(0xFFFFFFFFu, e != 0u)) {
-      int q = -1;
-      if (e) {
-        const int bit = __ffs(e) - 1;
-        e &= e - 1;
-        q = (lane + 32 * i) * kChunkBytes + (int)u8v_perm_byte((unsigned)bit);
-      }
-      int L = 0;
-      if (window) {
+  static_assert(kU == 4, "attribute_step takes one mask per chunk of a step");
+  // One flagged lane per lane and round, lowest chunk first.
+  while (__any_sync(0xFFFFFFFFu, (e0 | e1 | e2 | e3) != 0u)) {
+    int q = -1, c = lane;
+    uint32_t e = 0;
+    if (e0) {
+      e = e0;
+      e0 &= e0 - 1;
+    } else if (e1) {
+      e = e1;
+      e1 &= e1 - 1;
+      c += 32;
+    } else if (e2) {
+      e = e2;
+      e2 &= e2 - 1;
+      c += 64;
+    } else if (e3) {
+      e = e3;
+      e3 &= e3 - 1;
+      c += 96;
+    }
+    if (e) q = c * kChunkBytes + (int)u8v_perm_byte((unsigned)(__ffs(e) - 1));
+    int L = 0;
+    if (window) {
 #pragma unroll
-        for (int st = 16; st > 0; st >>= 1) {
-          const int cand = L + st;
-          const int t = __shfl_sync(0xFFFFFFFFu, o, cand & 31);
-          if (cand <= 31 && t <= q) L = cand;
-        }
+      for (int st = 16; st > 0; st >>= 1) {
+        const int cand = L + st;
+        const int t = __shfl_sync(0xFFFFFFFFu, o, cand & 31);
+        if (cand <= 31 && t <= q) L = cand;
       }
-      const int start = window ? __shfl_sync(0xFFFFFFFFu, o, L) : base_rel;
-      if (q >= 0 && q < hi_rel && q >= start) {
-        int64_t r = r0 + L;
-        int64_t st_abs = s0 + start;
-        if (full && L == 31) {  // more starts than one window holds: walk on
-          const int64_t qa = s0 + q;
-          while (r < d.n_records && rec_start(d, r + 1) <= qa) ++r;
-          st_abs = rec_start(d, r);
-        }
-        if (r < d.n_records && s0 + q - st_abs >= 3) d.verdicts[r] = 0;
+    }
+    const int start = window ? __shfl_sync(0xFFFFFFFFu, o, L) : base_rel;
+    if (q >= 0 && q < hi_rel && q >= start) {
+      int64_t r = r0 + L;
+      int64_t st_abs = s0 + start;
+      if (full && L == 31) {  // more starts than one window holds: walk on
+        const int64_t qa = s0 + q;
+        while (r < d.n_records && rec_start(d, r + 1) <= qa) ++r;
+        st_abs = rec_start(d, r);
       }
+      if (r < d.n_records && s0 + q - st_abs >= 3) d.verdicts[r] = 0;
     }
   }
 }
