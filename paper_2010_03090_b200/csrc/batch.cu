@@ -292,22 +292,20 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
     if (lane == 31) carry_word = v[kU - 1].w[kChunkWords - 1];
 
     if (__any_sync(0xFFFFFFFFu, any != 0u)) {
-      // The window of the step: lane L holds start(r_att + L) - s0, with
-      // r_att moved up to the last record starting at or before s0.
+      // The window from the attribution cursor (lane L: start(r_att + L) -
+      // s0; start(r_att) <= s0).  It may start a few records back: the
+      // search takes the last start <= q, and a window that ends inside the
+      // step walks on.  The cursor then moves to the last start <= s0.
       int o;
-      for (;;) {
+      for (;;) {  // gallop past a cursor left far behind
         o = rel32(rec_start(rv, r_in + ratt + lane), s0);
-        const unsigned le = __ballot_sync(0xFFFFFFFFu, o <= 0);
-        if (le == 0xFFFFFFFFu) {
-          ratt += 31;
-          continue;
-        }
-        const int top = le ? 31 - __clz(le) : 0;
-        if (top == 0) break;
-        ratt += top;
+        if (__ballot_sync(0xFFFFFFFFu, o <= 0) != 0xFFFFFFFFu) break;
+        ratt += 31;
       }
       attribute_step(rv, s0, d.hi, err[0], err[1], err[2], err[3], o, true, r_in + ratt,
                      __shfl_sync(0xFFFFFFFFu, o, 0));
+      const unsigned le = __ballot_sync(0xFFFFFFFFu, o <= 0);
+      if (le) ratt += 31 - __clz(le);
     }
     while (f_last < (j + 1) * kStepBytes) {
       fix_batch(rv, d.base, d.lo, d.hi, r_in + rf, range_lo, range_hi, d.k);
