@@ -240,24 +240,28 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
   int ratt = 0;
   bool was_ascii = true;
 
-  for (int j = 0; j < nsteps; ++j) {
-    const int64_t s0 = range_lo + (int64_t)j * kStepBytes;
-    const int64_t se = s0 + kStepBytes;
-    const int64_t cstep = s0 / kChunkBytes;
-    const bool direct = s0 >= d.lo && se + 4 <= d.hi;
+  // Steps [jb, jd) are interior (all bytes real, lookahead word in range):
+  // plain loads from a pointer advanced 4 KiB per step.
+  int jb = (int)((d.lo - range_lo + kStepBytes - 1) / kStepBytes);
+  int jd = d.hi - 4 - range_lo >= 0 ? (int)((d.hi - 4 - range_lo) / kStepBytes) : 0;
+  jb = jb < 0 ? 0 : jb;
+  jd = jd > nsteps ? nsteps : jd;
+  const uint8_t* p = d.base + range_lo + lane * kChunkBytes;
+  for (int j = 0; j < nsteps; ++j, p += kStepBytes) {
     Chunk v[kU];
     uint32_t nsw = 0;
-    if (direct) {
+    if (j >= jb && j < jd) {
 #pragma unroll
-      for (int i = 0; i < kU; ++i) v[i] = ld_chunk(d.base + (cstep + lane + 32 * i) * kChunkBytes);
-      if (lane == 0) nsw = __ldg(reinterpret_cast<const uint32_t*>(d.base + se));
+      for (int i = 0; i < kU; ++i) v[i] = ld_chunk(p + 32 * i * kChunkBytes);
+      if (lane == 0) nsw = __ldg(reinterpret_cast<const uint32_t*>(p + kStepBytes));
     } else {
+      const int64_t cstep = (range_lo + (int64_t)j * kStepBytes) / kChunkBytes;
 #pragma unroll
       for (int i = 0; i < kU; ++i) {
         const int64_t c = cstep + lane + 32 * i;
         v[i] = c <= d.c_end ? ld_chunk_masked(d.base, c, d.lo, d.hi) : zero_chunk();
       }
-      if (lane == 0) nsw = ld_word_guarded(d.base, se, d.lo, d.hi);
+      if (lane == 0) nsw = ld_word_guarded(d.base, (cstep + kStepChunks) * kChunkBytes, d.lo, d.hi);
     }
 
     // Unbounded lane flags (K1's chunk form); ASCII fast path voted only
@@ -292,6 +296,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
     if (lane == 31) carry_word = v[kU - 1].w[kChunkWords - 1];
 
     if (__any_sync(0xFFFFFFFFu, any != 0u)) {
+      const int64_t s0 = range_lo + (int64_t)j * kStepBytes;
       // The window from the attribution cursor (lane L: start(r_att + L) -
       // s0; start(r_att) <= s0).  It may start a few records back: the
       // search takes the last start <= q, and a window that ends inside the
