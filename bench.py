@@ -338,7 +338,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     traffic = ncu_traffic("k_validate")
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
-                "peak_source": peaks["source"], "kernel": "u8v::k_validate<false>",
+                "peak_source": peaks["source"], "kernel": "u8v::k_validate",
                 "kernel_ms": kernel_ms, "algorithmic_bytes_per_launch": alg_bytes}
 
     # ---- e2e through the public API with pinned host buffers ---------------

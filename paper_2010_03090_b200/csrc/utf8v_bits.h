@@ -199,41 +199,7 @@ U8V_HD uint32_t u8v_chunk_errors_planes(const uint32_t w[8], uint32_t prev, uint
   return u8v_chunk_errors_planes_k(w, prev, next, u8v_make_consts(), &hi7);
 }
 
-// Record-bounded form (K2): as u8v_chunk_errors_planes_k, for a chunk of a
-// record batch.  bnd bit j <-> a record starts at byte j - 4 of the chunk
-// (j < 36: bytes -4..31).  Look-back sources from an earlier record are
-// dropped (each record starts with a zero prev vector); *end_err gets, at
-// each record start i, the end check of the record before it (its lanes
-// i-3..i-1 expected continuations: u8v_word_errors_bounded_lead).  The rare
-// pair needs no mask in the lead form (utf8v_swar.h).
-U8V_HD uint32_t u8v_chunk_errors_planes_bounded_k(const uint32_t w[8], uint32_t prev, uint32_t next,
-                                                  u8v_consts k, uint64_t bnd, uint32_t* end_err,
-                                                  uint32_t* hi7) {
-  uint32_t p[8];
-  u8v_planes_k(w, p, k);
-  *hi7 = p[7];
-  const uint32_t l1 = p[7] & p[6];
-  const uint32_t l2 = l1 & p[5];
-  const uint32_t l3 = l2 & p[4];
-  const uint32_t q1 = prev & U8V_SHL(prev, 1, k);
-  const uint32_t q2 = q1 & U8V_SHL(prev, 2, k);
-  const uint32_t q3 = q2 & U8V_SHL(prev, 3, k);
-  const uint32_t e1 = u8v_fsl(u8v_movemask_top(q1, k), l1, 1);
-  const uint32_t e2 = u8v_fsl(u8v_movemask_top(q2, k), l2, 2);
-  const uint32_t e3 = u8v_fsl(u8v_movemask_top(q3, k), l3, 3);
-  const uint32_t B = (uint32_t)(bnd >> 4);           // a record starts at lane i
-  const uint32_t pre = (uint32_t)bnd << 28;          // bits 30, 31: starts at -2, -1
-  const uint32_t B1 = u8v_fsl(pre, B, 1);            // ... at i-1
-  const uint32_t B2 = u8v_fsl(pre, B, 2);            // ... at i-2
-  const uint32_t m2 = B | B1, m3 = m2 | B2;
-  const uint32_t S = (p[7] & ~p[6]) ^ ((e1 & ~B) | (e2 & ~m2) | (e3 & ~m3));
-  *end_err = B & (e1 | (e2 & ~B1) | (e3 & ~B1 & ~B2));
-  const uint32_t n5 = u8v_fsr(p[5], next >> 5, 1);
-  const uint32_t n4 = u8v_fsr(p[4], next >> 4, 1);
-  return S | u8v_rare_planes(l1, l2, l3, p[5], p[4], p[3], p[2], p[1], p[0], n5, n4);
-}
-
-// ---- permuted-order form (K1, K3) -----------------------------------------
+// ---- permuted-order form (K1, K2, K3) -------------------------------------
 // Without the PRMT row gather the eight words of a chunk already are the
 // rows of four 8x8 bit blocks -- block b = bytes {b, b+4, ..., b+28} -- so the
 // three cross-register stages alone give the planes, in the order
@@ -287,59 +253,6 @@ U8V_HD uint32_t u8v_chunk_errors_planes_perm_k(const uint32_t w[8], uint32_t pre
   // Follower bits 5 and 4 at the lead's position.
   const uint32_t nx5 = U8V_SHL(next, 2, k);  // bit 7 = next byte 0's bit 5
   const uint32_t nx4 = U8V_SHL(next, 3, k);  // bit 7 = next byte 0's bit 4
-  const uint32_t n5 = u8v_fsr(p5, U8V_BITSEL(0x7F, U8V_SHR(p5, 1, k), nx5), 8);
-  const uint32_t n4 = u8v_fsr(p4, U8V_BITSEL(0x7F, U8V_SHR(p4, 1, k), nx4), 8);
-  return S | u8v_rare_planes(l1, l2, l3, p5, p4, p3, p2, p1, p0, n5, n4);
-}
-
-// Record-bounded permuted-order form (K2).  B: the record-start plane in
-// permuted order (bit pos(i) = a record starts at byte i of the chunk);
-// pre: starts just before the chunk in the layout of the previous word's
-// bit-7 flags -- bit 31 = a start at byte -1, bit 23 = at byte -2, nothing
-// else -- so pre >> 31 and pre >> 23 are exactly the lag-1 / lag-2 carries.
-// Same lane flags as u8v_chunk_errors_planes_bounded_k at bit pos(i)
-// (tests/test_swar.py).
-U8V_HD uint32_t u8v_chunk_errors_planes_perm_bounded_k(const uint32_t w[8], uint32_t prev,
-                                                       uint32_t next, u8v_consts k, uint32_t B,
-                                                       uint32_t pre, uint32_t* end_err,
-                                                       uint32_t* hi7) {
-  uint32_t r0 = w[0], r1 = w[1], r2 = w[2], r3 = w[3], r4 = w[4], r5 = w[5], r6 = w[6], r7 = w[7];
-  U8V_XSTAGE(r0, r1, 1, 0xAAAAAAAA, 0x55555555, k);
-  U8V_XSTAGE(r2, r3, 1, 0xAAAAAAAA, 0x55555555, k);
-  U8V_XSTAGE(r4, r5, 1, 0xAAAAAAAA, 0x55555555, k);
-  U8V_XSTAGE(r6, r7, 1, 0xAAAAAAAA, 0x55555555, k);
-  U8V_XSTAGE(r0, r2, 2, 0xCCCCCCCC, 0x33333333, k);
-  U8V_XSTAGE(r1, r3, 2, 0xCCCCCCCC, 0x33333333, k);
-  U8V_XSTAGE(r4, r6, 2, 0xCCCCCCCC, 0x33333333, k);
-  U8V_XSTAGE(r5, r7, 2, 0xCCCCCCCC, 0x33333333, k);
-  U8V_XSTAGE(r0, r4, 4, 0xF0F0F0F0, 0x0F0F0F0F, k);
-  U8V_XSTAGE(r1, r5, 4, 0xF0F0F0F0, 0x0F0F0F0F, k);
-  U8V_XSTAGE(r2, r6, 4, 0xF0F0F0F0, 0x0F0F0F0F, k);
-  U8V_XSTAGE(r3, r7, 4, 0xF0F0F0F0, 0x0F0F0F0F, k);
-  const uint32_t p0 = r0, p1 = r1, p2 = r2, p3 = r3, p4 = r4, p5 = r5, p6 = r6, p7 = r7;
-  *hi7 = p7;
-  const uint32_t l1 = p7 & p6;
-  const uint32_t l2 = l1 & p5;
-  const uint32_t l3 = l2 & p4;
-  const uint32_t q1 = prev & U8V_SHL(prev, 1, k) & U8V_B7;
-  const uint32_t q2 = q1 & U8V_SHL(prev, 2, k);
-  const uint32_t q3 = q2 & U8V_SHL(prev, 3, k);
-  const uint32_t e1 =
-      U8V_SHLADD(l1, 8, U8V_BITSEL(0x000000FE, U8V_SHR(l1, 23, k), U8V_SHR(q1, 31, k)), k);
-  const uint32_t e2 =
-      U8V_SHLADD(l2, 16, U8V_BITSEL(0x0000FEFE, U8V_SHR(l2, 15, k), U8V_SHR(q2, 23, k)), k);
-  const uint32_t e3 =
-      U8V_SHLADD(l3, 24, U8V_BITSEL(0x00FEFEFE, U8V_SHR(l3, 7, k), U8V_SHR(q3, 15, k)), k);
-  // Record starts one / two bytes back, in permuted order (lags of B).
-  const uint32_t B1 =
-      U8V_SHLADD(B, 8, U8V_BITSEL(0x000000FE, U8V_SHR(B, 23, k), U8V_SHR(pre, 31, k)), k);
-  const uint32_t B2 =
-      U8V_SHLADD(B, 16, U8V_BITSEL(0x0000FEFE, U8V_SHR(B, 15, k), U8V_SHR(pre, 23, k)), k);
-  const uint32_t m2 = B | B1, m3 = m2 | B2;
-  const uint32_t S = (p7 & ~p6) ^ ((e1 & ~B) | (e2 & ~m2) | (e3 & ~m3));
-  *end_err = B & (e1 | (e2 & ~B1) | (e3 & ~B1 & ~B2));
-  const uint32_t nx5 = U8V_SHL(next, 2, k);
-  const uint32_t nx4 = U8V_SHL(next, 3, k);
   const uint32_t n5 = u8v_fsr(p5, U8V_BITSEL(0x7F, U8V_SHR(p5, 1, k), nx5), 8);
   const uint32_t n4 = u8v_fsr(p4, U8V_BITSEL(0x7F, U8V_SHR(p4, 1, k), nx4), 8);
   return S | u8v_rare_planes(l1, l2, l3, p5, p4, p3, p2, p1, p0, n5, n4);

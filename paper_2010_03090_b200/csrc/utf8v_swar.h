@@ -181,44 +181,6 @@ U8V_HD uint32_t u8v_word_errors_lead(uint32_t w, uint32_t wn, u8v_carry* c, u8v_
   return S | R;
 }
 
-// Record-bounded lead form (K2's reference in SWAR; the kernel runs the plane
-// form of utf8v_bits.h, proven equal to this one lane for lane): each record
-// is its own zero-extended stream.  bm / pbm carry, in bit 7 of byte k, "a
-// record starts at byte k" of this / the previous word.  Lane i drops every
-// look-back source that lies in an earlier record (i-1 if a record starts at
-// i; i-2 if one starts at i or i-1; i-3 if at i, i-1 or i-2) -- the
-// reference's zero prev vector at a record start (lookup_kernel.hpp:115).
-// *end_err receives, at each record start b, the previous record's
-// end-of-stream check (lookup_kernel.hpp:48-68, :111) restricted to that
-// record's own bytes.  The rare pair (j, j+1) is tested at lane j with no
-// boundary mask: a flag on a pair that crosses into the next record means
-// byte j is a lead that ends its record, which is invalid anyway (its end
-// check fires too), and the flag sits on that record's lane.
-U8V_HD uint32_t u8v_word_errors_bounded_lead(uint32_t w, uint32_t wn, u8v_carry* c, uint32_t bm,
-                                             uint32_t pbm, uint32_t* end_err, u8v_consts k) {
-  const uint32_t s1 = w << 1, s2 = w << 2, s3 = w << 3;
-  const uint32_t f1 = w & s1;
-  const uint32_t f2 = f1 & s2;
-  const uint32_t f3 = f2 & s3;
-  const uint32_t e1 = u8v_fsl(c->f1, f1, 8);
-  const uint32_t e2 = u8v_fsl(c->f2, f2, 16);
-  const uint32_t e3 = u8v_fsl(c->f3, f3, 24);
-  const uint32_t b1 = u8v_fsl(pbm, bm, 8);   // a record starts at i-1
-  const uint32_t b2 = u8v_fsl(pbm, bm, 16);  // a record starts at i-2
-  const uint32_t m2 = bm | b1;
-  const uint32_t m3 = m2 | b2;
-  const uint32_t S = ((e1 & ~bm) | (e2 & ~m2) | (e3 & ~m3)) ^ (w & ~s1);
-  const uint32_t t = u8v_fsr(w, wn, 12);
-  const uint32_t zl = (s2 & 0x7C7C7C7Cu) | (t & 0x03030303u);
-  const uint32_t R = u8v_rare_key(s2, zl, f1, k);
-  *end_err = bm & (e1 | (e2 & ~b1) | (e3 & ~b1 & ~b2)) & U8V_B7;
-  c->p = w;
-  c->f1 = f1;
-  c->f2 = f2;
-  c->f3 = f3;
-  return (S | R) & U8V_B7;
-}
-
 // A record boundary at byte s, for K2's unbounded sweep (batch.cu).  w8
 // holds bytes s-4 .. s+3 (byte k of w8 = byte s-4+k).  A = the record ending
 // at s owns bytes k in [ka, 4), B = the record starting at s owns bytes k in
@@ -227,8 +189,11 @@ U8V_HD uint32_t u8v_word_errors_bounded_lead(uint32_t w, uint32_t wn, u8v_carry*
 // A's end-of-stream lanes (n_A .. n_A+2, lookup_kernel.hpp:48-68, :111)
 // flag, bit 1 if one of B's first three lanes (look-back within B only,
 // from the zero prev vector of lookup_kernel.hpp:115) flags.  These are the
-// only lanes whose record-bounded flag can differ from the unbounded one
-// (the rare pair needs no bound: see u8v_word_errors_bounded_lead).
+// only lanes whose record-bounded flag can differ from the unbounded one.
+// The rare pair needs no bound in the lead form: a flagged pair (j, j+1)
+// that crosses into the next record means byte j is a lead that ends its
+// record, which is invalid anyway (its end check fires too), and the flag
+// sits on that record's lane.
 U8V_HD uint32_t u8v_boundary_errors(uint64_t w8, unsigned ka, unsigned kb, u8v_consts k) {
   const uint64_t keep_a = ka >= 4 ? 0ull : (0xFFFFFFFFull & ~((1ull << (8 * ka)) - 1ull));
   const uint64_t keep_b = kb <= 4 ? 0ull : ((kb >= 8 ? ~0ull : (1ull << (8 * kb)) - 1ull) & ~0xFFFFFFFFull);

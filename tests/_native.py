@@ -99,7 +99,6 @@ def swar():
     L.swar_exhaustive.argtypes = [C.c_uint, C.c_int] + [C.POINTER(C.c_uint64)] * 3
     L.swar_pairs.argtypes = [C.c_size_t, C.c_uint]
     L.swar_pairs.restype = C.c_uint64
-    L.swar_batch.argtypes = [u8p, u8p, C.c_size_t, C.c_uint, u8p]
     L.swar_batch_decomp.argtypes = [u8p, u8p, C.c_size_t, C.c_uint, u8p]
     L.oracle_exhaustive_verdicts.argtypes = [C.c_int, u8p]
     L.exhaustive_inputs.argtypes = [C.c_int, u8p]

@@ -112,59 +112,6 @@ uint64_t swar_pairs(size_t offset, unsigned align) {
   return mm;
 }
 
-/* Batch semantics through u8v_word_errors_bounded_lead (the SWAR statement of
- * K2), with the record-start masks built per word:
- * records [offsets[r], offsets[r+1]) of one contiguous buffer starting `off`
- * bytes into the word grid.  verdicts[r] = 1 / 0. */
-void swar_batch(const uint8_t* data, const uint64_t* offsets, size_t n_records, unsigned off,
-                uint8_t* verdicts) {
-  if (n_records == 0) return;
-  const int64_t lo = (int64_t)off + (int64_t)offsets[0];
-  const int64_t hi = (int64_t)off + (int64_t)offsets[n_records];
-  for (size_t r = 0; r < n_records; ++r) verdicts[r] = 1;
-  if (hi <= lo) return;
-  const int64_t words = (hi + 3 + 3) / 4;
-  u8v_carry c = u8v_carry_zero();
-  uint32_t pbm = 0;
-  size_t rcur = 0; /* record of the current lane */
-  const u8v_consts kc = u8v_make_consts();
-  for (int64_t k = lo / 4; k < words; ++k) {
-    uint32_t w = 0, wn = 0, bm = 0;
-    for (int j = 0; j < 4; ++j) {
-      const int64_t q = 4 * k + j;
-      if (q >= lo && q < hi) w |= (uint32_t)data[q - (int64_t)off] << (8 * j);
-      if (q + 4 >= lo && q + 4 < hi) wn |= (uint32_t)data[q + 4 - (int64_t)off] << (8 * j);
-      for (size_t r = 0; r <= n_records; ++r)
-        if ((int64_t)offsets[r] + (int64_t)off == q) bm |= 0x80u << (8 * j);
-    }
-    if (k == lo / 4) c = u8v_carry_zero();
-    uint32_t end_err = 0;
-    const uint32_t e = u8v_word_errors_bounded_lead(w, wn, &c, bm, pbm, &end_err, kc);
-    for (int j = 0; j < 4; ++j) {
-      const int64_t q = 4 * k + j - (int64_t)off; /* data coords */
-      /* record of lane q: largest r < n with offsets[r] <= q */
-      while (rcur + 1 < n_records && (int64_t)offsets[rcur + 1] <= q) ++rcur;
-      if ((e >> (8 * j + 7)) & 1) {
-        if (q >= (int64_t)offsets[0] && q < (int64_t)offsets[n_records] + 3) {
-          size_t r = 0;
-          while (r + 1 < n_records && (int64_t)offsets[r + 1] <= q) ++r;
-          if (q < (int64_t)offsets[n_records]) verdicts[r] = 0;
-          else verdicts[n_records - 1] = 0; /* lanes past the end: last record */
-        }
-      }
-      if ((end_err >> (8 * j + 7)) & 1) {
-        const int64_t qb = q - 1;
-        if (qb >= (int64_t)offsets[0]) {
-          size_t r = 0;
-          while (r + 1 < n_records && (int64_t)offsets[r + 1] <= qb) ++r;
-          verdicts[r] = 0;
-        }
-      }
-    }
-    pbm = bm;
-  }
-}
-
 /* K2's decomposition (batch.cu): the UNBOUNDED lane flags of the whole
  * buffer, attributed to the record of each flagged lane except the first
  * three lanes of a record, plus u8v_boundary_errors at every record start
@@ -390,44 +337,6 @@ uint64_t swar_planes_check(uint64_t seed, uint64_t trials) {
   return bad;
 }
 
-/* Record-bounded plane form vs the SWAR bounded lead form, lane for lane, on
- * random chunks with random record-start masks (bits for bytes -4..31). */
-uint64_t swar_bits_bounded_check(uint64_t seed, uint64_t trials) {
-  uint64_t s = seed, bad = 0;
-  const u8v_consts k = u8v_make_consts();
-  static const uint8_t hot[] = {0x00, 0x41, 0x80, 0x8F, 0x90, 0x9F, 0xA0, 0xBF, 0xC0, 0xC1,
-                                0xC2, 0xDF, 0xE0, 0xED, 0xEF, 0xF0, 0xF4, 0xF5, 0xFF};
-  for (uint64_t t = 0; t < trials; ++t) {
-    uint8_t buf[40];
-    const uint64_t mode = bits_rng(&s);
-    for (int q = 0; q < 40; ++q) {
-      const uint64_t r = bits_rng(&s);
-      buf[q] = (mode & 1) ? (uint8_t)r : hot[r % sizeof hot];
-    }
-    uint64_t bnd = bits_rng(&s) & bits_rng(&s) & ((1ull << 36) - 1); /* ~25% density */
-    if (mode & 2) bnd &= bits_rng(&s);                                /* sparser */
-    uint32_t w[8], prev, next;
-    memcpy(&prev, buf, 4);
-    memcpy(w, buf + 4, 32);
-    memcpy(&next, buf + 36, 4);
-    uint32_t end_pl = 0, hi7 = 0;
-    const uint32_t err_pl = u8v_chunk_errors_planes_bounded_k(w, prev, next, k, bnd, &end_pl, &hi7);
-    u8v_carry c = u8v_carry_of(prev);
-    for (int j = 0; j < 8; ++j) {
-      const uint32_t bm = u8v_spread4((uint32_t)(bnd >> (4 + 4 * j)));
-      const uint32_t pbm = u8v_spread4((uint32_t)(bnd >> (4 * j)));
-      uint32_t end_sw = 0;
-      const uint32_t e = u8v_word_errors_bounded_lead(w[j], j < 7 ? w[j + 1] : next, &c, bm, pbm,
-                                                      &end_sw, k);
-      for (int b = 0; b < 4; ++b) {
-        bad += ((e >> (8 * b + 7)) & 1u) != ((err_pl >> (4 * j + b)) & 1u);
-        bad += ((end_sw >> (8 * b + 7)) & 1u) != ((end_pl >> (4 * j + b)) & 1u);
-      }
-    }
-  }
-  return bad;
-}
-
 /* A stream fed in pieces (cut at `cuts`, n_cuts ascending inside [0, n]),
  * stitched with utf8v_stream.h exactly as the device session does it (edge
  * lanes from the carry, the rest in place over each piece); returns 1 when
@@ -504,41 +413,6 @@ uint64_t swar_bits_perm_check(uint64_t seed, uint64_t fuzz) {
       buf[q] = (mode & 1) ? (uint8_t)r : hot[r % sizeof hot];
     }
     bad += perm_compare(buf);
-  }
-  return bad;
-}
-
-/* Permuted bounded form vs natural bounded form (errors and end checks),
- * random chunks and random record-start masks. */
-uint64_t swar_bits_perm_bounded_check(uint64_t seed, uint64_t trials) {
-  uint64_t s = seed, bad = 0;
-  const u8v_consts k = u8v_make_consts();
-  static const uint8_t hot[] = {0x00, 0x41, 0x80, 0x8F, 0x90, 0x9F, 0xA0, 0xBF, 0xC0, 0xC1,
-                                0xC2, 0xDF, 0xE0, 0xED, 0xEF, 0xF0, 0xF4, 0xF5, 0xFF};
-  for (uint64_t t = 0; t < trials; ++t) {
-    uint8_t buf[40];
-    const uint64_t mode = bits_rng(&s);
-    for (int q = 0; q < 40; ++q) {
-      const uint64_t r = bits_rng(&s);
-      buf[q] = (mode & 1) ? (uint8_t)r : hot[r % sizeof hot];
-    }
-    uint64_t bnd = bits_rng(&s) & bits_rng(&s) & ((1ull << 36) - 1);
-    if (mode & 2) bnd &= bits_rng(&s);
-    uint32_t w[8], prev, next, e_nat, e_per, h7a, h7b;
-    memcpy(&prev, buf, 4);
-    memcpy(w, buf + 4, 32);
-    memcpy(&next, buf + 36, 4);
-    const uint32_t err_nat = u8v_chunk_errors_planes_bounded_k(w, prev, next, k, bnd, &e_nat, &h7a);
-    uint32_t B = 0;
-    for (unsigned i = 0; i < 32; ++i)
-      if ((bnd >> (i + 4)) & 1) B |= 1u << u8v_perm_pos(i);
-    /* starts at bytes -1 / -2 (natural mask bits 3 / 2) -> pre bits 31 / 23 */
-    const uint32_t pre2 = (uint32_t)((bnd >> 3) & 1) << 31 | (uint32_t)((bnd >> 2) & 1) << 23;
-    const uint32_t err_per = u8v_chunk_errors_planes_perm_bounded_k(w, prev, next, k, B, pre2, &e_per, &h7b);
-    for (unsigned i = 0; i < 32; ++i) {
-      bad += ((err_nat >> i) & 1u) != ((err_per >> u8v_perm_pos(i)) & 1u);
-      bad += ((e_nat >> i) & 1u) != ((e_per >> u8v_perm_pos(i)) & 1u);
-    }
   }
   return bad;
 }

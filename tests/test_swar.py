@@ -51,7 +51,7 @@ def _batch(parts):
     return data, offs
 
 
-def test_bounded_variant_matches_per_record_oracle():
+def test_k2_decomposition_matches_per_record_oracle():
     rng = np.random.default_rng(11)
     S = nat.swar()
     for trial in range(300):
@@ -73,9 +73,6 @@ def test_bounded_variant_matches_per_record_oracle():
         want = np.array([nat.oracle_verdict(p)[0] for p in parts], np.uint8)
         got = np.empty(len(parts), np.uint8)
         for align in range(4):
-            S.swar_batch(data.ctypes.data if data.size else None, offs.ctypes.data, len(parts), align,
-                         got.ctypes.data)
-            assert np.array_equal(got, want), (trial, align, parts)
             S.swar_batch_decomp(data.ctypes.data if data.size else None, offs.ctypes.data, len(parts), align,
                                 got.ctypes.data)
             assert np.array_equal(got, want), ("decomp", trial, align, parts)
@@ -96,15 +93,6 @@ def test_bit_sliced_form_equals_swar_form_lane_for_lane():
     S.swar_bits_check.restype = C.c_uint64
     S.swar_bits_check.argtypes = [C.c_uint64, C.c_uint64]
     assert S.swar_bits_check(11, 200000) == 0
-
-
-def test_bit_sliced_bounded_form_equals_swar_bounded_form():
-    """K2's record-bounded plane form == u8v_word_errors_bounded_lead lane for
-    lane (errors and end-of-record checks) under random record-start masks."""
-    S = nat.swar()
-    S.swar_bits_bounded_check.restype = C.c_uint64
-    S.swar_bits_bounded_check.argtypes = [C.c_uint64, C.c_uint64]
-    assert S.swar_bits_bounded_check(5, 300000) == 0
 
 
 def test_stream_stitching_equals_whole_stream():
@@ -154,16 +142,6 @@ def test_bit_sliced_permuted_form_equals_natural_form():
     S.swar_bits_perm_check.restype = C.c_uint64
     S.swar_bits_perm_check.argtypes = [C.c_uint64, C.c_uint64]
     assert S.swar_bits_perm_check(13, 300000) == 0
-
-
-def test_bit_sliced_permuted_bounded_form_equals_natural_bounded_form():
-    """K2's permuted record-bounded plane form (record-start plane and the
-    starts just before the chunk in permuted layout) flags the same lanes and
-    end checks as the natural bounded form."""
-    S = nat.swar()
-    S.swar_bits_perm_bounded_check.restype = C.c_uint64
-    S.swar_bits_perm_bounded_check.argtypes = [C.c_uint64, C.c_uint64]
-    assert S.swar_bits_perm_bounded_check(17, 300000) == 0
 
 
 def test_k2_boundary_decomposition_adversarial():
