@@ -12,16 +12,15 @@
 // form).  A lane's record-bounded flag can differ from its unbounded one
 // only for the first three lanes of a record (their look-back crosses the
 // start) and for the previous record's end-of-stream lanes, so:
-//   * a flagged lane (rare) is attributed, out of line, to its record unless
-//     it is one of that record's first three lanes;
-//   * every record start is checked on its own: the window lane that holds
-//     it reads the 8 bytes around it (L2-hot: the sweep just streamed them)
-//     and runs u8v_boundary_errors (utf8v_swar.h) for the record ending there
-//     and the record starting there.
+//   * a flagged lane is attributed, out of line, to its record (a shuffle
+//     search over a window of 32 record starts) unless it is one of that
+//     record's first three lanes or lies past the data;
+//   * every record start is checked on its own, 32 starts per warp pass once
+//     the sweep has passed them: each lane reads the 8 bytes around its start
+//     (mostly L2 hits) and runs u8v_boundary_errors (utf8v_swar.h) for the
+//     record ending there and the record starting there.
 // The decomposition is proven against per-record validation on the CPU
-// (tests/test_swar.py::test_k2_boundary_decomposition_adversarial).  Each
-// step reads a window of 32 record starts (one coalesced load) only when
-// the next start falls inside it.  Verdicts start at 1 (memset by the
+// (tests/test_swar.py::test_k2_*).  Verdicts start at 1 (memset by the
 // caller) and invalid records get a plain 0 store (idempotent, no atomics).
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -45,9 +44,9 @@ struct BatchDesc {
   u8v_consts k;  // runtime multipliers (FMA-pipe routing, utf8v_swar.h)
 };
 
-// What the record lookups need, passed by value: the out-of-line
-// attribution taking the whole descriptor by reference would pin it in local
-// memory and turn every offset lookup of the hot window loop into an LDL.
+// What the record lookups need, passed by value: out-of-line helpers taking
+// the whole descriptor by reference would pin it in local memory and turn
+// every offset lookup into an LDL.
 struct RecView {
   const uint64_t* offsets;
   uint8_t* verdicts;
@@ -84,8 +83,8 @@ __device__ int64_t find_record(const RecView& d, int64_t pos) {
   return r < d.n_records ? r : d.n_records - 1;
 }
 
-// Window positions are 32-bit offsets from the step start, clamped far out
-// of the step on either side (compares and shuffles stay 32-bit).
+// Positions as 32-bit offsets from a base (a step or the warp's range start),
+// clamped far out on either side, so compares and shuffles stay 32-bit.
 constexpr int kFar = 1 << 30;
 __device__ __forceinline__ int rel32(int64_t pos, int64_t s0) {
   const int64_t r = pos - s0;
@@ -94,16 +93,15 @@ __device__ __forceinline__ int rel32(int64_t pos, int64_t s0) {
 
 // Out of line, for steps with a flagged lane: each flagged lane q goes to
 // its record -- the last window start at or before q, found by a 5-step
-// shuffle search over the window (lane L holds start(r0 + L) - s0), or r0
-// when the step holds no start -- unless q is one of that record's first
-// three lanes or lies past the data (those lanes are settled by
-// fix_boundary).  e0..e3: lane bits of chunk (lane + 32 i) of the step in
-// the permuted plane order of utf8v_bits.h (bit pos(i) = byte i).
+// shuffle search over the window (lane L holds start(r0 + L) - s0, with
+// start(r0) <= s0 or r0 = 0) -- unless q is one of that record's first three
+// lanes or lies past the data (those lanes are settled by fix_boundary).
+// e0..e3: lane bits of chunk (lane + 32 i) of the step in the permuted plane
+// order of utf8v_bits.h (bit pos(i) = byte i).
 __device__ __noinline__ void attribute_step(RecView d, int64_t s0, int64_t hi, uint32_t e0, uint32_t e1,
-                                            uint32_t e2, uint32_t e3, int o, bool window, int64_t r0,
-                                            int base_rel) {
+                                            uint32_t e2, uint32_t e3, int o, int64_t r0) {
   const int lane = threadIdx.x & 31;
-  const bool full = window && __all_sync(0xFFFFFFFFu, o < kStepChunks * kChunkBytes);
+  const bool full = __all_sync(0xFFFFFFFFu, o < kStepChunks * kChunkBytes);
   const int hi_rel = rel32(hi, s0);
   static_assert(kU == 4, "attribute_step takes one mask per chunk of a step");
   // One flagged lane per lane and round, lowest chunk first.
@@ -128,15 +126,13 @@ __device__ __noinline__ void attribute_step(RecView d, int64_t s0, int64_t hi, u
     }
     if (e) q = c * kChunkBytes + (int)u8v_perm_byte((unsigned)(__ffs(e) - 1));
     int L = 0;
-    if (window) {
 #pragma unroll
-      for (int st = 16; st > 0; st >>= 1) {
-        const int cand = L + st;
-        const int t = __shfl_sync(0xFFFFFFFFu, o, cand & 31);
-        if (cand <= 31 && t <= q) L = cand;
-      }
+    for (int st = 16; st > 0; st >>= 1) {
+      const int cand = L + st;
+      const int t = __shfl_sync(0xFFFFFFFFu, o, cand & 31);
+      if (cand <= 31 && t <= q) L = cand;
     }
-    const int start = window ? __shfl_sync(0xFFFFFFFFu, o, L) : base_rel;
+    const int start = __shfl_sync(0xFFFFFFFFu, o, L);
     if (q >= 0 && q < hi_rel && q >= start) {
       int64_t r = r0 + L;
       int64_t st_abs = s0 + start;
@@ -223,13 +219,13 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
   const int nsteps = (int)(step_end - step0);
 
   constexpr int kStepBytes = kStepChunks * kChunkBytes;
-  // Loop state is kept 32-bit and relative (positions to range_lo, records
-  // to r_in) so it stays in registers across the chunk math.
   // A batch of 32 starts runs once the sweep passes its last start.  Its
   // oldest starts are ~6 steps back by then and some of their sectors have
   // left L2 (~6 % extra DRAM reads on C3); triggering at start 15 halves that
   // but stalls on DRAM reads ahead of the sweep (-1.6 %, measured).
   constexpr int kTrigger = 31;
+  // Loop state is kept 32-bit and relative (positions to range_lo, records
+  // to r_in) so it stays in registers across the chunk math.
   const int64_t range_lo = (d.c_begin + step0 * kStepChunks) * kChunkBytes;
   const int64_t range_hi = range_lo + (int64_t)nsteps * kStepBytes;
   uint32_t carry_word = 0;
@@ -312,8 +308,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
         if (__ballot_sync(0xFFFFFFFFu, o <= 0) != 0xFFFFFFFFu) break;
         ratt += 31;
       }
-      attribute_step(rv, s0, d.hi, err[0], err[1], err[2], err[3], o, true, r_in + ratt,
-                     __shfl_sync(0xFFFFFFFFu, o, 0));
+      attribute_step(rv, s0, d.hi, err[0], err[1], err[2], err[3], o, r_in + ratt);
       const unsigned le = __ballot_sync(0xFFFFFFFFu, o <= 0);
       if (le) ratt += 31 - __clz(le);
     }
