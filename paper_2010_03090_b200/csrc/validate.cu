@@ -101,7 +101,8 @@ __device__ __forceinline__ void interior_steps(const StreamDesc& d, int64_t* int
   const int64_t in_lo = d.lo > d.L0 ? d.lo : d.L0;
   const int64_t in_hi = d.hi < d.L1 ? d.hi : d.L1;
   const int64_t sb = kStepChunks * (int64_t)kChunkBytes;
-  int64_t b = (in_lo - d.c_begin * kChunkBytes + sb - 1) / sb;
+  // + 4: the word before an interior step is real too (plain halo load).
+  int64_t b = (in_lo + 4 - d.c_begin * kChunkBytes + sb - 1) / sb;
   if (b < 0) b = 0;
   int64_t e = (in_hi - d.c_begin * kChunkBytes) / sb;
   const int64_t h = (d.hi - 4 - d.c_begin * kChunkBytes) / sb;
@@ -127,7 +128,7 @@ __device__ __forceinline__ uint32_t any_step_errors(const StreamDesc& d, int64_t
     const uint8_t* p = d.base + s0 + lane * kChunkBytes;
 #pragma unroll
     for (int i = 0; i < kU; ++i) v[i] = ld_chunk(p + 32 * i * kChunkBytes);
-    if (lane == 31) carry_word = ld_word_guarded(d.base, s0 - 4, d.lo, d.hi);
+    if (lane == 31) carry_word = __ldg(reinterpret_cast<const uint32_t*>(d.base + s0 - 4));
     if (lane == 0) nsw = __ldg(reinterpret_cast<const uint32_t*>(d.base + s0 + sb));
     return step_errors<kPos, false>(d, v, cstep, lane, carry_word, nsw, first_i, was_ascii);
   }
@@ -180,7 +181,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_validate(StreamDesc d, uint32_t
 #pragma unroll
         for (int i = 0; i < kU; ++i) v[i] = ld_chunk(p + (lane + 32 * i) * kChunkBytes);
         uint32_t carry_word = 0, nsw = 0;
-        if (lane == 31) carry_word = ld_word_guarded(d.base, (int64_t)(p - d.base) - 4, d.lo, d.hi);
+        if (lane == 31) carry_word = __ldg(reinterpret_cast<const uint32_t*>(p - 4));
         if (lane == 0) nsw = __ldg(reinterpret_cast<const uint32_t*>(p + sb));
         acc |= step_errors<false, false>(d, v, 0, lane, carry_word, nsw, unused, was_ascii);
       }

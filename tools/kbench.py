@@ -1,4 +1,6 @@
-"""DEVELOPMENT HARNESS: time K1 inner-loop variants (tools/kbench.cu) on C1."""
+"""DEVELOPMENT HARNESS: time K1 inner-loop variants (tools/kbench.cu) on C1.
+`python tools/kbench.py [name-prefix ...]` times only the variants whose names
+start with one of the prefixes (all when none are given)."""
 import ctypes as C, json, subprocess, sys
 from pathlib import Path
 ROOT = Path(__file__).resolve().parent.parent
@@ -18,8 +20,11 @@ bad = d.clone(); bad[n // 3] = 0xC0
 flag = torch.zeros(1, dtype=torch.int32, device="cuda")
 st = torch.cuda.current_stream()
 res = {}
+only = tuple(sys.argv[1:])
 for i in range(L.kb_count()):
     name = L.kb_name(i).decode()
+    if only and not name.startswith(only):
+        continue
     flag.zero_(); L.kb_launch(i, d.data_ptr(), n, flag.data_ptr(), st.cuda_stream); torch.cuda.synchronize()
     ok = int(flag.item()) == 0
     flag.zero_(); L.kb_launch(i, bad.data_ptr(), n, flag.data_ptr(), st.cuda_stream); torch.cuda.synchronize()
@@ -34,7 +39,7 @@ for i in range(L.kb_count()):
     res[name] = {"GBps": n / ms / 1e6, "ms": ms, "valid_ok": ok, "detects": detects, "blocks_per_sm": occ}
     print(name, json.dumps(res[name]), flush=True)
 # ASCII (C0 recipe) 1 GiB: the fast path's case
-a = configs.gen_stream(n, seed=1, ascii_only=True)
+a = None if only else configs.gen_stream(n, seed=1, ascii_only=True)
 if a is not None:
     for i in range(L.kb_count()):
         name = L.kb_name(i).decode()
