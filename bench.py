@@ -408,7 +408,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             "data": "synthetic (seeded splitmix64 generator, DESIGN.md 'Synthetic inputs')",
             "config": {"workload": workload, "bytes_per_gpu": per, "bytes_total": per * world,
                        "l2": "input (>=1 GiB) larger than the 126 MB L2; no flush needed",
-                       "parallelism": f"dp{world}: byte-range shards (<=16-byte look-back head, 1-byte tail)"
+                       "parallelism": f"dp{world}: byte-range shards (<=16-byte look-back head, 3-byte tail)"
                                       + (" + 1-word NCCL allreduce(MAX) per step, overlapped with the next"
                                          " step's kernel" if world > 1 else "")},
             "per_gpu_GBps": per_gpu, "verdict_valid": verdict_ok,

@@ -53,7 +53,8 @@ extern "C" {
  *      utf8v_cuda_stream_feed is ordered after all work issued before the
  *      call to the legacy default stream, like a synchronous cudaMemcpy;
  *      writes made on a non-blocking stream must be synchronised by the
- *      caller */
+ *      caller
+ *   4  utf8v_cuda_validate_verdict_lanes (first error of a shard) */
 int utf8v_cuda_abi_version(void);
 
 /* Human-readable text of the last error on this thread ("" if none). */
@@ -71,6 +72,20 @@ int utf8v_cuda_validate(const uint8_t* p, size_t n, int is_device, uint8_t* out_
  * proj/include/utf8v/verdict.hpp:20-27). */
 int utf8v_cuda_validate_verdict(const uint8_t* p, size_t n, int is_device, uint8_t* out_valid,
                                 uint64_t* out_offset, int* out_kind);
+
+/* The verdict of lanes [lane_lo, lane_hi) of p[0..n) (lane_hi <= n + 3; lane
+ * i reads bytes i-3 .. i+1, zero outside [0, n)): the shard form of
+ * utf8v_cuda_validate_verdict for a stream split over GPUs.
+ * *out_valid = 1 iff none of the lanes is flagged; otherwise *out_offset /
+ * *out_kind are decoded from the bytes around the first flagged 32-byte
+ * chunk, in p's coordinates.  The result is the stream's first error when
+ * everything before that error is valid text, when p holds at least 6 bytes
+ * before lane_lo (or lane_lo < 6 and p starts the stream), and when it holds
+ * 3 bytes past the error's lead (sharding.py: a 16-byte head and a 3-byte
+ * tail).  Ranks combine their (offset, kind) with one allreduce(MIN). */
+int utf8v_cuda_validate_verdict_lanes(const uint8_t* p, uint64_t n, uint64_t lane_lo, uint64_t lane_hi,
+                                      int is_device, uint8_t* out_valid, uint64_t* out_offset,
+                                      int* out_kind);
 
 /* Records p[offsets[r] .. offsets[r+1]) for r < n_records, each validated as
  * its own stream (the reference loops validate_lookup per record); writes

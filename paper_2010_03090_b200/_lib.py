@@ -30,6 +30,8 @@ SIGNATURES: dict[str, tuple] = {
     "utf8v_cuda_validate": (C.c_int, [C.c_void_p, C.c_size_t, C.c_int, _u8p]),
     "utf8v_cuda_validate_verdict": (C.c_int, [C.c_void_p, C.c_size_t, C.c_int, _u8p, _u64p,
                                               C.POINTER(C.c_int)]),
+    "utf8v_cuda_validate_verdict_lanes": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int,
+                                                    _u8p, _u64p, C.POINTER(C.c_int)]),
     "utf8v_cuda_validate_batch": (C.c_int, [C.c_void_p, C.c_size_t, C.c_void_p, C.c_size_t, C.c_int,
                                             C.c_void_p]),
     "utf8v_cuda_classify_lanes": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),

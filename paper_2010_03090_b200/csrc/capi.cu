@@ -340,7 +340,7 @@ int validate_host_lanes(Ctx& c, const uint8_t* p, size_t n, uint64_t lane_lo, ui
 
 extern "C" {
 
-int utf8v_cuda_abi_version(void) { return 3; }
+int utf8v_cuda_abi_version(void) { return 4; }
 
 const char* utf8v_cuda_last_error(void) { return t_err.c_str(); }
 
@@ -377,32 +377,31 @@ int utf8v_cuda_validate(const uint8_t* p, size_t n, int is_device, uint8_t* out_
   return UTF8V_OK;
 }
 
-int utf8v_cuda_validate_verdict(const uint8_t* p, size_t n, int is_device, uint8_t* out_valid,
-                                uint64_t* out_offset, int* out_kind) {
+// Verdict of lanes [lane_lo, lane_hi) of p[0..n): K1 over the lanes first
+// (host input piece by piece as the bytes land, as in utf8v_cuda_validate),
+// and only a flagged input is rescanned by K3 + the window decode.
+static int verdict_lanes(const uint8_t* p, uint64_t n, uint64_t lane_lo, uint64_t lane_hi, int is_device,
+                         uint8_t* out_valid, uint64_t* out_offset, int* out_kind) {
   t_launches = 0;
   if (!out_valid || !out_offset || !out_kind) return fail(UTF8V_ERR_ARG, "NULL output");
+  if (lane_hi > n + 3 || lane_lo > lane_hi) return fail(UTF8V_ERR_ARG, "bad lane range");
   *out_offset = 0;
   *out_kind = -1;
-  if (n == 0) {
-    *out_valid = 1;
-    return UTF8V_OK;
-  }
+  *out_valid = 1;
+  if (n == 0 || lane_lo == lane_hi) return UTF8V_OK;
   if (!p) return fail(UTF8V_ERR_ARG, "NULL data with n > 0");
   Ctx* c;
   int st = get_ctx(&c);
   if (st) return st;
-  // Valid text (the common case) costs one K1 pass: K1 runs first (for host
-  // input piece by piece as the bytes land, as in utf8v_cuda_validate), and
-  // only a flagged input is rescanned by K3 + the window decode.
   const uint8_t* d = p;
   CK(cudaMemsetAsync(c->d_flag, 0, 4, c->s_comp));
   if (is_device) {
     st = after_legacy(c->s_comp, c->ev_legacy);
     if (st) return st;
-    u8v::launch_validate(u8v::make_desc(p, n, 0, n + 3), c->d_flag, c->s_comp);
+    u8v::launch_validate(u8v::make_desc(p, n, lane_lo, lane_hi), c->d_flag, c->s_comp);
     ++t_launches;
   } else {
-    st = validate_host_lanes(*c, p, n, 0, n + 3);
+    st = validate_host_lanes(*c, p, n, lane_lo, lane_hi);
     if (st) return st;
     d = c->d_stage;
   }
@@ -410,13 +409,10 @@ int utf8v_cuda_validate_verdict(const uint8_t* p, size_t n, int is_device, uint8
   if (st) return st;
   CK(cudaMemcpyAsync(c->h_res, c->d_flag, 4, cudaMemcpyDeviceToHost, c->s_comp));
   CK(cudaStreamSynchronize(c->s_comp));
-  if (c->h_res[0] == 0) {
-    *out_valid = 1;
-    return UTF8V_OK;
-  }
+  if (c->h_res[0] == 0) return UTF8V_OK;
   CK(cudaMemsetAsync(c->d_flag, 0, 4, c->s_comp));
   CK(cudaMemsetAsync(c->d_pos, 0xFF, 16, c->s_comp));
-  u8v::launch_first_error(u8v::make_desc(d, n, 0, n + 3), n, c->d_flag, c->d_pos, c->d_pos + 2,
+  u8v::launch_first_error(u8v::make_desc(d, n, lane_lo, lane_hi), n, c->d_flag, c->d_pos, c->d_pos + 2,
                           c->d_pos + 1, c->d_kind, c->s_comp);
   t_launches += 2;
   st = check_launch("first_error kernel");
@@ -425,10 +421,7 @@ int utf8v_cuda_validate_verdict(const uint8_t* p, size_t n, int is_device, uint8
   CK(cudaMemcpyAsync(c->h_res + 2, c->d_pos + 1, 8, cudaMemcpyDeviceToHost, c->s_comp));
   CK(cudaMemcpyAsync(c->h_res + 4, c->d_kind, 4, cudaMemcpyDeviceToHost, c->s_comp));
   CK(cudaStreamSynchronize(c->s_comp));
-  if (c->h_res[0] == 0) {
-    *out_valid = 1;
-    return UTF8V_OK;
-  }
+  if (c->h_res[0] == 0) return UTF8V_OK;
   *out_valid = 0;
   uint64_t off;
   memcpy(&off, c->h_res + 2, 8);
@@ -437,6 +430,17 @@ int utf8v_cuda_validate_verdict(const uint8_t* p, size_t n, int is_device, uint8
   *out_offset = off;
   *out_kind = kind;
   return UTF8V_OK;
+}
+
+int utf8v_cuda_validate_verdict(const uint8_t* p, size_t n, int is_device, uint8_t* out_valid,
+                                uint64_t* out_offset, int* out_kind) {
+  return verdict_lanes(p, n, 0, (uint64_t)n + 3, is_device, out_valid, out_offset, out_kind);
+}
+
+int utf8v_cuda_validate_verdict_lanes(const uint8_t* p, uint64_t n, uint64_t lane_lo, uint64_t lane_hi,
+                                      int is_device, uint8_t* out_valid, uint64_t* out_offset,
+                                      int* out_kind) {
+  return verdict_lanes(p, n, lane_lo, lane_hi, is_device, out_valid, out_offset, out_kind);
 }
 
 int utf8v_cuda_validate_lanes_async(const uint8_t* d_p, uint64_t n, uint64_t lane_lo,

@@ -278,13 +278,17 @@ __device__ int decode_window(const uint8_t* s, uint64_t from, uint64_t to, uint6
 // chunk_end) and the decode needs bytes up to E + 3.  The window starts at
 // the character boundary at or before chunk_start - 3 (at most 3
 // continuation bytes back; if there are more, E is at that point).
-__global__ void k_locate(const uint8_t* __restrict__ s, uint64_t n, int64_t off,
+// For a lane range [lane_lo, ...) the chunk may start before lane_lo, in
+// bytes another shard owns: the window then starts at lane_lo - 3 (still at
+// or before E, as E >= L - 3 >= lane_lo - 3), so it never decodes from the
+// middle of a character at the start of a shard's head.
+__global__ void k_locate(const uint8_t* __restrict__ s, uint64_t n, int64_t off, int64_t lane_lo,
                          const unsigned long long* __restrict__ first_chunk,
                          unsigned long long* __restrict__ out_offset, int* __restrict__ out_kind) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   const unsigned long long c = *first_chunk;
   const int64_t lmin = (int64_t)c * kChunkBytes - off;  // first lane of the chunk
-  int64_t b0 = lmin - 3;
+  int64_t b0 = (lmin > lane_lo ? lmin : lane_lo) - 3;
   if (b0 < 0) b0 = 0;
   if ((uint64_t)b0 > n) b0 = (int64_t)n;
   int64_t b = b0;
@@ -375,7 +379,7 @@ void launch_first_error(const StreamDesc& d, uint64_t n, uint32_t* flag, unsigne
     cudaMemsetAsync(next_round, 0, sizeof(*next_round), st);
     k_first_error<<<(unsigned)blocks, kThreads, 0, st>>>(d, flag, first_chunk, next_round);
   }
-  k_locate<<<1, 32, 0, st>>>(d.base + d.off32, n, d.off32, first_chunk, out_offset, out_kind);
+  k_locate<<<1, 32, 0, st>>>(d.base + d.off32, n, d.off32, d.L0 - d.off32, first_chunk, out_offset, out_kind);
 }
 
 }  // namespace u8v

@@ -3,9 +3,12 @@
 One process per GPU.  The stream [0, n) is cut into `world` byte-range
 shards [s_k, e_k); rank k holds its shard plus
   * a head of up to 16 bytes before s_k (the 3-byte look-back halo the
-    S check needs: x[i-1], x[i-2], x[i-3]), and
-  * a tail of 1 byte after e_k (the lookahead of the rare-pair check that
-    K1 evaluates at the lead's lane), except on the last shard,
+    S check needs: x[i-1], x[i-2], x[i-3]; the first-error decode steps back
+    up to 6), and
+  * a tail of up to 3 bytes after e_k (the 1-byte lookahead of the
+    rare-pair check that K1 evaluates at the lead's lane, and the rest of a
+    character whose lead ends the shard, for the first-error decode),
+    except on the last shard,
 and evaluates lanes [s_k, e_k) -- the last shard also the end-of-input lanes
 [n, n+3) (check_incomplete, proj/include/utf8v/lookup_kernel.hpp:48-68).
 Every lane of the whole stream is evaluated by exactly one rank with the
@@ -13,9 +16,11 @@ bytes the single-stream kernel would see, so
 
     stream valid  <=>  max over ranks of the error flag == 0,
 
-combined with one 4-byte allreduce(MAX) over NCCL (NVLink/NVSwitch).  There
-is no other data-path exchange: shards are independent.  Shard edges may cut
-characters anywhere (config 4 forces them inside 3-/4-byte characters).
+combined with one 4-byte allreduce(MAX) over NCCL (NVLink/NVSwitch).  The
+first error (offset, kind) is one 8-byte allreduce(MIN) of each rank's
+local decode (verdict_sharded).  There is no other data-path exchange:
+shards are independent.  Shard edges may cut characters anywhere (config 4
+forces them inside 3-/4-byte characters).
 """
 from __future__ import annotations
 
@@ -23,7 +28,8 @@ import ctypes as C
 from dataclasses import dataclass
 from typing import Callable, Optional
 
-HEAD = 16  # look-back bytes carried before each shard (>= 3)
+HEAD = 16  # look-back bytes carried before each shard (>= 3; >= 6 for positions)
+TAIL = 3   # bytes carried after each shard but the last (>= 1; 3 for positions)
 
 
 @dataclass(frozen=True)
@@ -44,7 +50,7 @@ class Shard:
 
     @property
     def tail(self) -> int:
-        return 0 if self.last or self.end >= self.n_total else 1
+        return 0 if self.last else min(TAIL, self.n_total - self.end)
 
     @property
     def lo(self) -> int:
@@ -112,6 +118,51 @@ def validate_sharded(local, shard: Shard, group=None, device=None,
     verdict of the whole stream."""
     flag = (shard_flag or shard_error_flag)(local, shard)
     return combine(flag, group=group, device=device)
+
+
+def shard_first_error(local, shard: Shard) -> Optional[tuple[int, int]]:
+    """(stream offset, kind) of the first error this rank's lanes show, decoded
+    from its own bytes (utf8v_cuda_validate_verdict_lanes), or None.  The
+    rank holding the stream's first flagged lane decodes the stream's first
+    error exactly (everything before it is valid text; the head and tail
+    hold the bytes the decode window needs); no rank decodes an earlier one,
+    so the minimum over ranks is the stream's first error."""
+    from . import _input, _lib
+    lib = _lib.load()
+    ptr, n, dev, _keep = _input(local)
+    if n != shard.n_local:
+        raise ValueError(f"shard buffer holds {n} bytes, expected {shard.n_local}")
+    lo, hi = shard.lanes
+    ok, off, kind = C.c_uint8(0), C.c_uint64(0), C.c_int(-1)
+    _lib.check(lib.utf8v_cuda_validate_verdict_lanes(ptr, n, lo, hi, dev, C.byref(ok), C.byref(off),
+                                                     C.byref(kind)))
+    if ok.value:
+        return None
+    return shard.lo + int(off.value), int(kind.value)
+
+
+_NO_ERROR = (1 << 63) - 1
+
+
+def combine_first_error(local_error: Optional[tuple[int, int]], group=None, device=None):
+    """One 8-byte allreduce(MIN) of offset * 8 + kind; returns the stream's
+    Verdict (the reference's validate_lookup_verdict result)."""
+    import torch
+    import torch.distributed as dist
+    from . import Verdict
+    key = _NO_ERROR if local_error is None else local_error[0] * 8 + local_error[1]
+    t = torch.tensor([key], dtype=torch.int64, device=device)
+    if dist.is_available() and dist.is_initialized():
+        dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+    key = int(t.item())
+    return Verdict() if key == _NO_ERROR else Verdict.fail(key >> 3, key & 7)
+
+
+def verdict_sharded(local, shard: Shard, group=None, device=None,
+                    shard_locate: Optional[Callable[[object, Shard], Optional[tuple[int, int]]]] = None):
+    """Collective: every rank calls it with its own shard; all get the
+    stream's Verdict, bit-exact with oracle_validate (proj/src/oracle.cpp:10-44)."""
+    return combine_first_error((shard_locate or shard_first_error)(local, shard), group=group, device=device)
 
 
 # ---- record batches (C2, C3) over G GPUs (SURVEY §8(e)) ---------------------

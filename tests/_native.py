@@ -100,6 +100,8 @@ def swar():
     L.swar_pairs.argtypes = [C.c_size_t, C.c_uint]
     L.swar_pairs.restype = C.c_uint64
     L.swar_batch_decomp.argtypes = [u8p, u8p, C.c_size_t, C.c_uint, u8p]
+    L.swar_first_lane_in.argtypes = [u8p, C.c_size_t, C.c_uint64, C.c_uint64]
+    L.swar_first_lane_in.restype = C.c_uint64
     L.oracle_exhaustive_verdicts.argtypes = [C.c_int, u8p]
     L.exhaustive_inputs.argtypes = [C.c_int, u8p]
     L.oracle_batch.argtypes = [u8p, u8p, C.c_size_t, C.c_int, u8p, u8p, u8p]

@@ -68,6 +68,25 @@ int swar_lanes(const uint8_t* p, size_t n, uint64_t lane_lo, uint64_t lane_hi) {
   return 0;
 }
 
+/* The first flagged lane in [lane_lo, lane_hi) of the zero-extended stream
+ * p[0..n), or UINT64_MAX: the CPU model of a shard's first-error lane. */
+uint64_t swar_first_lane_in(const uint8_t* p, size_t n, uint64_t lane_lo, uint64_t lane_hi) {
+  const int64_t hi = (int64_t)n;
+  const int64_t words = ((int64_t)lane_hi + 3) / 4 + 1;
+  const u8v_consts kc = u8v_make_consts();
+  u8v_carry c = u8v_carry_zero();
+  uint32_t w = word_at(p, 0, 0, hi);
+  for (int64_t k = 0; k < words; ++k) {
+    const uint32_t wn = word_at(p, k + 1, 0, hi);
+    const uint32_t e = u8v_mask_word(u8v_word_errors_lead(w, wn, &c, kc), 4 * k, (int64_t)lane_lo,
+                                     (int64_t)lane_hi) & U8V_B7;
+    w = wn;
+    for (int j = 0; j < 4; ++j)
+      if ((e >> (8 * j + 7)) & 1) return (uint64_t)(4 * k + j);
+  }
+  return UINT64_MAX;
+}
+
 /* Exhaustive agreement for every input of length 0..max_len (<= 3) at word
  * alignment `off`: counts verdict mismatches and first-lane bound violations
  * (E <= L <= E+3).  Mirrors proj/tests/acceptance.cpp:74-113. */

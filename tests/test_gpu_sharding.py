@@ -90,3 +90,45 @@ def test_python_sharded_wrapper():
         bad[(3 << 20) + 1] = 0xFF
         assert u8.validate_lookup_sharded(bad, g) is False
     assert u8.validate_lookup_sharded(d, 4) is True  # device input: its own GPU
+
+
+def test_byte_shards_first_error_positions():
+    """verdict_sharded's device half: each shard's local first-error decode
+    (utf8v_cuda_validate_verdict_lanes, device and host buffers), combined
+    by MIN as the allreduce would, equals the whole stream's oracle
+    (offset, kind) -- bad sequences straddling every shard edge, in the
+    head, in the 3-byte tail, and a truncated stream end."""
+    import torch
+    from paper_2010_03090_b200 import configs, sharding
+    from tests import _native as nat
+    base = configs.gen_c1(2 << 20, seed=6).cpu().numpy()
+    seqs = ([0xC0], [0xE0, 0x80, 0x80], [0xED, 0xA0, 0x80], [0xF4, 0x90, 0x80, 0x80], [0xF0, 0x80, 0x80, 0x80],
+            [0xE2, 0x82, 0x41], [0xFF], [0x80, 0x80])
+    cases = [base]
+    for world in (2, 3, 8):
+        for sh in sharding.plan(base.size, world)[1:3]:
+            for delta in (-5, -3, -2, -1, 0, 1, 2, 3):
+                for seq in seqs:
+                    d = base.copy()
+                    d[sh.start + delta:sh.start + delta + len(seq)] = seq
+                    cases.append((world, d))
+    t = base.copy()
+    t[-2:] = [0xF0, 0x9F]
+    cases += [(w, t) for w in (2, 3, 8)]
+    for i, case in enumerate(cases[1:]):
+        world, d = case
+        ok, off, kind = nat.oracle_verdict(d.tobytes())
+        want = None if ok else (off, kind)
+        dev = torch.from_numpy(d).cuda()
+        found = []
+        for sh in sharding.plan(d.size, world):
+            local = dev[sh.lo:sh.hi] if i % 2 == 0 else d[sh.lo:sh.hi].tobytes()
+            e = sharding.shard_first_error(local, sh)
+            if e is not None:
+                found.append(e)
+        got = min(found, key=lambda e: e[0] * 8 + e[1]) if found else None
+        assert got == want, (world, i, got, want)
+    # the whole valid stream: no rank reports anything
+    for world in (1, 2, 8):
+        for sh in sharding.plan(base.size, world):
+            assert sharding.shard_first_error(base[sh.lo:sh.hi].tobytes(), sh) is None

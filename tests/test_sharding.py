@@ -1,9 +1,11 @@
 """Multi-process (gloo, world_size 2 and 4) tests of the shard layer on the
 CPU: the shard plan, head/tail bytes and the allreduce(MAX) combine must
 reproduce the single-stream verdict for streams whose shard edges cut
-characters anywhere.  Each rank's lane-range flag comes from the device
-formula compiled for the CPU (tests/cpp/swar_host.c swar_lanes), so what is
-checked is exactly K1's lane contract."""
+characters anywhere, and the allreduce(MIN) of each rank's local first-error
+decode must reproduce the oracle's (offset, kind).  Each rank's lane-range
+flag comes from the device formula compiled for the CPU
+(tests/cpp/swar_host.c swar_lanes), so what is checked is exactly K1's lane
+contract."""
 from __future__ import annotations
 
 import os
@@ -19,6 +21,25 @@ def cpu_shard_flag(local, shard):
     a = np.ascontiguousarray(np.frombuffer(bytes(local), np.uint8))
     lo, hi = shard.lanes
     return int(nat.swar().swar_lanes(a.ctypes.data if a.size else None, a.size, lo, hi))
+
+
+def cpu_shard_locate(local, shard):
+    """CPU model of shard_first_error: the first flagged lane L of the rank's
+    lanes (device formula), then the recovery rule of SURVEY §8(a) 3 on the
+    rank's own bytes: B = L - 3 stepped back over <= 3 continuation bytes,
+    the oracle over [B, L + 4)."""
+    a = np.ascontiguousarray(np.frombuffer(bytes(local), np.uint8))
+    lo, hi = shard.lanes
+    L = int(nat.swar().swar_first_lane_in(a.ctypes.data if a.size else None, a.size, lo, hi))
+    if L == (1 << 64) - 1:
+        return None
+    b = max(0, L - 3)
+    for _ in range(3):
+        if b > 0 and b < a.size and (a[b] & 0xC0) == 0x80:
+            b -= 1
+    ok, off, kind = nat.oracle_verdict(a[b:min(a.size, L + 4)].tobytes())
+    assert not ok, "a flagged lane with no error in its window"
+    return shard.lo + b + off, kind
 
 
 def _streams():
@@ -41,6 +62,13 @@ def _streams():
                 e = base.copy()
                 e[sh.start + delta: sh.start + delta + 2] = [0xE0, 0x85]  # overlong pair
                 out.append(e)
+                # whole bad sequences straddling the edge: the kind depends on
+                # bytes past the lead, which may sit in the next rank's bytes
+                for seq in ([0xE0, 0x80, 0x80], [0xED, 0xA0, 0x80], [0xF4, 0x90, 0x80, 0x80],
+                            [0xF0, 0x80, 0x80, 0x80], [0xE2, 0x82, 0x41], [0xFF], [0x80, 0x80]):
+                    f = base.copy()
+                    f[sh.start + delta: sh.start + delta + len(seq)] = seq
+                    out.append(f)
     out.append(np.concatenate([base, np.array([0xF0, 0x9F, 0x98], np.uint8)]))  # truncated end
     return out
 
@@ -55,7 +83,9 @@ def _worker(rank, world, port, q):
         for d in _streams():
             sh = sharding.plan(d.size, world)[rank]
             local = d[sh.lo:sh.hi].tobytes()
-            res.append(sharding.validate_sharded(local, sh, shard_flag=cpu_shard_flag))
+            ok = sharding.validate_sharded(local, sh, shard_flag=cpu_shard_flag)
+            v = sharding.verdict_sharded(local, sh, shard_locate=cpu_shard_locate)
+            res.append((ok, None if v.valid() else (v.error.offset, int(v.error.kind))))
         q.put((rank, res))
     finally:
         dist.destroy_process_group()
@@ -78,7 +108,10 @@ def test_sharded_verdict_equals_single_stream(world):
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    want = [nat.oracle_verdict(d)[0] for d in _streams()]
+    want = []
+    for d in _streams():
+        ok, off, kind = nat.oracle_verdict(d.tobytes())
+        want.append((ok, None if ok else (off, kind)))
     for r in range(world):
         assert results[r] == want
 
@@ -91,7 +124,7 @@ def test_plan_covers_stream_and_lane_ranges():
             shards = sharding.plan(n, world)
             assert shards[0].start == 0 and shards[-1].end == n
             for a, b in zip(shards, shards[1:]):
-                assert a.end == b.start and b.head == min(b.start, sharding.HEAD) and a.tail == 1
+                assert a.end == b.start and b.head == min(b.start, sharding.HEAD) and a.tail == min(sharding.TAIL, n - a.end)
             covered = []
             for sh in shards:
                 lo, hi = sh.lanes
