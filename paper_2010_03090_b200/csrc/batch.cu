@@ -136,9 +136,22 @@ __device__ __noinline__ void attribute_step(RecView d, int64_t s0, int64_t hi, u
     if (q >= 0 && q < hi_rel && q >= start) {
       int64_t r = r0 + L;
       int64_t st_abs = s0 + start;
-      if (full && L == 31) {  // more starts than one window holds: walk on
+      if (full && L == 31) {
+        // More starts than one window holds (dense records): gallop, then
+        // binary search the offsets -- O(log) loads in the records skipped.
         const int64_t qa = s0 + q;
-        while (r < d.n_records && rec_start(d, r + 1) <= qa) ++r;
+        int64_t a = r, span = 4;  // start(a) <= qa
+        while (a + span <= d.n_records && rec_start(d, a + span) <= qa) {  // gallop
+          a += span;
+          span <<= 1;
+        }
+        int64_t b = a + span - 1 < d.n_records ? a + span - 1 : d.n_records;
+        while (a < b) {  // largest r in [a, b] with start(r) <= qa
+          const int64_t mid = (a + b + 1) >> 1;
+          if (rec_start(d, mid) <= qa) a = mid;
+          else b = mid - 1;
+        }
+        r = a;
         st_abs = rec_start(d, r);
       }
       if (r < d.n_records && s0 + q - st_abs >= 3) d.verdicts[r] = 0;
@@ -307,6 +320,16 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
         o = rel32(rec_start(rv, r_in + ratt + lane), s0);
         if (__ballot_sync(0xFFFFFFFFu, o <= 0) != 0xFFFFFFFFu) break;
         ratt += 31;
+      }
+      if (__all_sync(0xFFFFFFFFu, o < kStepBytes)) {
+        // The window ends inside the step: restart it at the step's first
+        // record so that fewer flagged lanes fall past it.
+        const unsigned le = __ballot_sync(0xFFFFFFFFu, o <= 0);
+        const int top = le ? 31 - __clz(le) : 0;
+        if (top > 0) {
+          ratt += top;
+          o = rel32(rec_start(rv, r_in + ratt + lane), s0);
+        }
       }
       attribute_step(rv, s0, d.hi, err[0], err[1], err[2], err[3], o, r_in + ratt);
       const unsigned le = __ballot_sync(0xFFFFFFFFu, o <= 0);
