@@ -110,6 +110,9 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
+HBM_SPEC_GBS = 8000.0  # B200 HBM3e datasheet figure; SURVEY §8(d) asks for both fractions
+
+
 def measured_peaks() -> dict:
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -338,6 +341,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     traffic = ncu_traffic("k_validate")
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
+                "frac_of_spec": achieved / HBM_SPEC_GBS, "spec_peak": HBM_SPEC_GBS,
                 "peak_source": peaks["source"], "kernel": "u8v::k_validate",
                 "kernel_ms": kernel_ms, "algorithmic_bytes_per_launch": alg_bytes}
 
