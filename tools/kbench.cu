@@ -676,6 +676,95 @@ KB_KERNEL_TMA(4, 2, 3)
 KB_KERNEL_TMA(4, 3, 2)
 KB_KERNEL_TMA(1, 6, 4)
 
+// V25: V17's per-warp TMA ring with the production permuted plane form, no
+// ASCII path, and bank-conflict-free shared reads: lane L reads half
+// (L >> 2) & 1 of its 32-byte chunk first, so each quarter-warp's 16-byte
+// reads hit 8 distinct 4-bank groups.
+__device__ __forceinline__ void ld_shared_chunk_swz(uint32_t (&w)[8], const uint8_t* p, int lane) {
+  const uint32_t a = smem_u32(p);
+  const uint32_t h = ((lane >> 2) & 1) * 16u;
+  uint32_t x[8];
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]) : "r"(a + h));
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(x[4]), "=r"(x[5]), "=r"(x[6]), "=r"(x[7]) : "r"(a + (16u - h)));
+  const bool sw = h != 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    w[j] = sw ? x[4 + j] : x[j];
+    w[4 + j] = sw ? x[j] : x[4 + j];
+  }
+}
+
+template <int U, int S>
+__device__ __forceinline__ void body25(const uint8_t* base, int64_t steps, int64_t spw, uint32_t* flag,
+                                       const Cfg& k) {
+  constexpr int STEP = U * 1024;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  uint8_t* ring = smem + wib * S * STEP;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (blockDim.x >> 5) * S * STEP) + wib * S;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int64_t step = warp * spw;
+  const int64_t se = step + spw < steps ? step + spw : steps;
+  if (step >= se) return;
+  u8v_consts kk;
+  kk.one = k.one; kk.m256 = k.m256; kk.mshr4 = k.mshr4;
+  if (lane == 0) {
+    for (int j = 0; j < S; ++j) mb_init(bars + j, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int j = 0; j < S; ++j)
+      if (step + j < se) {
+        mb_expect_tx(bars + j, STEP);
+        tma_load(ring + j * STEP, base + (step + j) * (int64_t)STEP, STEP, bars + j);
+      }
+  }
+  __syncwarp();
+  uint32_t carry_word = 0, acc = 0, phase = 0;
+  if (lane == 31 && step > 0) carry_word = __ldg(reinterpret_cast<const uint32_t*>(base + step * (int64_t)STEP - 4));
+  for (int it = 0; step < se; ++step, ++it) {
+    const int st = it % S;
+    mb_wait(bars + st, (phase >> st) & 1);
+    phase ^= 1u << st;
+    const uint8_t* sb = ring + st * STEP;
+    uint32_t v[U][8];
+#pragma unroll
+    for (int i = 0; i < U; ++i) ld_shared_chunk_swz(v[i], sb + (i * 32 + lane) * 32, lane);
+    uint32_t nsw = 0;
+    if (lane == 0 && step + 1 < steps) nsw = __ldg(reinterpret_cast<const uint32_t*>(base + (step + 1) * (int64_t)STEP));
+    // Stage st is in registers: refill it S steps ahead before computing.
+    __syncwarp();
+    if (lane == 0 && step + S < se) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mb_expect_tx(bars + st, STEP);
+      tma_load(ring + st * STEP, base + (step + S) * (int64_t)STEP, STEP, bars + st);
+    }
+#pragma unroll
+    for (int i = 0; i < U; ++i) {
+      const uint32_t supply = lane == 31 ? (i == 0 ? carry_word : v[i - 1][7]) : v[i][7];
+      const uint32_t prev = __shfl_sync(0xFFFFFFFFu, supply, (lane + 31) & 31);
+      const uint32_t dn = lane == 0 ? (i + 1 < U ? v[i + 1][0] : nsw) : v[i][0];
+      const uint32_t nextw = __shfl_sync(0xFFFFFFFFu, dn, (lane + 1) & 31);
+      uint32_t hi;
+      acc |= u8v_chunk_errors_planes_perm_k(v[i], prev, nextw, kk, &hi);
+    }
+    if (lane == 31) carry_word = v[U - 1][7];
+  }
+  const unsigned any = __reduce_or_sync(0xFFFFFFFFu, acc);
+  if (lane == 0 && any) atomicOr(flag, 1u);
+}
+#define KB_KERNEL25(U, S, MINB)                                                                  \
+  __global__ void __launch_bounds__(256, MINB)                                                 \
+      k_v25_u##U##_s##S##_b##MINB(const uint8_t* base, int64_t steps, int64_t spw, uint32_t* flag, \
+                                  Cfg k) {                                                     \
+    body25<U, S>(base, steps, spw, flag, k);                                                   \
+  }
+KB_KERNEL25(4, 3, 2)
+KB_KERNEL25(4, 2, 3)
+KB_KERNEL25(2, 3, 4)
+KB_KERNEL25(2, 2, 4)
+KB_KERNEL25(4, 4, 1)
+
 // V18: rolling reload.  Each chunk slot is refilled with the next step's
 // chunk right after it is consumed, so every load overlaps ~3/4 of a step of
 // compute, with no extra registers.
@@ -1125,6 +1214,11 @@ static const Entry kEntries[] = {
     {"v21_u4_b4", k_v21_u4_b4, 4}, {"v21_u4_b8", k_v21_u4_b8, 4},
     {"v20_u4_b4", k_v20_u4_b4, 4}, {"v19_u4_b4", k_v19_u4_b4, 4}, {"v19_u2_b4", k_v19_u2_b4, 2},
     {"v18_u4_b4", k_v18_u4_b4, 4}, {"v18_u4_b3", k_v18_u4_b3, 4}, {"v18_u2_b4", k_v18_u2_b4, 2},
+    {"v25_u4_s3_b2", k_v25_u4_s3_b2, 4, 8 * 3 * 4096 + 8 * 3 * 8},
+    {"v25_u4_s2_b3", k_v25_u4_s2_b3, 4, 8 * 2 * 4096 + 8 * 2 * 8},
+    {"v25_u2_s3_b4", k_v25_u2_s3_b4, 2, 8 * 3 * 2048 + 8 * 3 * 8},
+    {"v25_u2_s2_b4", k_v25_u2_s2_b4, 2, 8 * 2 * 2048 + 8 * 2 * 8},
+    {"v25_u4_s4_b1", k_v25_u4_s4_b1, 4, 8 * 4 * 4096 + 8 * 4 * 8},
     {"tma_u2_s3_b4", k_tma_u2_s3_b4, 2, 8 * 3 * 2048 + 8 * 3 * 8},
     {"tma_u2_s4_b3", k_tma_u2_s4_b3, 2, 8 * 4 * 2048 + 8 * 4 * 8},
     {"tma_u4_s2_b3", k_tma_u4_s2_b3, 4, 8 * 2 * 4096 + 8 * 2 * 8},
