@@ -76,8 +76,12 @@ void build_tables(uint8_t t1[16], uint8_t t2[16], uint8_t t3[16]) {
 
 std::once_flag g_dev_once[kMaxDevices];
 
+// Per thread and device: streams, small result buffers, the device stage
+// for host input (grown to the largest input seen) and the pinned ring for
+// pageable input.  Released when the thread exits.
 struct Ctx {
   bool ready = false;
+  int dev = -1;
   cudaStream_t s_comp = nullptr, s_copy = nullptr;
   uint32_t* d_flag = nullptr;               // [0] verdict flag
   unsigned long long* d_pos = nullptr;      // [0] first chunk, [1] offset, [2] K3 round
@@ -93,6 +97,32 @@ struct Ctx {
   uint8_t* h_ring = nullptr;
   cudaEvent_t slot_done[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t ev_legacy = nullptr;          // see after_legacy()
+
+  ~Ctx() { release(); }
+  // Errors are ignored: at process exit the runtime may already be gone.
+  void release() {
+    if (dev < 0) return;
+    int cur = -1;
+    cudaGetDevice(&cur);
+    cudaSetDevice(dev);
+    if (s_comp) cudaStreamSynchronize(s_comp);
+    if (s_copy) cudaStreamSynchronize(s_copy);
+    for (void* p : {(void*)d_flag, (void*)d_pos, (void*)d_kind, (void*)d_lanes, (void*)d_ok, (void*)d_stage})
+      if (p) cudaFree(p);
+    if (h_res) cudaFreeHost(h_res);
+    if (h_ring) cudaFreeHost(h_ring);
+    for (cudaEvent_t e : events) cudaEventDestroy(e);
+    for (cudaEvent_t e : slot_done)
+      if (e) cudaEventDestroy(e);
+    if (ev_legacy) cudaEventDestroy(ev_legacy);
+    if (s_comp) cudaStreamDestroy(s_comp);
+    if (s_copy) cudaStreamDestroy(s_copy);
+    if (cur >= 0) cudaSetDevice(cur);
+    cudaGetLastError();
+    *this = Ctx();
+  }
+  Ctx() = default;
+  Ctx& operator=(const Ctx&) = default;
 };
 constexpr int kSlots = 4;
 thread_local Ctx t_ctx[kMaxDevices];
@@ -112,6 +142,8 @@ int get_ctx(Ctx** out) {
   });
   Ctx& c = t_ctx[dev];
   if (!c.ready) {
+    c.release();  // a failed earlier initialisation
+    c.dev = dev;
     CK(cudaStreamCreateWithFlags(&c.s_comp, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&c.s_copy, cudaStreamNonBlocking));
     CK(cudaMalloc(&c.d_flag, 64));
@@ -245,6 +277,66 @@ class CopyPool {
   uint8_t* dst_ = nullptr;
   const uint8_t* src_ = nullptr;
   size_t n_ = 0, seg_ = 0;
+};
+
+// Shard workers for utf8v_cuda_validate_sharded: worker g runs shard slot g
+// of every call and persists, so its per-thread device contexts (stage,
+// pinned ring) are built once, not per call.  Concurrent calls take turns.
+class ShardPool {
+ public:
+  static ShardPool& get() {
+    static ShardPool* pool = new ShardPool();  // never destroyed: workers outlive exit
+    return *pool;
+  }
+  // fn(g) for g in [0, n), slot g on worker g; returns when all are done.
+  void run(int n, const std::function<void(int)>& fn) {
+    std::lock_guard<std::mutex> turn(call_m_);
+    while ((int)workers_.size() < n) {
+      const int id = (int)workers_.size();
+      uint64_t gen;
+      {
+        std::lock_guard<std::mutex> g(m_);
+        gen = gen_;
+      }
+      workers_.emplace_back([this, id, gen] { loop(id, gen); });
+      workers_.back().detach();
+    }
+    {
+      std::lock_guard<std::mutex> g(m_);
+      fn_ = &fn;
+      n_ = n;
+      pending_ = n;
+      ++gen_;
+    }
+    cv_.notify_all();
+    std::unique_lock<std::mutex> lk(m_);
+    done_cv_.wait(lk, [&] { return pending_ == 0; });
+  }
+
+ private:
+  void loop(int id, uint64_t seen) {
+    for (;;) {
+      const std::function<void(int)>* fn;
+      int n;
+      {
+        std::unique_lock<std::mutex> lk(m_);
+        cv_.wait(lk, [&] { return gen_ != seen; });
+        seen = gen_;
+        fn = fn_;
+        n = n_;
+      }
+      if (id >= n) continue;
+      (*fn)(id);
+      std::lock_guard<std::mutex> g(m_);
+      if (--pending_ == 0) done_cv_.notify_all();
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex call_m_, m_;
+  std::condition_variable cv_, done_cv_;
+  uint64_t gen_ = 0;
+  const std::function<void(int)>* fn_ = nullptr;
+  int n_ = 0, pending_ = 0;
 };
 
 bool is_pinned(const void* p) {
@@ -625,25 +717,22 @@ int utf8v_cuda_validate_sharded(const uint8_t* p, size_t n, int n_gpus, int is_d
   std::vector<int> launches(n_gpus, 0);
   int caller_dev = 0;
   cudaGetDevice(&caller_dev);
-  std::vector<std::thread> th;
-  for (int g = 0; g < n_gpus; ++g)
-    th.emplace_back([&, g] {
-      // Shards go round-robin over the visible devices.
-      if (cudaSetDevice(g % count) != cudaSuccess) {
-        status[g] = fail(UTF8V_ERR_CUDA, "cudaSetDevice", cudaGetLastError());
-        errs[g] = t_err;
-        return;
-      }
-      const uint64_t s = cut[g], e = cut[g + 1];
-      const uint64_t head = s < 16 ? s : 16;
-      const bool last = g == n_gpus - 1;
-      const uint64_t lo = s - head, hi = last ? e : e + 1;
-      const uint64_t lane_hi = last ? (hi - lo) + 3 : head + (e - s);
-      status[g] = utf8v_cuda_validate_lanes(p + lo, hi - lo, head, lane_hi, 0, &flags[g]);
-      launches[g] = t_launches;
-      if (status[g]) errs[g] = t_err;
-    });
-  for (auto& t : th) t.join();
+  ShardPool::get().run(n_gpus, [&](int g) {
+    // Shards go round-robin over the visible devices.
+    if (cudaSetDevice(g % count) != cudaSuccess) {
+      status[g] = fail(UTF8V_ERR_CUDA, "cudaSetDevice", cudaGetLastError());
+      errs[g] = t_err;
+      return;
+    }
+    const uint64_t s = cut[g], e = cut[g + 1];
+    const uint64_t head = s < 16 ? s : 16;
+    const bool last = g == n_gpus - 1;
+    const uint64_t lo = s - head, hi = last ? e : e + 1;
+    const uint64_t lane_hi = last ? (hi - lo) + 3 : head + (e - s);
+    status[g] = utf8v_cuda_validate_lanes(p + lo, hi - lo, head, lane_hi, 0, &flags[g]);
+    launches[g] = t_launches;
+    if (status[g]) errs[g] = t_err;
+  });
   cudaSetDevice(caller_dev);
   uint32_t any = 0;
   for (int g = 0; g < n_gpus; ++g) {

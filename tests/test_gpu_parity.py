@@ -579,3 +579,34 @@ def test_k1_structural_boundaries():
 def torch_from(seq):
     import torch
     return torch.tensor(list(seq), dtype=torch.uint8, device="cuda")
+
+
+def test_thread_contexts_are_released(torch):
+    """Per-thread contexts (streams, the device stage grown to the input, the
+    pinned ring for pageable input) are freed when the thread exits: many
+    short-lived threads validating 32 MiB of host input leave device memory
+    where it was."""
+    import threading
+    h = configs.gen_c1(32 << 20, seed=13).cpu().numpy()
+    torch.cuda.synchronize()
+
+    def work(out, i):
+        out[i] = u8.validate_lookup(h)
+
+    def round_of(k):
+        out = [None] * k
+        ts = [threading.Thread(target=work, args=(out, i)) for i in range(k)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        return out
+
+    assert all(round_of(4))
+    free0 = torch.cuda.mem_get_info()[0]
+    for _ in range(3):
+        assert all(round_of(4))
+    free1 = torch.cuda.mem_get_info()[0]
+    # 12 more threads, each with a 32 MiB stage: without release this would
+    # hold 384 MiB; allow allocator slack of 96 MiB.
+    assert free0 - free1 < (96 << 20), (free0, free1)
