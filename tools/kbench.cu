@@ -1072,6 +1072,8 @@ KB_KERNEL23(4, 5)
 KB_KERNEL23(2, 6)
 KB_KERNEL23(2, 8)
 KB_KERNEL23(1, 8)
+KB_KERNEL23(3, 5)
+KB_KERNEL23(3, 4)
 
 // V24: V23 (grid-stride, permuted planes) with rolling reload: each chunk
 // slot is refilled with the same chunk of this warp's next step as soon as
@@ -1208,6 +1210,7 @@ static const Entry kEntries[] = {
     {"v23_u4_b4", k_v23_u4_b4, 4}, {"v23_u4_b3", k_v23_u4_b3, 4}, {"v23_u8_b2", k_v23_u8_b2, 8},
     {"v23_u2_b5", k_v23_u2_b5, 2}, {"v23_u2_b4", k_v23_u2_b4, 2}, {"v23_u4_b5", k_v23_u4_b5, 4},
     {"v23_u2_b6", k_v23_u2_b6, 2}, {"v23_u2_b8", k_v23_u2_b8, 2}, {"v23_u1_b8", k_v23_u1_b8, 1},
+    {"v23_u3_b5", k_v23_u3_b5, 3}, {"v23_u3_b4", k_v23_u3_b4, 3},
     {"v19_u8_b2", k_v19_u8_b2, 8}, {"v19_u2_b6", k_v19_u2_b6, 2}, {"v19_u2_b5", k_v19_u2_b5, 2},
     {"v19_u4_b3", k_v19_u4_b3, 4},
     {"v22a_u4_b4", k_v22a_u4_b4, 4}, {"v22b_u4_b4", k_v22b_u4_b4, 4},
