@@ -610,3 +610,47 @@ def test_thread_contexts_are_released(torch):
     # 12 more threads, each with a 32 MiB stage: without release this would
     # hold 384 MiB; allow allocator slack of 96 MiB.
     assert free0 - free1 < (96 << 20), (free0, free1)
+
+
+def _encode(cps, length):
+    """UTF-8 style encoding of each code point in exactly `length` bytes
+    (shortest form when it fits, overlong otherwise); rows of `length` bytes."""
+    cps = np.asarray(cps, np.uint32)
+    out = np.zeros((cps.size, length), np.uint8)
+    if length == 1:
+        out[:, 0] = cps
+        return out
+    lead = {2: 0xC0, 3: 0xE0, 4: 0xF0}[length]
+    for k in range(length - 1, 0, -1):
+        out[:, k] = 0x80 | (cps & 0x3F)
+        cps = cps >> 6
+    out[:, 0] = lead | cps
+    return out
+
+
+def test_code_point_sweep_on_device():
+    """The acceptance gate's sweep (proj/tests/acceptance.cpp:117-175) on the
+    GPU: every code point 0..0x1FFFFF in shortest form, plus every overlong
+    form that fits in 4 bytes, each as its own record of one 2.2 M-record
+    batch (K2, dense 1-4-byte records), against the expected verdicts and
+    the oracle; and K1 over the concatenation of all valid encodings."""
+    import torch
+    parts, expect = [], []
+    for length, lo, hi in ((1, 0, 0x80), (2, 0x80, 0x800), (3, 0x800, 0x10000), (4, 0x10000, 0x200000)):
+        cps = np.arange(lo, hi, dtype=np.uint32)
+        parts.append(_encode(cps, length))
+        expect.append(((cps < 0xD800) | (cps > 0xDFFF)) & (cps <= 0x10FFFF))
+    for length, hi in ((2, 0x80), (3, 0x800), (4, 0x10000)):  # overlongs
+        parts.append(_encode(np.arange(hi, dtype=np.uint32), length))
+        expect.append(np.zeros(hi, bool))
+    lens = np.concatenate([np.full(p.shape[0], p.shape[1], np.uint64) for p in parts])
+    data = np.concatenate([p.reshape(-1) for p in parts])
+    offs = np.zeros(lens.size + 1, np.uint64)
+    np.cumsum(lens, out=offs[1:])
+    want = np.concatenate(expect).astype(np.uint8)
+    assert want.sum() == 1112064
+    got = u8.validate_lookup_batch(torch.from_numpy(data).cuda(), torch.from_numpy(offs.view(np.int64)).cuda())
+    assert np.array_equal(got, want)
+    assert np.array_equal(nat.oracle_batch(data, offs), want)
+    valid_stream = np.concatenate([p[e].reshape(-1) for p, e in zip(parts[:4], expect[:4])])
+    assert u8.validate_lookup(torch.from_numpy(valid_stream).cuda()) is True
