@@ -208,7 +208,15 @@ def validate_lookup_batch(data, offsets) -> np.ndarray:
     lib = _lib.load()
     if _is_cuda_tensor(data):
         import torch
-        off = offsets if _is_cuda_tensor(offsets) else torch.as_tensor(np.asarray(offsets, np.uint64).view(np.int64), device=data.device)
+        if data.dtype.itemsize != 1 or not data.is_contiguous():
+            raise ValueError("device input must be a contiguous 1-byte tensor")
+        if _is_cuda_tensor(offsets):
+            # any integer dtype (Arrow string columns use int32 offsets): the
+            # kernel reads 64-bit offsets on the data's device
+            off = offsets.to(device=data.device, dtype=torch.int64).contiguous()
+        else:
+            off = torch.as_tensor(np.asarray(offsets, np.uint64).view(np.int64), device=data.device)
+        _after_current_stream(data)
         nrec = int(off.numel()) - 1
         if nrec <= 0:
             return np.zeros(0, np.uint8)

@@ -654,3 +654,16 @@ def test_code_point_sweep_on_device():
     assert np.array_equal(nat.oracle_batch(data, offs), want)
     valid_stream = np.concatenate([p[e].reshape(-1) for p, e in zip(parts[:4], expect[:4])])
     assert u8.validate_lookup(torch.from_numpy(valid_stream).cuda()) is True
+
+
+def test_batch_offsets_of_any_integer_dtype(torch):
+    """Device offsets may come as int32 (Arrow string columns) or int64; host
+    offsets as any integer array: same verdicts."""
+    b = configs.gen_c3(n_records=3000, seed=12)
+    want = b.expected
+    for dt in (torch.int32, torch.int64):
+        got = u8.validate_lookup_batch(b.data, b.d_offsets.to(dt))
+        assert np.array_equal(got, want), dt
+    for dt in (np.int32, np.int64, np.uint64):
+        got = u8.validate_lookup_batch(b.data, b.offsets.astype(dt))
+        assert np.array_equal(got, want), dt
