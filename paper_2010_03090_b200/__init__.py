@@ -79,6 +79,8 @@ def _is_cuda_tensor(x) -> bool:
 
 def _host_view(data):
     """(pointer, size, keepalive) for host bytes-like input."""
+    if type(data).__module__.startswith("torch") and hasattr(data, "numpy"):  # CPU tensor
+        data = data.contiguous().numpy()
     if isinstance(data, np.ndarray):
         a = np.ascontiguousarray(data).view(np.uint8).reshape(-1)
     else:

@@ -79,3 +79,22 @@ def test_library_is_built_for_sm100a():
     out = subprocess.run([cuobjdump, "--list-elf", str(ROOT / "paper_2010_03090_b200" / "libutf8v_cuda.so")],
                          capture_output=True, text=True).stdout
     assert "sm_100a" in out
+
+
+def test_host_views_of_every_input_kind():
+    """Host input may be bytes, bytearray, memoryview, numpy (also strided) or
+    a CPU torch tensor (also strided): one contiguous uint8 view each."""
+    import numpy as np
+    import torch
+    from paper_2010_03090_b200 import _host_view
+    raw = bytes(range(16))
+    cases = [raw, bytearray(raw), memoryview(raw), np.frombuffer(raw, np.uint8),
+             torch.tensor(list(raw), dtype=torch.uint8)]
+    for c in cases:
+        ptr, n, keep = _host_view(c)
+        assert n == 16 and bytes(keep) == raw
+    ptr, n, keep = _host_view(np.arange(16, dtype=np.uint8)[::2])
+    assert n == 8 and list(keep) == list(range(0, 16, 2))
+    ptr, n, keep = _host_view(torch.arange(16, dtype=torch.uint8)[::2])
+    assert n == 8 and list(keep) == list(range(0, 16, 2))
+    assert _host_view(b"")[:2] == (None, 0)
