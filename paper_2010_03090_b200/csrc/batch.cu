@@ -367,7 +367,15 @@ void launch_batch(const uint8_t* data, uint64_t n, const uint64_t* d_offsets, ui
   d.k = u8v_make_consts();
   d.lo = d.hi = d.c_begin = d.c_end = d.steps = d.steps_per_warp = 0;  // set by the kernel
   const int64_t max_steps = ((int64_t)n + d.off32 + 2 * kChunkBytes) / (kStepChunks * kChunkBytes) + 1;
-  int64_t warps = max_resident_warps();
+  static int resident = 0;  // K2's own resident warps (its occupancy may differ from K1's)
+  if (resident == 0) {
+    int dev = 0, sms = 0, blocks = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_batch, kThreads, 0);
+    resident = sms * (blocks < 1 ? 1 : blocks) * (kThreads / 32);
+  }
+  int64_t warps = resident;
   if (warps > max_steps) warps = max_steps;
   const int64_t blocks = (warps * 32 + kThreads - 1) / kThreads;
   k_batch<<<(unsigned)blocks, kThreads, 0, st>>>(d);
