@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the C0/C2/C3/C4 side measurements")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: functional check of the N>1 path with fewer GPUs than ranks "
+                         "(ranks share GPUs; no kernel waits on another rank; numbers not meaningful)")
     return ap.parse_args()
 
 
@@ -413,8 +416,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             "config": {"workload": workload, "bytes_per_gpu": per, "bytes_total": per * world,
                        "l2": "input (>=1 GiB) larger than the 126 MB L2; no flush needed",
                        "parallelism": f"dp{world}: byte-range shards (<=16-byte look-back head, 3-byte tail)"
-                                      + (" + 1-word NCCL allreduce(MAX) per step, overlapped with the next"
-                                         " step's kernel" if world > 1 else "")},
+                                      + (f" + 1-word {args.dist_backend.upper()} allreduce(MAX) per step, overlapped"
+                                         " with the next step's kernel" if world > 1 else "")},
             "per_gpu_GBps": per_gpu, "verdict_valid": verdict_ok,
             "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks,
             "gpu_launches": args.steps, "other_configs": extras,
@@ -575,8 +578,12 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
+        local_rank %= torch.cuda.device_count()  # one GPU per rank; shared only under --dist-backend gloo
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group("gloo")
     try:
         run_ours(args, rank, world, local_rank)
     finally:
