@@ -159,51 +159,77 @@ __device__ __noinline__ void attribute_step(RecView d, int64_t s0, int64_t hi, u
   }
 }
 
-// Bytes s-4 .. s+3 (base coords) as one little-endian word: two aligned
-// 8-byte loads when they lie in chunks the sweep reads anyway, else byte by
-// byte inside [lo, hi).  Bytes outside the two records are masked later.
-__device__ __forceinline__ uint64_t bytes_around(const uint8_t* base, int64_t s, int64_t lo, int64_t hi) {
-  const int64_t a0 = (s - 4) & ~(int64_t)7;
-  if (a0 >= (lo & ~(int64_t)31) && a0 + 16 <= ((hi + 31) & ~(int64_t)31)) {
-    const uint64_t w0 = __ldg(reinterpret_cast<const unsigned long long*>(base + a0));
-    const uint64_t w1 = __ldg(reinterpret_cast<const unsigned long long*>(base + a0 + 8));
-    const unsigned sh = (unsigned)(s - 4 - a0) * 8u;
-    return sh ? (w0 >> sh) | (w1 << (64u - sh)) : w0;
+// Record boundaries, a batch of 32 starts at a time (lane L: start rb + L
+// at o, relative to the warp's range_lo, a multiple of 32).  The taken
+// batch waits in shared memory, not registers (the sweep needs them all):
+// take_batch stores each lane's start and issues asynchronous copies of the
+// bytes s-4 .. s+3 around it -- two aligned 8-byte words when they lie in
+// chunks the sweep reads anyway, else the word is assembled byte by byte
+// inside [lo, hi) and stored pre-shifted, so check_batch combines both cases
+// the same way.  Bytes outside the two records are masked by check_batch.
+struct WarpCtx {
+  int64_t lo, hi, c_end, range_lo, rb;
+  int prev_last, range_rel;
+};
+
+struct BatchSlot {
+  unsigned long long w[32][2];
+  int o[32];
+  int a0;  // start(rb - 1)
+};
+
+__device__ __forceinline__ void take_batch(BatchSlot* sl, const uint8_t* base, int64_t lo, int64_t hi,
+                                           int64_t range_lo, int o, int a0, int range_rel) {
+  const int lane = threadIdx.x & 31;
+  sl->o[lane] = o;
+  if (lane == 0) sl->a0 = a0;
+  if (o < 0 || o >= range_rel) return;
+  const int64_t s = range_lo + o;
+  const int64_t w0 = (s - 4) & ~(int64_t)7;
+  if (w0 >= (lo & ~(int64_t)31) && w0 + 16 <= ((hi + 31) & ~(int64_t)31)) {
+    const unsigned dst = (unsigned)__cvta_generic_to_shared(&sl->w[lane][0]);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(base + w0) : "memory");
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst + 8), "l"(base + w0 + 8) : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    return;
   }
   uint64_t w = 0;
   for (int k = 0; k < 8; ++k) {
     const int64_t q = s - 4 + k;
     if (q >= lo && q < hi) w |= (uint64_t)base[q] << (8 * k);
   }
-  return w;
+  const unsigned sh = (unsigned)((o - 4) & 7) * 8u;
+  sl->w[lane][0] = w << sh;
+  sl->w[lane][1] = sh ? w >> (64u - sh) : 0ull;
 }
 
-// The record boundary at s: record rr-1 = [a, s) ends there, record rr =
-// [s, b) starts there (either may be empty or absent).
-__device__ __forceinline__ void fix_boundary(const RecView& rv, const uint8_t* base, int64_t lo, int64_t hi,
-                                             int64_t s, int64_t a, int64_t b, int64_t rr, u8v_consts k) {
-  const uint64_t w8 = bytes_around(base, s, lo, hi);
-  int64_t ka = a - (s - 4), kb = b - (s - 4);
-  ka = ka < 0 ? 0 : (ka > 4 ? 4 : ka);
-  kb = kb < 4 ? 4 : (kb > 8 ? 8 : kb);
-  const uint32_t f = u8v_boundary_errors(w8, (unsigned)ka, (unsigned)kb, k);
-  if ((f & 1u) && rr > 0) rv.verdicts[rr - 1] = 0;
-  if ((f & 2u) && rr < rv.n_records) rv.verdicts[rr] = 0;
-}
-
-// One batch of record boundaries: lane L takes start(r_f + L) when it lies in
-// the warp's byte range [range_lo, range_hi).
-__device__ __noinline__ void fix_batch(RecView rv, const uint8_t* base, int64_t lo, int64_t hi, int64_t r_f,
-                                       int64_t range_lo, int64_t range_hi, u8v_consts k) {
+// The boundary at start o of record rr = rf + lane: record rr-1 = [a, o)
+// ends there, record rr = [o, b) starts there (either may be empty or
+// absent).  nx: the following batch (lane 0 = start(rf + 32)).
+__device__ __forceinline__ void check_batch(const RecView& rv, BatchSlot* sl, int nx, int64_t rf, int range_rel,
+                                            u8v_consts k) {
   const int lane = threadIdx.x & 31;
-  const int64_t o = rec_start(rv, r_f + lane);
-  int64_t a = __shfl_up_sync(0xFFFFFFFFu, o, 1);
-  if (lane == 0) a = r_f > 0 ? rec_start(rv, r_f - 1) : o;
-  int64_t b = __shfl_down_sync(0xFFFFFFFFu, o, 1);
-  if (lane == 31) b = rec_start(rv, r_f + 32);
-  const int64_t rr = r_f + lane;
-  if (o >= range_lo && o < range_hi)
-    fix_boundary(rv, base, lo, hi, o, rr > 0 ? a : o, rr < rv.n_records ? b : o, rr, k);
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncwarp();
+  const int o = sl->o[lane];
+  int a = __shfl_up_sync(0xFFFFFFFFu, o, 1);
+  if (lane == 0) a = sl->a0;
+  int b = __shfl_down_sync(0xFFFFFFFFu, o, 1);
+  const int nb = __shfl_sync(0xFFFFFFFFu, nx, 0);
+  if (lane == 31) b = nb;
+  const int64_t rr = rf + lane;
+  if (o >= 0 && o < range_rel) {
+    const uint64_t w0 = sl->w[lane][0], w1 = sl->w[lane][1];
+    const unsigned sh = (unsigned)((o - 4) & 7) * 8u;
+    const uint64_t w8 = sh ? (w0 >> sh) | (w1 << (64u - sh)) : w0;
+    int ka = rr > 0 ? a - (o - 4) : 4, kb = rr < rv.n_records ? b - (o - 4) : 4;
+    ka = ka < 0 ? 0 : (ka > 4 ? 4 : ka);
+    kb = kb < 4 ? 4 : (kb > 8 ? 8 : kb);
+    const uint32_t f = u8v_boundary_errors(w8, (unsigned)ka, (unsigned)kb, k);
+    if ((f & 1u) && rr > 0) rv.verdicts[rr - 1] = 0;
+    if ((f & 2u) && rr < rv.n_records) rv.verdicts[rr] = 0;
+  }
+  __syncwarp();  // the slot is refilled next
 }
 
 __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
@@ -240,19 +266,50 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
   // Loop state is kept 32-bit and relative (positions to range_lo, records
   // to r_in) so it stays in registers across the chunk math.
   const int64_t range_lo = (d.c_begin + step0 * kStepChunks) * kChunkBytes;
-  const int64_t range_hi = range_lo + (int64_t)nsteps * kStepBytes;
   uint32_t carry_word = 0;
   if (lane == 31 && range_lo > 0) carry_word = ld_word_masked(d.base, range_lo - 4, d.lo, d.hi);
-  // Boundary cursor: batches of 32 record starts from r_in + rf, the first
-  // start in the warp's range; a batch runs once the sweep has passed its
-  // last start (f_last, clamped: a batch is correct whenever it runs), so
-  // its bytes are still L2-hot.
+  // Record starts are consumed in batches of 32 (lane L: start(rb + L),
+  // 32-bit relative to range_lo), each batch prefetched one batch ahead:
+  //   nx      the next batch's starts (loaded when the previous one was taken)
+  //   p_*     the taken batch: its bytes around each start are loaded when
+  //           the sweep passes its last start (L2-hot) and checked one step
+  //           later, so neither load sits on the sweep's critical path.
+  // A batch is correct whenever it is checked (verdicts only go 1 -> 0).
+  // The same registers give the attribution window: start(rb - 1) (the
+  // taken batch's last start, before the current step) followed by nx.
+  {  // the first steps' bytes travel while the record search below waits on offsets
+    const uint8_t* q = d.base + range_lo + lane * kChunkBytes;
+    const int npf = nsteps < 2 ? nsteps : 2;
+    for (int j = 0; j < npf; ++j)
+#pragma unroll
+      for (int i = 0; i < kU; ++i)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(q + j * kStepBytes + 32 * i * kChunkBytes));
+  }
   const int64_t r_in = find_record(rv, range_lo - 1);  // last start before the range (or 0)
-  int rf = rec_start(rv, r_in) < range_lo ? 1 : 0;
-  int f_last = rel32(rec_start(rv, r_in + rf + kTrigger), range_lo);
-  // Attribution cursor (advanced lazily, on steps with a flagged lane).
-  int ratt = 0;
+  const int64_t s_in = rec_start(rv, r_in);
+  int64_t rb = r_in + (s_in < range_lo ? 1 : 0);
+  int nx = rel32(rec_start(rv, rb + lane), range_lo);
+  int prev_last = rb > r_in ? rel32(s_in, range_lo) : -kFar;  // start(rb - 1); rb == r_in only at rb = 0
+  const int range_rel = nsteps * kStepBytes;
+  __shared__ BatchSlot slots[kThreads / 32];
+  BatchSlot* const sl = &slots[threadIdx.x >> 5];
+  // Warp-uniform state the sweep does not touch each step lives in shared
+  // memory (every lane writes the same value), so the hot loop's registers
+  // hold only the chunk math and its cursor (no spills).
+  __shared__ WarpCtx ctxs[kThreads / 32];
+  volatile WarpCtx* const cx = &ctxs[threadIdx.x >> 5];
+  cx->lo = d.lo;
+  cx->hi = d.hi;
+  cx->c_end = d.c_end;
+  cx->range_lo = range_lo;
+  cx->rb = rb;
+  cx->prev_last = prev_last;
+  cx->range_rel = range_rel;
+  bool pend = false;
   bool was_ascii = true;
+#ifdef U8V_K2_SKIP_ATTR
+  uint32_t skip_any = 0;
+#endif
 
   // Steps [jb, jd) are interior (all bytes real, lookahead word in range):
   // plain loads from a pointer advanced 4 KiB per step.
@@ -269,13 +326,14 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
       for (int i = 0; i < kU; ++i) v[i] = ld_chunk(p + 32 * i * kChunkBytes);
       if (lane == 0) nsw = __ldg(reinterpret_cast<const uint32_t*>(p + kStepBytes));
     } else {
-      const int64_t cstep = (range_lo + (int64_t)j * kStepBytes) / kChunkBytes;
+      const int64_t lo = cx->lo, hi = cx->hi, c_end = cx->c_end;
+      const int64_t cstep = (cx->range_lo + (int64_t)j * kStepBytes) / kChunkBytes;
 #pragma unroll
       for (int i = 0; i < kU; ++i) {
         const int64_t c = cstep + lane + 32 * i;
-        v[i] = c <= d.c_end ? ld_chunk_masked(d.base, c, d.lo, d.hi) : zero_chunk();
+        v[i] = c <= c_end ? ld_chunk_masked(d.base, c, lo, hi) : zero_chunk();
       }
-      if (lane == 0) nsw = ld_word_guarded(d.base, (cstep + kStepChunks) * kChunkBytes, d.lo, d.hi);
+      if (lane == 0) nsw = ld_word_guarded(d.base, (cstep + kStepChunks) * kChunkBytes, lo, hi);
     }
 
     // Unbounded lane flags (K1's chunk form); ASCII fast path voted only
@@ -309,45 +367,59 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
     was_ascii = all_ascii || __all_sync(0xFFFFFFFFu, h7 == 0);
     if (lane == 31) carry_word = v[kU - 1].w[kChunkWords - 1];
 
+#ifndef U8V_K2_SKIP_ATTR
     if (__any_sync(0xFFFFFFFFu, any != 0u)) {
-      const int64_t s0 = range_lo + (int64_t)j * kStepBytes;
-      // The window from the attribution cursor (lane L: start(r_att + L) -
-      // s0; start(r_att) <= s0).  It may start a few records back: the
-      // search takes the last start <= q, and a window that ends inside the
-      // step walks on.  The cursor then moves to the last start <= s0.
-      int o;
-      for (;;) {  // gallop past a cursor left far behind
-        o = rel32(rec_start(rv, r_in + ratt + lane), s0);
-        if (__ballot_sync(0xFFFFFFFFu, o <= 0) != 0xFFFFFFFFu) break;
-        ratt += 31;
-      }
-      if (__all_sync(0xFFFFFFFFu, o < kStepBytes)) {
-        // The window ends inside the step: restart it at the step's first
-        // record so that fewer flagged lanes fall past it.
-        const unsigned le = __ballot_sync(0xFFFFFFFFu, o <= 0);
-        const int top = le ? 31 - __clz(le) : 0;
-        if (top > 0) {
-          ratt += top;
-          o = rel32(rec_start(rv, r_in + ratt + lane), s0);
-        }
-      }
-      attribute_step(rv, s0, d.hi, err[0], err[1], err[2], err[3], o, r_in + ratt);
-      const unsigned le = __ballot_sync(0xFFFFFFFFu, o <= 0);
-      if (le) ratt += 31 - __clz(le);
+      // Window: lane L = start(r0 + L) - s0 with start(r0) <= s0 (or r0 = 0):
+      // the taken batch's last start (< s0, else that batch would not have
+      // been taken) followed by the next batch's first 31.
+      const int s0 = j * kStepBytes;
+      const int up = __shfl_up_sync(0xFFFFFFFFu, nx, 1);
+      const int64_t rbc = cx->rb;
+      const bool first = rbc == 0;
+      const int o = (first ? nx : (lane == 0 ? cx->prev_last : up)) - s0;
+      attribute_step(rv, cx->range_lo + s0, cx->hi, err[0], err[1], err[2], err[3], o, first ? 0 : rbc - 1);
     }
-    while (f_last < (j + 1) * kStepBytes) {
-      fix_batch(rv, d.base, d.lo, d.hi, r_in + rf, range_lo, range_hi, d.k);
-      rf += 32;
-      f_last = rel32(rec_start(rv, r_in + rf + kTrigger), range_lo);
+#else
+    skip_any |= any;
+#endif
+#ifndef U8V_K2_SKIP_FIX
+    if (pend) {
+      check_batch(rv, sl, nx, cx->rb - 32, cx->range_rel, d.k);
+      pend = false;
     }
+    // The trigger reads nx a step after it was loaded (no stall on the load).
+    while (__shfl_sync(0xFFFFFFFFu, nx, kTrigger) < (j + 1) * kStepBytes) {
+      const int64_t rbc = cx->rb;
+      if (pend) check_batch(rv, sl, nx, rbc - 32, cx->range_rel, d.k);
+      take_batch(sl, d.base, cx->lo, cx->hi, cx->range_lo, nx, cx->prev_last, cx->range_rel);
+      pend = true;
+      cx->prev_last = __shfl_sync(0xFFFFFFFFu, nx, 31);
+      cx->rb = rbc + 32;
+      nx = rel32(rec_start(rv, rbc + 32 + lane), cx->range_lo);
+    }
+#endif
   }
+#ifdef U8V_K2_SKIP_ATTR
+  if (skip_any) d.verdicts[warp % d.n_records] = 0;
+#endif
+#ifndef U8V_K2_SKIP_FIX
   // The range's remaining boundaries.
-  while (rec_start(rv, r_in + rf) < range_hi) {
-    fix_batch(rv, d.base, d.lo, d.hi, r_in + rf, range_lo, range_hi, d.k);
-    rf += 32;
+  {
+    int64_t rbc = cx->rb;
+    int pl = cx->prev_last;
+    const int64_t lo = cx->lo, hi = cx->hi, rlo = cx->range_lo;
+    const int rrel = cx->range_rel;
+    if (pend) check_batch(rv, sl, nx, rbc - 32, rrel, d.k);
+    while (__shfl_sync(0xFFFFFFFFu, nx, 0) < rrel) {
+      take_batch(sl, d.base, lo, hi, rlo, nx, pl, rrel);
+      pl = __shfl_sync(0xFFFFFFFFu, nx, 31);
+      rbc += 32;
+      nx = rel32(rec_start(rv, rbc + lane), rlo);
+      check_batch(rv, sl, nx, rbc - 32, rrel, d.k);
+    }
   }
+#endif
 }
-
 }  // namespace u8v
 
 // Launcher used by capi.cu.  Fully asynchronous: the kernel reads the first

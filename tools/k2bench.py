@@ -1,5 +1,7 @@
 """DEVELOPMENT HARNESS: time (and, under ncu, profile) the batch kernel K2 on
-C2 and C3 alone.  `python tools/k2bench.py [c2|c3|both] [reps]`."""
+C2 and C3 alone.  `python tools/k2bench.py [c2|c3|both] [reps] [lib.so ...]`
+(several library variants from tools/k2var.sh: timed interleaved, medians)."""
+import os
 import ctypes as C
 import sys
 from pathlib import Path
@@ -12,7 +14,15 @@ from paper_2010_03090_b200 import _lib, configs
 
 which = sys.argv[1] if len(sys.argv) > 1 else "both"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 20
+libs = sys.argv[3:] or [str(_lib.LIB_PATH)]
+if len(libs) > 1 or libs[0] != str(_lib.LIB_PATH):
+    _lib.LIB_PATH = Path(libs[0])
 lib = _lib.load()
+variants = []
+for path in libs:
+    v = C.CDLL(os.path.abspath(path))
+    v.utf8v_cuda_validate_batch_async.argtypes = _lib.SIGNATURES["utf8v_cuda_validate_batch_async"][1]
+    variants.append((Path(path).parent.name, v))
 st = torch.cuda.current_stream()
 scratch = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 for name, gen in (("c2", configs.gen_c2), ("c3", configs.gen_c3)):
@@ -21,25 +31,49 @@ for name, gen in (("c2", configs.gen_c2), ("c3", configs.gen_c3)):
     b = gen()
     ver = torch.empty(b.n_records, dtype=torch.uint8, device="cuda")
 
-    def run():
-        _lib.check(lib.utf8v_cuda_validate_batch_async(b.data.data_ptr(), b.nbytes, b.d_offsets.data_ptr(),
-                                                       b.n_records, ver.data_ptr(), None, st.cuda_stream))
+    def run(v):
+        ver.fill_(1)
+        _lib.check(v.utf8v_cuda_validate_batch_async(b.data.data_ptr(), b.nbytes, b.d_offsets.data_ptr(),
+                                                     b.n_records, ver.data_ptr(), None, st.cuda_stream))
 
-    for _ in range(3):
-        run()
+    for _, v in variants:
+        for _ in range(3):
+            run(v)
     torch.cuda.synchronize()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
-    for a, z in ev:
-        scratch.fill_(1)  # flush L2 (write, then read: no dirty lines left)
+    times = {vn: [] for vn, _ in variants}
+    oks = {}
+    for _ in range(reps):
+        for vn, v in variants:
+            scratch.fill_(1)  # flush L2 (write, then read: no dirty lines left)
+            scratch.view(torch.int64).sum()
+            ver.fill_(1)
+            a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(st)
+            _lib.check(v.utf8v_cuda_validate_batch_async(b.data.data_ptr(), b.nbytes, b.d_offsets.data_ptr(),
+                                                         b.n_records, ver.data_ptr(), None, st.cuda_stream))
+            z.record(st)
+            z.synchronize()
+            times[vn].append(a.elapsed_time(z))
+            oks[vn] = bool((ver.cpu().numpy() == b.expected).all())
+    # K1 on the same bytes as one stream (the sweep's own ceiling at this size)
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    k1 = []
+    for _ in range(reps):
+        scratch.fill_(1)
         scratch.view(torch.int64).sum()
+        a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(st)
-        run()
+        _lib.check(lib.utf8v_cuda_validate_lanes_async(b.data.data_ptr(), b.nbytes, 0, b.nbytes + 3,
+                                                       flag.data_ptr(), st.cuda_stream))
         z.record(st)
-    torch.cuda.synchronize()
-    ms = sum(a.elapsed_time(z) for a, z in ev) / reps
-    ok = bool((ver.cpu().numpy() == b.expected).all())
+        z.synchronize()
+        k1.append(a.elapsed_time(z))
+    times["K1-same-bytes"] = k1
+    oks["K1-same-bytes"] = None
     alg = b.nbytes + 8 * (b.n_records + 1) + b.n_records
-    print(f"{name}: {ms:.3f} ms  {b.n_records / ms / 1e6:.3f} G records/s  {alg / ms / 1e6:.1f} GB/s  "
-          f"verdicts_ok={ok}", flush=True)
+    for vn, ts in times.items():
+        ms = sorted(ts)[len(ts) // 2]
+        print(f"{name} {vn}: {ms:.3f} ms  {b.n_records / ms / 1e6:.3f} G records/s  {alg / ms / 1e6:.1f} GB/s  "
+              f"verdicts_ok={oks[vn]}", flush=True)
     del b, ver
     torch.cuda.empty_cache()
