@@ -667,3 +667,48 @@ def test_batch_offsets_of_any_integer_dtype(torch):
     for dt in (np.int32, np.int64, np.uint64):
         got = u8.validate_lookup_batch(b.data, b.offsets.astype(dt))
         assert np.array_equal(got, want), dt
+
+
+def test_batch_mixed_density_large(torch):
+    # K2's record cursor over long per-warp ranges: 64 MiB of the C1 mix cut
+    # into regions of very different record density (mean 3 B .. 64 KiB,
+    # empty records included), so warps take several boundary batches per
+    # step in dense regions and none for many steps in sparse ones; cuts
+    # mostly at character boundaries, some inside characters; 1 % of records
+    # get a random byte.  Device and host input, vs the oracle per record.
+    n = 64 << 20
+    h = configs.gen_c1(n, seed=21).cpu().numpy()
+    rng = np.random.default_rng(21)
+    cuts = [0]
+    pos = 0
+    means = (3, 16, 48, 300, 4096, 65536)
+    while pos < n:
+        m = means[int(rng.integers(0, len(means)))]
+        region_end = min(n, pos + int(rng.integers(1 << 18, 1 << 21)))
+        lens = rng.exponential(m, size=max(4, 2 * (region_end - pos) // m)).astype(np.int64)
+        ends = pos + np.cumsum(lens)
+        ends = ends[ends < region_end]
+        cuts.extend(ends.tolist())
+        cuts.append(region_end)
+        pos = region_end
+    cuts = np.array(cuts, dtype=np.int64)
+    snap = rng.random(cuts.size) < 0.9
+    for _ in range(3):  # move most cuts forward to a character boundary
+        inside = snap & (cuts < n) & ((h[np.minimum(cuts, n - 1)] & 0xC0) == 0x80)
+        cuts[inside] += 1
+    cuts = np.maximum.accumulate(np.minimum(cuts, n))
+    cuts[0], cuts[-1] = 0, n
+    offs = cuts.astype(np.uint64)
+    nrec = offs.size - 1
+    bad = rng.choice(nrec, size=nrec // 100, replace=False)
+    data = h.copy()
+    for r in bad:
+        a, b = int(offs[r]), int(offs[r + 1])
+        if b > a:
+            data[int(rng.integers(a, b))] = int(rng.integers(0x80, 0x100))
+    want = nat.oracle_batch(data, offs)
+    assert 0 < int((want == 0).sum()) < nrec
+    d_offs = torch.from_numpy(offs.view(np.int64)).cuda()
+    got = u8.validate_lookup_batch(torch.from_numpy(data).cuda(), d_offs)
+    assert np.array_equal(got, want)
+    assert np.array_equal(u8.validate_lookup_batch(data, offs), want)
