@@ -341,66 +341,78 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
       if (lane == 0) nsw = ld_word_guarded(d.base, (cstep + kStepChunks) * kChunkBytes, lo, hi);
     }
 
-    // Unbounded lane flags (K1's chunk form); ASCII fast path voted only
-    // after an all-ASCII step.
+    // Unbounded lane flags (K1's chunk form).  ASCII fast path (voted only
+    // after an all-ASCII step): a step of bytes < 0x80 only needs the
+    // pending incomplete check of the bytes before each chunk; if that
+    // fires, the step is recomputed exactly (attribution needs the lanes).
     bool all_ascii = false;
     if (was_ascii) {
       uint32_t hibits = 0;
 #pragma unroll
       for (int i = 0; i < kU; ++i) hibits |= chunk_hibits(v[i]);
       all_ascii = __all_sync(0xFFFFFFFFu, (hibits & U8V_B7) == 0);
-    }
-    uint32_t h7 = 0, err[kU], any = 0;
-#pragma unroll
-    for (int i = 0; i < kU; ++i) {
-      const uint32_t up =
-          lane == 31 ? (i == 0 ? carry_word : v[i - 1].w[kChunkWords - 1]) : v[i].w[kChunkWords - 1];
-      const uint32_t prev = __shfl_sync(0xFFFFFFFFu, up, (lane + 31) & 31);
-      const uint32_t dn = lane == 0 ? (i + 1 < kU ? v[i + 1].w[0] : nsw) : v[i].w[0];
-      const uint32_t next = __shfl_sync(0xFFFFFFFFu, dn, (lane + 1) & 31);
-      uint32_t hi7 = 0;
       if (all_ascii) {
-        u8v_carry cr = u8v_carry_of(prev);
-        err[i] = u8v_ascii_word_errors(v[i].w[0], &cr) & U8V_B7;
-        if (err[i]) err[i] = u8v_chunk_errors_planes_perm_k(v[i].w, prev, next, d.k, &hi7);  // exact lanes
-      } else {
-        err[i] = u8v_chunk_errors_planes_perm_k(v[i].w, prev, next, d.k, &hi7);
+        uint32_t ae = 0;
+#pragma unroll
+        for (int i = 0; i < kU; ++i) {
+          const uint32_t up =
+              lane == 31 ? (i == 0 ? carry_word : v[i - 1].w[kChunkWords - 1]) : v[i].w[kChunkWords - 1];
+          u8v_carry cr = u8v_carry_of(__shfl_sync(0xFFFFFFFFu, up, (lane + 31) & 31));
+          ae |= u8v_ascii_word_errors(v[i].w[0], &cr) & U8V_B7;
+        }
+        all_ascii = !__any_sync(0xFFFFFFFFu, ae != 0u);
       }
-      h7 |= hi7;
-      any |= err[i];
     }
-    was_ascii = all_ascii || __all_sync(0xFFFFFFFFu, h7 == 0);
+    if (!all_ascii) {
+      uint32_t h7 = 0, err[kU], any = 0;
+#pragma unroll
+      for (int i = 0; i < kU; ++i) {
+        const uint32_t up =
+            lane == 31 ? (i == 0 ? carry_word : v[i - 1].w[kChunkWords - 1]) : v[i].w[kChunkWords - 1];
+        const uint32_t prev = __shfl_sync(0xFFFFFFFFu, up, (lane + 31) & 31);
+        const uint32_t dn = lane == 0 ? (i + 1 < kU ? v[i + 1].w[0] : nsw) : v[i].w[0];
+        const uint32_t next = __shfl_sync(0xFFFFFFFFu, dn, (lane + 1) & 31);
+        uint32_t hi7 = 0;
+        err[i] = u8v_chunk_errors_planes_perm_k(v[i].w, prev, next, d.k, &hi7);
+        h7 |= hi7;
+        any |= err[i];
+      }
+      was_ascii = __all_sync(0xFFFFFFFFu, h7 == 0);
+#ifndef U8V_K2_SKIP_ATTR
+      if (__any_sync(0xFFFFFFFFu, any != 0u)) {
+        // Window: lane L = start(r0 + L) - s0 with start(r0) <= s0 (or r0 = 0):
+        // the taken batch's last start (< s0, else that batch would not have
+        // been taken) followed by the next batch's first 31.
+        const int s0 = j * kStepBytes;
+        const int up = __shfl_up_sync(0xFFFFFFFFu, nx, 1);
+        const int64_t rbc = cx->rb;
+        const bool first = rbc == 0;
+        const int o = (first ? nx : (lane == 0 ? cx->prev_last : up)) - s0;
+        attribute_step(rv, cx->range_lo + s0, cx->hi, err[0], err[1], err[2], err[3], o, first ? 0 : rbc - 1);
+      }
+#else
+      skip_any |= any;
+#endif
+    }
     if (lane == 31) carry_word = v[kU - 1].w[kChunkWords - 1];
 
-#ifndef U8V_K2_SKIP_ATTR
-    if (__any_sync(0xFFFFFFFFu, any != 0u)) {
-      // Window: lane L = start(r0 + L) - s0 with start(r0) <= s0 (or r0 = 0):
-      // the taken batch's last start (< s0, else that batch would not have
-      // been taken) followed by the next batch's first 31.
-      const int s0 = j * kStepBytes;
-      const int up = __shfl_up_sync(0xFFFFFFFFu, nx, 1);
-      const int64_t rbc = cx->rb;
-      const bool first = rbc == 0;
-      const int o = (first ? nx : (lane == 0 ? cx->prev_last : up)) - s0;
-      attribute_step(rv, cx->range_lo + s0, cx->hi, err[0], err[1], err[2], err[3], o, first ? 0 : rbc - 1);
-    }
-#else
-    skip_any |= any;
-#endif
 #ifndef U8V_K2_SKIP_FIX
-    if (pend) {
-      check_batch(rv, sl, nx, cx->rb - 32, cx->range_rel, d.k);
-      pend = false;
-    }
-    // The trigger reads nx a step after it was loaded (no stall on the load).
-    while (__shfl_sync(0xFFFFFFFFu, nx, kTrigger) < (j + 1) * kStepBytes) {
-      const int64_t rbc = cx->rb;
-      if (pend) check_batch(rv, sl, nx, rbc - 32, cx->range_rel, d.k);
-      take_batch(sl, d.base, cx->lo, cx->hi, cx->range_lo, nx, cx->prev_last, cx->range_rel);
-      pend = true;
-      cx->prev_last = __shfl_sync(0xFFFFFFFFu, nx, 31);
-      cx->rb = rbc + 32;
-      nx = rel32(rec_start(rv, rbc + 32 + lane), cx->range_lo);
+    // Boundary batches: the pending one is checked a step after it was
+    // taken; the trigger reads nx a step after it was loaded (no stall).
+    if (pend || __shfl_sync(0xFFFFFFFFu, nx, kTrigger) < (j + 1) * kStepBytes) {
+      if (pend) {
+        check_batch(rv, sl, nx, cx->rb - 32, cx->range_rel, d.k);
+        pend = false;
+      }
+      while (__shfl_sync(0xFFFFFFFFu, nx, kTrigger) < (j + 1) * kStepBytes) {
+        const int64_t rbc = cx->rb;
+        if (pend) check_batch(rv, sl, nx, rbc - 32, cx->range_rel, d.k);
+        take_batch(sl, d.base, cx->lo, cx->hi, cx->range_lo, nx, cx->prev_last, cx->range_rel);
+        pend = true;
+        cx->prev_last = __shfl_sync(0xFFFFFFFFu, nx, 31);
+        cx->rb = rbc + 32;
+        nx = rel32(rec_start(rv, rbc + 32 + lane), cx->range_lo);
+      }
     }
 #endif
   }
