@@ -84,7 +84,7 @@ struct Ctx {
   int dev = -1;
   cudaStream_t s_comp = nullptr, s_copy = nullptr;
   uint32_t* d_flag = nullptr;               // [0] verdict flag
-  unsigned long long* d_pos = nullptr;      // [0] first chunk, [1] offset, [2] K3 round
+  unsigned long long* d_pos = nullptr;      // [0] first flagged step (chunk index), [1] offset
   int* d_kind = nullptr;
   uint8_t* d_lanes = nullptr;               // 3 x UTF8V_CUDA_WIDTH
   int* d_ok = nullptr;
@@ -405,14 +405,19 @@ int pipeline_h2d(Ctx& c, const uint8_t* p, size_t n, F each) {
 
 // Lanes [lane_lo, lane_hi) of the host stream p[0..n) on this thread's
 // device: pieces are copied on s_copy and piece k-1's lanes are validated on
-// s_comp once piece k has landed (lane j reads byte j+1).  ORs into c.d_flag.
-int validate_host_lanes(Ctx& c, const uint8_t* p, size_t n, uint64_t lane_lo, uint64_t lane_hi) {
+// s_comp once piece k has landed (lane j reads byte j+1).  ORs into c.d_flag;
+// first_step non-null: the pieces also record the first flagged step there
+// (all pieces share d_stage's chunk coordinates).
+int validate_host_lanes(Ctx& c, const uint8_t* p, size_t n, uint64_t lane_lo, uint64_t lane_hi,
+                        unsigned long long* first_step = nullptr) {
   size_t prev_off = 0, prev_len = 0;
   bool have_prev = false;
   auto launch = [&](uint64_t a, uint64_t b) {
     const uint64_t lo = a > lane_lo ? a : lane_lo, hi = b < lane_hi ? b : lane_hi;
     if (lo < hi) {
-      u8v::launch_validate(u8v::make_desc(c.d_stage, n, lo, hi), c.d_flag, c.s_comp);
+      u8v::StreamDesc d = u8v::make_desc(c.d_stage, n, lo, hi);
+      d.first_step = first_step;
+      u8v::launch_validate(d, c.d_flag, c.s_comp);
       ++t_launches;
     }
   };
@@ -469,9 +474,11 @@ int utf8v_cuda_validate(const uint8_t* p, size_t n, int is_device, uint8_t* out_
   return UTF8V_OK;
 }
 
-// Verdict of lanes [lane_lo, lane_hi) of p[0..n): K1 over the lanes first
-// (host input piece by piece as the bytes land, as in utf8v_cuda_validate),
-// and only a flagged input is rescanned by K3 + the window decode.
+// Verdict of lanes [lane_lo, lane_hi) of p[0..n): one K1 pass over the lanes
+// (host input piece by piece as the bytes land, as in utf8v_cuda_validate)
+// that also records its first flagged step; only a flagged input then runs
+// K3, one warp that recomputes that step and decodes the window around its
+// first flagged chunk.
 static int verdict_lanes(const uint8_t* p, uint64_t n, uint64_t lane_lo, uint64_t lane_hi, int is_device,
                          uint8_t* out_valid, uint64_t* out_offset, int* out_kind) {
   t_launches = 0;
@@ -486,34 +493,33 @@ static int verdict_lanes(const uint8_t* p, uint64_t n, uint64_t lane_lo, uint64_
   int st = get_ctx(&c);
   if (st) return st;
   const uint8_t* d = p;
-  CK(cudaMemsetAsync(c->d_flag, 0, 4, c->s_comp));
+  // d_pos[0] = ~0: "no flagged step" is also the verdict (K1's flag word is
+  // not read here, so it needs no reset).
+  CK(cudaMemsetAsync(c->d_pos, 0xFF, 8, c->s_comp));
   if (is_device) {
     st = after_legacy(c->s_comp, c->ev_legacy);
     if (st) return st;
-    u8v::launch_validate(u8v::make_desc(p, n, lane_lo, lane_hi), c->d_flag, c->s_comp);
+    u8v::StreamDesc sd = u8v::make_desc(p, n, lane_lo, lane_hi);
+    sd.first_step = c->d_pos;
+    u8v::launch_validate(sd, c->d_flag, c->s_comp);
     ++t_launches;
   } else {
-    st = validate_host_lanes(*c, p, n, lane_lo, lane_hi);
+    st = validate_host_lanes(*c, p, n, lane_lo, lane_hi, c->d_pos);
     if (st) return st;
     d = c->d_stage;
   }
   st = check_launch("validate kernel");
   if (st) return st;
-  CK(cudaMemcpyAsync(c->h_res, c->d_flag, 4, cudaMemcpyDeviceToHost, c->s_comp));
+  CK(cudaMemcpyAsync(c->h_res, c->d_pos, 8, cudaMemcpyDeviceToHost, c->s_comp));
   CK(cudaStreamSynchronize(c->s_comp));
-  if (c->h_res[0] == 0) return UTF8V_OK;
-  CK(cudaMemsetAsync(c->d_flag, 0, 4, c->s_comp));
-  CK(cudaMemsetAsync(c->d_pos, 0xFF, 16, c->s_comp));
-  u8v::launch_first_error(u8v::make_desc(d, n, lane_lo, lane_hi), n, c->d_flag, c->d_pos, c->d_pos + 2,
-                          c->d_pos + 1, c->d_kind, c->s_comp);
-  t_launches += 2;
-  st = check_launch("first_error kernel");
+  if (c->h_res[0] == ~0u && c->h_res[1] == ~0u) return UTF8V_OK;
+  u8v::launch_locate(u8v::make_desc(d, n, lane_lo, lane_hi), n, c->d_pos, c->d_pos + 1, c->d_kind, c->s_comp);
+  ++t_launches;
+  st = check_launch("locate kernel");
   if (st) return st;
-  CK(cudaMemcpyAsync(c->h_res, c->d_flag, 4, cudaMemcpyDeviceToHost, c->s_comp));
   CK(cudaMemcpyAsync(c->h_res + 2, c->d_pos + 1, 8, cudaMemcpyDeviceToHost, c->s_comp));
   CK(cudaMemcpyAsync(c->h_res + 4, c->d_kind, 4, cudaMemcpyDeviceToHost, c->s_comp));
   CK(cudaStreamSynchronize(c->s_comp));
-  if (c->h_res[0] == 0) return UTF8V_OK;
   *out_valid = 0;
   uint64_t off;
   memcpy(&off, c->h_res + 2, 8);

@@ -29,6 +29,8 @@ struct StreamDesc {
   u8v_consts k;  // runtime multipliers (FMA-pipe routing, utf8v_swar.h)
   uint32_t* session;  // non-null: K1's first thread also runs the stream-session
                       // edge of this piece (stream_edge.cuh) on session[0..1]
+  unsigned long long* first_step;  // non-null: K1 records its first flagged step
+                                   // there (atomicMin of the step's first chunk)
 };
 
 int max_resident_warps();
@@ -38,9 +40,10 @@ void launch_validate(const StreamDesc& d, uint32_t* flag, cudaStream_t st);
 // stream: K1 launched with programmatic stream serialization, so consecutive
 // feeds overlap; the edge thread waits for the previous feed (validate.cu).
 void launch_validate_piece(const StreamDesc& d, uint32_t* flag, cudaStream_t st);
-void launch_first_error(const StreamDesc& d, uint64_t n, uint32_t* flag, unsigned long long* first_chunk,
-                        unsigned long long* next_round, unsigned long long* out_offset, int* out_kind,
-                        cudaStream_t st);
+// After K1 with d.first_step set flagged the stream: the first error's
+// (offset, kind) from the recorded step (one warp).
+void launch_locate(const StreamDesc& d, uint64_t n, const unsigned long long* first_step,
+                   unsigned long long* out_offset, int* out_kind, cudaStream_t st);
 
 // batch.cu
 // Caller sets d_verdicts[] = 1 first.  Asynchronous: the kernel reads

@@ -3,11 +3,12 @@
 //   k_validate          K1: OR of the per-lane error flags of one stream (or
 //                       of one lane range of it: a pipeline piece, a shard),
 //                       reduced with REDUX + one atomicOr per warp.
-//   k_first_error       K3: the same per-step scan over steps claimed in
-//                       order, recording the first 32-byte chunk that holds a
-//                       flagged lane (atomicMin); stops past that chunk.
-//   k_locate            K3b: one thread decodes the <= 42-byte window around
-//                       that chunk and writes the reference's (offset, kind).
+//   k_validate_track    K1 for the verdict path: also records the first
+//                       flagged step (each lane's first, atomicMin).
+//   k_locate_step       K3: one warp recomputes that step, takes its first
+//                       flagged 32-byte chunk, and one thread decodes the
+//                       <= 42-byte window around it into the reference's
+//                       (offset, kind).
 //
 // Reference path replaced: validate_with<V> / lookup_checker<V>
 // (proj/include/utf8v/lookup_kernel.hpp:82-134) reached through
@@ -147,18 +148,17 @@ __device__ __forceinline__ uint32_t any_step_errors(const StreamDesc& d, int64_t
 // pages open (+2.5% over contiguous per-warp ranges, tools/kbench.cu V19).
 // Steps are therefore independent: each loads its own halo word (lane 31,
 // the word before the step) and lookahead word (lane 0, the word after).
-__global__ void __launch_bounds__(kThreads, 4) k_validate(StreamDesc d, uint32_t* __restrict__ flag) {
-  if (d.session != nullptr) {
-    // Session feeds are launched with programmatic stream serialization
-    // (launch_validate_piece): the next piece's grid may start as soon as
-    // every block of this one has started, and only the edge thread, which
-    // reads the carry the previous feed wrote, waits for that feed.
-    asm volatile("griddepcontrol.launch_dependents;");
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      asm volatile("griddepcontrol.wait;" ::: "memory");
-      stream_edge_piece(d.session, d.base + d.off32, (uint64_t)(d.hi - d.lo), 0);
-    }
-  }
+// A lane's first flagged step: the chunk index of the step's first chunk
+// goes to *first_step (atomicMin, one elected lane of those that saw it).
+// Warps sweep their steps in increasing order, so the minimum over lanes and
+// warps is the step holding the stream's first flagged chunk.
+__device__ __forceinline__ void note_first_step(unsigned long long* first_step, int64_t cstep) {
+  const unsigned m = __activemask();
+  if ((int)(threadIdx.x & 31) == __ffs(m) - 1) atomicMin(first_step, (unsigned long long)cstep);
+}
+
+template <bool kTrack>
+__device__ __forceinline__ void sweep(const StreamDesc& d, uint32_t* __restrict__ flag) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * kThreads) >> 5;
@@ -168,6 +168,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_validate(StreamDesc d, uint32_t
 
   uint32_t acc = 0;
   bool was_ascii = true;  // try the vote on the first step
+  bool noted = false;     // kTrack: this lane has recorded its first flagged step
   int unused = kU;
   for (int64_t step = warp; step < d.steps; step += nwarps) {
     if (step >= int_b && step < int_d) {
@@ -183,63 +184,48 @@ __global__ void __launch_bounds__(kThreads, 4) k_validate(StreamDesc d, uint32_t
         uint32_t carry_word = 0, nsw = 0;
         if (lane == 31) carry_word = __ldg(reinterpret_cast<const uint32_t*>(p - 4));
         if (lane == 0) nsw = __ldg(reinterpret_cast<const uint32_t*>(p + sb));
-        acc |= step_errors<false, false>(d, v, 0, lane, carry_word, nsw, unused, was_ascii);
+        const uint32_t e = step_errors<false, false>(d, v, 0, lane, carry_word, nsw, unused, was_ascii);
+        acc |= e;
+        if (kTrack && e != 0u && !noted) {
+          noted = true;
+          note_first_step(d.first_step, (int64_t)((p - d.base) / kChunkBytes));
+        }
       }
       step += (int64_t)(n - 1) * nwarps;
       continue;
     }
-    acc |= any_step_errors<false>(d, step, false, lane, unused, was_ascii);
+    const uint32_t e = any_step_errors<false>(d, step, false, lane, unused, was_ascii);
+    acc |= e;
+    if (kTrack && e != 0u && !noted) {
+      noted = true;
+      note_first_step(d.first_step, d.c_begin + step * kStepChunks);
+    }
   }
   const unsigned any = __reduce_or_sync(0xFFFFFFFFu, acc);
   if (lane == 0 && any) atomicOr(flag, 1u);
 }
 
-// K3: the first 32-byte chunk that holds a flagged lane.  Steps are claimed
-// in order, one round of kThreads/32 consecutive steps per CTA and atomicAdd,
-// together with the earliest flagged chunk recorded so far: a round that
-// starts after it cannot hold an earlier one, and every later round starts
-// later still, so the CTA stops.  K3 therefore scans about the prefix up to
-// the first error (plus the rounds in flight, <= one per resident CTA).
-// Chunks of a step are ordered (i, lane): the warp's first flagged chunk is
-// the minimum over lanes of cstep + lane + 32 * first_i.
-__global__ void __launch_bounds__(kThreads, 4)
-    k_first_error(StreamDesc d, uint32_t* __restrict__ flag, unsigned long long* __restrict__ first_chunk,
-                  unsigned long long* __restrict__ next_round) {
-  constexpr int kWarps = kThreads / 32;
-  __shared__ unsigned long long s_round, s_seen;
-  const int lane = threadIdx.x & 31;
-  const int wib = threadIdx.x >> 5;
-  int64_t int_b, int_d;
-  interior_steps(d, &int_b, &int_d);
-  bool was_ascii = true;
-  for (;;) {
-    if (threadIdx.x == 0) {
-      s_round = atomicAdd(next_round, 1ull);
-      s_seen = *reinterpret_cast<volatile const unsigned long long*>(first_chunk);
-    }
-    __syncthreads();
-    const int64_t step0 = (int64_t)s_round * kWarps;
-    const unsigned long long seen = s_seen;
-    __syncthreads();
-    if (step0 >= d.steps || (unsigned long long)(d.c_begin + step0 * kStepChunks) > seen) break;
-    const int64_t step = step0 + wib;
-    if (step >= d.steps) continue;
-    int first_i = kU;
-    any_step_errors<true>(d, step, step >= int_b && step < int_d, lane, first_i, was_ascii);
-    if (__any_sync(0xFFFFFFFFu, first_i < kU)) {
-      const int64_t cstep = d.c_begin + step * kStepChunks;
-      unsigned long long m = first_i < kU ? (unsigned long long)(cstep + lane + 32 * first_i) : ~0ull;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const unsigned long long t = __shfl_xor_sync(0xFFFFFFFFu, m, o);
-        m = t < m ? t : m;
-      }
-      if (lane == 0) {
-        atomicMin(first_chunk, m);
-        atomicOr(flag, 1u);
-      }
+__global__ void __launch_bounds__(kThreads, 4) k_validate(StreamDesc d, uint32_t* __restrict__ flag) {
+  if (d.session != nullptr) {
+    // Session feeds are launched with programmatic stream serialization
+    // (launch_validate_piece): the next piece's grid may start as soon as
+    // every block of this one has started, and only the edge thread, which
+    // reads the carry the previous feed wrote, waits for that feed.
+    asm volatile("griddepcontrol.launch_dependents;");
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      stream_edge_piece(d.session, d.base + d.off32, (uint64_t)(d.hi - d.lo), 0);
     }
   }
+  sweep<false>(d, flag);
+}
+
+// K1 for the verdict path: also records the first flagged step
+// (d.first_step), so an invalid stream needs no second pass -- k_locate_step
+// recomputes that one step and decodes the window around its first flagged
+// chunk.
+__global__ void __launch_bounds__(kThreads, 4) k_validate_track(StreamDesc d, uint32_t* __restrict__ flag) {
+  sweep<true>(d, flag);
 }
 
 // The reference decode of oracle.cpp:10-44 run over [from, to) of the stream;
@@ -272,7 +258,7 @@ __device__ int decode_window(const uint8_t* s, uint64_t from, uint64_t to, uint6
   return -1;
 }
 
-// K3b: turn the first flagged chunk into (offset, kind).  Every flagged lane L
+// Turn the first flagged chunk into (offset, kind).  Every flagged lane L
 // satisfies E <= L <= E + 3 for the sequential first error E (proven for the
 // lane formula by tests/test_swar.py), so E lies in [chunk_start - 3,
 // chunk_end) and the decode needs bytes up to E + 3.  The window starts at
@@ -282,11 +268,9 @@ __device__ int decode_window(const uint8_t* s, uint64_t from, uint64_t to, uint6
 // bytes another shard owns: the window then starts at lane_lo - 3 (still at
 // or before E, as E >= L - 3 >= lane_lo - 3), so it never decodes from the
 // middle of a character at the start of a shard's head.
-__global__ void k_locate(const uint8_t* __restrict__ s, uint64_t n, int64_t off, int64_t lane_lo,
-                         const unsigned long long* __restrict__ first_chunk,
-                         unsigned long long* __restrict__ out_offset, int* __restrict__ out_kind) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  const unsigned long long c = *first_chunk;
+__device__ void locate_chunk(const uint8_t* __restrict__ s, uint64_t n, int64_t off, int64_t lane_lo,
+                             unsigned long long c, unsigned long long* __restrict__ out_offset,
+                             int* __restrict__ out_kind) {
   const int64_t lmin = (int64_t)c * kChunkBytes - off;  // first lane of the chunk
   int64_t b0 = (lmin > lane_lo ? lmin : lane_lo) - 3;
   if (b0 < 0) b0 = 0;
@@ -300,6 +284,37 @@ __global__ void k_locate(const uint8_t* __restrict__ s, uint64_t n, int64_t off,
   const int kind = decode_window(s, (uint64_t)b, to, &o);
   *out_kind = kind;
   *out_offset = kind < 0 ? ~0ull : o;
+}
+
+
+// K3: one warp recomputes the step K1 recorded as the first flagged one
+// (every lane range of the stream, masked loads), takes its first flagged
+// chunk (chunks ordered (i, lane)), and lane 0 decodes the window around it.
+// Lane flags are a function of the bytes alone, so the step recomputed over
+// the stream's whole lane range flags the same chunks K1 (or a pipeline
+// piece of it) did, and no chunk before it is flagged.
+__global__ void k_locate_step(StreamDesc d, uint64_t n, const unsigned long long* __restrict__ first_step,
+                              unsigned long long* __restrict__ out_offset, int* __restrict__ out_kind) {
+  const int lane = threadIdx.x & 31;
+  const unsigned long long cs = *first_step;
+  StreamDesc w = d;
+  w.c_begin = (int64_t)cs;
+  int first_i = kU;
+  bool was_ascii = false;
+  any_step_errors<true>(w, 0, false, lane, first_i, was_ascii);
+  unsigned long long m = first_i < kU ? cs + (unsigned long long)(lane + 32 * first_i) : ~0ull;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long t = __shfl_xor_sync(0xFFFFFFFFu, m, o);
+    m = t < m ? t : m;
+  }
+  if (lane != 0) return;
+  if (m == ~0ull) {  // no flagged chunk (cannot happen after a flagged K1)
+    *out_kind = -1;
+    *out_offset = ~0ull;
+    return;
+  }
+  locate_chunk(d.base + d.off32, n, d.off32, d.L0 - d.off32, m, out_offset, out_kind);
 }
 
 }  // namespace u8v
@@ -343,6 +358,7 @@ StreamDesc make_desc(const uint8_t* p, uint64_t n, uint64_t lane_lo, uint64_t la
   if (warps < 1) warps = 1;
   d.steps_per_warp = (d.steps + warps - 1) / warps;
   d.session = nullptr;
+  d.first_step = nullptr;
   return d;
 }
 
@@ -350,7 +366,10 @@ void launch_validate(const StreamDesc& d, uint32_t* flag, cudaStream_t st) {
   if (d.steps <= 0) return;
   const int64_t warps = (d.steps + d.steps_per_warp - 1) / d.steps_per_warp;
   const int64_t blocks = (warps * 32 + kThreads - 1) / kThreads;
-  k_validate<<<(unsigned)blocks, kThreads, 0, st>>>(d, flag);
+  if (d.first_step)
+    k_validate_track<<<(unsigned)blocks, kThreads, 0, st>>>(d, flag);
+  else
+    k_validate<<<(unsigned)blocks, kThreads, 0, st>>>(d, flag);
 }
 
 void launch_validate_piece(const StreamDesc& d, uint32_t* flag, cudaStream_t st) {
@@ -367,19 +386,9 @@ void launch_validate_piece(const StreamDesc& d, uint32_t* flag, cudaStream_t st)
   cudaLaunchKernelEx(&cfg, k_validate, d, flag);
 }
 
-void launch_first_error(const StreamDesc& d, uint64_t n, uint32_t* flag, unsigned long long* first_chunk,
-                        unsigned long long* next_round, unsigned long long* out_offset, int* out_kind,
-                        cudaStream_t st) {
-  if (d.steps > 0) {
-    // Enough CTAs to fill the GPU; each claims rounds until the stream (or
-    // the prefix before the first error) is exhausted.
-    const int64_t rounds = (d.steps + kThreads / 32 - 1) / (kThreads / 32);
-    const int64_t resident = max_resident_warps() / (kThreads / 32);
-    const int64_t blocks = rounds < resident ? rounds : resident;
-    cudaMemsetAsync(next_round, 0, sizeof(*next_round), st);
-    k_first_error<<<(unsigned)blocks, kThreads, 0, st>>>(d, flag, first_chunk, next_round);
-  }
-  k_locate<<<1, 32, 0, st>>>(d.base + d.off32, n, d.off32, d.L0 - d.off32, first_chunk, out_offset, out_kind);
+void launch_locate(const StreamDesc& d, uint64_t n, const unsigned long long* first_step,
+                   unsigned long long* out_offset, int* out_kind, cudaStream_t st) {
+  k_locate_step<<<1, 32, 0, st>>>(d, n, first_step, out_offset, out_kind);
 }
 
 }  // namespace u8v

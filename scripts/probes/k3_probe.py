@@ -1,5 +1,7 @@
-"""Verdict-path cost vs the first error's position (1 GiB C1): separates the
-K1 pass, the K3 prefix scan and the fixed per-call overhead."""
+"""Verdict-path cost vs the first error's position (1 GiB C1).  With the
+tracking K1 (first flagged step recorded in the same pass) the cost no longer
+depends on the position; the numbers DESIGN.md quotes for 25/50/75/100 % are
+from the earlier design, whose second kernel rescanned the prefix."""
 import sys
 from pathlib import Path
 

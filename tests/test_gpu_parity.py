@@ -329,9 +329,11 @@ def test_lane_ranges_compose(torch):
 
 
 def test_first_error_ordered_claims(torch):
-    """K3 claims 32 KiB rounds (8 warp steps) in order and stops past the
-    earliest flagged chunk recorded so far: with several errors, at round
-    and step boundaries, the reported one is always the first."""
+    """K1 (verdict path) records every lane's first flagged step with
+    atomicMin and K3 recomputes the earliest: with several errors -- in one
+    step, at step boundaries, in different warps -- the reported one is
+    always the first, for device input and for host input (pipelined
+    pieces, each recording into the same minimum)."""
     d = configs.gen_c1(64 << 20, seed=21)
     h = d.cpu().numpy()
     n = h.size
@@ -347,13 +349,17 @@ def test_first_error_ordered_claims(torch):
             bad[p] = 0xFF if trial % 3 else 0x80
         exp = nat.oracle_verdict(bad, threads=16)
         v = u8.validate_lookup_verdict(torch.from_numpy(bad).cuda())
+        vh = u8.validate_lookup_verdict(bad)
         if exp[0]:  # 0x80 over a continuation byte can stay valid
-            assert v.valid()
+            assert v.valid() and vh.valid()
             continue
         assert (v.error.offset, int(v.error.kind)) == (exp[1], exp[2]), (picks, trial)
+        assert (vh.error.offset, int(vh.error.kind)) == (exp[1], exp[2]), (picks, trial)
     # garbage everywhere: every round flags, the answer is the first byte's
     g = torch.from_numpy(np.full(n, 0xFF, np.uint8)).cuda()
     v = u8.validate_lookup_verdict(g)
+    assert (v.error.offset, int(v.error.kind)) == (0, int(u8.ErrorKind.HEADER_BITS))
+    v = u8.validate_lookup_verdict(np.full(n, 0xFF, np.uint8))
     assert (v.error.offset, int(v.error.kind)) == (0, int(u8.ErrorKind.HEADER_BITS))
 
 
