@@ -1,7 +1,7 @@
 #!/usr/bin/env python3
 """bench.py -- B200 Lookup UTF-8 validation throughput (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c1|c0|c4|c3]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c1|c0|c4]
 
 One step = one pass of the hot path over one batch of synthetic input
 resident in HBM: validate_lanes (K1) over the rank's 1 GiB shard of the
@@ -37,6 +37,7 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 GiB = 1 << 30
+C4_BYTES = 16 * GiB
 METRIC = "validated GB/s per GPU and box (device-timed) vs HBM roofline; records/sec"
 
 
@@ -46,7 +47,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c1", choices=["c0", "c1", "c3", "c4"])
+    ap.add_argument("--config", default="c1", choices=["c0", "c1", "c4"])  # C2/C3: other_configs
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the C0/C2/C3/C4 side measurements")
@@ -193,18 +194,33 @@ def host_stream(n: int, seed: int, ascii_only: bool) -> np.ndarray:
 
 
 # ---------------------------------------------------------------------------
+WORKLOADS = {"c1": "C1: valid UTF-8, 0.4/0.2/0.3/0.1 length mix, seed 2, 1 GiB per GPU",
+             "c0": "C0: 64 MiB ASCII + 2% LF, seed 1, per GPU",
+             "c4": "C4: 16 GiB mix, seed 5, sharded over the GPUs (strong scaling)"}
+SEEDS = {"c0": 1, "c1": 2, "c4": 5}
+DATA = "synthetic (seeded splitmix64 generator, DESIGN.md 'Synthetic inputs')"
+
+
+def workload_bytes(config: str, world: int) -> tuple[int, int]:
+    """(bytes per GPU, bytes in the whole job) of a bench config."""
+    if config == "c4":
+        return C4_BYTES // world, C4_BYTES
+    per = (64 << 20) if config == "c0" else GiB
+    return per, per * world
+
+
 def run_reference(args, rank: int, world: int):
     if rank != 0:
         return
     L = ref_lib()
     base = {"metric": METRIC, "unit": "GB/s", "impl": "reference", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "u8", "data": "synthetic"}
+            "dtype": "u8", "data": DATA}
     if L is None:
         print(json.dumps({**base, "unavailable": "oracle/_ref/libutf8v_ref.so not built (no reference checkout)"}))
         return
-    n_total = GiB * max(1, args.gpus) if args.config == "c1" else (64 << 20)
-    seed, ascii_only = (2, False) if args.config != "c0" else (1, True)
+    per, n_total = workload_bytes(args.config, max(1, args.gpus))
+    seed, ascii_only = SEEDS[args.config], args.config == "c0"
     # The sample: the whole workload when it fits in host RAM comfortably.
     n = min(n_total, 4 * GiB)
     buf = host_stream(n, seed, ascii_only)
@@ -219,7 +235,7 @@ def run_reference(args, rank: int, world: int):
     value = n * args.steps / dt / 1e9
     sample = f"{n} bytes of config {args.config} (seed {seed}) per step, {args.steps} steps"
     print(json.dumps({**base, "value": value, "ms_per_step": dt / args.steps * 1e3,
-                      "config": {"workload": f"{args.config.upper()} stream, {n_total} bytes total over {args.gpus} GPU(s)",
+                      "config": {"workload": WORKLOADS[args.config], "bytes_per_gpu": per, "bytes_total": n_total,
                                  "sample_bytes": n, "cpu": cpu_model()},
                       "valid": bool(ok),
                       "cpu_baseline": {"value": value, "unit": "GB/s", "cores": T, "kind": "reference",
@@ -240,16 +256,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     lib = _lib.load()
 
     # ---- workload: this rank's shard (+ up to 16 bytes of halo) ----------
-    if args.config == "c4":
-        n_total = configs.C4["n"]
-        per = n_total // world
-    elif args.config == "c0":
-        per = configs.C0["n"]
-        n_total = per * world
-    else:
-        per = GiB
-        n_total = per * world
-    seed = {"c0": 1, "c1": 2, "c4": 5}.get(args.config, 2)
+    per, n_total = workload_bytes(args.config, world)
+    assert (args.config != "c4" or n_total == configs.C4["n"]) and (args.config != "c0" or per == configs.C0["n"])
+    seed = SEEDS[args.config]
     ascii_only = args.config == "c0"
     s, e = rank * per, (rank + 1) * per
     from paper_2010_03090_b200 import sharding
@@ -405,14 +414,12 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         extras = measure_extras(lib, dev, max(5, min(args.steps, 50)))
 
     if rank == 0:
-        workload = {"c1": "C1: valid UTF-8, 0.4/0.2/0.3/0.1 length mix, seed 2, 1 GiB per GPU",
-                    "c0": "C0: 64 MiB ASCII + 2% LF, seed 1, per GPU",
-                    "c4": "C4: 16 GiB mix, seed 5, sharded over the GPUs (strong scaling)"}[args.config]
+        workload = WORKLOADS[args.config]
         out = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong" if args.config == "c4" else "weak", "vs_baseline": None, "dtype": "u8",
-            "data": "synthetic (seeded splitmix64 generator, DESIGN.md 'Synthetic inputs')",
+            "data": DATA,
             "config": {"workload": workload, "bytes_per_gpu": per, "bytes_total": per * world,
                        "l2": "input (>=1 GiB) larger than the 126 MB L2; no flush needed",
                        "parallelism": f"dp{world}: byte-range shards (<=16-byte look-back head, 3-byte tail)"
