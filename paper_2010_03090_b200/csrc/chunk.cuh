@@ -26,17 +26,6 @@ __device__ __forceinline__ Chunk ld_chunk(const uint8_t* p) {
   return c;
 }
 
-// The same load allocating in L1: K2 re-reads the bytes around each record
-// start right after the sweep (batch.cu), which then hits L1, not L2.
-__device__ __forceinline__ Chunk ld_chunk_l1(const uint8_t* p) {
-  Chunk c;
-  asm("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-      : "=r"(c.w[0]), "=r"(c.w[1]), "=r"(c.w[2]), "=r"(c.w[3]), "=r"(c.w[4]), "=r"(c.w[5]),
-        "=r"(c.w[6]), "=r"(c.w[7])
-      : "l"(p));
-  return c;
-}
-
 __device__ __forceinline__ Chunk zero_chunk() {
   Chunk r;
 #pragma unroll
