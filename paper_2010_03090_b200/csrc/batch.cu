@@ -98,12 +98,7 @@ __device__ __forceinline__ int rel32(int64_t pos, int64_t s0) {
 // lanes or lies past the data (those lanes are settled by fix_boundary).
 // e0..e3: lane bits of chunk (lane + 32 i) of the step in the permuted plane
 // order of utf8v_bits.h (bit pos(i) = byte i).
-#ifdef U8V_K2_ATTR_INLINE
-#define U8V_ATTR_LINKAGE __forceinline__
-#else
-#define U8V_ATTR_LINKAGE __noinline__
-#endif
-__device__ U8V_ATTR_LINKAGE void attribute_step(RecView d, int64_t s0, int64_t hi, uint32_t e0, uint32_t e1,
+__device__ __noinline__ void attribute_step(RecView d, int64_t s0, int64_t hi, uint32_t e0, uint32_t e1,
                                             uint32_t e2, uint32_t e3, int o, int64_t r0) {
   const int lane = threadIdx.x & 31;
   const bool full = __all_sync(0xFFFFFFFFu, o < kStepChunks * kChunkBytes);
@@ -312,9 +307,6 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
   cx->range_rel = range_rel;
   bool pend = false;
   bool was_ascii = true;
-#ifdef U8V_K2_SKIP_ATTR
-  uint32_t skip_any = 0;
-#endif
 
   // Steps [jb, jd) are interior (all bytes real, lookahead word in range):
   // plain loads from a pointer advanced 4 KiB per step.
@@ -378,7 +370,6 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
         any |= err[i];
       }
       was_ascii = __all_sync(0xFFFFFFFFu, h7 == 0);
-#ifndef U8V_K2_SKIP_ATTR
       if (__any_sync(0xFFFFFFFFu, any != 0u)) {
         // Window: lane L = start(r0 + L) - s0 with start(r0) <= s0 (or r0 = 0):
         // the taken batch's last start (< s0, else that batch would not have
@@ -390,13 +381,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
         const int o = (first ? nx : (lane == 0 ? cx->prev_last : up)) - s0;
         attribute_step(rv, cx->range_lo + s0, cx->hi, err[0], err[1], err[2], err[3], o, first ? 0 : rbc - 1);
       }
-#else
-      skip_any |= any;
-#endif
     }
     if (lane == 31) carry_word = v[kU - 1].w[kChunkWords - 1];
 
-#ifndef U8V_K2_SKIP_FIX
     // Boundary batches: the pending one is checked a step after it was
     // taken; the trigger reads nx a step after it was loaded (no stall).
     if (pend || __shfl_sync(0xFFFFFFFFu, nx, kTrigger) < (j + 1) * kStepBytes) {
@@ -414,12 +401,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
         nx = rel32(rec_start(rv, rbc + 32 + lane), cx->range_lo);
       }
     }
-#endif
   }
-#ifdef U8V_K2_SKIP_ATTR
-  if (skip_any) d.verdicts[warp % d.n_records] = 0;
-#endif
-#ifndef U8V_K2_SKIP_FIX
   // The range's remaining boundaries.
   {
     int64_t rbc = cx->rb;
@@ -435,7 +417,6 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
       check_batch(rv, sl, nx, rbc - 32, rrel, d.k);
     }
   }
-#endif
 }
 }  // namespace u8v
 
