@@ -426,6 +426,7 @@ namespace u8v {
 void launch_batch(const uint8_t* data, uint64_t n, const uint64_t* d_offsets, uint64_t n_records,
                   uint8_t* d_verdicts, cudaStream_t st) {
   if (n_records == 0 || n == 0) return;
+  if (launch_batch_large(data, n, d_offsets, n_records, d_verdicts, st)) return;
   BatchDesc d;
   const uintptr_t up = (uintptr_t)data;
   d.off32 = (int64_t)(up & (kChunkBytes - 1));

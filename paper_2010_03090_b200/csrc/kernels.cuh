@@ -51,6 +51,15 @@ void launch_locate(const StreamDesc& d, uint64_t n, const unsigned long long* fi
 void launch_batch(const uint8_t* data, uint64_t n, const uint64_t* d_offsets, uint64_t n_records,
                   uint8_t* d_verdicts, cudaStream_t st);
 
+// validate.cu: K2L, the batch kernel for few, large records (<= 2048
+// records of >= 64 KiB on average): K1's sweep + out-of-line attribution.
+// Returns false (nothing launched) outside that range; same contract as
+// launch_batch otherwise.
+constexpr int kLargeMaxRecords = 2048;
+constexpr uint64_t kLargeMinAvgBytes = 64 << 10;
+bool launch_batch_large(const uint8_t* data, uint64_t n, const uint64_t* d_offsets, uint64_t n_records,
+                        uint8_t* d_verdicts, cudaStream_t st);
+
 // stream.cu: d_state[0] = carry, d_state[1] = error flag (utf8v_stream.h).
 void launch_stream_edge(uint32_t* d_state, const uint8_t* d_piece, uint64_t n, int finish,
                         cudaStream_t st);

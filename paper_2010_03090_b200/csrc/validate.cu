@@ -317,6 +317,163 @@ __global__ void k_locate_step(StreamDesc d, uint64_t n, const unsigned long long
   locate_chunk(d.base + d.off32, n, d.off32, d.L0 - d.off32, m, out_offset, out_kind);
 }
 
+// ---- K2L: batches of few, large records (C2) ------------------------------
+// Same decomposition as K2 (batch.cu): the unbounded lane flags of the data
+// buffer, each flagged lane attributed to its record unless it is one of
+// the record's first three lanes or lies past the data, plus one boundary
+// check per record start.  With few records (launch_batch dispatches here
+// for <= kLargeMaxRecords records of >= 64 KiB on average) the sweep is K1's
+// own round-robin loop with no record cursor: a flagged step (rare -- at
+// most a few per invalid record, none inside a record already known
+// invalid) is recomputed out of line in natural lane order and each flagged
+// lane finds its record by binary search over the offsets held in shared
+// memory.
+
+// Largest r in [-1, N] with s_off[r] <= q (s_off[-1] = -inf).
+__device__ __forceinline__ int rec_of(const int64_t* s_off, int N, int64_t q) {
+  int a = -1, b = N;  // s_off[a] <= q (a = -1: none), answer in [a, b]
+  while (a < b) {
+    const int m = (a + b + 1) >> 1;
+    if (s_off[m] <= q) a = m;
+    else b = m - 1;
+  }
+  return a;
+}
+
+__device__ __forceinline__ void attribute_large(const StreamDesc& d, int64_t cstep, uint32_t e_or, const int64_t* s_off,
+                                             int N, uint8_t* verdicts) {
+  const int lane = threadIdx.x & 31;
+  const int64_t sb = kStepChunks * (int64_t)kChunkBytes;
+  const int64_t s0 = cstep * kChunkBytes;
+  const int64_t data_hi = s_off[N];
+  // A flagged lane whose four chunks all lie inside one record r, past its
+  // first three lanes and before the data end, settles r without knowing
+  // which lane fired (the common case for large records).
+  bool open = false;
+  if (e_or) {
+    const int64_t a = (cstep + lane) * kChunkBytes, z = (cstep + lane + 32 * (kU - 1) + 1) * kChunkBytes;
+    const int r = rec_of(s_off, N, a);
+    if (r >= 0 && r < N && a - s_off[r] >= 3 && z <= s_off[r + 1] && z <= data_hi)
+      verdicts[r] = 0;
+    else
+      open = true;
+  }
+  if (!__any_sync(0xFFFFFFFFu, open)) return;
+  // Otherwise the step's lane flags again, natural order (bit i = lane 32 c
+  // + i), for the lanes still open.
+  Chunk v[kU];
+#pragma unroll
+  for (int i = 0; i < kU; ++i) {
+    const int64_t c = cstep + lane + 32 * i;
+    v[i] = c <= d.c_end ? ld_chunk_masked(d.base, c, d.lo, d.hi) : zero_chunk();
+  }
+  uint32_t carry_word = 0, nsw = 0;
+  if (lane == 31) carry_word = ld_word_guarded(d.base, s0 - 4, d.lo, d.hi);
+  if (lane == 0) nsw = ld_word_guarded(d.base, s0 + sb, d.lo, d.hi);
+  uint32_t e[kU];
+#pragma unroll
+  for (int i = 0; i < kU; ++i) {
+    const uint32_t up =
+        lane == 31 ? (i == 0 ? carry_word : v[i - 1].w[kChunkWords - 1]) : v[i].w[kChunkWords - 1];
+    const uint32_t prev = __shfl_sync(0xFFFFFFFFu, up, (lane + 31) & 31);
+    const uint32_t dn = lane == 0 ? (i + 1 < kU ? v[i + 1].w[0] : nsw) : v[i].w[0];
+    const uint32_t next = __shfl_sync(0xFFFFFFFFu, dn, (lane + 1) & 31);
+    const int64_t c = cstep + lane + 32 * i;
+    uint32_t hi7;
+    e[i] = c < d.c_end ? chunk_errors<true>(v[i], prev, next, d.k, c * kChunkBytes, d.L0, d.L1, &hi7) : 0u;
+  }
+  // Each flagged lane q goes to its record r; once r is marked invalid every
+  // other flagged lane of r in the chunk is dropped with it.
+#pragma unroll
+  for (int i = 0; i < kU; ++i) {
+    const int64_t c0 = (cstep + lane + 32 * i) * kChunkBytes;
+    uint32_t m = open ? e[i] : 0u;
+    while (m) {
+      const int b = __ffs(m) - 1;
+      const int64_t q = c0 + b;
+      m &= m - 1;
+      if (q >= data_hi) break;  // past the data: the boundary at data_hi settles it
+      const int r = rec_of(s_off, N, q);
+      if (r < 0 || q - s_off[r] < 3) continue;  // before the data / a record's first lanes
+      verdicts[r] = 0;
+      const int64_t end = s_off[r + 1] - c0;  // drop the rest of record r
+      m = end >= 32 ? 0u : (end <= 0 ? m : (m & ~((1u << end) - 1u)));
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 4)
+    k_batch_large(StreamDesc d, const uint64_t* __restrict__ offsets, int N, uint8_t* __restrict__ verdicts) {
+  extern __shared__ int64_t s_off[];  // start(r) in base coordinates, clamped to the data
+  const int64_t nb = d.hi - d.lo;
+  for (int i = threadIdx.x; i <= N; i += blockDim.x) {
+    const uint64_t o = __ldg(offsets + i);
+    s_off[i] = d.off32 + (int64_t)(o < (uint64_t)nb ? o : (uint64_t)nb);
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  // Record boundaries: thread g of the grid takes start(g), g <= N (record
+  // g-1 = [a, s) ends there, record g = [s, b) starts there).
+  const int64_t g = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  if (g <= N) {
+    const int64_t s = s_off[g], lo = s_off[0], hi = s_off[N];
+    const int64_t a = g > 0 ? s_off[g - 1] : s, b = g < N ? s_off[g + 1] : s;
+    uint64_t w8 = 0;
+    for (int k = 0; k < 8; ++k) {
+      const int64_t q = s - 4 + k;
+      if (q >= lo && q < hi) w8 |= (uint64_t)d.base[q] << (8 * k);
+    }
+    int64_t ka = a - (s - 4), kb = b - (s - 4);
+    ka = ka < 0 ? 0 : (ka > 4 ? 4 : ka);
+    kb = kb < 4 ? 4 : (kb > 8 ? 8 : kb);
+    const uint32_t f = u8v_boundary_errors(w8, (unsigned)ka, (unsigned)kb, d.k);
+    if ((f & 1u) && g > 0) verdicts[g - 1] = 0;
+    if ((f & 2u) && g < N) verdicts[g] = 0;
+  }
+  // The sweep: K1's loop; a flagged step is attributed out of line.
+  const int64_t warp = g >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * kThreads) >> 5;
+  const int64_t sb = kStepChunks * (int64_t)kChunkBytes;
+  int64_t int_b, int_d;
+  interior_steps(d, &int_b, &int_d);
+  bool was_ascii = true;
+  int unused = kU;
+  for (int64_t step = warp; step < d.steps; step += nwarps) {
+    uint32_t e = 0;
+    int64_t cs;
+    if (step >= int_b && step < int_d) {
+      // K1's interior loop; it stops at a flagged step, which is attributed
+      // below (out of the loop, so the loop keeps K1's registers), and the
+      // outer loop resumes with the next step.
+      const int n = (int)((int_d - 1 - step) / nwarps) + 1;
+      const int64_t stride = nwarps * sb;
+      const uint8_t* p = d.base + (d.c_begin + step * kStepChunks) * kChunkBytes;
+      int j = 0;
+      for (; j < n; ++j, p += stride) {
+        Chunk v[kU];
+#pragma unroll
+        for (int i = 0; i < kU; ++i) v[i] = ld_chunk(p + (lane + 32 * i) * kChunkBytes);
+        uint32_t carry_word = 0, nsw = 0;
+        if (lane == 31) carry_word = __ldg(reinterpret_cast<const uint32_t*>(p - 4));
+        if (lane == 0) nsw = __ldg(reinterpret_cast<const uint32_t*>(p + sb));
+        e = step_errors<false, false>(d, v, 0, lane, carry_word, nsw, unused, was_ascii);
+        if (__any_sync(0xFFFFFFFFu, e != 0u)) break;
+      }
+      if (j == n) {
+        step += (int64_t)(n - 1) * nwarps;
+        continue;
+      }
+      step += (int64_t)j * nwarps;
+      cs = (int64_t)((p - d.base) / kChunkBytes);
+    } else {
+      e = any_step_errors<false>(d, step, false, lane, unused, was_ascii);
+      if (!__any_sync(0xFFFFFFFFu, e != 0u)) continue;
+      cs = d.c_begin + step * kStepChunks;
+    }
+    attribute_large(d, cs, e, s_off, N, verdicts);
+  }
+}
+
 }  // namespace u8v
 
 // ---- host-side launchers (called by capi.cu) ------------------------------
@@ -384,6 +541,21 @@ void launch_validate_piece(const StreamDesc& d, uint32_t* flag, cudaStream_t st)
   cfg.attrs = at;
   cfg.numAttrs = 1;
   cudaLaunchKernelEx(&cfg, k_validate, d, flag);
+}
+
+bool launch_batch_large(const uint8_t* data, uint64_t n, const uint64_t* d_offsets, uint64_t n_records,
+                        uint8_t* d_verdicts, cudaStream_t st) {
+  if (n_records == 0 || n_records > (uint64_t)kLargeMaxRecords || n / n_records < kLargeMinAvgBytes) return false;
+  // Lanes [0, n) of the data buffer: lanes past offsets[N] are ignored and
+  // the last record's end is settled by the boundary check at offsets[N].
+  const StreamDesc d = make_desc(data, n, 0, n);
+  const int64_t warps = (d.steps + d.steps_per_warp - 1) / d.steps_per_warp;
+  int64_t blocks = (warps * 32 + kThreads - 1) / kThreads;
+  const int64_t need = ((int64_t)n_records + kThreads) / kThreads;  // boundary threads: N + 1
+  if (blocks < need) blocks = need;
+  const size_t smem = (n_records + 1) * sizeof(int64_t);
+  k_batch_large<<<(unsigned)blocks, kThreads, smem, st>>>(d, d_offsets, (int)n_records, d_verdicts);
+  return true;
 }
 
 void launch_locate(const StreamDesc& d, uint64_t n, const unsigned long long* first_step,

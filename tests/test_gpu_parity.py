@@ -718,3 +718,52 @@ def test_batch_mixed_density_large(torch):
     got = u8.validate_lookup_batch(torch.from_numpy(data).cuda(), d_offs)
     assert np.array_equal(got, want)
     assert np.array_equal(u8.validate_lookup_batch(data, offs), want)
+
+
+@pytest.mark.parametrize("n_rec", [1, 2, 17, 64, 300, 2048])
+def test_batch_few_large_records(n_rec, torch):
+    # K2L (<= 2048 records of >= 64 KiB on average, launch_batch): K1's sweep
+    # with out-of-line attribution over offsets in shared memory.  Records of
+    # 0 B .. ~1 MiB (empty and tiny ones among them), cuts inside characters,
+    # errors in a record's first three bytes, at its end and inside it,
+    # all-garbage records, bytes before offsets[0] and after offsets[N], and
+    # unaligned data; vs the oracle per record, device and host input.
+    rng = np.random.default_rng(1000 + n_rec)
+    lens = rng.lognormal(np.log(160 << 10), 1.0, n_rec).astype(np.int64)
+    lens[rng.random(n_rec) < 0.1] = 0
+    lens[rng.random(n_rec) < 0.1] = rng.integers(1, 40)
+    lens = np.minimum(lens, 1 << 20)
+    if lens.sum() < n_rec * (64 << 10):  # keep the batch on the K2L path
+        lens = lens + ((n_rec * (64 << 10) - lens.sum()) // n_rec + 1)
+    lead, tail = int(rng.integers(0, 100)), int(rng.integers(0, 100))
+    total = int(lens.sum()) + lead + tail
+    h = configs.gen_c1(total + 64, seed=n_rec).cpu().numpy()[:total].copy()
+    offs = np.zeros(n_rec + 1, np.uint64)
+    offs[1:] = np.cumsum(lens)
+    offs += np.uint64(lead)
+    for r in range(n_rec):
+        a, b = int(offs[r]), int(offs[r + 1])
+        if b - a < 4:
+            continue
+        kind = int(rng.integers(0, 8))
+        if kind == 0:
+            h[a + int(rng.integers(0, 3))] = 0x80  # stray continuation at the start
+        elif kind == 1:
+            h[b - 1] = 0xE2  # truncated at the end
+        elif kind == 2:
+            h[int(rng.integers(a, b))] = 0xFF
+        elif kind == 3 and b - a < (300 << 10):
+            h[a:b] = 0xFF  # garbage record
+        elif kind == 4:
+            h[int(rng.integers(a, b - 1))] = 0xC0  # overlong lead
+    h[:lead] = 0xFF
+    h[total - tail:] = 0xC3
+    want = nat.oracle_batch(h, offs)
+    t = torch.from_numpy(h).cuda()
+    d_offs = torch.from_numpy(offs.view(np.int64)).cuda()
+    for shift in (0, 1, 7):
+        buf = torch.zeros(t.numel() + 32, dtype=torch.uint8, device="cuda")
+        buf[shift:shift + t.numel()] = t
+        got = u8.validate_lookup_batch(buf[shift:shift + t.numel()], d_offs)
+        assert np.array_equal(got, want), (n_rec, shift, np.nonzero(got != want)[0][:10])
+    assert np.array_equal(u8.validate_lookup_batch(h, offs), want)
