@@ -767,3 +767,51 @@ def test_batch_few_large_records(n_rec, torch):
         got = u8.validate_lookup_batch(buf[shift:shift + t.numel()], d_offs)
         assert np.array_equal(got, want), (n_rec, shift, np.nonzero(got != want)[0][:10])
     assert np.array_equal(u8.validate_lookup_batch(h, offs), want)
+
+
+def test_concurrent_callers_mixed_entry_points(torch):
+    """Validators are pure and callable concurrently (the
+    reference bench runs them from several threads, proj/src/bench.cpp:112-118):
+    8 host threads at once, each looping over every entry point -- verdicts
+    on host and device input with and without an error, record batches, a
+    stream session -- on its own data, all checked against the oracle."""
+    import threading
+    base = configs.gen_c1(24 << 20, seed=31).cpu().numpy()
+    cases = []
+    rng = np.random.default_rng(31)
+    for k in range(8):
+        h = base[k << 20: (k << 20) + (16 << 20) + 7 * k].copy()
+        if k % 2:
+            h[int(rng.integers(0, h.size))] = 0xF8
+        exp = nat.oracle_verdict(h, threads=8)
+        cuts = np.sort(rng.choice(np.arange(1, h.size), 300, replace=False)).astype(np.uint64)
+        offs = np.concatenate([[0], cuts, [h.size]]).astype(np.uint64)
+        cases.append((h, exp, offs, nat.oracle_batch(h, offs)))
+    errors = []
+
+    def work(k):
+        try:
+            h, exp, offs, want = cases[k]
+            d = torch.from_numpy(h).cuda()
+            d_offs = torch.from_numpy(offs.view(np.int64)).cuda()
+            for it in range(4):
+                for src in (h, d):
+                    v = u8.validate_lookup_verdict(src)
+                    got = (v.valid(), None if v.valid() else (v.error.offset, int(v.error.kind)))
+                    assert got == (exp[0], None if exp[0] else (exp[1], exp[2])), (k, it)
+                    assert u8.validate_lookup(src) is exp[0]
+                assert np.array_equal(u8.validate_lookup_batch(h, offs), want)
+                assert np.array_equal(u8.validate_lookup_batch(d, d_offs), want)
+                with u8.LookupStream() as s:
+                    for a in range(0, h.size, 5 << 20):
+                        s.feed(h[a:a + (5 << 20)])
+                    assert s.finish() is exp[0]
+        except Exception as e:  # noqa: BLE001 -- reported below
+            errors.append(repr(e))
+
+    ts = [threading.Thread(target=work, args=(k,)) for k in range(8)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors[:3]
