@@ -75,8 +75,31 @@ def test_malformed_device_offsets_stay_in_bounds():
                                                        b.n_records, buf.data_ptr(), None, st))
         torch.cuda.synchronize()
         assert int(buf[-1].item()) == 0xAB, mutate
+    # the few-large-records kernel (K2L: <= 2048 records of >= 64 KiB on
+    # average) with the same mutations and with offsets that are pure noise
+    d = configs.gen_c1(16 << 20, seed=7)
+    n = d.numel()
+    good = torch.from_numpy((np.arange(65, dtype=np.int64) * (n // 64))).cuda()
+    rng = np.random.default_rng(3)
+    for mutate in ("past_end", "non_monotonic", "last_before_first", "noise"):
+        offs = good.clone()
+        if mutate == "past_end":
+            offs[-1] = n + (1 << 24)
+        elif mutate == "non_monotonic":
+            offs[5] = n - 3
+        elif mutate == "last_before_first":
+            offs[-1] = 0
+            offs[0] = 100
+        else:
+            offs = torch.from_numpy(rng.integers(0, 2 * n, 65).astype(np.int64)).cuda()
+        buf = torch.full((65,), 0xAB, dtype=torch.uint8, device="cuda")
+        _lib.check(lib.utf8v_cuda_validate_batch_async(d.data_ptr(), n, offs.data_ptr(), 64, buf.data_ptr(),
+                                                       None, st))
+        torch.cuda.synchronize()
+        assert int(buf[-1].item()) == 0xAB, mutate
     # the library still validates correctly afterwards
     assert (np.asarray(u8.validate_lookup_batch(b.data, b.d_offsets)) == b.expected).all()
+    assert np.asarray(u8.validate_lookup_batch(d, good)).all()
 
 
 def test_python_sharded_wrapper():
