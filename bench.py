@@ -475,8 +475,10 @@ def _time_device_flushed(fn, reps: int, stream, dev) -> float:
 
 def measure_extras(lib, dev, reps: int) -> dict:
     """The other BASELINE configs at N=1 (not the headline): C0 GB/s, C2/C3
-    records/s through the batch kernel (K2), C4's 16 GiB stream through K1 and
-    its three variants' verdicts + first-error offsets (K3)."""
+    records/s through the batch kernels (K2L for C2's 64 large segments, K2 for
+    C3), C4's 16 GiB stream through K1 and its three variants' verdicts +
+    first-error offsets (K3).  roofline_frac: algorithmic GB/s over the
+    measured HBM peak; traffic: ncu DRAM bytes per launch (profiles/)."""
     import torch
 
     from paper_2010_03090_b200 import _lib, configs
@@ -505,9 +507,13 @@ def measure_extras(lib, dev, reps: int) -> dict:
         ms = _time_device_flushed(fn, reps, st, dev) if small else _time_device(fn, reps, st)
         got = ver.cpu().numpy()
         alg = b.nbytes + 8 * (b.n_records + 1) + b.n_records
+        kernel = "k_batch_large" if name == "c2" else "k_batch"  # launch_batch's dispatch (kernels.cuh)
+        peak = measured_peaks()["hbm_gbs"]
         out[name] = {"records_per_s": b.n_records / (ms / 1e3), "GBps": alg / ms / 1e6, "ms": ms,
                      "records": b.n_records, "bytes": b.nbytes, "invalid_records": int((got == 0).sum()),
-                     "verdicts_match_expected": bool((got == b.expected).all()), "l2_flushed": small}
+                     "verdicts_match_expected": bool((got == b.expected).all()), "l2_flushed": small,
+                     "kernel": f"u8v::{kernel}", "algorithmic_bytes": alg,
+                     "roofline_frac": alg / ms / 1e6 / peak, "traffic": ncu_traffic(kernel)}
         del b, ver
         torch.cuda.empty_cache()
 

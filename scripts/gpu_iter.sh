@@ -10,5 +10,5 @@ SMALL="python bench.py --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 1"
 timeout 600 $SMALL > gpurun_out/bench_small.json 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $SMALL > gpurun_out/ncu_launch.log 2>&1; echo ncu_launches=$?
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_validate -s 8 -c 1 -o gpurun_out/prof_k_validate -f $SMALL > gpurun_out/ncu_full.log 2>&1; echo ncu_k1=$?
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_batch -s 3 -c 1 -o gpurun_out/prof_k_batch -f $SMALL > gpurun_out/ncu_full_batch.log 2>&1; echo ncu_k2=$?
+timeout 900 ncu --set full --clock-control none --import-source on -k k_batch -s 3 -c 1 -o gpurun_out/prof_k_batch -f $SMALL > gpurun_out/ncu_full_batch.log 2>&1; echo ncu_k2=$?
 fi
