@@ -22,6 +22,8 @@
 // The decomposition is proven against per-record validation on the CPU
 // (tests/test_swar.py::test_k2_*).  Verdicts start at 1 (memset by the
 // caller) and invalid records get a plain 0 store (idempotent, no atomics).
+// Batches of few, large records (C2) go to K2L instead (validate.cu,
+// launch_batch_large): K1's own sweep needs no record cursor there.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -421,7 +423,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
 }  // namespace u8v
 
 // Launcher used by capi.cu.  Fully asynchronous: the kernel reads the first
-// and last offsets itself; the grid is sized from the data size n.
+// and last offsets itself; the grid is sized from the data size n.  K2L
+// takes the batch when it has <= kLargeMaxRecords records of >= 64 KiB on
+// average (known here from n and n_records).
 namespace u8v {
 void launch_batch(const uint8_t* data, uint64_t n, const uint64_t* d_offsets, uint64_t n_records,
                   uint8_t* d_verdicts, cudaStream_t st) {
