@@ -172,6 +172,7 @@ __device__ __noinline__ void attribute_step(RecView d, int64_t s0, int64_t hi, u
 struct WarpCtx {
   int64_t lo, hi, c_end, range_lo, rb;
   int prev_last, range_rel;
+  int taken;  // a batch sits in the slot (starts rb-32 .. rb-1)
 };
 
 struct BatchSlot {
@@ -260,11 +261,12 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
   const int nsteps = (int)(step_end - step0);
 
   constexpr int kStepBytes = kStepChunks * kChunkBytes;
-  // A batch of 32 starts runs once the sweep passes its last start.  Its
-  // oldest starts are ~6 steps back by then and some of their sectors have
-  // left L2 (~6 % extra DRAM reads on C3); triggering at start 15 halves that
-  // but stalls on DRAM reads ahead of the sweep (-1.6 %, measured).
-  constexpr int kTrigger = 31;
+  // A batch of 32 starts is taken once the sweep passes its 16th start: its
+  // bytes are copied asynchronously (no stall), the older half from L2, the
+  // newer half from DRAM just ahead of the sweep, which then finds them in
+  // L2.  Taking it at its last start left the oldest sectors ~6 steps back,
+  // partly evicted: 0.210 -> 0.206 ms on C3 (tools/k2bench.py).
+  constexpr int kTrigger = 15;
   // Loop state is kept 32-bit and relative (positions to range_lo, records
   // to r_in) so it stays in registers across the chunk math.
   const int64_t range_lo = (d.c_begin + step0 * kStepChunks) * kChunkBytes;
@@ -306,6 +308,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
   cx->range_lo = range_lo;
   cx->rb = rb;
   cx->prev_last = prev_last;
+  cx->taken = 0;
   cx->range_rel = range_rel;
   bool pend = false;
   bool was_ascii = true;
@@ -377,11 +380,27 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
         // the taken batch's last start (< s0, else that batch would not have
         // been taken) followed by the next batch's first 31.
         const int s0 = j * kStepBytes;
-        const int up = __shfl_up_sync(0xFFFFFFFFu, nx, 1);
         const int64_t rbc = cx->rb;
-        const bool first = rbc == 0;
-        const int o = (first ? nx : (lane == 0 ? cx->prev_last : up)) - s0;
-        attribute_step(rv, cx->range_lo + s0, cx->hi, err[0], err[1], err[2], err[3], o, first ? 0 : rbc - 1);
+        int o;
+        int64_t r0;
+        if (cx->taken) {
+          // The taken batch T (starts rbc-32 ..) and the next one (nx) are
+          // consecutive: the window is T[k ..] then nx, k = T's last start
+          // <= s0 (T[kTrigger] < s0: T was taken at an earlier step's end).
+          const int tv = sl->o[lane];
+          const unsigned le = __ballot_sync(0xFFFFFFFFu, tv <= s0);
+          const int k = 31 - __clz(le);
+          const int src = lane + k;
+          const int a = __shfl_sync(0xFFFFFFFFu, tv, src & 31);
+          const int b = __shfl_sync(0xFFFFFFFFu, nx, (src - 32) & 31);
+          o = (src < 32 ? a : b) - s0;
+          r0 = rbc - 32 + k;
+        } else {
+          const int up = __shfl_up_sync(0xFFFFFFFFu, nx, 1);
+          o = (rbc == 0 ? nx : (lane == 0 ? cx->prev_last : up)) - s0;
+          r0 = rbc == 0 ? 0 : rbc - 1;
+        }
+        attribute_step(rv, cx->range_lo + s0, cx->hi, err[0], err[1], err[2], err[3], o, r0);
       }
     }
     if (lane == 31) carry_word = v[kU - 1].w[kChunkWords - 1];
@@ -398,6 +417,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
         if (pend) check_batch(rv, sl, nx, rbc - 32, cx->range_rel, d.k);
         take_batch(sl, d.base, cx->lo, cx->hi, cx->range_lo, nx, cx->prev_last, cx->range_rel);
         pend = true;
+        cx->taken = 1;
         cx->prev_last = __shfl_sync(0xFFFFFFFFu, nx, 31);
         cx->rb = rbc + 32;
         nx = rel32(rec_start(rv, rbc + 32 + lane), cx->range_lo);
