@@ -100,7 +100,7 @@ __device__ __forceinline__ int rel32(int64_t pos, int64_t s0) {
 // lanes or lies past the data (those lanes are settled by fix_boundary).
 // e0..e3: lane bits of chunk (lane + 32 i) of the step in the permuted plane
 // order of utf8v_bits.h (bit pos(i) = byte i).
-__device__ __noinline__ void attribute_step(RecView d, int64_t s0, int64_t hi, uint32_t e0, uint32_t e1,
+__device__ __forceinline__ void attribute_step(RecView d, int64_t s0, int64_t hi, uint32_t e0, uint32_t e1,
                                             uint32_t e2, uint32_t e3, int o, int64_t r0) {
   const int lane = threadIdx.x & 31;
   const bool full = __all_sync(0xFFFFFFFFu, o < kStepChunks * kChunkBytes);
