@@ -323,11 +323,12 @@ __global__ void k_locate_step(StreamDesc d, uint64_t n, const unsigned long long
 // the record's first three lanes or lies past the data, plus one boundary
 // check per record start.  With few records (launch_batch dispatches here
 // for <= kLargeMaxRecords records of >= 64 KiB on average) the sweep is K1's
-// own round-robin loop with no record cursor: a flagged step (rare -- at
-// most a few per invalid record, none inside a record already known
-// invalid) is recomputed out of line in natural lane order and each flagged
-// lane finds its record by binary search over the offsets held in shared
-// memory.
+// own round-robin loop with no record cursor; the interior loop breaks out
+// at a flagged step (rare: a few per invalid record), which is attributed
+// out of the loop, so the loop keeps K1's registers.  A flagged lane whose
+// four chunks lie inside one record settles that record directly; the
+// others recompute the step in natural lane order and find each flagged
+// lane's record by binary search over the offsets held in shared memory.
 
 // Largest r in [-1, N] with s_off[r] <= q (s_off[-1] = -inf).
 __device__ __forceinline__ int rec_of(const int64_t* s_off, int N, int64_t q) {
@@ -340,8 +341,8 @@ __device__ __forceinline__ int rec_of(const int64_t* s_off, int N, int64_t q) {
   return a;
 }
 
-__device__ __forceinline__ void attribute_large(const StreamDesc& d, int64_t cstep, uint32_t e_or, const int64_t* s_off,
-                                             int N, uint8_t* verdicts) {
+__device__ __forceinline__ void attribute_large(const StreamDesc& d, int64_t cstep, uint32_t e_or,
+                                                const int64_t* s_off, int N, uint8_t* verdicts) {
   const int lane = threadIdx.x & 31;
   const int64_t sb = kStepChunks * (int64_t)kChunkBytes;
   const int64_t s0 = cstep * kChunkBytes;
