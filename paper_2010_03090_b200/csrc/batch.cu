@@ -281,14 +281,6 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
   // A batch is correct whenever it is checked (verdicts only go 1 -> 0).
   // The same registers give the attribution window: start(rb - 1) (the
   // taken batch's last start, before the current step) followed by nx.
-  {  // the first steps' bytes travel while the record search below waits on offsets
-    const uint8_t* q = d.base + range_lo + lane * kChunkBytes;
-    const int npf = nsteps < 2 ? nsteps : 2;
-    for (int j = 0; j < npf; ++j)
-#pragma unroll
-      for (int i = 0; i < kU; ++i)
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(q + j * kStepBytes + 32 * i * kChunkBytes));
-  }
   const int64_t r_in = find_record(rv, range_lo - 1);  // last start before the range (or 0)
   const int64_t s_in = rec_start(rv, r_in);
   int64_t rb = r_in + (s_in < range_lo ? 1 : 0);
