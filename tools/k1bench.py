@@ -1,5 +1,5 @@
 """DEVELOPMENT HARNESS: K1 on the 1 GiB C1 stream, several library variants
-(tools/k2var.sh-style builds) timed interleaved, medians.
+(tools/kvar.sh builds) timed interleaved, medians.
 `python tools/k1bench.py reps lib.so [lib.so ...]`"""
 import ctypes as C
 import os

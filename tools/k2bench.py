@@ -1,6 +1,6 @@
 """DEVELOPMENT HARNESS: time (and, under ncu, profile) the batch kernel K2 on
 C2 and C3 alone.  `python tools/k2bench.py [c2|c3|both] [reps] [lib.so ...]`
-(several library variants from tools/k2var.sh: timed interleaved, medians)."""
+(several library variants from tools/kvar.sh: timed interleaved, medians)."""
 import os
 import ctypes as C
 import sys
