@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
         const uint32_t next = __shfl_sync(0xFFFFFFFFu, dn, (lane + 1) & 31);
         uint32_t hi7 = 0;
         err[i] = u8v_chunk_errors_planes_perm_k(v[i].w, prev, next, d.k, &hi7);
-        h7 |= hi7;
+        if (i == kU - 1) h7 = hi7;  // the step's last KiB predicts the next step (K1)
         any |= err[i];
       }
       was_ascii = __all_sync(0xFFFFFFFFu, h7 == 0);
