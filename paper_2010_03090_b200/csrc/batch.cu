@@ -340,7 +340,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
     if (j >= jb && j < jd) {
 #pragma unroll
       for (int i = 0; i < kU; ++i) v[i] = ld_chunk(p + 32 * i * kChunkBytes);
-      if (lane == 0) nsw = __ldg(reinterpret_cast<const uint32_t*>(p + kStepBytes));
+      ld_word_if(lane == 0, p + kStepBytes, nsw);
     } else {
       const int64_t lo = cx->lo, hi = cx->hi, c_end = cx->c_end;
       const int64_t cstep = (cx->range_lo + (int64_t)j * kStepBytes) / kChunkBytes;

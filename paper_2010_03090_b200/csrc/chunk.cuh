@@ -26,6 +26,15 @@ __device__ __forceinline__ Chunk ld_chunk(const uint8_t* p) {
   return c;
 }
 
+// w = the 32-bit word at p when pred, else w unchanged: one predicated LDG
+// (the halo and lookahead words of a step are loaded by one lane each; an
+// `if` there compiles to a branch with convergence barriers).
+__device__ __forceinline__ void ld_word_if(bool pred, const uint8_t* p, uint32_t& w) {
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.global.nc.u32 %0, [%1];\n\t}"
+      : "+r"(w)
+      : "l"(p), "r"((unsigned)pred));
+}
+
 __device__ __forceinline__ Chunk zero_chunk() {
   Chunk r;
 #pragma unroll

@@ -132,8 +132,8 @@ __device__ __forceinline__ uint32_t any_step_errors(const StreamDesc& d, int64_t
     const uint8_t* p = d.base + s0 + lane * kChunkBytes;
 #pragma unroll
     for (int i = 0; i < kU; ++i) v[i] = ld_chunk(p + 32 * i * kChunkBytes);
-    if (lane == 31) carry_word = __ldg(reinterpret_cast<const uint32_t*>(d.base + s0 - 4));
-    if (lane == 0) nsw = __ldg(reinterpret_cast<const uint32_t*>(d.base + s0 + sb));
+    ld_word_if(lane == 31, d.base + s0 - 4, carry_word);
+    ld_word_if(lane == 0, d.base + s0 + sb, nsw);
     return step_errors<kPos, false>(d, v, cstep, lane, carry_word, nsw, first_i, was_ascii);
   }
 #pragma unroll
@@ -185,8 +185,8 @@ __device__ __forceinline__ void sweep(const StreamDesc& d, uint32_t* __restrict_
 #pragma unroll
         for (int i = 0; i < kU; ++i) v[i] = ld_chunk(p + (lane + 32 * i) * kChunkBytes);
         uint32_t carry_word = 0, nsw = 0;
-        if (lane == 31) carry_word = __ldg(reinterpret_cast<const uint32_t*>(p - 4));
-        if (lane == 0) nsw = __ldg(reinterpret_cast<const uint32_t*>(p + sb));
+        ld_word_if(lane == 31, p - 4, carry_word);
+        ld_word_if(lane == 0, p + sb, nsw);
         const uint32_t e = step_errors<false, false>(d, v, 0, lane, carry_word, nsw, unused, was_ascii);
         acc |= e;
         if (kTrack && e != 0u && !noted) {
@@ -458,8 +458,8 @@ __global__ void __launch_bounds__(kThreads, 4)
 #pragma unroll
         for (int i = 0; i < kU; ++i) v[i] = ld_chunk(p + (lane + 32 * i) * kChunkBytes);
         uint32_t carry_word = 0, nsw = 0;
-        if (lane == 31) carry_word = __ldg(reinterpret_cast<const uint32_t*>(p - 4));
-        if (lane == 0) nsw = __ldg(reinterpret_cast<const uint32_t*>(p + sb));
+        ld_word_if(lane == 31, p - 4, carry_word);
+        ld_word_if(lane == 0, p + sb, nsw);
         e = step_errors<false, false>(d, v, 0, lane, carry_word, nsw, unused, was_ascii);
         if (__any_sync(0xFFFFFFFFu, e != 0u)) break;
       }
