@@ -98,6 +98,55 @@ __device__ __forceinline__ uint32_t step_errors(const StreamDesc& d, const Chunk
   return step_err;
 }
 
+// Interior steps of K1's sweep use a paired chunk layout: lane L holds
+// chunks 2L, 2L+1, 64+2L, 64+2L+1 of the step (v[0..3]).  The odd chunks take
+// their halo word, and the even ones their lookahead word, from the same
+// lane; the rest come by one rotate-shuffle each: 4 SHFL + 4 SEL per step
+// instead of 8 + 8 (+1.7 % on C1, tools/k1bench.py).  Each load instruction
+// then covers 16 half-used 128-byte lines instead of 8 full ones; the step's
+// four instructions still read every sector once.  Lane flags do not depend
+// on the layout, so edge steps, K3's recompute and the batch kernels keep
+// the one-chunk-per-lane layout of step_errors.
+__device__ __forceinline__ uint32_t step_errors_pairs(const StreamDesc& d, const Chunk (&v)[kU], int lane,
+                                                      uint32_t carry_word, uint32_t nsw, bool& was_ascii) {
+  const uint32_t up0 = lane == 31 ? carry_word : v[1].w[kChunkWords - 1];
+  const uint32_t up2 = lane == 31 ? v[1].w[kChunkWords - 1] : v[3].w[kChunkWords - 1];
+  const uint32_t p0 = __shfl_sync(0xFFFFFFFFu, up0, (lane + 31) & 31);
+  const uint32_t p2 = __shfl_sync(0xFFFFFFFFu, up2, (lane + 31) & 31);
+  const uint32_t prev[kU] = {p0, v[0].w[kChunkWords - 1], p2, v[2].w[kChunkWords - 1]};
+  bool all_ascii = false;
+  if (was_ascii) {
+    uint32_t hibits = 0;
+#pragma unroll
+    for (int i = 0; i < kU; ++i) hibits |= chunk_hibits(v[i]);
+    all_ascii = __all_sync(0xFFFFFFFFu, (hibits & U8V_B7) == 0);
+  }
+  uint32_t step_err = 0;
+  if (all_ascii) {
+#pragma unroll
+    for (int i = 0; i < kU; ++i) {
+      u8v_carry cr = u8v_carry_of(prev[i]);
+      step_err |= u8v_ascii_word_errors(v[i].w[0], &cr) & U8V_B7;
+    }
+  } else {
+    const uint32_t dn1 = lane == 0 ? v[2].w[0] : v[0].w[0];
+    const uint32_t dn3 = lane == 0 ? nsw : v[2].w[0];
+    const uint32_t n1 = __shfl_sync(0xFFFFFFFFu, dn1, (lane + 1) & 31);
+    const uint32_t n3 = __shfl_sync(0xFFFFFFFFu, dn3, (lane + 1) & 31);
+    const uint32_t next[kU] = {v[1].w[0], n1, v[3].w[0], n3};
+    uint32_t h7 = 0;
+#pragma unroll
+    for (int i = 0; i < kU; ++i) {
+      uint32_t hi7;
+      step_err |= u8v_chunk_errors_planes_perm_k(v[i].w, prev[i], next[i], d.k, &hi7);
+      if (i == kU - 1) h7 = hi7;
+    }
+    all_ascii = __all_sync(0xFFFFFFFFu, h7 == 0);
+  }
+  was_ascii = all_ascii;
+  return step_err;
+}
+
 // Interior steps (all bytes real, all lanes wanted, lookahead word in range)
 // form one contiguous run [*int_b, *int_d) of step indices; only the
 // head/tail steps take masked loads.
@@ -183,11 +232,11 @@ __device__ __forceinline__ void sweep(const StreamDesc& d, uint32_t* __restrict_
       for (int j = 0; j < n; ++j, p += stride) {
         Chunk v[kU];
 #pragma unroll
-        for (int i = 0; i < kU; ++i) v[i] = ld_chunk(p + (lane + 32 * i) * kChunkBytes);
+        for (int i = 0; i < kU; ++i) v[i] = ld_chunk(p + ((i >> 1) * 64 + 2 * lane + (i & 1)) * kChunkBytes);
         uint32_t carry_word = 0, nsw = 0;
         ld_word_if(lane == 31, p - 4, carry_word);
         ld_word_if(lane == 0, p + sb, nsw);
-        const uint32_t e = step_errors<false, false>(d, v, 0, lane, carry_word, nsw, unused, was_ascii);
+        const uint32_t e = step_errors_pairs(d, v, lane, carry_word, nsw, was_ascii);
         acc |= e;
         if (kTrack && e != 0u && !noted) {
           noted = true;
