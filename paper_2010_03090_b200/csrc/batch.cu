@@ -130,7 +130,8 @@ __device__ __forceinline__ void attribute_step(RecView d, int64_t s0, int64_t hi
   static_assert(kU == 4, "attribute_step takes one mask per chunk of a step");
   // One flagged lane per lane and round, lowest chunk first.
   while (__any_sync(0xFFFFFFFFu, (e0 | e1 | e2 | e3) != 0u)) {
-    int q = -1, c = lane;
+    // chunks of lane L in the paired layout: 2L, 2L+1, 64+2L, 64+2L+1
+    int q = -1, c = 2 * lane;
     uint32_t e = 0;
     if (e0) {
       e = e0;
@@ -138,7 +139,7 @@ __device__ __forceinline__ void attribute_step(RecView d, int64_t s0, int64_t hi
     } else if (e1) {
       e = e1;
       e1 &= e1 - 1;
-      c += 32;
+      c += 1;
     } else if (e2) {
       e = e2;
       e2 &= e2 - 1;
@@ -146,7 +147,7 @@ __device__ __forceinline__ void attribute_step(RecView d, int64_t s0, int64_t hi
     } else if (e3) {
       e = e3;
       e3 &= e3 - 1;
-      c += 96;
+      c += 65;
     }
     if (e) q = c * kChunkBytes + (int)u8v_perm_byte((unsigned)(__ffs(e) - 1));
     int L = 0;
@@ -339,19 +340,26 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
     uint32_t nsw = 0;
     if (j >= jb && j < jd) {
 #pragma unroll
-      for (int i = 0; i < kU; ++i) v[i] = ld_chunk(p + 32 * i * kChunkBytes);
+      for (int i = 0; i < kU; ++i) v[i] = ld_chunk(p + ((i >> 1) * 64 + (i & 1) + lane) * kChunkBytes);
       ld_word_if(lane == 0, p + kStepBytes, nsw);
     } else {
       const int64_t lo = cx->lo, hi = cx->hi, c_end = cx->c_end;
       const int64_t cstep = (cx->range_lo + (int64_t)j * kStepBytes) / kChunkBytes;
 #pragma unroll
       for (int i = 0; i < kU; ++i) {
-        const int64_t c = cstep + lane + 32 * i;
+        const int64_t c = cstep + (i >> 1) * 64 + 2 * lane + (i & 1);
         v[i] = c <= c_end ? ld_chunk_masked(d.base, c, lo, hi) : zero_chunk();
       }
       if (lane == 0) nsw = ld_word_guarded(d.base, (cstep + kStepChunks) * kChunkBytes, lo, hi);
     }
 
+    // Paired layout (K1's interior steps): lane L holds chunks 2L, 2L+1,
+    // 64+2L, 64+2L+1; the odd chunks' halo words and the even chunks'
+    // lookahead words come from the lane itself.
+    const uint32_t up0 = lane == 31 ? carry_word : v[1].w[kChunkWords - 1];
+    const uint32_t up2 = lane == 31 ? v[1].w[kChunkWords - 1] : v[3].w[kChunkWords - 1];
+    const uint32_t prev[kU] = {__shfl_sync(0xFFFFFFFFu, up0, (lane + 31) & 31), v[0].w[kChunkWords - 1],
+                               __shfl_sync(0xFFFFFFFFu, up2, (lane + 31) & 31), v[2].w[kChunkWords - 1]};
     // Unbounded lane flags (K1's chunk form).  ASCII fast path (voted only
     // after an all-ASCII step): a step of bytes < 0x80 only needs the
     // pending incomplete check of the bytes before each chunk; if that
@@ -366,9 +374,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
         uint32_t ae = 0;
 #pragma unroll
         for (int i = 0; i < kU; ++i) {
-          const uint32_t up =
-              lane == 31 ? (i == 0 ? carry_word : v[i - 1].w[kChunkWords - 1]) : v[i].w[kChunkWords - 1];
-          u8v_carry cr = u8v_carry_of(__shfl_sync(0xFFFFFFFFu, up, (lane + 31) & 31));
+          u8v_carry cr = u8v_carry_of(prev[i]);
           ae |= u8v_ascii_word_errors(v[i].w[0], &cr) & U8V_B7;
         }
         all_ascii = !__any_sync(0xFFFFFFFFu, ae != 0u);
@@ -377,14 +383,14 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
     if (!all_ascii) {
       uint32_t h7 = 0, err[kU], any = 0;
 #pragma unroll
+      const uint32_t dn1 = lane == 0 ? v[2].w[0] : v[0].w[0];
+      const uint32_t dn3 = lane == 0 ? nsw : v[2].w[0];
+      const uint32_t n1 = __shfl_sync(0xFFFFFFFFu, dn1, (lane + 1) & 31);
+      const uint32_t n3 = __shfl_sync(0xFFFFFFFFu, dn3, (lane + 1) & 31);
+      const uint32_t next[kU] = {v[1].w[0], n1, v[3].w[0], n3};
       for (int i = 0; i < kU; ++i) {
-        const uint32_t up =
-            lane == 31 ? (i == 0 ? carry_word : v[i - 1].w[kChunkWords - 1]) : v[i].w[kChunkWords - 1];
-        const uint32_t prev = __shfl_sync(0xFFFFFFFFu, up, (lane + 31) & 31);
-        const uint32_t dn = lane == 0 ? (i + 1 < kU ? v[i + 1].w[0] : nsw) : v[i].w[0];
-        const uint32_t next = __shfl_sync(0xFFFFFFFFu, dn, (lane + 1) & 31);
         uint32_t hi7 = 0;
-        err[i] = u8v_chunk_errors_planes_perm_k(v[i].w, prev, next, d.k, &hi7);
+        err[i] = u8v_chunk_errors_planes_perm_k(v[i].w, prev[i], next[i], d.k, &hi7);
         if (i == kU - 1) h7 = hi7;  // the step's last KiB predicts the next step (K1)
         any |= err[i];
       }
