@@ -467,6 +467,12 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
 // takes the batch when it has <= kLargeMaxRecords records of >= 64 KiB on
 // average (known here from n and n_records).
 namespace u8v {
+int batch_blocks_per_sm() {
+  int b = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_batch, kThreads, 0) != cudaSuccess) cudaGetLastError();
+  return b < 1 ? 1 : b;
+}
+
 void launch_batch(const uint8_t* data, uint64_t n, const uint64_t* d_offsets, uint64_t n_records,
                   uint8_t* d_verdicts, cudaStream_t st) {
   if (n_records == 0 || n == 0) return;
@@ -482,15 +488,7 @@ void launch_batch(const uint8_t* data, uint64_t n, const uint64_t* d_offsets, ui
   d.k = u8v_make_consts();
   d.lo = d.hi = d.c_begin = d.c_end = d.steps = d.steps_per_warp = 0;  // set by the kernel
   const int64_t max_steps = ((int64_t)n + d.off32 + 2 * kChunkBytes) / (kStepChunks * kChunkBytes) + 1;
-  static int resident = 0;  // K2's own resident warps (its occupancy may differ from K1's)
-  if (resident == 0) {
-    int dev = 0, sms = 0, blocks = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_batch, kThreads, 0);
-    resident = sms * (blocks < 1 ? 1 : blocks) * (kThreads / 32);
-  }
-  int64_t warps = resident;
+  int64_t warps = k2_resident_warps();
   if (warps > max_steps) warps = max_steps;
   const int64_t blocks = (warps * 32 + kThreads - 1) / kThreads;
   k_batch<<<(unsigned)blocks, kThreads, 0, st>>>(d);

@@ -7,7 +7,9 @@
 
 namespace u8v {
 
-constexpr int kThreads = 256;              // 8 warps per CTA
+constexpr int kThreads = 256;              // K2/K2L: 8 warps per CTA
+constexpr int kK1Threads = 1024;           // K1: one 32-warp CTA per SM
+constexpr int kK1Warps = kK1Threads / 32;
 // K1/K3 (validate.cu) and K2 (batch.cu): 32-byte lane chunks, one 256-bit
 // LDG each; a warp step is 4 chunks per lane.
 constexpr int kChunkBytes = 32;
@@ -25,7 +27,6 @@ struct StreamDesc {
   int64_t L0, L1;          // lanes evaluated: [L0, L1) relative to base
   int64_t c_begin, c_end;  // chunks evaluated: [c_begin, c_end)
   int64_t steps;           // ceil((c_end - c_begin) / kStepChunks)
-  int64_t steps_per_warp;
   u8v_consts k;  // runtime multipliers (FMA-pipe routing, utf8v_swar.h)
   uint32_t* session;  // non-null: K1's first thread also runs the stream-session
                       // edge of this piece (stream_edge.cuh) on session[0..1]
@@ -33,7 +34,10 @@ struct StreamDesc {
                                    // there (atomicMin of the step's first chunk)
 };
 
-int max_resident_warps();
+// Resident K2 warps on the current device (cached per device).
+int k2_resident_warps();
+// batch.cu: k_batch's resident CTAs per SM (occupancy query).
+int batch_blocks_per_sm();
 StreamDesc make_desc(const uint8_t* p, uint64_t n, uint64_t lane_lo, uint64_t lane_hi);
 void launch_validate(const StreamDesc& d, uint32_t* flag, cudaStream_t st);
 // A stream-session piece (d.session set, d.steps > 0) on the session's own

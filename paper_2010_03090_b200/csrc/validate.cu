@@ -28,6 +28,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
+
 #include "chunk.cuh"
 #include "kernels.cuh"
 #include "stream_edge.cuh"
@@ -195,15 +197,23 @@ __device__ __forceinline__ uint32_t any_step_errors(const StreamDesc& d, int64_t
   return step_errors<kPos, true>(d, v, cstep, lane, carry_word, nsw, first_i, was_ascii);
 }
 
-// K1.  Steps are dealt to warps round-robin (step = warp + j * nwarps): at
-// any moment all warps sweep one window of ~nwarps * 4 KiB, which keeps DRAM
-// pages open (+2.5% over contiguous per-warp ranges, tools/kbench.cu V19).
-// Steps are therefore independent: each loads its own halo word (lane 31,
-// the word before the step) and lookahead word (lane 0, the word after).
-// A lane's first flagged step: the chunk index of the step's first chunk
-// goes to *first_step (atomicMin, one elected lane of those that saw it).
-// Warps sweep their steps in increasing order, so the minimum over lanes and
-// warps is the step holding the stream's first flagged chunk.
+// K1.  One CTA of kK1Threads (32 warps) per SM; CTA c owns the steps
+// c, c + G, c + 2G, ... (G = grid size), so at any moment the grid sweeps one
+// window of ~G x 32 x 4 KiB, which keeps DRAM pages open.  Inside the CTA the
+// warps take those steps from a shared-memory ticket counter: warp w starts
+// with the CTA's step w, then each ticket t is the CTA's step 32 + t.  The
+// SM's warp scheduler favours older warps strongly (with four static 8-warp
+// CTAs per SM the oldest finished its equal share at 100 us of a 172 us C1
+// launch, the youngest at 169 us; scripts/probes/k1_timeline.py), so static
+// shares leave the SM running on a few warps for the last ~15 % of a launch;
+// with the shared pool every warp of the SM stays busy until the pool is dry.
+// A warp asks for its next ticket when it starts a step, so the shared
+// atomic's latency hides behind the step.
+// Each warp's steps increase, so a lane's first flagged step is recorded
+// once (kTrack): the chunk index of the step's first chunk goes to
+// *first_step (atomicMin, one elected lane of those that saw it), and the
+// minimum over lanes and warps is the step holding the stream's first
+// flagged chunk.
 __device__ __forceinline__ void note_first_step(unsigned long long* first_step, int64_t cstep) {
   const unsigned m = __activemask();
   if ((int)(threadIdx.x & 31) == __ffs(m) - 1) atomicMin(first_step, (unsigned long long)cstep);
@@ -211,72 +221,97 @@ __device__ __forceinline__ void note_first_step(unsigned long long* first_step, 
 
 template <bool kTrack>
 __device__ __forceinline__ void sweep(const StreamDesc& d, uint32_t* __restrict__ flag) {
+  __shared__ unsigned s_ticket;
+  if (threadIdx.x == 0) s_ticket = 0;
+  __syncthreads();
   const int lane = threadIdx.x & 31;
-  const int64_t warp = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * kThreads) >> 5;
   const int64_t sb = kStepChunks * (int64_t)kChunkBytes;
   int64_t int_b, int_d;
   interior_steps(d, &int_b, &int_d);
+  // Step indices fit 32 bits (make_desc: fewer than 2^31 steps, 8 TiB).
+  const unsigned G = gridDim.x, nsteps = (unsigned)d.steps;
+  const unsigned ib = (unsigned)int_b, id = (unsigned)int_d;
+  const uint8_t* const base = d.base + d.c_begin * kChunkBytes;
 
   uint32_t acc = 0;
   bool was_ascii = true;  // try the vote on the first step
   bool noted = false;     // kTrack: this lane has recorded its first flagged step
   int unused = kU;
-  for (int64_t step = warp; step < d.steps; step += nwarps) {
-    if (step >= int_b && step < int_d) {
-      // Hot loop over this warp's interior steps: a pointer advanced by
-      // nwarps steps and a 32-bit trip count keep the state in registers.
-      const int n = (int)((int_d - 1 - step) / nwarps) + 1;
-      const int64_t stride = nwarps * sb;
-      const uint8_t* p = d.base + (d.c_begin + step * kStepChunks) * kChunkBytes;
-      for (int j = 0; j < n; ++j, p += stride) {
-        Chunk v[kU];
+  unsigned step = blockIdx.x + G * (threadIdx.x >> 5);
+  unsigned next = 0;
+  if (step < nsteps && lane == 0) next = atomicAdd(&s_ticket, 1u);
+  while (step < nsteps) {
+    uint32_t e;
+    if (step >= ib && step < id) {
+      const uint8_t* p = base + (int64_t)step * sb;
+      Chunk v[kU];
 #pragma unroll
-        for (int i = 0; i < kU; ++i) v[i] = ld_chunk(p + ((i >> 1) * 64 + 2 * lane + (i & 1)) * kChunkBytes);
-        uint32_t carry_word = 0, nsw = 0;
-        ld_word_if(lane == 31, p - 4, carry_word);
-        ld_word_if(lane == 0, p + sb, nsw);
-        const uint32_t e = step_errors_pairs(d, v, lane, carry_word, nsw, was_ascii);
-        acc |= e;
-        if (kTrack && e != 0u && !noted) {
-          noted = true;
-          note_first_step(d.first_step, (int64_t)((p - d.base) / kChunkBytes));
-        }
-      }
-      step += (int64_t)(n - 1) * nwarps;
-      continue;
+      for (int i = 0; i < kU; ++i) v[i] = ld_chunk(p + ((i >> 1) * 64 + 2 * lane + (i & 1)) * kChunkBytes);
+      uint32_t carry_word = 0, nsw = 0;
+      ld_word_if(lane == 31, p - 4, carry_word);
+      ld_word_if(lane == 0, p + sb, nsw);
+      e = step_errors_pairs(d, v, lane, carry_word, nsw, was_ascii);
+    } else {
+      e = any_step_errors<false>(d, step, false, lane, unused, was_ascii);
     }
-    const uint32_t e = any_step_errors<false>(d, step, false, lane, unused, was_ascii);
     acc |= e;
     if (kTrack && e != 0u && !noted) {
       noted = true;
-      note_first_step(d.first_step, d.c_begin + step * kStepChunks);
+      note_first_step(d.first_step, d.c_begin + (int64_t)step * kStepChunks);
     }
+    const unsigned t = __shfl_sync(0xFFFFFFFFu, next, 0);
+    step = blockIdx.x + G * (kK1Warps + t);
+    if (step < nsteps && lane == 0) next = atomicAdd(&s_ticket, 1u);
   }
   const unsigned any = __reduce_or_sync(0xFFFFFFFFu, acc);
   if (lane == 0 && any) atomicOr(flag, 1u);
 }
 
-__global__ void __launch_bounds__(kThreads, 4) k_validate(StreamDesc d, uint32_t* __restrict__ flag) {
+#ifdef U8V_TIMELINE
+// DEVELOPMENT (tools/kvar.sh builds only): per-warp start/end %globaltimer
+// and SM id of K1, to measure the launch ramp and the drain.
+__device__ unsigned long long* g_timeline;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
+
+__global__ void __launch_bounds__(kK1Threads, 1) k_validate(StreamDesc d, uint32_t* __restrict__ flag) {
+#ifdef U8V_TIMELINE
+  const unsigned long long t_start = gtimer();
+#endif
+  // Dependents (a following K1 launched with PDL, see launch_k1) may start
+  // as soon as every CTA of this grid has started.
+  asm volatile("griddepcontrol.launch_dependents;");
   if (d.session != nullptr) {
-    // Session feeds are launched with programmatic stream serialization
-    // (launch_validate_piece): the next piece's grid may start as soon as
-    // every block of this one has started, and only the edge thread, which
-    // reads the carry the previous feed wrote, waits for that feed.
-    asm volatile("griddepcontrol.launch_dependents;");
+    // A session feed: only the edge thread, which reads the carry the
+    // previous feed wrote, waits for that feed.
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       asm volatile("griddepcontrol.wait;" ::: "memory");
       stream_edge_piece(d.session, d.base + d.off32, (uint64_t)(d.hi - d.lo), 0);
     }
   }
   sweep<false>(d, flag);
+#ifdef U8V_TIMELINE
+  if ((threadIdx.x & 31) == 0 && g_timeline != nullptr) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    const int64_t w = ((int64_t)blockIdx.x * kK1Threads + threadIdx.x) >> 5;
+    g_timeline[3 * w] = t_start;
+    g_timeline[3 * w + 1] = gtimer();
+    g_timeline[3 * w + 2] = smid;
+  }
+#endif
 }
 
 // K1 for the verdict path: also records the first flagged step
 // (d.first_step), so an invalid stream needs no second pass -- k_locate_step
 // recomputes that one step and decodes the window around its first flagged
 // chunk.
-__global__ void __launch_bounds__(kThreads, 4) k_validate_track(StreamDesc d, uint32_t* __restrict__ flag) {
+__global__ void __launch_bounds__(kK1Threads, 1) k_validate_track(StreamDesc d, uint32_t* __restrict__ flag) {
+  asm volatile("griddepcontrol.launch_dependents;");
   sweep<true>(d, flag);
 }
 
@@ -532,18 +567,43 @@ __global__ void __launch_bounds__(kThreads, 4)
 // ---- host-side launchers (called by capi.cu) ------------------------------
 namespace u8v {
 
-int max_resident_warps() {
-  static int warps = 0;
-  if (warps == 0) {
-    int dev = 0, sms = 0, blocks = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_validate, kThreads, 0);
-    if (blocks < 1) blocks = 1;
-    warps = sms * blocks * (kThreads / 32);
-  }
-  return warps;
+// Grid sizes from each kernel's occupancy, per device (queried once per
+// device, thread-safe: ShardPool workers on different devices launch at the
+// same time).
+namespace {
+struct DevInfo {
+  int k1_ctas = 1;    // resident K1 CTAs (kK1Threads each) on the device
+  int k2l_warps = 1;  // resident K2L warps
+  int k2_warps = 1;   // resident K2 warps (batch.cu)
+};
+constexpr int kMaxDev = 64;
+DevInfo g_info[kMaxDev];
+std::once_flag g_info_once[kMaxDev];
+}  // namespace
+
+static int blocks_per_sm(const void* fn, int threads, size_t smem) {
+  int b = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, threads, smem) != cudaSuccess) cudaGetLastError();
+  return b < 1 ? 1 : b;
 }
+
+static const DevInfo& dev_info() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDev) dev = 0;
+  std::call_once(g_info_once[dev], [dev] {
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms < 1) sms = 1;
+    DevInfo& i = g_info[dev];
+    i.k1_ctas = sms * blocks_per_sm((const void*)k_validate, kK1Threads, 0);
+    i.k2l_warps = sms * blocks_per_sm((const void*)k_batch_large, kThreads, 0) * (kThreads / 32);
+    i.k2_warps = sms * batch_blocks_per_sm() * (kThreads / 32);
+  });
+  return g_info[dev];
+}
+
+int k2_resident_warps() { return dev_info().k2_warps; }
 
 StreamDesc make_desc(const uint8_t* p, uint64_t n, uint64_t lane_lo, uint64_t lane_hi) {
   // Stream coordinates: byte i of the stream is p[i]; lanes [lane_lo,
@@ -563,37 +623,50 @@ StreamDesc make_desc(const uint8_t* p, uint64_t n, uint64_t lane_lo, uint64_t la
   d.c_end = (d.L1 + kChunkBytes - 1) / kChunkBytes;
   const int64_t chunks = d.c_end - d.c_begin;
   d.steps = (chunks + kStepChunks - 1) / kStepChunks;
-  int64_t warps = max_resident_warps();
-  if (warps > d.steps) warps = d.steps;
-  if (warps < 1) warps = 1;
-  d.steps_per_warp = (d.steps + warps - 1) / warps;
   d.session = nullptr;
   d.first_step = nullptr;
   return d;
 }
 
-void launch_validate(const StreamDesc& d, uint32_t* flag, cudaStream_t st) {
-  if (d.steps <= 0) return;
-  const int64_t warps = (d.steps + d.steps_per_warp - 1) / d.steps_per_warp;
-  const int64_t blocks = (warps * 32 + kThreads - 1) / kThreads;
-  if (d.first_step)
-    k_validate_track<<<(unsigned)blocks, kThreads, 0, st>>>(d, flag);
-  else
-    k_validate<<<(unsigned)blocks, kThreads, 0, st>>>(d, flag);
+// K1 grid: one CTA per SM, fewer for inputs of fewer steps (every CTA gets
+// at least one step).
+static unsigned k1_grid(const StreamDesc& d) {
+  int64_t g = dev_info().k1_ctas;
+  if (g > d.steps) g = d.steps;
+  return (unsigned)(g < 1 ? 1 : g);
 }
 
-void launch_validate_piece(const StreamDesc& d, uint32_t* flag, cudaStream_t st) {
-  const int64_t warps = (d.steps + d.steps_per_warp - 1) / d.steps_per_warp;
+// Every K1 launch allows programmatic stream serialization (PDL), and every
+// K1 grid triggers its dependents on entry: when K1 follows K1 on a stream,
+// the next grid's CTAs take each SM as soon as the previous grid's CTA there
+// retires, so one launch's ramp overlaps the other's drain.  This is safe
+// because K1 consumes nothing a preceding K1 produces (both only OR into
+// flags / atomicMin positions), and any other predecessor (a kernel that does
+// not trigger early, a copy, a memset, an event wait) is waited for in full;
+// by induction every K1 starts after the last non-K1 work before it on the
+// stream has completed.  Successors that read K1's results are not launched
+// with PDL and wait for it in full.
+static void launch_k1(void (*kernel)(StreamDesc, uint32_t*), const StreamDesc& d, uint32_t* flag,
+                      cudaStream_t st) {
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)((warps * 32 + kThreads - 1) / kThreads));
-  cfg.blockDim = dim3(kThreads);
+  cfg.gridDim = dim3(k1_grid(d));
+  cfg.blockDim = dim3(kK1Threads);
   cfg.stream = st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, k_validate, d, flag);
+  cudaLaunchKernelEx(&cfg, kernel, d, flag);
+}
+
+void launch_validate(const StreamDesc& d, uint32_t* flag, cudaStream_t st) {
+  if (d.steps <= 0) return;
+  launch_k1(d.first_step ? k_validate_track : k_validate, d, flag, st);
+}
+
+void launch_validate_piece(const StreamDesc& d, uint32_t* flag, cudaStream_t st) {
+  launch_k1(k_validate, d, flag, st);
 }
 
 bool launch_batch_large(const uint8_t* data, uint64_t n, const uint64_t* d_offsets, uint64_t n_records,
@@ -602,7 +675,11 @@ bool launch_batch_large(const uint8_t* data, uint64_t n, const uint64_t* d_offse
   // Lanes [0, n) of the data buffer: lanes past offsets[N] are ignored and
   // the last record's end is settled by the boundary check at offsets[N].
   const StreamDesc d = make_desc(data, n, 0, n);
-  const int64_t warps = (d.steps + d.steps_per_warp - 1) / d.steps_per_warp;
+  int64_t warps = dev_info().k2l_warps;
+  if (warps > d.steps) warps = d.steps;
+  if (warps < 1) warps = 1;
+  const int64_t spw = (d.steps + warps - 1) / warps;
+  warps = (d.steps + spw - 1) / spw;
   int64_t blocks = (warps * 32 + kThreads - 1) / kThreads;
   const int64_t need = ((int64_t)n_records + kThreads) / kThreads;  // boundary threads: N + 1
   if (blocks < need) blocks = need;
@@ -610,6 +687,12 @@ bool launch_batch_large(const uint8_t* data, uint64_t n, const uint64_t* d_offse
   k_batch_large<<<(unsigned)blocks, kThreads, smem, st>>>(d, d_offsets, (int)n_records, d_verdicts);
   return true;
 }
+
+#ifdef U8V_TIMELINE
+extern "C" int u8v_timeline_set(unsigned long long* p) {
+  return (int)cudaMemcpyToSymbol(g_timeline, &p, sizeof(p));
+}
+#endif
 
 void launch_locate(const StreamDesc& d, uint64_t n, const unsigned long long* first_step,
                    unsigned long long* out_offset, int* out_kind, cudaStream_t st) {
