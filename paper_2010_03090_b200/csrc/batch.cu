@@ -33,6 +33,17 @@
 
 namespace u8v {
 
+// CTA shape of K2: one 32-warp CTA per SM.  With four 8-warp CTAs per SM
+// the warp scheduler's preference for older CTAs left the youngest CTA's
+// equal share running alone at the end of the launch (as for K1,
+// scripts/probes/k1_timeline.py); one CTA per SM keeps the warps in step:
+// C3 0.200 -> 0.179 ms (tools/k2bench.py; 512 threads: 0.189).
+#ifndef U8V_K2_THREADS
+#define U8V_K2_THREADS 1024
+#endif
+constexpr int kK2Threads = U8V_K2_THREADS;
+constexpr int kK2Blocks = 1024 / kK2Threads;
+
 struct BatchDesc {
   const uint8_t* base;   // 32-aligned; data byte i is base[off32 + i]
   const uint64_t* offsets;
@@ -258,10 +269,10 @@ __device__ __forceinline__ void check_batch(const RecView& rv, BatchSlot* sl, in
   __syncwarp();  // the slot is refilled next
 }
 
-__global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
+__global__ void __launch_bounds__(kK2Threads, kK2Blocks) k_batch(BatchDesc d) {
   const int lane = threadIdx.x & 31;
-  const int64_t warp = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * kThreads) >> 5;
+  const int64_t warp = ((int64_t)blockIdx.x * kK2Threads + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * kK2Threads) >> 5;
   // The byte range comes from the offsets themselves (read here, so the
   // launch needs no host round trip).  Malformed offsets are clamped to the
   // data: the kernel never reads outside [0, n).
@@ -310,12 +321,12 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
   int nx = rel32(rec_start(rv, rb + lane), range_lo);
   int prev_last = rb > r_in ? rel32(s_in, range_lo) : -kFar;  // start(rb - 1); rb == r_in only at rb = 0
   const int range_rel = nsteps * kStepBytes;
-  __shared__ BatchSlot slots[kThreads / 32];
+  __shared__ BatchSlot slots[kK2Threads / 32];
   BatchSlot* const sl = &slots[threadIdx.x >> 5];
   // Warp-uniform state the sweep does not touch each step lives in shared
   // memory (every lane writes the same value), so the hot loop's registers
   // hold only the chunk math and its cursor (no spills).
-  __shared__ WarpCtx ctxs[kThreads / 32];
+  __shared__ WarpCtx ctxs[kK2Threads / 32];
   volatile WarpCtx* const cx = &ctxs[threadIdx.x >> 5];
   cx->lo = d.lo;
   cx->hi = d.hi;
@@ -382,12 +393,12 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
     }
     if (!all_ascii) {
       uint32_t h7 = 0, err[kU], any = 0;
-#pragma unroll
       const uint32_t dn1 = lane == 0 ? v[2].w[0] : v[0].w[0];
       const uint32_t dn3 = lane == 0 ? nsw : v[2].w[0];
       const uint32_t n1 = __shfl_sync(0xFFFFFFFFu, dn1, (lane + 1) & 31);
       const uint32_t n3 = __shfl_sync(0xFFFFFFFFu, dn3, (lane + 1) & 31);
       const uint32_t next[kU] = {v[1].w[0], n1, v[3].w[0], n3};
+#pragma unroll
       for (int i = 0; i < kU; ++i) {
         uint32_t hi7 = 0;
         err[i] = u8v_chunk_errors_planes_perm_k(v[i].w, prev[i], next[i], d.k, &hi7);
@@ -467,9 +478,11 @@ __global__ void __launch_bounds__(kThreads, 4) k_batch(BatchDesc d) {
 // takes the batch when it has <= kLargeMaxRecords records of >= 64 KiB on
 // average (known here from n and n_records).
 namespace u8v {
+int batch_threads() { return kK2Threads; }
+
 int batch_blocks_per_sm() {
   int b = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_batch, kThreads, 0) != cudaSuccess) cudaGetLastError();
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_batch, kK2Threads, 0) != cudaSuccess) cudaGetLastError();
   return b < 1 ? 1 : b;
 }
 
@@ -490,7 +503,7 @@ void launch_batch(const uint8_t* data, uint64_t n, const uint64_t* d_offsets, ui
   const int64_t max_steps = ((int64_t)n + d.off32 + 2 * kChunkBytes) / (kStepChunks * kChunkBytes) + 1;
   int64_t warps = k2_resident_warps();
   if (warps > max_steps) warps = max_steps;
-  const int64_t blocks = (warps * 32 + kThreads - 1) / kThreads;
-  k_batch<<<(unsigned)blocks, kThreads, 0, st>>>(d);
+  const int64_t blocks = (warps * 32 + kK2Threads - 1) / kK2Threads;
+  k_batch<<<(unsigned)blocks, kK2Threads, 0, st>>>(d);
 }
 }  // namespace u8v

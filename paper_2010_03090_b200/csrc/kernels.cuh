@@ -38,6 +38,7 @@ struct StreamDesc {
 int k2_resident_warps();
 // batch.cu: k_batch's resident CTAs per SM (occupancy query).
 int batch_blocks_per_sm();
+int batch_threads();
 StreamDesc make_desc(const uint8_t* p, uint64_t n, uint64_t lane_lo, uint64_t lane_hi);
 void launch_validate(const StreamDesc& d, uint32_t* flag, cudaStream_t st);
 // A stream-session piece (d.session set, d.steps > 0) on the session's own

@@ -573,8 +573,8 @@ namespace u8v {
 namespace {
 struct DevInfo {
   int k1_ctas = 1;    // resident K1 CTAs (kK1Threads each) on the device
-  int k2l_warps = 1;  // resident K2L warps
   int k2_warps = 1;   // resident K2 warps (batch.cu)
+  int k2l_warps = 1;  // resident K2L warps
 };
 constexpr int kMaxDev = 64;
 DevInfo g_info[kMaxDev];
@@ -597,8 +597,8 @@ static const DevInfo& dev_info() {
     if (sms < 1) sms = 1;
     DevInfo& i = g_info[dev];
     i.k1_ctas = sms * blocks_per_sm((const void*)k_validate, kK1Threads, 0);
+    i.k2_warps = sms * batch_blocks_per_sm() * (batch_threads() / 32);
     i.k2l_warps = sms * blocks_per_sm((const void*)k_batch_large, kThreads, 0) * (kThreads / 32);
-    i.k2_warps = sms * batch_blocks_per_sm() * (kThreads / 32);
   });
   return g_info[dev];
 }
