@@ -502,7 +502,7 @@ def measure_extras(lib, dev, reps: int) -> dict:
         b = gen()
         ver = torch.empty(b.n_records, dtype=torch.uint8, device=dev)
         fn = lambda: _lib.check(lib.utf8v_cuda_validate_batch_async(  # noqa: E731
-            b.data.data_ptr(), b.nbytes, b.d_offsets.data_ptr(), b.n_records, ver.data_ptr(), None, sp))
+            b.data.data_ptr(), b.nbytes, b.d_offsets.data_ptr(), b.n_records, ver.data_ptr(), sp))
         small = b.nbytes + 8 * b.n_records < (512 << 20)
         ms = _time_device_flushed(fn, reps, st, dev) if small else _time_device(fn, reps, st)
         got = ver.cpu().numpy()

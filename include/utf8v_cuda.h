@@ -54,7 +54,10 @@ extern "C" {
  *      call to the legacy default stream, like a synchronous cudaMemcpy;
  *      writes made on a non-blocking stream must be synchronised by the
  *      caller
- *   4  utf8v_cuda_validate_verdict_lanes (first error of a shard) */
+ *   4  utf8v_cuda_validate_verdict_lanes (first error of a shard)
+ *   5  multi-GPU combine in the native layer (NCCL comms, P2P flags);
+ *      utf8v_cuda_validate_batch_async lost its unused d_scratch argument
+ *      (utf8v_cuda_batch_scratch_bytes removed) */
 int utf8v_cuda_abi_version(void);
 
 /* Human-readable text of the last error on this thread ("" if none). */
@@ -146,11 +149,9 @@ int utf8v_cuda_validate_sharded(const uint8_t* p, size_t n, int n_gpus, int is_d
  * d_offsets[n_records] <= n; malformed device offsets give unspecified
  * verdicts but never an access outside d_data[0..n) (the synchronous host
  * entry point, utf8v_cuda_validate_batch with is_device = 0, checks them).
- * d_scratch: NULL or >= utf8v_cuda_batch_scratch_bytes(n) device bytes. */
+ * No scratch memory is needed. */
 int utf8v_cuda_validate_batch_async(const uint8_t* d_data, uint64_t n, const uint64_t* d_offsets,
-                                    uint64_t n_records, uint8_t* d_verdicts, void* d_scratch,
-                                    void* stream);
-uint64_t utf8v_cuda_batch_scratch_bytes(uint64_t n);
+                                    uint64_t n_records, uint8_t* d_verdicts, void* stream);
 
 /* ---- streaming: one stream validated in pieces -------------------------
  * The device-side restatement of threading fsm_state through
@@ -169,6 +170,83 @@ int utf8v_cuda_stream_feed(utf8v_cuda_stream* s, const uint8_t* p, size_t n, int
 int utf8v_cuda_stream_finish(utf8v_cuda_stream* s, uint8_t* out_valid);
 uint64_t utf8v_cuda_stream_bytes(const utf8v_cuda_stream* s);
 void utf8v_cuda_stream_destroy(utf8v_cuda_stream* s);
+
+/* ---- multi-GPU combine in the native layer (comm.cu) -------
+ * A stream sharded over ranks (one GPU each) is valid iff no rank's lanes
+ * hold an error: the rank flags combine with one 4-byte allreduce(MAX), the
+ * first error with one 8-byte allreduce(MIN) of offset*8+kind.  The shard
+ * plan (heads, tails, lanes) is sharding.py's; each rank passes its own
+ * bytes and lane range with the contract of utf8v_cuda_validate_lanes.
+ *
+ * NCCL form.  libnccl.so.2 is loaded on first use (dlopen); without it
+ * these entry points return UTF8V_ERR_NCCL, as do NCCL failures.  A comm is
+ * bound to the device current at creation and used by one host thread at a
+ * time. */
+#define UTF8V_COMM_ID_BYTES 128
+typedef struct utf8v_cuda_comm utf8v_cuda_comm;
+
+/* ncclGetUniqueId: rank 0 creates it, the caller's bootstrap (MPI,
+ * torch.distributed, a file) hands the 128 bytes to every rank. */
+int utf8v_cuda_comm_unique_id(uint8_t* out_id);
+/* ncclCommInitRank on the current device (collective over the nranks). */
+int utf8v_cuda_comm_init_rank(const uint8_t* id, int nranks, int rank, utf8v_cuda_comm** out);
+/* One process driving several GPUs (ncclCommInitAll): out_comms[i] is rank
+ * i on devices[i] (devices NULL: 0 .. ndev-1). */
+int utf8v_cuda_comm_init_all(int ndev, const int* devices, utf8v_cuda_comm** out_comms);
+void utf8v_cuda_comm_destroy(utf8v_cuda_comm* c);
+
+/* K1 over this rank's lanes of d_p[0..n) on `stream`, OR-ing into
+ * *d_local_flag (zeroed by the caller), then ncclAllReduce(MAX) of that word
+ * into *d_global_flag on the same stream: once the stream's work completes
+ * every rank's *d_global_flag is 0 iff the whole stream is valid.  No host
+ * synchronisation. */
+int utf8v_cuda_validate_shard_allreduce_async(utf8v_cuda_comm* c, const uint8_t* d_p, uint64_t n,
+                                              uint64_t lane_lo, uint64_t lane_hi, uint32_t* d_local_flag,
+                                              uint32_t* d_global_flag, void* stream);
+/* Synchronous, host (pipelined H2D) or device shard: *out_valid = verdict of
+ * the whole stream, on every rank. */
+int utf8v_cuda_validate_shard_allreduce(utf8v_cuda_comm* c, const uint8_t* p, uint64_t n, uint64_t lane_lo,
+                                        uint64_t lane_hi, int is_device, uint8_t* out_valid);
+/* The whole stream's first error (oracle_validate, proj/src/oracle.cpp:10-44)
+ * on every rank: this rank's utf8v_cuda_validate_verdict_lanes, shifted by
+ * p_stream_offset (the stream offset of p[0]), combined by one 8-byte
+ * allreduce(MIN).  Exact under the conditions stated for
+ * utf8v_cuda_validate_verdict_lanes (sharding.py's 16-byte head, 3-byte tail). */
+int utf8v_cuda_verdict_shard_allreduce(utf8v_cuda_comm* c, const uint8_t* p, uint64_t n, uint64_t lane_lo,
+                                       uint64_t lane_hi, uint64_t p_stream_offset, int is_device,
+                                       uint8_t* out_valid, uint64_t* out_offset, int* out_kind);
+/* One process, device-resident shards on several GPUs: comms from one
+ * utf8v_cuda_comm_init_all; shard g (d_shards[g], shard_bytes[g] bytes, lanes
+ * [lane_lo[g], lane_hi[g])) lives on comms[g]'s device.  K1 on every device,
+ * then one grouped 4-byte ncclAllReduce(MAX); *out_valid = the stream's
+ * verdict. */
+int utf8v_cuda_validate_sharded_device(utf8v_cuda_comm* const* comms, int n_gpus, const uint8_t* const* d_shards,
+                                       const uint64_t* shard_bytes, const uint64_t* lane_lo,
+                                       const uint64_t* lane_hi, uint8_t* out_valid);
+
+/* P2P form: the combine folded into K1.  Every rank owns one flag word; the
+ * words are mapped into every other rank with CUDA IPC (NVLink peer
+ * memory), and a K1 warp that finds an error ORs 1 into all of them -- on
+ * valid input nothing crosses NVLink and no collective is launched.  Each
+ * rank: create (-> its 64-byte IPC handle), gather all ranks' handles with
+ * the bootstrap, connect; then per stream: reset, validate_async, the
+ * caller's barrier after its stream completes, read.  Ranks may share a
+ * GPU (separate processes). */
+#define UTF8V_P2P_HANDLE_BYTES 64
+typedef struct utf8v_cuda_p2p utf8v_cuda_p2p;
+int utf8v_cuda_p2p_create(utf8v_cuda_p2p** out, uint8_t* out_handle);
+/* handles: nranks x UTF8V_P2P_HANDLE_BYTES, rank order. */
+int utf8v_cuda_p2p_connect(utf8v_cuda_p2p* g, const uint8_t* handles, int nranks, int rank);
+/* K1 over this rank's lanes on `stream`; errors reach every rank's word. */
+int utf8v_cuda_p2p_validate_async(utf8v_cuda_p2p* g, const uint8_t* d_p, uint64_t n, uint64_t lane_lo,
+                                  uint64_t lane_hi, void* stream);
+/* This rank's flag word (device pointer). */
+uint32_t* utf8v_cuda_p2p_flag(utf8v_cuda_p2p* g);
+/* Synchronous read / zeroing of this rank's word (0 = no rank saw an error,
+ * once every rank's work has completed). */
+int utf8v_cuda_p2p_read(utf8v_cuda_p2p* g, uint32_t* out_flag);
+int utf8v_cuda_p2p_reset(utf8v_cuda_p2p* g);
+void utf8v_cuda_p2p_destroy(utf8v_cuda_p2p* g);
 
 /* Number of kernel launches the last call on this thread enqueued. */
 int utf8v_cuda_last_launch_count(void);

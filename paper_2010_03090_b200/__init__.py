@@ -243,7 +243,7 @@ def validate_lanes_async(d_ptr: int, n: int, lane_lo: int, lane_hi: int, d_flag_
 
 
 def validate_batch_async(d_data: int, n: int, d_offsets: int, n_records: int, d_verdicts: int, stream: int = 0) -> None:
-    _lib.check(_lib.load().utf8v_cuda_validate_batch_async(d_data, n, d_offsets, n_records, d_verdicts, None, stream))
+    _lib.check(_lib.load().utf8v_cuda_validate_batch_async(d_data, n, d_offsets, n_records, d_verdicts, stream))
 
 
 class LookupStream:

@@ -25,7 +25,7 @@ LIB = PKG / "libutf8v_cuda.so"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC,-O3",
                      f"-I{ROOT / 'include'}", "--expt-relaxed-constexpr"]
-CU_SOURCES = ["validate.cu", "batch.cu", "lanes.cu", "gen.cu", "stream.cu", "capi.cu"]
+CU_SOURCES = ["validate.cu", "batch.cu", "lanes.cu", "gen.cu", "stream.cu", "capi.cu", "comm.cu"]
 CXX_SOURCES = ["lookup.cpp"]
 
 
@@ -65,7 +65,7 @@ def build_cuda(force: bool = False, verbose: bool = False) -> Path:
         for f in [ex.submit(_run, j) for j in jobs]:
             f.result()
     if force or _stale(LIB, objs):
-        _run([nvcc, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcudart"])
+        _run([nvcc, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcudart", "-ldl"])
     if verbose:
         print(f"built {LIB}")
     return LIB

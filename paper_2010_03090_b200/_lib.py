@@ -17,6 +17,8 @@ UTF8V_ERR_ARG = 2
 UTF8V_ERR_NO_DEVICE = 3
 UTF8V_ERR_NCCL = 4
 WIDTH = 64
+COMM_ID_BYTES = 128
+P2P_HANDLE_BYTES = 64
 
 _u8p = C.POINTER(C.c_uint8)
 _u64p = C.POINTER(C.c_uint64)
@@ -43,9 +45,28 @@ SIGNATURES: dict[str, tuple] = {
     "utf8v_cuda_validate_lanes": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int,
                                             C.POINTER(C.c_uint32)]),
     "utf8v_cuda_validate_batch_async": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64,
-                                                  C.c_void_p, C.c_void_p, C.c_void_p]),
-    "utf8v_cuda_batch_scratch_bytes": (C.c_uint64, [C.c_uint64]),
+                                                  C.c_void_p, C.c_void_p]),
     "utf8v_cuda_validate_sharded": (C.c_int, [C.c_void_p, C.c_size_t, C.c_int, C.c_int, _u8p]),
+    "utf8v_cuda_comm_unique_id": (C.c_int, [C.c_void_p]),
+    "utf8v_cuda_comm_init_rank": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
+    "utf8v_cuda_comm_init_all": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p]),
+    "utf8v_cuda_comm_destroy": (None, [C.c_void_p]),
+    "utf8v_cuda_validate_shard_allreduce_async": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64,
+                                                            C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "utf8v_cuda_validate_shard_allreduce": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64,
+                                                      C.c_int, _u8p]),
+    "utf8v_cuda_verdict_shard_allreduce": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64,
+                                                     C.c_uint64, C.c_int, _u8p, _u64p, C.POINTER(C.c_int)]),
+    "utf8v_cuda_validate_sharded_device": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                                                     C.c_void_p, _u8p]),
+    "utf8v_cuda_p2p_create": (C.c_int, [C.POINTER(C.c_void_p), C.c_void_p]),
+    "utf8v_cuda_p2p_connect": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int]),
+    "utf8v_cuda_p2p_validate_async": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64,
+                                                C.c_void_p]),
+    "utf8v_cuda_p2p_flag": (C.c_void_p, [C.c_void_p]),
+    "utf8v_cuda_p2p_read": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint32)]),
+    "utf8v_cuda_p2p_reset": (C.c_int, [C.c_void_p]),
+    "utf8v_cuda_p2p_destroy": (None, [C.c_void_p]),
     "utf8v_cuda_stream_create": (C.c_int, [C.POINTER(C.c_void_p)]),
     "utf8v_cuda_stream_feed": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int]),
     "utf8v_cuda_stream_finish": (C.c_int, [C.c_void_p, _u8p]),

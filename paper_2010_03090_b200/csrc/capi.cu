@@ -16,17 +16,15 @@
 #include <vector>
 
 #include "../../include/utf8v_cuda.h"
+#include "capi_internal.h"
 #include "kernels.cuh"
 
-namespace {
-
-constexpr int kMaxDevices = 64;
-constexpr size_t kPiece = 32ull << 20;  // H2D pipeline piece (multiple of 16)
+namespace u8v_capi {
 
 thread_local std::string t_err;
 thread_local int t_launches = 0;
 
-int fail(int code, const std::string& what, cudaError_t e = cudaSuccess) {
+int fail(int code, const std::string& what, cudaError_t e) {
   t_err = what;
   if (e != cudaSuccess) {
     t_err += ": ";
@@ -35,11 +33,14 @@ int fail(int code, const std::string& what, cudaError_t e = cudaSuccess) {
   return code;
 }
 
-#define CK(call)                                              \
-  do {                                                        \
-    cudaError_t _e = (call);                                  \
-    if (_e != cudaSuccess) return fail(UTF8V_ERR_CUDA, #call, _e); \
-  } while (0)
+}  // namespace u8v_capi
+
+using namespace u8v_capi;
+
+namespace {
+
+constexpr int kMaxDevices = 64;
+constexpr size_t kPiece = 32ull << 20;  // H2D pipeline piece (multiple of 16)
 
 // The reference's eight 2-byte error patterns -> three nibble tables
 // (proj/include/utf8v/tables.hpp:60-99, same construction).
@@ -437,7 +438,7 @@ int validate_host_lanes(Ctx& c, const uint8_t* p, size_t n, uint64_t lane_lo, ui
 
 extern "C" {
 
-int utf8v_cuda_abi_version(void) { return 4; }
+int utf8v_cuda_abi_version(void) { return 5; }
 
 const char* utf8v_cuda_last_error(void) { return t_err.c_str(); }
 
@@ -584,12 +585,8 @@ int utf8v_cuda_validate_lanes(const uint8_t* p, uint64_t n, uint64_t lane_lo, ui
   return UTF8V_OK;
 }
 
-uint64_t utf8v_cuda_batch_scratch_bytes(uint64_t) { return 0; }
-
 int utf8v_cuda_validate_batch_async(const uint8_t* d_data, uint64_t n, const uint64_t* d_offsets,
-                                    uint64_t n_records, uint8_t* d_verdicts, void* d_scratch,
-                                    void* stream) {
-  (void)d_scratch;
+                                    uint64_t n_records, uint8_t* d_verdicts, void* stream) {
   t_launches = 0;
   if (n_records == 0) return UTF8V_OK;
   if (!d_offsets || !d_verdicts) return fail(UTF8V_ERR_ARG, "NULL offsets/verdicts");
@@ -616,7 +613,7 @@ int utf8v_cuda_validate_batch(const uint8_t* data, size_t n, const uint64_t* off
     if (st) return st;
     st = after_legacy(c->s_comp, c->ev_legacy);
     if (st) return st;
-    st = utf8v_cuda_validate_batch_async(data, n, offsets, n_records, verdicts, nullptr, c->s_comp);
+    st = utf8v_cuda_validate_batch_async(data, n, offsets, n_records, verdicts, c->s_comp);
     if (st) return st;
     CK(cudaStreamSynchronize(c->s_comp));
     return UTF8V_OK;

@@ -32,6 +32,9 @@ struct StreamDesc {
                       // edge of this piece (stream_edge.cuh) on session[0..1]
   unsigned long long* first_step;  // non-null: K1 records its first flagged step
                                    // there (atomicMin of the step's first chunk)
+  uint32_t* const* peer_flags;     // n_peers device pointers (other GPUs' flag words,
+  int n_peers;                     // NVLink peer memory): a warp that finds an
+                                   // error also ORs 1 into each (comm.cu, P2P combine)
 };
 
 // Resident K2 warps on the current device (cached per device).

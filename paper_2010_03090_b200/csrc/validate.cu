@@ -264,7 +264,13 @@ __device__ __forceinline__ void sweep(const StreamDesc& d, uint32_t* __restrict_
     if (step < nsteps && lane == 0) next = atomicAdd(&s_ticket, 1u);
   }
   const unsigned any = __reduce_or_sync(0xFFFFFFFFu, acc);
-  if (lane == 0 && any) atomicOr(flag, 1u);
+  if (lane == 0 && any) {
+    atomicOr(flag, 1u);
+    // P2P combine (comm.cu): the error also goes straight to every other
+    // rank's flag word over NVLink, so the 4-byte allreduce(MAX) costs
+    // nothing on valid input.
+    for (int r = 0; r < d.n_peers; ++r) atomicOr(d.peer_flags[r], 1u);
+  }
 }
 
 #ifdef U8V_TIMELINE
@@ -625,6 +631,8 @@ StreamDesc make_desc(const uint8_t* p, uint64_t n, uint64_t lane_lo, uint64_t la
   d.steps = (chunks + kStepChunks - 1) / kStepChunks;
   d.session = nullptr;
   d.first_step = nullptr;
+  d.peer_flags = nullptr;
+  d.n_peers = 0;
   return d;
 }
 

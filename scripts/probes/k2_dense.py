@@ -18,7 +18,7 @@ for median, n_rec in ((32, 16 << 20), (128, 4 << 20), (512, 1 << 20)):
     def run():
         ver.fill_(1)
         _lib.check(lib.utf8v_cuda_validate_batch_async(b.data.data_ptr(), b.nbytes, b.d_offsets.data_ptr(),
-                                                       b.n_records, ver.data_ptr(), None, st.cuda_stream))
+                                                       b.n_records, ver.data_ptr(), st.cuda_stream))
     for _ in range(3):
         run()
     torch.cuda.synchronize()

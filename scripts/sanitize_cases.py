@@ -39,7 +39,7 @@ offs[5] = offs[-1] + 1000        # non-monotonic and past the data
 offs[-1] = offs[-1] + (1 << 20)  # last offset past the data
 vv = torch.empty(b.n_records, dtype=torch.uint8, device="cuda")
 _lib.check(lib.utf8v_cuda_validate_batch_async(b.data.data_ptr(), b.nbytes, offs.data_ptr(), b.n_records,
-                                               vv.data_ptr(), None, st))
+                                               vv.data_ptr(), st))
 torch.cuda.synchronize()
 
 # Streaming session with device pieces, and the sharded entry point.

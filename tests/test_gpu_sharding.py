@@ -72,7 +72,7 @@ def test_malformed_device_offsets_stay_in_bounds():
             offs[0] = 100
         buf = torch.full((b.n_records + 1,), 0xAB, dtype=torch.uint8, device="cuda")
         _lib.check(lib.utf8v_cuda_validate_batch_async(b.data.data_ptr(), b.nbytes, offs.data_ptr(),
-                                                       b.n_records, buf.data_ptr(), None, st))
+                                                       b.n_records, buf.data_ptr(), st))
         torch.cuda.synchronize()
         assert int(buf[-1].item()) == 0xAB, mutate
     # the few-large-records kernel (K2L: <= 2048 records of >= 64 KiB on
@@ -93,8 +93,7 @@ def test_malformed_device_offsets_stay_in_bounds():
         else:
             offs = torch.from_numpy(rng.integers(0, 2 * n, 65).astype(np.int64)).cuda()
         buf = torch.full((65,), 0xAB, dtype=torch.uint8, device="cuda")
-        _lib.check(lib.utf8v_cuda_validate_batch_async(d.data_ptr(), n, offs.data_ptr(), 64, buf.data_ptr(),
-                                                       None, st))
+        _lib.check(lib.utf8v_cuda_validate_batch_async(d.data_ptr(), n, offs.data_ptr(), 64, buf.data_ptr(), st))
         torch.cuda.synchronize()
         assert int(buf[-1].item()) == 0xAB, mutate
     # the library still validates correctly afterwards

@@ -54,7 +54,7 @@ for name, gen in (("c2", configs.gen_c2), ("c3", configs.gen_c3), ("c3v", gen_c3
     def run(v):
         ver.fill_(1)
         _lib.check(v.utf8v_cuda_validate_batch_async(b.data.data_ptr(), b.nbytes, b.d_offsets.data_ptr(),
-                                                     b.n_records, ver.data_ptr(), None, st.cuda_stream))
+                                                     b.n_records, ver.data_ptr(), st.cuda_stream))
 
     for _, v in variants:
         for _ in range(3):
@@ -70,7 +70,7 @@ for name, gen in (("c2", configs.gen_c2), ("c3", configs.gen_c3), ("c3v", gen_c3
             a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(st)
             _lib.check(v.utf8v_cuda_validate_batch_async(b.data.data_ptr(), b.nbytes, b.d_offsets.data_ptr(),
-                                                         b.n_records, ver.data_ptr(), None, st.cuda_stream))
+                                                         b.n_records, ver.data_ptr(), st.cuda_stream))
             z.record(st)
             z.synchronize()
             times[vn].append(a.elapsed_time(z))
