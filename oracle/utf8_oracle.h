@@ -91,6 +91,13 @@ size_t orc_generate_valid(unsigned kinds_mask, size_t target_size, uint64_t seed
 size_t orc_generate_invalid(unsigned kinds_mask, size_t target_size, uint64_t seed,
                             int strategy, uint8_t* out, size_t cap);
 
+/* gen_host.c: the n-byte BASELINE config stream (C0 recipe when ascii_only,
+ * else the C1/C4 mix) of `seed`, byte-identical to csrc/gen.cu. */
+int orc_gen_stream(uint8_t* out, uint64_t n, uint64_t seed, int ascii_only, int threads);
+/* gen_host.c: config 4 (variant 0/1/2 = A/B/C), byte-identical to
+ * utf8v_gen_c4; *err_offset = the first error (~0 for A). */
+int orc_gen_c4(uint8_t* out, uint64_t n, uint64_t seed, int variant, int threads, uint64_t* err_offset);
+
 #ifdef __cplusplus
 }
 #endif

@@ -52,7 +52,26 @@ def oracle() -> C.CDLL:
     L.orc_generate_valid.restype = C.c_size_t
     L.orc_generate_invalid.argtypes = [C.c_uint, C.c_size_t, C.c_uint64, C.c_int, u8p, C.c_size_t]
     L.orc_generate_invalid.restype = C.c_size_t
+    L.orc_gen_stream.argtypes = [u8p, C.c_uint64, C.c_uint64, C.c_int, C.c_int]
+    L.orc_gen_stream.restype = C.c_int
+    L.orc_gen_c4.argtypes = [u8p, C.c_uint64, C.c_uint64, C.c_int, C.c_int, C.POINTER(C.c_uint64)]
+    L.orc_gen_c4.restype = C.c_int
     return L
+
+
+def gen_stream_host(n: int, seed: int, ascii_only: bool = False, threads: int = 4) -> np.ndarray:
+    """The config stream from the oracle's CPU generator (oracle/gen_host.c)."""
+    out = np.empty(n, np.uint8)
+    assert oracle().orc_gen_stream(out.ctypes.data, n, seed, int(ascii_only), threads) == 0
+    return out
+
+
+def gen_c4_host(n: int, seed: int, variant: int, threads: int = 8):
+    """(bytes, first error offset or None) of config 4 (oracle/gen_host.c)."""
+    out = np.empty(n, np.uint8)
+    err = C.c_uint64(0)
+    assert oracle().orc_gen_c4(out.ctypes.data, n, seed, variant, threads, C.byref(err)) == 0
+    return out, (None if err.value == (1 << 64) - 1 else int(err.value))
 
 
 @functools.lru_cache(None)

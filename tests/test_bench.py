@@ -1,0 +1,68 @@
+"""bench.py's launch path and reference arm on the CPU (no GPU needed).
+
+  * `--gpus N` without WORLD_SIZE relaunches itself under
+    torch.distributed.run with N ranks; the line rank 0 prints says
+    n_gpus == N (the driver's SCALE run depends on it).  --dry-run keeps it to
+    the launch path: shard plans + a gloo allreduce, no GPU work.
+  * `--impl reference` builds its input with the oracle's CPU generator and
+    times oracle/_ref only -- the product library is never loaded on that
+    arm -- and prints the same `config` object as our arm.
+"""
+from __future__ import annotations
+
+import json
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def _run(args, timeout=300, env=None):
+    e = dict(os.environ)
+    for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "LOCAL_WORLD_SIZE", "MASTER_ADDR", "MASTER_PORT"):
+        e.pop(k, None)
+    e.update(env or {})
+    e.setdefault("OMP_NUM_THREADS", "1")
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), *args], capture_output=True, text=True,
+                       timeout=timeout, cwd=ROOT, env=e)
+    lines = [json.loads(ln) for ln in r.stdout.splitlines() if ln.startswith("{")]
+    return r, lines
+
+
+@pytest.mark.parametrize("n", [2, 4])
+def test_self_launch_reports_n_gpus(n):
+    r, lines = _run(["--gpus", str(n), "--dry-run", "--dist-backend", "gloo"])
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert len(lines) == 1, (r.stdout, r.stderr[-2000:])
+    line = lines[0]
+    assert line["n_gpus"] == n and line["dry_run"] is True
+    import bench
+    assert line["config"] == bench.make_config("c1", n)
+    assert line["max_shard_bytes"] >= (1 << 30)
+
+
+def test_world_size_must_match_gpus():
+    r, _ = _run(["--gpus", "2", "--dry-run"], env={"WORLD_SIZE": "1", "RANK": "0", "LOCAL_RANK": "0"})
+    assert r.returncode != 0 and "must agree" in (r.stderr + r.stdout)
+
+
+def test_reference_arm_isolated_from_product_library():
+    from tests import _native as nat
+    if nat.ref() is None:
+        pytest.skip("oracle/_ref not built (no reference checkout)")
+    r, lines = _run(["--impl", "reference", "--config", "c0", "--steps", "2", "--warmup", "1"])
+    assert r.returncode == 0, r.stderr[-2000:]
+    (line,) = lines
+    assert line["impl"] == "reference" and line["valid"] is True and line["value"] > 0
+    assert line["native_so_loaded"] == ["oracle/_ref/libutf8v_ref.so"], line["native_so_loaded"]
+    import bench
+    assert line["config"] == bench.make_config("c0", 1)
+    assert line["e2e"]["h2d_bytes_per_step"] == 0
+    # under torchrun only rank 0 prints
+    r, lines = _run(["--impl", "reference", "--config", "c0", "--gpus", "2", "--steps", "1", "--warmup", "1"],
+                    env={"WORLD_SIZE": "2", "RANK": "1", "LOCAL_RANK": "1"})
+    assert r.returncode == 0 and lines == []

@@ -84,7 +84,7 @@ def test_all_pairs_across_the_seam(cuda):
     bad = []
     for b1 in range(0, 256, 1):
         prev[w - 1] = b1
-        for b2 in range(0, 256, 17):  # full b2 sweep below through the batch path
+        for b2 in range(256):  # all 65,536 pairs, one GPU round trip each (as the reference test)
             inp[0] = b2
             out = cuda.classify_lanes(bytes(inp), bytes(prev))[0]
             exp_invalid = bool(nat.oracle().orc_pair_always_invalid(b1, b2))
@@ -521,6 +521,44 @@ def test_c4_structure_scaled(variant):
                                     flag.data_ptr(), 0)
         torch.cuda.synchronize()
         assert (int(flag.item()) == 0) == exp[0]
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("variant", [0, 1, 2])
+def test_c4_full_size_vs_oracle(variant):
+    """C4 at its full 16 GiB, variants A/B/C: the device verdict and first
+    error (K1 tracking + K3) equal the multi-threaded CPU oracle's
+    (oracle_validate, proj/src/oracle.cpp:10-44) on the same bytes, copied
+    back from HBM; and the generator's recorded error agrees."""
+    import os
+    import torch
+    n = configs.C4["n"]
+    d, err = configs.gen_c4(n, seed=configs.C4["seed"], variant=variant)
+    v = u8.validate_lookup_verdict(d)
+    host = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    host.copy_(d)
+    del d
+    torch.cuda.empty_cache()
+    h = host.numpy()
+    for k in range(1, 8):  # every k*n/8 edge inside a 3- or 4-byte character
+        assert (h[k * (n // 8)] & 0xC0) == 0x80
+    ok, off, kind = nat.oracle_verdict(h, threads=max(1, len(os.sched_getaffinity(0))))
+    assert ok == (variant == 0) and (ok or off == err)
+    got = (v.valid(), None if v.valid() else (v.error.offset, int(v.error.kind)))
+    assert got == (ok, None if ok else (off, kind)), (got, ok, off, kind)
+
+
+def test_host_generators_equal_device_generators(torch):
+    """oracle/gen_host.c (the reference arm's input) equals the device
+    generators byte for byte: C0/C1 streams and C4 A/B/C (scaled)."""
+    for n, seed, ascii_only in ((1 << 20, 1, True), ((3 << 20) + 5, 2, False), (777_777, 5, False)):
+        dev = configs.gen_stream(n, seed, ascii_only).cpu().numpy()
+        assert np.array_equal(dev, nat.gen_stream_host(n, seed, ascii_only)), (n, seed, ascii_only)
+    n = 64 << 20
+    for variant in (0, 1, 2):
+        d, err = configs.gen_c4(n, seed=5, variant=variant)
+        h, herr = nat.gen_c4_host(n, 5, variant)
+        assert herr == err and np.array_equal(d.cpu().numpy(), h), variant
 
 
 def test_stream_range_generator_matches_full_stream(torch):
