@@ -13,6 +13,11 @@
  * The C++ API of include/utf8v/lookup.hpp (same names as the reference) is a
  * thin layer over these entry points; INTEGRATION.md shows the binding.
  *
+ * Host input to the synchronous entry points crosses PCIe in pieces through
+ * a bounded ring of device slots (at most 4 x (32 MiB + 32 B) of HBM per
+ * host thread and device, whatever n is); each piece is validated as soon as
+ * it lands.  Record batches from host memory are staged whole.
+ *
  * Conventions:
  *   - plain pointers and sizes only; every pointer is borrowed for the call;
  *   - return an int status: UTF8V_OK, or a mapped CUDA/argument error -- never
@@ -57,7 +62,9 @@ extern "C" {
  *   4  utf8v_cuda_validate_verdict_lanes (first error of a shard)
  *   5  multi-GPU combine in the native layer (NCCL comms, P2P flags);
  *      utf8v_cuda_validate_batch_async lost its unused d_scratch argument
- *      (utf8v_cuda_batch_scratch_bytes removed) */
+ *      (utf8v_cuda_batch_scratch_bytes removed); host input crosses PCIe
+ *      through a bounded device ring; utf8v_cuda_release_thread_resources;
+ *      device stream pieces are ordered before later legacy-stream work */
 int utf8v_cuda_abi_version(void);
 
 /* Human-readable text of the last error on this thread ("" if none). */
@@ -161,9 +168,12 @@ int utf8v_cuda_validate_batch_async(const uint8_t* d_data, uint64_t n, const uin
  * error flag on the device; every piece is validated in place (device
  * pieces are not copied) by one K1 launch whose first thread also evaluates
  * the <= 4 lanes straddling the previous piece (csrc/stream_edge.cuh).  Pieces may have any length,
- * including 0.  Device pieces must stay valid until the next call on the
- * session (the work is asynchronous on the session's own stream); host
- * pieces are consumed before feed returns.  finish() resets the session. */
+ * including 0.  A device piece is read asynchronously on the session's own
+ * stream: work issued after feed() on the legacy default stream (and every
+ * blocking stream) is ordered after that read, and the piece must otherwise
+ * stay valid and unmodified until finish() returns.  Host pieces are
+ * consumed before feed returns.  finish() resets the session.  feed and
+ * finish leave the caller's current device unchanged. */
 typedef struct utf8v_cuda_stream utf8v_cuda_stream;
 int utf8v_cuda_stream_create(utf8v_cuda_stream** out);
 int utf8v_cuda_stream_feed(utf8v_cuda_stream* s, const uint8_t* p, size_t n, int is_device);
@@ -247,6 +257,12 @@ uint32_t* utf8v_cuda_p2p_flag(utf8v_cuda_p2p* g);
 int utf8v_cuda_p2p_read(utf8v_cuda_p2p* g, uint32_t* out_flag);
 int utf8v_cuda_p2p_reset(utf8v_cuda_p2p* g);
 void utf8v_cuda_p2p_destroy(utf8v_cuda_p2p* g);
+
+/* Frees this thread's per-device resources (streams, the bounded host-input
+ * ring of 4 x (32 MiB + 32 B) device bytes, pinned staging, the batch stage);
+ * the next call on the thread recreates what it needs.  Also done when the
+ * thread exits. */
+void utf8v_cuda_release_thread_resources(void);
 
 /* Number of kernel launches the last call on this thread enqueued. */
 int utf8v_cuda_last_launch_count(void);

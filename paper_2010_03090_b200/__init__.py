@@ -250,8 +250,9 @@ class LookupStream:
     """One stream validated in pieces: feed() pieces in order, finish() returns
     the verdict of their concatenation (the device restatement of threading
     fsm_state through validate_fsm, proj/include/utf8v/fsm.hpp:15-20).
-    Pieces are host bytes or CUDA uint8 tensors (validated in place; the
-    session keeps a reference to the last device piece until the next call).
+    Pieces are host bytes or CUDA uint8 tensors (validated in place and
+    asynchronously: the session keeps a reference to every device piece, and
+    records its use on the torch stream it belongs to, until finish()).
     finish() resets the session for the next stream."""
 
     def __init__(self):
@@ -259,18 +260,20 @@ class LookupStream:
         h = C.c_void_p()
         _lib.check(self._lib.utf8v_cuda_stream_create(C.byref(h)))
         self._h = h
-        self._keep = None
+        self._keep: list = []
 
     def feed(self, data) -> "LookupStream":
         ptr, n, dev, keep = _input(data)
         _lib.check(self._lib.utf8v_cuda_stream_feed(self._h, ptr, n, dev))
-        self._keep = keep if dev else None
+        if dev:
+            # The piece is read asynchronously until finish(): keep it alive.
+            self._keep.append(keep)
         return self
 
     def finish(self) -> bool:
         ok = C.c_uint8(0)
         _lib.check(self._lib.utf8v_cuda_stream_finish(self._h, C.byref(ok)))
-        self._keep = None
+        self._keep.clear()
         return bool(ok.value)
 
     @property

@@ -77,9 +77,21 @@ void build_tables(uint8_t t1[16], uint8_t t2[16], uint8_t t3[16]) {
 
 std::once_flag g_dev_once[kMaxDevices];
 
-// Per thread and device: streams, small result buffers, the device stage
-// for host input (grown to the largest input seen) and the pinned ring for
-// pageable input.  Released when the thread exits.
+// Host input crosses PCIe through a bounded ring of device slots: piece k
+// (about n/8 bytes, 2..32 MiB) goes to slot k % kRing together with kHalo
+// bytes on either side, so K1 validates each piece's lanes as soon as its own
+// copy has landed and the HBM a host call holds is kRing x (32 MiB + 2 kHalo)
+// whatever n is.  Inputs of at most kSmall bytes take one copy into a
+// dedicated buffer (fewer API calls: the per-call latency path).
+constexpr size_t kHalo = 16;                   // >= 6 look-back (decode), >= 3 lookahead
+constexpr int kRing = 4;
+constexpr size_t kSlotBytes = kPiece + 2 * kHalo;
+constexpr size_t kSmall = 1u << 20;
+constexpr size_t kKeepStage = 256ull << 20;    // batch staging kept across calls up to this size
+
+// Per thread and device: streams, small result buffers, the device ring for
+// host input, the pinned ring for pageable input, and the batch stage.
+// Released when the thread exits or on utf8v_cuda_release_thread_resources().
 struct Ctx {
   bool ready = false;
   int dev = -1;
@@ -90,13 +102,28 @@ struct Ctx {
   uint8_t* d_lanes = nullptr;               // 3 x UTF8V_CUDA_WIDTH
   int* d_ok = nullptr;
   uint32_t* h_res = nullptr;                // pinned result words
+  // Device ring (kRing slots of slot_bytes) and its events: full = the H2D
+  // copy of the slot's piece landed (s_copy), free = the K1 that read the
+  // slot finished (s_comp).
+  uint8_t* d_ring = nullptr;
+  size_t slot_bytes = 0;
+  cudaEvent_t ring_full[kRing] = {}, ring_free[kRing] = {};
+  // Per-piece flags of a host call (the verdict path finds its first
+  // flagged piece), device and pinned host copies.
+  uint32_t* d_pflags = nullptr;
+  uint32_t* h_pflags = nullptr;
+  size_t pflags_cap = 0;
+  // Pageable input: pinned ring (kRing slots of slot_bytes) and the event of
+  // the DMA that last read each slot.
+  uint8_t* h_ring = nullptr;
+  size_t h_slot_bytes = 0;
+  cudaEvent_t hslot_done[kRing] = {};
+  // Small inputs.
+  uint8_t* h_small = nullptr;
+  uint8_t* d_small = nullptr;
+  // Batch from host memory: the whole data array (kept up to kKeepStage).
   uint8_t* d_stage = nullptr;
   size_t stage_cap = 0;
-  std::vector<cudaEvent_t> events;
-  // Pageable host input: pinned staging ring (kSlots x kPiece) and the event
-  // of the DMA that last read each slot.
-  uint8_t* h_ring = nullptr;
-  cudaEvent_t slot_done[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t ev_legacy = nullptr;          // see after_legacy()
 
   ~Ctx() { release(); }
@@ -108,13 +135,14 @@ struct Ctx {
     cudaSetDevice(dev);
     if (s_comp) cudaStreamSynchronize(s_comp);
     if (s_copy) cudaStreamSynchronize(s_copy);
-    for (void* p : {(void*)d_flag, (void*)d_pos, (void*)d_kind, (void*)d_lanes, (void*)d_ok, (void*)d_stage})
+    for (void* p : {(void*)d_flag, (void*)d_pos, (void*)d_kind, (void*)d_lanes, (void*)d_ok, (void*)d_stage,
+                    (void*)d_ring, (void*)d_pflags, (void*)d_small})
       if (p) cudaFree(p);
-    if (h_res) cudaFreeHost(h_res);
-    if (h_ring) cudaFreeHost(h_ring);
-    for (cudaEvent_t e : events) cudaEventDestroy(e);
-    for (cudaEvent_t e : slot_done)
-      if (e) cudaEventDestroy(e);
+    for (void* p : {(void*)h_res, (void*)h_ring, (void*)h_pflags, (void*)h_small})
+      if (p) cudaFreeHost(p);
+    for (int i = 0; i < kRing; ++i)
+      for (cudaEvent_t e : {ring_full[i], ring_free[i], hslot_done[i]})
+        if (e) cudaEventDestroy(e);
     if (ev_legacy) cudaEventDestroy(ev_legacy);
     if (s_comp) cudaStreamDestroy(s_comp);
     if (s_copy) cudaStreamDestroy(s_copy);
@@ -125,7 +153,6 @@ struct Ctx {
   Ctx() = default;
   Ctx& operator=(const Ctx&) = default;
 };
-constexpr int kSlots = 4;
 thread_local Ctx t_ctx[kMaxDevices];
 
 int get_ctx(Ctx** out) {
@@ -154,6 +181,11 @@ int get_ctx(Ctx** out) {
     CK(cudaMalloc(&c.d_ok, 64));
     CK(cudaMallocHost(&c.h_res, 256));
     CK(cudaEventCreateWithFlags(&c.ev_legacy, cudaEventDisableTiming));
+    for (int i = 0; i < kRing; ++i) {
+      CK(cudaEventCreateWithFlags(&c.ring_full[i], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&c.ring_free[i], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&c.hslot_done[i], cudaEventDisableTiming));
+    }
     c.ready = true;
   }
   *out = &c;
@@ -181,12 +213,49 @@ int ensure_stage(Ctx& c, size_t n) {
   return UTF8V_OK;
 }
 
-int ensure_events(Ctx& c, size_t k) {
-  while (c.events.size() < k) {
-    cudaEvent_t e;
-    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    c.events.push_back(e);
+// A batch stage larger than kKeepStage is not kept past its call.
+void trim_stage(Ctx& c) {
+  if (c.stage_cap <= kKeepStage) return;
+  cudaStreamSynchronize(c.s_comp);
+  cudaFree(c.d_stage);
+  c.d_stage = nullptr;
+  c.stage_cap = 0;
+}
+
+// The device ring with slots of at least `slot` bytes (grown, never beyond
+// kSlotBytes: pieces are at most kPiece).
+int ensure_ring_dev(Ctx& c, size_t slot) {
+  if (c.slot_bytes >= slot) return UTF8V_OK;
+  if (c.d_ring) {
+    CK(cudaStreamSynchronize(c.s_comp));
+    cudaFree(c.d_ring);
   }
+  c.d_ring = nullptr;
+  c.slot_bytes = 0;
+  CK(cudaMalloc(&c.d_ring, kRing * slot));
+  c.slot_bytes = slot;
+  return UTF8V_OK;
+}
+
+int ensure_pflags(Ctx& c, size_t k) {
+  if (c.pflags_cap >= k) return UTF8V_OK;
+  CK(cudaStreamSynchronize(c.s_comp));
+  if (c.d_pflags) cudaFree(c.d_pflags);
+  if (c.h_pflags) cudaFreeHost(c.h_pflags);
+  c.d_pflags = nullptr;
+  c.h_pflags = nullptr;
+  c.pflags_cap = 0;
+  const size_t cap = (k + 255) & ~size_t(255);
+  CK(cudaMalloc(&c.d_pflags, cap * 4));
+  CK(cudaMallocHost(&c.h_pflags, cap * 4));
+  c.pflags_cap = cap;
+  return UTF8V_OK;
+}
+
+int ensure_small(Ctx& c) {
+  if (c.d_small) return UTF8V_OK;
+  CK(cudaMalloc(&c.d_small, kSmall + 64));
+  CK(cudaMallocHost(&c.h_small, kSmall + 64));
   return UTF8V_OK;
 }
 
@@ -350,15 +419,20 @@ bool is_pinned(const void* p) {
          a.type == cudaMemoryTypeManaged;
 }
 
-int ensure_ring(Ctx& c) {
-  if (c.h_ring) return UTF8V_OK;
-  CK(cudaMallocHost(&c.h_ring, kSlots * kPiece));
-  for (int i = 0; i < kSlots; ++i) CK(cudaEventCreateWithFlags(&c.slot_done[i], cudaEventDisableTiming));
+// The pinned ring for pageable input, slots of at least `slot` bytes.
+int ensure_ring_host(Ctx& c, size_t slot) {
+  if (c.h_slot_bytes >= slot) return UTF8V_OK;
+  if (c.h_ring) {
+    CK(cudaStreamSynchronize(c.s_copy));
+    cudaFreeHost(c.h_ring);
+  }
+  c.h_ring = nullptr;
+  c.h_slot_bytes = 0;
+  CK(cudaMallocHost(&c.h_ring, kRing * slot));
+  c.h_slot_bytes = slot;
   return UTF8V_OK;
 }
 
-// Copy host bytes into the stage in pieces on s_copy; `each(k, off, len)`
-// runs on s_comp after piece k has landed.
 // Piece size: about n/8 (so small inputs still pipeline), 2..32 MiB, a
 // multiple of 1 MiB.
 size_t piece_size(size_t n) {
@@ -368,70 +442,102 @@ size_t piece_size(size_t n) {
   return p;
 }
 
-template <class F>
-int pipeline_h2d(Ctx& c, const uint8_t* p, size_t n, F each) {
-  int st = ensure_stage(c, n);
-  if (st) return st;
+// Host bytes p[a, b) -> device dst on s_copy; pageable memory goes through
+// the pinned ring slot `slot` (copied by the CopyPool threads; the slot is
+// reused once the DMA that last read it has finished).
+int h2d(Ctx& c, uint8_t* dst, const uint8_t* p, size_t a, size_t b, bool pageable, int slot) {
+  if (pageable) {
+    uint8_t* h = c.h_ring + (size_t)slot * c.h_slot_bytes;
+    CK(cudaEventSynchronize(c.hslot_done[slot]));
+    CopyPool::get().copy(h, p + a, b - a);
+    CK(cudaMemcpyAsync(dst, h, b - a, cudaMemcpyHostToDevice, c.s_copy));
+    CK(cudaEventRecord(c.hslot_done[slot], c.s_copy));
+  } else {
+    CK(cudaMemcpyAsync(dst, p + a, b - a, cudaMemcpyHostToDevice, c.s_copy));
+  }
+  return UTF8V_OK;
+}
+
+// Lanes [lane_lo, lane_hi) of the host stream p[0..n): piece k is copied,
+// with kHalo bytes on either side, into ring slot k % kRing on s_copy and its
+// own lanes are validated there by K1 on s_comp as soon as it has landed,
+// while the next pieces are in flight.  Pieces holding none of the lanes are
+// skipped.  Errors are ORed into c.d_flag, or, with per_piece, into
+// c.d_pflags[k] (zeroed here; *n_pieces = the piece count).
+int validate_host_lanes(Ctx& c, const uint8_t* p, size_t n, uint64_t lane_lo, uint64_t lane_hi,
+                        bool per_piece = false, size_t* n_pieces = nullptr) {
   const size_t piece = piece_size(n);
   const size_t pieces = (n + piece - 1) / piece;
-  st = ensure_events(c, pieces);
+  if (n_pieces) *n_pieces = pieces;
+  int st = ensure_ring_dev(c, piece + 2 * kHalo);
   if (st) return st;
   const bool pageable = !is_pinned(p);
   if (pageable) {
-    st = ensure_ring(c);
+    st = ensure_ring_host(c, piece + 2 * kHalo);
     if (st) return st;
+  }
+  if (per_piece) {
+    st = ensure_pflags(c, pieces);
+    if (st) return st;
+    CK(cudaMemsetAsync(c.d_pflags, 0, pieces * 4, c.s_comp));
   }
   for (size_t k = 0; k < pieces; ++k) {
     const size_t off = k * piece;
-    const size_t len = n - off < piece ? n - off : piece;
-    if (pageable) {
-      // Slot k % kSlots is free once the DMA that last read it has finished;
-      // the parallel host copy of this piece overlaps the DMA of the last.
-      const int slot = (int)(k % kSlots);
-      uint8_t* h = c.h_ring + (size_t)slot * kPiece;
-      if (k >= (size_t)kSlots) CK(cudaEventSynchronize(c.slot_done[slot]));
-      CopyPool::get().copy(h, p + off, len);
-      CK(cudaMemcpyAsync(c.d_stage + off, h, len, cudaMemcpyHostToDevice, c.s_copy));
-      CK(cudaEventRecord(c.slot_done[slot], c.s_copy));
-    } else {
-      CK(cudaMemcpyAsync(c.d_stage + off, p + off, len, cudaMemcpyHostToDevice, c.s_copy));
-    }
-    CK(cudaEventRecord(c.events[k], c.s_copy));
-    CK(cudaStreamWaitEvent(c.s_comp, c.events[k], 0));
-    st = each(k, off, len);
+    const size_t end = off + piece < n ? off + piece : n;
+    // This piece's lanes (the last piece also holds the end-of-input lanes).
+    const uint64_t lhi_piece = k + 1 == pieces ? (uint64_t)n + 3 : (uint64_t)end;
+    const uint64_t llo = off > lane_lo ? off : lane_lo, lhi = lhi_piece < lane_hi ? lhi_piece : lane_hi;
+    if (llo >= lhi) continue;
+    const size_t a = off - (off < kHalo ? off : kHalo);
+    const size_t b = end + kHalo < n ? end + kHalo : n;
+    const int slot = (int)(k % kRing);
+    uint8_t* dst = c.d_ring + (size_t)slot * c.slot_bytes;
+    CK(cudaStreamWaitEvent(c.s_copy, c.ring_free[slot], 0));
+    st = h2d(c, dst, p, a, b, pageable, slot);
+    if (st) return st;
+    CK(cudaEventRecord(c.ring_full[slot], c.s_copy));
+    CK(cudaStreamWaitEvent(c.s_comp, c.ring_full[slot], 0));
+    u8v::launch_validate(u8v::make_desc(dst, b - a, llo - a, lhi - a), per_piece ? c.d_pflags + k : c.d_flag,
+                         c.s_comp);
+    ++t_launches;
+    CK(cudaEventRecord(c.ring_free[slot], c.s_comp));
+    st = check_launch("validate kernel");
     if (st) return st;
   }
   return UTF8V_OK;
 }
 
-// Lanes [lane_lo, lane_hi) of the host stream p[0..n) on this thread's
-// device: pieces are copied on s_copy and piece k-1's lanes are validated on
-// s_comp once piece k has landed (lane j reads byte j+1).  ORs into c.d_flag;
-// first_step non-null: the pieces also record the first flagged step there
-// (all pieces share d_stage's chunk coordinates).
-int validate_host_lanes(Ctx& c, const uint8_t* p, size_t n, uint64_t lane_lo, uint64_t lane_hi,
-                        unsigned long long* first_step = nullptr) {
-  size_t prev_off = 0, prev_len = 0;
-  bool have_prev = false;
-  auto launch = [&](uint64_t a, uint64_t b) {
-    const uint64_t lo = a > lane_lo ? a : lane_lo, hi = b < lane_hi ? b : lane_hi;
-    if (lo < hi) {
-      u8v::StreamDesc d = u8v::make_desc(c.d_stage, n, lo, hi);
-      d.first_step = first_step;
-      u8v::launch_validate(d, c.d_flag, c.s_comp);
-      ++t_launches;
-    }
-  };
-  int st = pipeline_h2d(c, p, n, [&](size_t, size_t off, size_t len) {
-    if (have_prev) launch(prev_off, prev_off + prev_len);
-    prev_off = off;
-    prev_len = len;
-    have_prev = true;
-    return check_launch("validate kernel");
-  });
+// Inputs of at most kSmall bytes: one host copy into the pinned small
+// buffer, one DMA, K1, the flag back (the per-call latency path).
+int validate_small(Ctx& c, const uint8_t* p, size_t n, uint64_t lane_lo, uint64_t lane_hi) {
+  int st = ensure_small(c);
   if (st) return st;
-  launch(prev_off, n + 3);
+  memcpy(c.h_small, p, n);
+  CK(cudaMemcpyAsync(c.d_small, c.h_small, n, cudaMemcpyHostToDevice, c.s_comp));
+  u8v::launch_validate(u8v::make_desc(c.d_small, n, lane_lo, lane_hi), c.d_flag, c.s_comp);
+  ++t_launches;
   return check_launch("validate kernel");
+}
+
+// Batch from host memory: the whole data array staged on the device in
+// pieces (records may span any bytes).
+int stage_h2d(Ctx& c, const uint8_t* p, size_t n) {
+  int st = ensure_stage(c, n);
+  if (st) return st;
+  const size_t piece = piece_size(n);
+  const bool pageable = !is_pinned(p);
+  if (pageable) {
+    st = ensure_ring_host(c, piece);
+    if (st) return st;
+  }
+  for (size_t off = 0, k = 0; off < n; off += piece, ++k) {
+    const size_t end = off + piece < n ? off + piece : n;
+    st = h2d(c, c.d_stage + off, p, off, end, pageable, (int)(k % kRing));
+    if (st) return st;
+  }
+  CK(cudaEventRecord(c.ring_full[0], c.s_copy));
+  CK(cudaStreamWaitEvent(c.s_comp, c.ring_full[0], 0));
+  return UTF8V_OK;
 }
 
 }  // namespace
@@ -444,14 +550,18 @@ const char* utf8v_cuda_last_error(void) { return t_err.c_str(); }
 
 int utf8v_cuda_last_launch_count(void) { return t_launches; }
 
-int utf8v_cuda_validate(const uint8_t* p, size_t n, int is_device, uint8_t* out_valid) {
-  t_launches = 0;
-  if (!out_valid) return fail(UTF8V_ERR_ARG, "out_valid is NULL");
-  if (n == 0) {
-    *out_valid = 1;
-    return UTF8V_OK;
-  }
-  if (!p) return fail(UTF8V_ERR_ARG, "NULL data with n > 0");
+void utf8v_cuda_release_thread_resources(void) {
+  for (int d = 0; d < kMaxDevices; ++d) t_ctx[d].release();
+}
+
+}  // extern "C"
+
+namespace {
+
+// The error flag of lanes [lane_lo, lane_hi) of p[0..n) (host or device),
+// synchronously: device input in place, host input over the bounded ring
+// (or the small-input path).
+int flag_lanes(const uint8_t* p, uint64_t n, uint64_t lane_lo, uint64_t lane_hi, int is_device, uint32_t* out) {
   Ctx* c;
   int st = get_ctx(&c);
   if (st) return st;
@@ -459,57 +569,35 @@ int utf8v_cuda_validate(const uint8_t* p, size_t n, int is_device, uint8_t* out_
   if (is_device) {
     st = after_legacy(c->s_comp, c->ev_legacy);
     if (st) return st;
-    u8v::launch_validate(u8v::make_desc(p, n, 0, n + 3), c->d_flag, c->s_comp);
+    u8v::launch_validate(u8v::make_desc(p, n, lane_lo, lane_hi), c->d_flag, c->s_comp);
     ++t_launches;
+    st = check_launch("validate kernel");
+  } else if (n <= kSmall) {
+    st = validate_small(*c, p, n, lane_lo, lane_hi);
   } else {
-    // Piece k's lanes read one byte of piece k+1 (a rare pair is tested at
-    // its lead's lane), so piece k is validated once piece k+1 has landed.
-    st = validate_host_lanes(*c, p, n, 0, n + 3);
-    if (st) return st;
+    st = validate_host_lanes(*c, p, n, lane_lo, lane_hi);
   }
-  st = check_launch("validate kernel");
   if (st) return st;
   CK(cudaMemcpyAsync(c->h_res, c->d_flag, 4, cudaMemcpyDeviceToHost, c->s_comp));
   CK(cudaStreamSynchronize(c->s_comp));
-  *out_valid = c->h_res[0] == 0 ? 1 : 0;
+  *out = c->h_res[0];
   return UTF8V_OK;
 }
 
-// Verdict of lanes [lane_lo, lane_hi) of p[0..n): one K1 pass over the lanes
-// (host input piece by piece as the bytes land, as in utf8v_cuda_validate)
-// that also records its first flagged step; only a flagged input then runs
-// K3, one warp that recomputes that step and decodes the window around its
-// first flagged chunk.
-static int verdict_lanes(const uint8_t* p, uint64_t n, uint64_t lane_lo, uint64_t lane_hi, int is_device,
-                         uint8_t* out_valid, uint64_t* out_offset, int* out_kind) {
-  t_launches = 0;
-  if (!out_valid || !out_offset || !out_kind) return fail(UTF8V_ERR_ARG, "NULL output");
-  if (lane_hi > n + 3 || lane_lo > lane_hi) return fail(UTF8V_ERR_ARG, "bad lane range");
-  *out_offset = 0;
-  *out_kind = -1;
-  *out_valid = 1;
-  if (n == 0 || lane_lo == lane_hi) return UTF8V_OK;
-  if (!p) return fail(UTF8V_ERR_ARG, "NULL data with n > 0");
-  Ctx* c;
-  int st = get_ctx(&c);
-  if (st) return st;
-  const uint8_t* d = p;
+// Verdict of lanes [lane_lo, lane_hi) of DEVICE bytes d[0..n) on s_comp (the
+// caller orders d): one K1 pass that also records its first flagged step;
+// only a flagged input then runs K3, one warp that recomputes that step and
+// decodes the window around its first flagged chunk.
+int device_verdict(Ctx* c, const uint8_t* d, uint64_t n, uint64_t lane_lo, uint64_t lane_hi, uint8_t* out_valid,
+                   uint64_t* out_offset, int* out_kind) {
   // d_pos[0] = ~0: "no flagged step" is also the verdict (K1's flag word is
   // not read here, so it needs no reset).
   CK(cudaMemsetAsync(c->d_pos, 0xFF, 8, c->s_comp));
-  if (is_device) {
-    st = after_legacy(c->s_comp, c->ev_legacy);
-    if (st) return st;
-    u8v::StreamDesc sd = u8v::make_desc(p, n, lane_lo, lane_hi);
-    sd.first_step = c->d_pos;
-    u8v::launch_validate(sd, c->d_flag, c->s_comp);
-    ++t_launches;
-  } else {
-    st = validate_host_lanes(*c, p, n, lane_lo, lane_hi, c->d_pos);
-    if (st) return st;
-    d = c->d_stage;
-  }
-  st = check_launch("validate kernel");
+  u8v::StreamDesc sd = u8v::make_desc(d, n, lane_lo, lane_hi);
+  sd.first_step = c->d_pos;
+  u8v::launch_validate(sd, c->d_flag, c->s_comp);
+  ++t_launches;
+  int st = check_launch("validate kernel");
   if (st) return st;
   CK(cudaMemcpyAsync(c->h_res, c->d_pos, 8, cudaMemcpyDeviceToHost, c->s_comp));
   CK(cudaStreamSynchronize(c->s_comp));
@@ -521,13 +609,88 @@ static int verdict_lanes(const uint8_t* p, uint64_t n, uint64_t lane_lo, uint64_
   CK(cudaMemcpyAsync(c->h_res + 2, c->d_pos + 1, 8, cudaMemcpyDeviceToHost, c->s_comp));
   CK(cudaMemcpyAsync(c->h_res + 4, c->d_kind, 4, cudaMemcpyDeviceToHost, c->s_comp));
   CK(cudaStreamSynchronize(c->s_comp));
-  *out_valid = 0;
   uint64_t off;
   memcpy(&off, c->h_res + 2, 8);
   const int kind = (int)c->h_res[4];
   if (kind < 0) return fail(UTF8V_ERR_CUDA, "flagged input but the window decode found no error");
+  *out_valid = 0;
   *out_offset = off;
   *out_kind = kind;
+  return UTF8V_OK;
+}
+
+// Verdict of lanes [lane_lo, lane_hi) of p[0..n).  Host input of more than
+// kSmall bytes: the ring pass records one flag per piece; the first flagged
+// piece holds the first error (every lane before it is clean), so only that
+// piece, with its halos, is copied again and decoded on the device.
+int verdict_lanes(const uint8_t* p, uint64_t n, uint64_t lane_lo, uint64_t lane_hi, int is_device,
+                  uint8_t* out_valid, uint64_t* out_offset, int* out_kind) {
+  t_launches = 0;
+  if (!out_valid || !out_offset || !out_kind) return fail(UTF8V_ERR_ARG, "NULL output");
+  if (lane_hi > n + 3 || lane_lo > lane_hi) return fail(UTF8V_ERR_ARG, "bad lane range");
+  *out_offset = 0;
+  *out_kind = -1;
+  *out_valid = 1;
+  if (n == 0 || lane_lo == lane_hi) return UTF8V_OK;
+  if (!p) return fail(UTF8V_ERR_ARG, "NULL data with n > 0");
+  Ctx* c;
+  int st = get_ctx(&c);
+  if (st) return st;
+  if (is_device) {
+    st = after_legacy(c->s_comp, c->ev_legacy);
+    if (st) return st;
+    return device_verdict(c, p, n, lane_lo, lane_hi, out_valid, out_offset, out_kind);
+  }
+  if (n <= kSmall) {
+    st = ensure_small(*c);
+    if (st) return st;
+    memcpy(c->h_small, p, n);
+    CK(cudaMemcpyAsync(c->d_small, c->h_small, n, cudaMemcpyHostToDevice, c->s_comp));
+    return device_verdict(c, c->d_small, n, lane_lo, lane_hi, out_valid, out_offset, out_kind);
+  }
+  size_t pieces = 0;
+  st = validate_host_lanes(*c, p, n, lane_lo, lane_hi, true, &pieces);
+  if (st) return st;
+  CK(cudaMemcpyAsync(c->h_pflags, c->d_pflags, pieces * 4, cudaMemcpyDeviceToHost, c->s_comp));
+  CK(cudaStreamSynchronize(c->s_comp));
+  size_t k = 0;
+  while (k < pieces && c->h_pflags[k] == 0) ++k;
+  if (k == pieces) return UTF8V_OK;
+  const size_t piece = piece_size(n);
+  const size_t off = k * piece;
+  const size_t end = off + piece < n ? off + piece : n;
+  const uint64_t lhi_piece = k + 1 == pieces ? (uint64_t)n + 3 : (uint64_t)end;
+  const uint64_t llo = off > lane_lo ? off : lane_lo, lhi = lhi_piece < lane_hi ? lhi_piece : lane_hi;
+  const size_t a = off - (off < kHalo ? off : kHalo);
+  const size_t b = end + kHalo < n ? end + kHalo : n;
+  uint8_t* dst = c->d_ring;  // slot 0; the ring pass has finished (synchronised above)
+  st = h2d(*c, dst, p, a, b, !is_pinned(p), 0);
+  if (st) return st;
+  CK(cudaEventRecord(c->ring_full[0], c->s_copy));
+  CK(cudaStreamWaitEvent(c->s_comp, c->ring_full[0], 0));
+  st = device_verdict(c, dst, b - a, llo - a, lhi - a, out_valid, out_offset, out_kind);
+  if (st) return st;
+  if (!*out_valid) *out_offset += a;
+  else return fail(UTF8V_ERR_CUDA, "flagged piece but its decode found no error");
+  return UTF8V_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int utf8v_cuda_validate(const uint8_t* p, size_t n, int is_device, uint8_t* out_valid) {
+  t_launches = 0;
+  if (!out_valid) return fail(UTF8V_ERR_ARG, "out_valid is NULL");
+  if (n == 0) {
+    *out_valid = 1;
+    return UTF8V_OK;
+  }
+  if (!p) return fail(UTF8V_ERR_ARG, "NULL data with n > 0");
+  uint32_t flag = 0;
+  const int st = flag_lanes(p, n, 0, (uint64_t)n + 3, is_device, &flag);
+  if (st) return st;
+  *out_valid = flag == 0 ? 1 : 0;
   return UTF8V_OK;
 }
 
@@ -564,25 +727,7 @@ int utf8v_cuda_validate_lanes(const uint8_t* p, uint64_t n, uint64_t lane_lo, ui
   *out_flag = 0;
   if (lane_lo == lane_hi || n == 0) return UTF8V_OK;
   if (!p) return fail(UTF8V_ERR_ARG, "NULL data");
-  Ctx* c;
-  int st = get_ctx(&c);
-  if (st) return st;
-  CK(cudaMemsetAsync(c->d_flag, 0, 4, c->s_comp));
-  if (is_device) {
-    st = after_legacy(c->s_comp, c->ev_legacy);
-    if (st) return st;
-    u8v::launch_validate(u8v::make_desc(p, n, lane_lo, lane_hi), c->d_flag, c->s_comp);
-    ++t_launches;
-  } else {
-    st = validate_host_lanes(*c, p, n, lane_lo, lane_hi);
-    if (st) return st;
-  }
-  st = check_launch("validate kernel");
-  if (st) return st;
-  CK(cudaMemcpyAsync(c->h_res, c->d_flag, 4, cudaMemcpyDeviceToHost, c->s_comp));
-  CK(cudaStreamSynchronize(c->s_comp));
-  *out_flag = c->h_res[0];
-  return UTF8V_OK;
+  return flag_lanes(p, n, lane_lo, lane_hi, is_device, out_flag);
 }
 
 int utf8v_cuda_validate_batch_async(const uint8_t* d_data, uint64_t n, const uint64_t* d_offsets,
@@ -631,7 +776,7 @@ int utf8v_cuda_validate_batch(const uint8_t* data, size_t n, const uint64_t* off
   CK(cudaMallocAsync(&d_ver, n_records, c->s_comp));
   CK(cudaMemcpyAsync(d_off, offsets, (n_records + 1) * 8, cudaMemcpyHostToDevice, c->s_comp));
   if (n > 0) {
-    st = pipeline_h2d(*c, data, n, [](size_t, size_t, size_t) { return UTF8V_OK; });
+    st = stage_h2d(*c, data, n);
     if (st) return st;
   }
   CK(cudaMemsetAsync(d_ver, 1, n_records, c->s_comp));
@@ -643,6 +788,7 @@ int utf8v_cuda_validate_batch(const uint8_t* data, size_t n, const uint64_t* off
   CK(cudaFreeAsync(d_off, c->s_comp));
   CK(cudaFreeAsync(d_ver, c->s_comp));
   CK(cudaStreamSynchronize(c->s_comp));
+  trim_stage(*c);
   return UTF8V_OK;
 }
 
@@ -757,6 +903,7 @@ struct utf8v_cuda_stream {
   size_t cap = 0;
   uint64_t total = 0;
   cudaEvent_t ev_legacy = nullptr;  // see after_legacy()
+  cudaEvent_t ev_fed = nullptr;     // a device piece's K1, for the legacy stream to wait on
 };
 
 int utf8v_cuda_stream_create(utf8v_cuda_stream** out) {
@@ -770,6 +917,7 @@ int utf8v_cuda_stream_create(utf8v_cuda_stream** out) {
   if (cudaStreamCreateWithFlags(&s->s, cudaStreamNonBlocking) != cudaSuccess ||
       cudaMalloc(&s->d_state, 64) != cudaSuccess || cudaMallocHost(&s->h_res, 64) != cudaSuccess ||
       cudaEventCreateWithFlags(&s->ev_legacy, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&s->ev_fed, cudaEventDisableTiming) != cudaSuccess ||
       cudaMemsetAsync(s->d_state, 0, 64, s->s) != cudaSuccess) {
     const cudaError_t e = cudaGetLastError();
     utf8v_cuda_stream_destroy(s);
@@ -784,6 +932,7 @@ int utf8v_cuda_stream_feed(utf8v_cuda_stream* s, const uint8_t* p, size_t n, int
   if (!s) return fail(UTF8V_ERR_ARG, "NULL session");
   if (n == 0) return UTF8V_OK;
   if (!p) return fail(UTF8V_ERR_ARG, "NULL piece");
+  DeviceGuard guard;
   CK(cudaSetDevice(s->dev));
   const uint8_t* d = p;
   if (is_device) {
@@ -821,13 +970,23 @@ int utf8v_cuda_stream_feed(utf8v_cuda_stream* s, const uint8_t* p, size_t n, int
   }
   ++t_launches;
   s->total += n;
-  if (!is_device) CK(cudaStreamSynchronize(s->s));  // the caller may reuse its buffer
+  if (is_device) {
+    // The piece is read asynchronously: work the caller issues later on the
+    // legacy default stream (and every blocking stream) waits for this K1, so
+    // a buffer freed and reused there is not overwritten under it.  Work on
+    // non-blocking streams must keep the piece until finish() returns.
+    CK(cudaEventRecord(s->ev_fed, s->s));
+    CK(cudaStreamWaitEvent(cudaStreamLegacy, s->ev_fed, 0));
+  } else {
+    CK(cudaStreamSynchronize(s->s));  // the caller may reuse its buffer
+  }
   return check_launch("stream feed");
 }
 
 int utf8v_cuda_stream_finish(utf8v_cuda_stream* s, uint8_t* out_valid) {
   t_launches = 0;
   if (!s || !out_valid) return fail(UTF8V_ERR_ARG, "NULL session/out_valid");
+  DeviceGuard guard;
   CK(cudaSetDevice(s->dev));
   u8v::launch_stream_edge(s->d_state, nullptr, 0, 1, s->s);
   ++t_launches;
@@ -848,6 +1007,7 @@ void utf8v_cuda_stream_destroy(utf8v_cuda_stream* s) {
   if (s->d_state) cudaFree(s->d_state);
   if (s->h_res) cudaFreeHost(s->h_res);
   if (s->ev_legacy) cudaEventDestroy(s->ev_legacy);
+  if (s->ev_fed) cudaEventDestroy(s->ev_fed);
   if (s->s) cudaStreamDestroy(s->s);
   delete s;
 }

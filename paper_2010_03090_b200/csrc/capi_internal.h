@@ -17,6 +17,16 @@ extern thread_local int t_launches;
 // returns `code`.
 int fail(int code, const std::string& what, cudaError_t e = cudaSuccess);
 
+// Restores the caller's current device on scope exit (entry points that
+// switch to a session's or a communicator's device).
+struct DeviceGuard {
+  int prev = -1;
+  DeviceGuard() { cudaGetDevice(&prev); }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
 }  // namespace u8v_capi
 
 #define CK(call)                                                             \

@@ -103,15 +103,6 @@ int nccl_fail(const char* what, ncclResult_t r) {
     if (!nccl().ok) return fail(UTF8V_ERR_NCCL, nccl().why);             \
   } while (0)
 
-// Restores the caller's current device on scope exit.
-struct DeviceGuard {
-  int prev = -1;
-  DeviceGuard() { cudaGetDevice(&prev); }
-  ~DeviceGuard() {
-    if (prev >= 0) cudaSetDevice(prev);
-  }
-};
-
 }  // namespace
 
 struct utf8v_cuda_comm {

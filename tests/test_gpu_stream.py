@@ -104,3 +104,41 @@ def test_large_device_stream_and_launch_count():
             s.feed(d[prev:c])
             prev = c
         assert s.finish() is False
+
+
+def test_device_piece_reused_on_the_default_stream_after_feed():
+    """A device piece is read asynchronously; work the caller issues after
+    feed() on the legacy default stream is ordered after that read, so
+    overwriting (or freeing and reusing) the piece there cannot change the
+    verdict (utf8v_cuda_stream_feed, include/utf8v_cuda.h)."""
+    import ctypes as C
+    import torch
+    from paper_2010_03090_b200 import _lib, configs
+    lib = _lib.load()
+    torch.cuda.set_device(0)
+    assert torch.cuda.current_stream().cuda_stream == 0  # torch's default stream is the legacy one
+    h = C.c_void_p()
+    _lib.check(lib.utf8v_cuda_stream_create(C.byref(h)))
+    try:
+        for trial in range(4):
+            pieces = [configs.gen_c1(64 << 20, seed=30 + trial + k) for k in range(2)]
+            # each piece on its own is a valid stream; concatenated at a
+            # character boundary they stay valid
+            for t in pieces:
+                _lib.check(lib.utf8v_cuda_stream_feed(h, t.data_ptr(), t.numel(), 1))
+                t.fill_(0xFF)  # right after feed, on the default stream
+            ok = C.c_uint8(9)
+            _lib.check(lib.utf8v_cuda_stream_finish(h, C.byref(ok)))
+            assert ok.value == 1, trial
+    finally:
+        lib.utf8v_cuda_stream_destroy(h)
+
+
+def test_stream_calls_keep_the_callers_device():
+    import torch
+    u8 = _u8()
+    torch.cuda.set_device(0)
+    with u8.LookupStream() as s:
+        s.feed(b"abc")
+        assert torch.cuda.current_device() == 0
+        assert s.finish() is True

@@ -25,6 +25,7 @@
 #include <iostream>
 #include <iterator>
 #include <limits>
+#include <stdexcept>
 #include <string>
 #include <vector>
 
@@ -103,8 +104,21 @@ struct timing {
   double best, mean;
 };
 
-int run_bench(const std::string& file, std::uint64_t size, std::uint64_t seed, int repeats,
-              bool device, bool compensate, bool as_json) {
+// A CUDA / environment failure inside `bench` (exit 2, as `validate`).
+struct env_error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+// Device copies of the bench input, freed on every return path.
+struct dev_buffers {
+  std::vector<std::uint8_t*> v;
+  ~dev_buffers() {
+    for (std::uint8_t* d : v) cudaFree(d);
+  }
+};
+
+int run_bench_impl(const std::string& file, std::uint64_t size, std::uint64_t seed, int repeats, bool device,
+                   bool compensate, bool as_json) {
   std::vector<std::uint8_t> bytes;
   std::string input_name;
   bool expect_valid = true;
@@ -116,7 +130,7 @@ int run_bench(const std::string& file, std::uint64_t size, std::uint64_t seed, i
     bytes.resize(size);
     if (utf8v_gen_stream_host(bytes.data(), size, seed, 0, 0) != UTF8V_OK) {
       std::cerr << "error: generator: " << utf8v_cuda_last_error() << "\n";
-      return k_exit_inconsistent;
+      return k_exit_usage;
     }
     input_name = "c1-mix seed=" + std::to_string(seed);
   }
@@ -131,25 +145,23 @@ int run_bench(const std::string& file, std::uint64_t size, std::uint64_t seed, i
     doubled.insert(doubled.end(), bytes.begin(), bytes.end());
     doubled.insert(doubled.end(), bytes.begin(), bytes.end());
   }
-  std::vector<std::uint8_t*> dev_bufs;
+  dev_buffers dev_bufs;
   auto place = [&](const std::vector<std::uint8_t>& b) -> const std::uint8_t* {
     if (!device) return b.data();
     std::uint8_t* d = nullptr;
-    if (cudaMalloc(&d, b.size() ? b.size() : 1) != cudaSuccess ||
-        cudaMemcpy(d, b.data(), b.size(), cudaMemcpyHostToDevice) != cudaSuccess)
-      return nullptr;
-    dev_bufs.push_back(d);
+    cudaError_t e = cudaMalloc(&d, b.size() ? b.size() : 1);
+    if (e == cudaSuccess) {
+      dev_bufs.v.push_back(d);
+      e = cudaMemcpy(d, b.data(), b.size(), cudaMemcpyHostToDevice);
+    }
+    if (e != cudaSuccess) throw env_error(std::string("device buffer: ") + cudaGetErrorString(e));
     return d;
   };
   const std::uint8_t* p1 = place(bytes);
   const std::uint8_t* p2 = compensate ? place(doubled) : nullptr;
-  if (!p1 || (compensate && !p2)) {
-    std::cerr << "error: device buffer\n";
-    return k_exit_inconsistent;
-  }
   auto once = [&](const std::uint8_t* p, std::size_t n) -> int {
     std::uint8_t ok = 0;
-    if (utf8v_cuda_validate(p, n, device ? 1 : 0, &ok) != UTF8V_OK) return -1;
+    if (utf8v_cuda_validate(p, n, device ? 1 : 0, &ok) != UTF8V_OK) throw env_error(utf8v_cuda_last_error());
     return ok;
   };
   // Correctness gate before timing (proj/src/bench.cpp:80-86).
@@ -181,7 +193,6 @@ int run_bench(const std::string& file, std::uint64_t size, std::uint64_t seed, i
     t.best = std::max(td.best - t.best, 0.0);
     t.mean = std::max(td.mean - t.mean, t.best);
   }
-  for (std::uint8_t* d : dev_bufs) cudaFree(d);
   const double best = t.best, mean = t.mean;
   const double n = (double)bytes.size();
   const std::string name = device ? "cuda-device" : "cuda";
@@ -199,6 +210,19 @@ int run_bench(const std::string& file, std::uint64_t size, std::uint64_t seed, i
                 n / best / 1e9, n / mean / 1e9);
   }
   return k_exit_ok;
+}
+
+int run_bench(const std::string& file, std::uint64_t size, std::uint64_t seed, int repeats, bool device,
+              bool compensate, bool as_json) {
+  try {
+    return run_bench_impl(file, size, seed, repeats, device, compensate, as_json);
+  } catch (const utf8v::cuda_error& e) {
+    std::cerr << "error: " << e.what() << "\n";
+    return k_exit_usage;
+  } catch (const env_error& e) {
+    std::cerr << "error: " << e.what() << "\n";
+    return k_exit_usage;
+  }
 }
 
 }  // namespace
