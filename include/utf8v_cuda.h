@@ -64,7 +64,8 @@ extern "C" {
  *      utf8v_cuda_validate_batch_async lost its unused d_scratch argument
  *      (utf8v_cuda_batch_scratch_bytes removed); host input crosses PCIe
  *      through a bounded device ring; utf8v_cuda_release_thread_resources;
- *      device stream pieces are ordered before later legacy-stream work */
+ *      device stream pieces are ordered before later legacy-stream work;
+ *      composable segment states (utf8v_state) */
 int utf8v_cuda_abi_version(void);
 
 /* Human-readable text of the last error on this thread ("" if none). */
@@ -180,6 +181,41 @@ int utf8v_cuda_stream_feed(utf8v_cuda_stream* s, const uint8_t* p, size_t n, int
 int utf8v_cuda_stream_finish(utf8v_cuda_stream* s, uint8_t* out_valid);
 uint64_t utf8v_cuda_stream_bytes(const utf8v_cuda_stream* s);
 void utf8v_cuda_stream_destroy(utf8v_cuda_stream* s);
+
+/* ---- composable segment states -----------------------
+ * The Lookup counterpart of the reference's fsm_state threading
+ * (proj/include/utf8v/fsm.hpp:15-20: "a stream can be validated in segments
+ * by threading the returned state"), made order-free: a segment validated on
+ * its own -- any device, any time -- yields a 24-byte state, and states
+ * merge with an associative combine (csrc/utf8v_state.h states the rule).
+ * The stream [0, n) is valid iff utf8v_state_valid() of the in-order combine
+ * of its segments' states.  Empty segments are the identity. */
+typedef struct utf8v_state {
+  uint64_t len;      /* segment length */
+  uint32_t flag;     /* nonzero: an interior lane [3, len-1) of the segment is flagged */
+  uint8_t head[4];   /* first min(len, 4) bytes, zero after */
+  uint8_t tail[4];   /* last min(len, 4) bytes, right-aligned, zero before */
+  uint32_t reserved;
+} utf8v_state;
+
+/* Host, pure: *out = a followed by b (out may alias a or b). */
+int utf8v_state_combine(const utf8v_state* a, const utf8v_state* b, utf8v_state* out);
+/* Host, pure: 1 iff the stream whose whole state is *s is valid UTF-8. */
+int utf8v_state_valid(const utf8v_state* s);
+/* The state of one segment p[0..n) (host or device bytes; K1 over its
+ * interior lanes). */
+int utf8v_cuda_segment_state(const uint8_t* p, size_t n, int is_device, utf8v_state* out);
+/* Per-record states of a CSR batch (records as in utf8v_cuda_validate_batch,
+ * each a segment): K2 in state mode + one pass over the record edges.
+ * Device form asynchronous on `stream` (d_states: n_records entries). */
+int utf8v_cuda_batch_states_async(const uint8_t* d_data, uint64_t n, const uint64_t* d_offsets,
+                                  uint64_t n_records, utf8v_state* d_states, void* stream);
+int utf8v_cuda_batch_states(const uint8_t* data, size_t n, const uint64_t* offsets, size_t n_records,
+                            int is_device, utf8v_state* states);
+/* *d_out = the in-order combine of d_states[0 .. count) on the device (one
+ * CTA; asynchronous on `stream`). */
+int utf8v_cuda_states_reduce_async(const utf8v_state* d_states, uint64_t count, utf8v_state* d_out,
+                                   void* stream);
 
 /* ---- multi-GPU combine in the native layer (comm.cu) -------
  * A stream sharded over ranks (one GPU each) is valid iff no rank's lanes

@@ -11,6 +11,8 @@ Python face of libutf8v_cuda.so, mirroring the reference's Lookup API
     validate_lookup_batch(d, offsets)  one verdict per CSR record
     LookupStream()               one stream validated in pieces (feed / finish)
     validate_lookup_sharded(d, g)  host input over g GPUs in this process
+    segment_state(d) / combine_states(a, b) / state_valid(s) / batch_states(d, offsets)
+                                 composable per-segment states (order-free stitching)
 
 `data` is host bytes (bytes / bytearray / memoryview / numpy uint8) or a CUDA
 torch.uint8 tensor (device-resident, validated in place).  All compute runs on
@@ -32,6 +34,8 @@ __all__ = [
     "validate_lookup", "validate_lookup_fallback", "validate_lookup_verdict", "validate_lookup_batch",
     "LookupStream", "validate_lookup_sharded",
     "validate_lanes_async", "validate_batch_async", "WIDTH",
+    "SegmentState", "STATE_DTYPE", "empty_state", "combine_states", "state_valid", "fold_states",
+    "segment_state", "batch_states",
 ]
 
 WIDTH = _lib.WIDTH
@@ -244,6 +248,93 @@ def validate_lanes_async(d_ptr: int, n: int, lane_lo: int, lane_hi: int, d_flag_
 
 def validate_batch_async(d_data: int, n: int, d_offsets: int, n_records: int, d_verdicts: int, stream: int = 0) -> None:
     _lib.check(_lib.load().utf8v_cuda_validate_batch_async(d_data, n, d_offsets, n_records, d_verdicts, stream))
+
+
+# ---- composable segment states (utf8v_state, csrc/utf8v_state.h) -------------
+
+class SegmentState(C.Structure):
+    """utf8v_state: the state of a segment validated on its own; states of
+    consecutive segments merge with combine_states() in any grouping
+    (associative), and state_valid() of the whole stream's state is its
+    verdict -- the order-free counterpart of threading the reference's
+    fsm_state (proj/include/utf8v/fsm.hpp:15-20)."""
+    _fields_ = [("len", C.c_uint64), ("flag", C.c_uint32), ("head", C.c_uint8 * 4), ("tail", C.c_uint8 * 4),
+                ("reserved", C.c_uint32)]
+
+    def __repr__(self) -> str:
+        return (f"SegmentState(len={self.len}, flag={self.flag}, head={bytes(self.head).hex()}, "
+                f"tail={bytes(self.tail).hex()})")
+
+    def __eq__(self, other) -> bool:
+        return isinstance(other, SegmentState) and bytes(self) == bytes(other)
+
+
+STATE_DTYPE = np.dtype([("len", "<u8"), ("flag", "<u4"), ("head", "u1", 4), ("tail", "u1", 4),
+                        ("reserved", "<u4")])
+assert STATE_DTYPE.itemsize == C.sizeof(SegmentState) == 24
+
+
+def empty_state() -> SegmentState:
+    return SegmentState()
+
+
+def combine_states(a: SegmentState, b: SegmentState) -> SegmentState:
+    """The state of segment a followed by segment b (host, pure)."""
+    out = SegmentState()
+    _lib.check(_lib.load().utf8v_state_combine(C.byref(a), C.byref(b), C.byref(out)))
+    return out
+
+
+def state_valid(s: SegmentState) -> bool:
+    """Verdict of the stream whose whole state is s."""
+    return bool(_lib.load().utf8v_state_valid(C.byref(s)))
+
+
+def fold_states(states) -> SegmentState:
+    """In-order combine of a sequence of SegmentState (or a STATE_DTYPE array)."""
+    acc = SegmentState()
+    if isinstance(states, np.ndarray):
+        states = [SegmentState.from_buffer_copy(states[i:i + 1].tobytes()) for i in range(states.size)]
+    for s in states:
+        acc = combine_states(acc, s)
+    return acc
+
+
+def segment_state(data) -> SegmentState:
+    """The state of one segment (host bytes or a CUDA uint8 tensor)."""
+    ptr, n, dev, _keep = _input(data)
+    out = SegmentState()
+    _lib.check(_lib.load().utf8v_cuda_segment_state(ptr, n, dev, C.byref(out)))
+    return out
+
+
+def batch_states(data, offsets) -> np.ndarray:
+    """Per-record states of a CSR batch (STATE_DTYPE array, one per record)."""
+    lib = _lib.load()
+    if _is_cuda_tensor(data):
+        import torch
+        if _is_cuda_tensor(offsets):
+            off = offsets.to(device=data.device, dtype=torch.int64).contiguous()
+        else:
+            off = torch.as_tensor(np.asarray(offsets, np.uint64).view(np.int64), device=data.device)
+        _after_current_stream(data)
+        nrec = int(off.numel()) - 1
+        out = np.zeros(max(nrec, 0), STATE_DTYPE)
+        if nrec <= 0:
+            return out
+        d_out = torch.empty(nrec * STATE_DTYPE.itemsize, dtype=torch.uint8, device=data.device)
+        _lib.check(lib.utf8v_cuda_batch_states(data.data_ptr() if data.numel() else None, int(data.numel()),
+                                               off.data_ptr(), nrec, 1, d_out.data_ptr()))
+        return d_out.cpu().numpy().view(STATE_DTYPE)
+    ptr, n, keep = _host_view(data)
+    off = np.ascontiguousarray(np.asarray(offsets, dtype=np.uint64))
+    nrec = int(off.size) - 1
+    out = np.zeros(max(nrec, 0), STATE_DTYPE)
+    if nrec <= 0:
+        return out
+    _lib.check(lib.utf8v_cuda_batch_states(ptr, n, off.ctypes.data, nrec, 0, out.ctypes.data))
+    del keep
+    return out
 
 
 class LookupStream:

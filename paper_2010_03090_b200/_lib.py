@@ -48,6 +48,13 @@ SIGNATURES: dict[str, tuple] = {
     "utf8v_cuda_validate_batch_async": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64,
                                                   C.c_void_p, C.c_void_p]),
     "utf8v_cuda_validate_sharded": (C.c_int, [C.c_void_p, C.c_size_t, C.c_int, C.c_int, _u8p]),
+    "utf8v_state_combine": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "utf8v_state_valid": (C.c_int, [C.c_void_p]),
+    "utf8v_cuda_segment_state": (C.c_int, [C.c_void_p, C.c_size_t, C.c_int, C.c_void_p]),
+    "utf8v_cuda_batch_states_async": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, C.c_void_p,
+                                                C.c_void_p]),
+    "utf8v_cuda_batch_states": (C.c_int, [C.c_void_p, C.c_size_t, C.c_void_p, C.c_size_t, C.c_int, C.c_void_p]),
+    "utf8v_cuda_states_reduce_async": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p]),
     "utf8v_cuda_comm_unique_id": (C.c_int, [C.c_void_p]),
     "utf8v_cuda_comm_init_rank": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
     "utf8v_cuda_comm_init_all": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p]),

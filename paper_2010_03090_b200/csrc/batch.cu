@@ -29,6 +29,7 @@
 
 #include "chunk.cuh"
 #include "kernels.cuh"
+#include "utf8v_state.h"
 #include "utf8v_swar.h"
 
 namespace u8v {
@@ -133,6 +134,10 @@ __device__ __forceinline__ int rel32(int64_t pos, int64_t s0) {
 // lanes or lies past the data (those lanes are settled by fix_boundary).
 // e0..e3: lane bits of chunk (lane + 32 i) of the step in the permuted plane
 // order of utf8v_bits.h (bit pos(i) = byte i).
+// kState (segment states, utf8v_state.h): a flagged lane counts only when it
+// is one of its record's interior lanes [start+3, end-1) -- it also must not
+// read the next record's first byte.
+template <bool kState>
 __device__ __forceinline__ void attribute_step(RecView d, int64_t s0, int64_t hi, uint32_t e0, uint32_t e1,
                                             uint32_t e2, uint32_t e3, int o, int64_t r0) {
   const int lane = threadIdx.x & 31;
@@ -169,9 +174,11 @@ __device__ __forceinline__ void attribute_step(RecView d, int64_t s0, int64_t hi
       if (cand <= 31 && t <= q) L = cand;
     }
     const int start = __shfl_sync(0xFFFFFFFFu, o, L);
+    const int nxt = kState ? __shfl_sync(0xFFFFFFFFu, o, (L + 1) & 31) : 0;
     if (q >= 0 && q < hi_rel && q >= start) {
       int64_t r = r0 + L;
       int64_t st_abs = s0 + start;
+      int64_t end_abs = s0 + nxt;  // kState: start(r + 1) when L < 31
       if (full && L == 31) {
         // More starts than one window holds (dense records): gallop, then
         // binary search the offsets -- O(log) loads in the records skipped.
@@ -190,7 +197,8 @@ __device__ __forceinline__ void attribute_step(RecView d, int64_t s0, int64_t hi
         r = a;
         st_abs = rec_start(d, r);
       }
-      if (r < d.n_records && s0 + q - st_abs >= 3) d.verdicts[r] = 0;
+      if (kState && (L == 31 || r != r0 + L)) end_abs = rec_start(d, r + 1);
+      if (r < d.n_records && s0 + q - st_abs >= 3 && (!kState || s0 + q < end_abs - 1)) d.verdicts[r] = 0;
     }
   }
 }
@@ -243,6 +251,7 @@ __device__ __forceinline__ void take_batch(BatchSlot* sl, const uint8_t* base, i
 // The boundary at start o of record rr = rf + lane: record rr-1 = [a, o)
 // ends there, record rr = [o, b) starts there (either may be empty or
 // absent).  nx: the following batch (lane 0 = start(rf + 32)).
+template <bool kState>
 __device__ __forceinline__ void check_batch(const RecView& rv, BatchSlot* sl, int nx, int64_t rf, int range_rel,
                                             u8v_consts k) {
   const int lane = threadIdx.x & 31;
@@ -255,7 +264,8 @@ __device__ __forceinline__ void check_batch(const RecView& rv, BatchSlot* sl, in
   const int nb = __shfl_sync(0xFFFFFFFFu, nx, 0);
   if (lane == 31) b = nb;
   const int64_t rr = rf + lane;
-  if (o >= 0 && o < range_rel) {
+  // kState: the boundary lanes are seam lanes, evaluated by combine().
+  if (!kState && o >= 0 && o < range_rel) {
     const uint64_t w0 = sl->w[lane][0], w1 = sl->w[lane][1];
     const unsigned sh = (unsigned)((o - 4) & 7) * 8u;
     const uint64_t w8 = sh ? (w0 >> sh) | (w1 << (64u - sh)) : w0;
@@ -269,6 +279,7 @@ __device__ __forceinline__ void check_batch(const RecView& rv, BatchSlot* sl, in
   __syncwarp();  // the slot is refilled next
 }
 
+template <bool kState>
 __global__ void __launch_bounds__(kK2Threads, kK2Blocks) k_batch(BatchDesc d) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * kK2Threads + threadIdx.x) >> 5;
@@ -431,7 +442,7 @@ __global__ void __launch_bounds__(kK2Threads, kK2Blocks) k_batch(BatchDesc d) {
           o = (rbc == 0 ? nx : (lane == 0 ? cx->prev_last : up)) - s0;
           r0 = rbc == 0 ? 0 : rbc - 1;
         }
-        attribute_step(rv, cx->range_lo + s0, cx->hi, err[0], err[1], err[2], err[3], o, r0);
+        attribute_step<kState>(rv, cx->range_lo + s0, cx->hi, err[0], err[1], err[2], err[3], o, r0);
       }
     }
     if (lane == 31) carry_word = v[kU - 1].w[kChunkWords - 1];
@@ -440,12 +451,12 @@ __global__ void __launch_bounds__(kK2Threads, kK2Blocks) k_batch(BatchDesc d) {
     // taken; the trigger reads nx a step after it was loaded (no stall).
     if (pend || __shfl_sync(0xFFFFFFFFu, nx, kTrigger) < (j + 1) * kStepBytes) {
       if (pend) {
-        check_batch(rv, sl, nx, cx->rb - 32, cx->range_rel, d.k);
+        check_batch<kState>(rv, sl, nx, cx->rb - 32, cx->range_rel, d.k);
         pend = false;
       }
       while (__shfl_sync(0xFFFFFFFFu, nx, kTrigger) < (j + 1) * kStepBytes) {
         const int64_t rbc = cx->rb;
-        if (pend) check_batch(rv, sl, nx, rbc - 32, cx->range_rel, d.k);
+        if (pend) check_batch<kState>(rv, sl, nx, rbc - 32, cx->range_rel, d.k);
         take_batch(sl, d.base, cx->lo, cx->hi, cx->range_lo, nx, cx->prev_last, cx->range_rel);
         pend = true;
         cx->taken = 1;
@@ -461,13 +472,13 @@ __global__ void __launch_bounds__(kK2Threads, kK2Blocks) k_batch(BatchDesc d) {
     int pl = cx->prev_last;
     const int64_t lo = cx->lo, hi = cx->hi, rlo = cx->range_lo;
     const int rrel = cx->range_rel;
-    if (pend) check_batch(rv, sl, nx, rbc - 32, rrel, d.k);
+    if (pend) check_batch<kState>(rv, sl, nx, rbc - 32, rrel, d.k);
     while (__shfl_sync(0xFFFFFFFFu, nx, 0) < rrel) {
       take_batch(sl, d.base, lo, hi, rlo, nx, pl, rrel);
       pl = __shfl_sync(0xFFFFFFFFu, nx, 31);
       rbc += 32;
       nx = rel32(rec_start(rv, rbc + lane), rlo);
-      check_batch(rv, sl, nx, rbc - 32, rrel, d.k);
+      check_batch<kState>(rv, sl, nx, rbc - 32, rrel, d.k);
     }
   }
 }
@@ -482,14 +493,15 @@ int batch_threads() { return kK2Threads; }
 
 int batch_blocks_per_sm() {
   int b = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_batch, kK2Threads, 0) != cudaSuccess) cudaGetLastError();
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_batch<false>, kK2Threads, 0) != cudaSuccess)
+    cudaGetLastError();
   return b < 1 ? 1 : b;
 }
 
 void launch_batch(const uint8_t* data, uint64_t n, const uint64_t* d_offsets, uint64_t n_records,
-                  uint8_t* d_verdicts, cudaStream_t st) {
+                  uint8_t* d_verdicts, cudaStream_t st, bool states) {
   if (n_records == 0 || n == 0) return;
-  if (launch_batch_large(data, n, d_offsets, n_records, d_verdicts, st)) return;
+  if (!states && launch_batch_large(data, n, d_offsets, n_records, d_verdicts, st)) return;
   BatchDesc d;
   const uintptr_t up = (uintptr_t)data;
   d.off32 = (int64_t)(up & (kChunkBytes - 1));
@@ -504,6 +516,62 @@ void launch_batch(const uint8_t* data, uint64_t n, const uint64_t* d_offsets, ui
   int64_t warps = k2_resident_warps();
   if (warps > max_steps) warps = max_steps;
   const int64_t blocks = (warps * 32 + kK2Threads - 1) / kK2Threads;
-  k_batch<<<(unsigned)blocks, kK2Threads, 0, st>>>(d);
+  if (states)
+    k_batch<true><<<(unsigned)blocks, kK2Threads, 0, st>>>(d);
+  else
+    k_batch<false><<<(unsigned)blocks, kK2Threads, 0, st>>>(d);
+}
+
+// Per-record segment states (utf8v_state.h) from K2's state-mode output
+// (clean[r] = 1 iff none of record r's interior lanes is flagged): length,
+// first and last four bytes.  One thread per record; offsets clamped to the
+// data as in K2.
+__global__ void k_record_states(const uint8_t* __restrict__ data, uint64_t n, const uint64_t* __restrict__ offsets,
+                                uint64_t n_records, const uint8_t* __restrict__ clean, u8v_state* __restrict__ out) {
+  const uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n_records) return;
+  uint64_t a = __ldg(offsets + r), b = __ldg(offsets + r + 1);
+  a = a < n ? a : n;
+  b = b < n ? b : n;
+  b = b > a ? b : a;
+  u8v_state s = u8v_state_empty();
+  s.len = b - a;
+  s.flag = s.len > 4 && clean[r] == 0 ? 1u : 0u;
+  const uint64_t k = s.len < 4 ? s.len : 4;
+  for (uint64_t i = 0; i < k; ++i) {
+    s.head[i] = data[a + i];
+    s.tail[4 - k + i] = data[b - k + i];
+  }
+  out[r] = s;
+}
+
+void launch_record_states(const uint8_t* data, uint64_t n, const uint64_t* d_offsets, uint64_t n_records,
+                          const uint8_t* d_clean, u8v_state* d_out, cudaStream_t st) {
+  if (n_records == 0) return;
+  k_record_states<<<(unsigned)((n_records + 255) / 256), 256, 0, st>>>(data, n, d_offsets, n_records, d_clean,
+                                                                       d_out);
+}
+
+// In-order fold of count states into *out (one CTA): each thread folds a
+// contiguous run, then the runs are combined pairwise in order, a tree over
+// shared memory (combine() is associative, not commutative).
+__global__ void __launch_bounds__(256) k_states_reduce(const u8v_state* __restrict__ in, uint64_t count,
+                                                       u8v_state* __restrict__ out) {
+  __shared__ u8v_state part[256];
+  const uint64_t t = threadIdx.x, T = blockDim.x;
+  const uint64_t a = count * t / T, b = count * (t + 1) / T;
+  u8v_state s = u8v_state_empty();
+  for (uint64_t i = a; i < b; ++i) s = u8v_state_combine(s, in[i]);
+  part[t] = s;
+  __syncthreads();
+  for (uint64_t w = 1; w < T; w <<= 1) {
+    if ((t & (2 * w - 1)) == 0 && t + w < T) part[t] = u8v_state_combine(part[t], part[t + w]);
+    __syncthreads();
+  }
+  if (t == 0) *out = part[0];
+}
+
+void launch_states_reduce(const u8v_state* d_in, uint64_t count, u8v_state* d_out, cudaStream_t st) {
+  k_states_reduce<<<1, 256, 0, st>>>(d_in, count, d_out);
 }
 }  // namespace u8v

@@ -839,6 +839,128 @@ int utf8v_cuda_ops_self_test(uint64_t seed, int* out_ok) {
   return UTF8V_OK;
 }
 
+// ---- composable segment states (utf8v_state.h) -------------------------------
+static_assert(sizeof(utf8v_state) == sizeof(u8v_state) && sizeof(utf8v_state) == 24, "utf8v_state layout");
+
+static u8v_state to_u8v(const utf8v_state* s) {
+  u8v_state r;
+  memcpy(&r, s, sizeof r);
+  return r;
+}
+
+int utf8v_state_combine(const utf8v_state* a, const utf8v_state* b, utf8v_state* out) {
+  if (!a || !b || !out) return fail(UTF8V_ERR_ARG, "NULL state");
+  const u8v_state r = u8v_state_combine(to_u8v(a), to_u8v(b));
+  memcpy(out, &r, sizeof r);
+  return UTF8V_OK;
+}
+
+int utf8v_state_valid(const utf8v_state* s) { return s && u8v_state_errors(to_u8v(s)) == 0 ? 1 : 0; }
+
+int utf8v_cuda_segment_state(const uint8_t* p, size_t n, int is_device, utf8v_state* out) {
+  t_launches = 0;
+  if (!out) return fail(UTF8V_ERR_ARG, "NULL state");
+  u8v_state s = u8v_state_empty();
+  s.len = n;
+  if (n > 0 && !p) return fail(UTF8V_ERR_ARG, "NULL data with n > 0");
+  const size_t k = n < 4 ? n : 4;
+  if (n > 4) {
+    uint32_t flag = 0;
+    const int st = flag_lanes(p, n, 3, n - 1, is_device, &flag);  // the interior lanes
+    if (st) return st;
+    s.flag = flag ? 1u : 0u;
+  }
+  if (k > 0) {
+    if (is_device) {
+      Ctx* c;
+      const int st = get_ctx(&c);
+      if (st) return st;
+      uint8_t* h = reinterpret_cast<uint8_t*>(c->h_res);
+      CK(cudaMemcpyAsync(h, p, k, cudaMemcpyDeviceToHost, c->s_comp));
+      CK(cudaMemcpyAsync(h + 8, p + n - k, k, cudaMemcpyDeviceToHost, c->s_comp));
+      CK(cudaStreamSynchronize(c->s_comp));
+      memcpy(s.head, h, k);
+      memcpy(s.tail + 4 - k, h + 8, k);
+    } else {
+      memcpy(s.head, p, k);
+      memcpy(s.tail + 4 - k, p + n - k, k);
+    }
+  }
+  memcpy(out, &s, sizeof s);
+  return UTF8V_OK;
+}
+
+int utf8v_cuda_batch_states_async(const uint8_t* d_data, uint64_t n, const uint64_t* d_offsets,
+                                  uint64_t n_records, utf8v_state* d_states, void* stream) {
+  t_launches = 0;
+  if (n_records == 0) return UTF8V_OK;
+  if (!d_offsets || !d_states) return fail(UTF8V_ERR_ARG, "NULL offsets/states");
+  if (n > 0 && !d_data) return fail(UTF8V_ERR_ARG, "NULL data");
+  Ctx* c;
+  int st = get_ctx(&c);
+  if (st) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  uint8_t* d_clean = nullptr;
+  CK(cudaMallocAsync(&d_clean, n_records, s));
+  CK(cudaMemsetAsync(d_clean, 1, n_records, s));
+  u8v::launch_batch(d_data, n, d_offsets, n_records, d_clean, s, true);
+  u8v::launch_record_states(d_data, n, d_offsets, n_records, d_clean, reinterpret_cast<u8v_state*>(d_states), s);
+  t_launches += 2;
+  CK(cudaFreeAsync(d_clean, s));
+  return check_launch("batch state kernels");
+}
+
+int utf8v_cuda_batch_states(const uint8_t* data, size_t n, const uint64_t* offsets, size_t n_records,
+                            int is_device, utf8v_state* states) {
+  t_launches = 0;
+  if (n_records == 0) return UTF8V_OK;
+  if (!offsets || !states) return fail(UTF8V_ERR_ARG, "NULL offsets/states");
+  Ctx* c;
+  int st = get_ctx(&c);
+  if (st) return st;
+  if (is_device) {
+    st = after_legacy(c->s_comp, c->ev_legacy);
+    if (st) return st;
+    st = utf8v_cuda_batch_states_async(data, n, offsets, n_records, states, c->s_comp);
+    if (st) return st;
+    CK(cudaStreamSynchronize(c->s_comp));
+    return UTF8V_OK;
+  }
+  for (size_t r = 0; r < n_records; ++r)
+    if (offsets[r + 1] < offsets[r]) return fail(UTF8V_ERR_ARG, "offsets not non-decreasing");
+  if (offsets[n_records] > n) return fail(UTF8V_ERR_ARG, "offsets exceed data size");
+  uint64_t* d_off = nullptr;
+  utf8v_state* d_st = nullptr;
+  CK(cudaMallocAsync(&d_off, (n_records + 1) * 8, c->s_comp));
+  CK(cudaMallocAsync(&d_st, n_records * sizeof(utf8v_state), c->s_comp));
+  CK(cudaMemcpyAsync(d_off, offsets, (n_records + 1) * 8, cudaMemcpyHostToDevice, c->s_comp));
+  if (n > 0) {
+    st = stage_h2d(*c, data, n);
+    if (st) return st;
+  }
+  st = utf8v_cuda_batch_states_async(n > 0 ? c->d_stage : nullptr, n, d_off, n_records, d_st, c->s_comp);
+  if (st) return st;
+  CK(cudaMemcpyAsync(states, d_st, n_records * sizeof(utf8v_state), cudaMemcpyDeviceToHost, c->s_comp));
+  CK(cudaFreeAsync(d_off, c->s_comp));
+  CK(cudaFreeAsync(d_st, c->s_comp));
+  CK(cudaStreamSynchronize(c->s_comp));
+  trim_stage(*c);
+  return UTF8V_OK;
+}
+
+int utf8v_cuda_states_reduce_async(const utf8v_state* d_states, uint64_t count, utf8v_state* d_out,
+                                   void* stream) {
+  t_launches = 0;
+  if (!d_out || (count > 0 && !d_states)) return fail(UTF8V_ERR_ARG, "NULL states");
+  Ctx* c;
+  const int st = get_ctx(&c);
+  if (st) return st;
+  u8v::launch_states_reduce(reinterpret_cast<const u8v_state*>(d_states), count,
+                            reinterpret_cast<u8v_state*>(d_out), (cudaStream_t)stream);
+  ++t_launches;
+  return check_launch("state reduce kernel");
+}
+
 // ---- one process, several GPUs ----
 int utf8v_cuda_validate_sharded(const uint8_t* p, size_t n, int n_gpus, int is_device,
                                 uint8_t* out_valid) {

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "utf8v_state.h"
 #include "utf8v_swar.h"
 
 namespace u8v {
@@ -56,8 +57,16 @@ void launch_locate(const StreamDesc& d, uint64_t n, const unsigned long long* fi
 // batch.cu
 // Caller sets d_verdicts[] = 1 first.  Asynchronous: the kernel reads
 // offsets[0] and offsets[n_records] itself (clamped to the n data bytes).
+// states = true: K2 in segment-state mode -- d_verdicts[r] = 1 iff none of
+// record r's interior lanes [start+3, end-1) is flagged (no boundary checks;
+// always K2, never K2L).
 void launch_batch(const uint8_t* data, uint64_t n, const uint64_t* d_offsets, uint64_t n_records,
-                  uint8_t* d_verdicts, cudaStream_t st);
+                  uint8_t* d_verdicts, cudaStream_t st, bool states = false);
+// Segment states (utf8v_state.h) of the records from launch_batch(states) output.
+void launch_record_states(const uint8_t* data, uint64_t n, const uint64_t* d_offsets, uint64_t n_records,
+                          const uint8_t* d_clean, u8v_state* d_out, cudaStream_t st);
+// *d_out = the in-order combine of d_in[0 .. count) (one CTA).
+void launch_states_reduce(const u8v_state* d_in, uint64_t count, u8v_state* d_out, cudaStream_t st);
 
 // validate.cu: K2L, the batch kernel for few, large records (<= 2048
 // records of >= 64 KiB on average): K1's sweep + out-of-line attribution.

@@ -420,3 +420,31 @@ class P2PFlags:
 
     def __exit__(self, *exc):
         self.close()
+
+
+# ---- per-shard composable states (utf8v_state; csrc/utf8v_state.h) ------------
+
+def shard_state(local, shard: Shard, state_fn: Optional[Callable[[object], object]] = None):
+    """The SegmentState of this rank's own bytes [start, end) -- no head or
+    tail needed: the lanes that read across a shard edge are evaluated when
+    the states are combined.  `local` holds [shard.lo, shard.hi) as for the
+    flag path; state_fn defaults to the GPU (segment_state)."""
+    own = local[shard.head:shard.head + (shard.end - shard.start)]
+    if state_fn is None:
+        from . import segment_state as state_fn  # noqa: N813
+    return state_fn(own)
+
+
+def combine_states_sharded(state, group=None) -> bool:
+    """Collective: every rank's state gathered (all_gather_object, gloo or
+    NCCL) and folded in rank order; True when the whole stream is valid.
+    Ranks may finish their shards in any order -- only the fold is ordered."""
+    import torch.distributed as dist
+    from . import SegmentState, fold_states, state_valid
+    raw = bytes(state)
+    if dist.is_available() and dist.is_initialized():
+        parts = [None] * dist.get_world_size(group)
+        dist.all_gather_object(parts, raw, group=group)
+    else:
+        parts = [raw]
+    return state_valid(fold_states([SegmentState.from_buffer_copy(p) for p in parts]))

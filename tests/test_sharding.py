@@ -253,3 +253,57 @@ def test_pipelined_flags_reduce_every_step():
         assert p.exitcode == 0
     for r in range(world):
         assert results[r] == [0, 1, 1, 1]
+
+
+def _state_worker(rank, world, port, q, data: bytes):
+    import os
+    import numpy as np
+    import torch.distributed as dist
+    from paper_2010_03090_b200 import sharding
+    from tests.test_states import leaf
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        b = np.frombuffer(data, np.uint8)
+        sh = sharding.plan(b.size, world)[rank]
+        st = sharding.shard_state(b[sh.lo:sh.hi], sh, state_fn=lambda own: leaf(own.tobytes()))
+        q.put((rank, sharding.combine_states_sharded(st)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_shard_states_combine_over_gloo(world):
+    """Per-shard states (the CPU model of segment_state) gathered over gloo
+    and folded in rank order: every rank gets the oracle's verdict, for
+    errors straddling the shard edges."""
+    import multiprocessing as mp
+    import socket
+    import numpy as np
+    from tests import _native as nat
+    from paper_2010_03090_b200 import sharding
+    rng = np.random.default_rng(world)
+    base = nat.gen_stream_host(1 << 16, 7)
+    ctx = mp.get_context("spawn")
+    for case in range(4):
+        b = base.copy()
+        if case:
+            edge = sharding.plan(b.size, world)[1 + case % (world - 1)].start
+            seq = [[0xE0, 0x80, 0x80], [0xF0, 0x9F], [0xC1, 0x80]][case - 1]
+            at = edge + int(rng.integers(-2, 2))
+            b[at:at + len(seq)] = seq
+        want = nat.oracle_verdict(b)[0]
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+        s.close()
+        q = ctx.Queue()
+        procs = [ctx.Process(target=_state_worker, args=(r, world, port, q, b.tobytes())) for r in range(world)]
+        for p in procs:
+            p.start()
+        res = dict(q.get(timeout=120) for _ in procs)
+        for p in procs:
+            p.join(timeout=60)
+            assert p.exitcode == 0
+        assert all(v == want for v in res.values()), (case, res, want)
