@@ -87,6 +87,7 @@ constexpr size_t kHalo = 16;                   // >= 6 look-back (decode), >= 3 
 constexpr int kRing = 4;
 constexpr size_t kSlotBytes = kPiece + 2 * kHalo;
 constexpr size_t kSmall = 1u << 20;
+constexpr size_t kZeroCopy = 256u << 10;       // K1 reads host memory in place up to this size
 constexpr size_t kKeepStage = 256ull << 20;    // batch staging kept across calls up to this size
 
 // Per thread and device: streams, small result buffers, the device ring for
@@ -119,8 +120,9 @@ struct Ctx {
   size_t h_slot_bytes = 0;
   cudaEvent_t hslot_done[kRing] = {};
   // Small inputs.
-  uint8_t* h_small = nullptr;
-  uint8_t* d_small = nullptr;
+  uint8_t* h_small = nullptr;   // mapped pinned: K1 reads it over PCIe (zero copy)
+  uint8_t* dh_small = nullptr;  // its device address
+  uint8_t* d_small = nullptr;   // device copy for the small verdict path
   // Batch from host memory: the whole data array (kept up to kKeepStage).
   uint8_t* d_stage = nullptr;
   size_t stage_cap = 0;
@@ -254,8 +256,9 @@ int ensure_pflags(Ctx& c, size_t k) {
 
 int ensure_small(Ctx& c) {
   if (c.d_small) return UTF8V_OK;
+  CK(cudaHostAlloc(&c.h_small, kSmall + 64, cudaHostAllocMapped));
+  CK(cudaHostGetDevicePointer((void**)&c.dh_small, c.h_small, 0));
   CK(cudaMalloc(&c.d_small, kSmall + 64));
-  CK(cudaMallocHost(&c.h_small, kSmall + 64));
   return UTF8V_OK;
 }
 
@@ -507,16 +510,25 @@ int validate_host_lanes(Ctx& c, const uint8_t* p, size_t n, uint64_t lane_lo, ui
   return UTF8V_OK;
 }
 
-// Inputs of at most kSmall bytes: one host copy into the pinned small
-// buffer, one DMA, K1, the flag back (the per-call latency path).
-int validate_small(Ctx& c, const uint8_t* p, size_t n, uint64_t lane_lo, uint64_t lane_hi) {
+// Inputs of at most kZeroCopy bytes (the per-call latency path): one host copy
+// into the mapped pinned buffer, and K1 reads it there over PCIe and stores
+// its flag into a mapped word -- one launch and one synchronisation, no
+// copies or memsets on the stream.
+int validate_small(Ctx& c, const uint8_t* p, size_t n, uint64_t lane_lo, uint64_t lane_hi, uint32_t* out) {
   int st = ensure_small(c);
   if (st) return st;
+  volatile uint32_t* hflag = reinterpret_cast<volatile uint32_t*>(c.h_small + kSmall + 32);
+  *hflag = 0;
   memcpy(c.h_small, p, n);
-  CK(cudaMemcpyAsync(c.d_small, c.h_small, n, cudaMemcpyHostToDevice, c.s_comp));
-  u8v::launch_validate(u8v::make_desc(c.d_small, n, lane_lo, lane_hi), c.d_flag, c.s_comp);
+  u8v::StreamDesc d = u8v::make_desc(c.dh_small, n, lane_lo, lane_hi);
+  d.flag_store = 1;
+  u8v::launch_validate(d, reinterpret_cast<uint32_t*>(c.dh_small + kSmall + 32), c.s_comp);
   ++t_launches;
-  return check_launch("validate kernel");
+  st = check_launch("validate kernel");
+  if (st) return st;
+  CK(cudaStreamSynchronize(c.s_comp));
+  *out = *hflag;
+  return UTF8V_OK;
 }
 
 // Batch from host memory: the whole data array staged on the device in
@@ -565,6 +577,7 @@ int flag_lanes(const uint8_t* p, uint64_t n, uint64_t lane_lo, uint64_t lane_hi,
   Ctx* c;
   int st = get_ctx(&c);
   if (st) return st;
+  if (!is_device && n <= kZeroCopy) return validate_small(*c, p, n, lane_lo, lane_hi, out);
   CK(cudaMemsetAsync(c->d_flag, 0, 4, c->s_comp));
   if (is_device) {
     st = after_legacy(c->s_comp, c->ev_legacy);
@@ -573,7 +586,14 @@ int flag_lanes(const uint8_t* p, uint64_t n, uint64_t lane_lo, uint64_t lane_hi,
     ++t_launches;
     st = check_launch("validate kernel");
   } else if (n <= kSmall) {
-    st = validate_small(*c, p, n, lane_lo, lane_hi);
+    // one staged copy: host memcpy into pinned memory, one DMA, K1
+    st = ensure_small(*c);
+    if (st) return st;
+    memcpy(c->h_small, p, n);
+    CK(cudaMemcpyAsync(c->d_small, c->h_small, n, cudaMemcpyHostToDevice, c->s_comp));
+    u8v::launch_validate(u8v::make_desc(c->d_small, n, lane_lo, lane_hi), c->d_flag, c->s_comp);
+    ++t_launches;
+    st = check_launch("validate kernel");
   } else {
     st = validate_host_lanes(*c, p, n, lane_lo, lane_hi);
   }

@@ -36,6 +36,8 @@ struct StreamDesc {
   uint32_t* const* peer_flags;     // n_peers device pointers (other GPUs' flag words,
   int n_peers;                     // NVLink peer memory): a warp that finds an
                                    // error also ORs 1 into each (comm.cu, P2P combine)
+  int flag_store;                  // nonzero: the flag is mapped host memory (the
+                                   // small-input path) and takes a plain store of 1
 };
 
 // Resident K2 warps on the current device (cached per device).

@@ -265,7 +265,10 @@ __device__ __forceinline__ void sweep(const StreamDesc& d, uint32_t* __restrict_
   }
   const unsigned any = __reduce_or_sync(0xFFFFFFFFu, acc);
   if (lane == 0 && any) {
-    atomicOr(flag, 1u);
+    if (d.flag_store)
+      *(volatile uint32_t*)flag = 1u;  // host-mapped word: a store, no PCIe atomic
+    else
+      atomicOr(flag, 1u);
     // P2P combine (comm.cu): the error also goes straight to every other
     // rank's flag word over NVLink, so the 4-byte allreduce(MAX) costs
     // nothing on valid input.
@@ -633,6 +636,7 @@ StreamDesc make_desc(const uint8_t* p, uint64_t n, uint64_t lane_lo, uint64_t la
   d.first_step = nullptr;
   d.peer_flags = nullptr;
   d.n_peers = 0;
+  d.flag_store = 0;
   return d;
 }
 
