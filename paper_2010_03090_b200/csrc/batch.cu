@@ -279,8 +279,39 @@ __device__ __forceinline__ void check_batch(const RecView& rv, BatchSlot* sl, in
   __syncwarp();  // the slot is refilled next
 }
 
+#ifdef U8V_TIMELINE
+// DEVELOPMENT (tools/kvar.sh builds only): per-warp start/end %globaltimer
+// and SM id of K2 (scripts/probes/k2_timeline.py).
+__device__ unsigned long long* g_timeline_k2;
+__device__ __forceinline__ unsigned long long k2_gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+template <bool kState>
+__device__ void batch_body(BatchDesc d);
 template <bool kState>
 __global__ void __launch_bounds__(kK2Threads, kK2Blocks) k_batch(BatchDesc d) {
+  const unsigned long long t0 = k2_gtimer();
+  batch_body<kState>(d);
+  if ((threadIdx.x & 31) == 0 && g_timeline_k2 != nullptr) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    const int64_t w = ((int64_t)blockIdx.x * kK2Threads + threadIdx.x) >> 5;
+    g_timeline_k2[3 * w] = t0;
+    g_timeline_k2[3 * w + 1] = k2_gtimer();
+    g_timeline_k2[3 * w + 2] = smid;
+  }
+}
+extern "C" int u8v_timeline_k2_set(unsigned long long* p) {
+  return (int)cudaMemcpyToSymbol(g_timeline_k2, &p, sizeof(p));
+}
+template <bool kState>
+__device__ __forceinline__ void batch_body(BatchDesc d) {
+#else
+template <bool kState>
+__global__ void __launch_bounds__(kK2Threads, kK2Blocks) k_batch(BatchDesc d) {
+#endif
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * kK2Threads + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * kK2Threads) >> 5;
@@ -357,6 +388,11 @@ __global__ void __launch_bounds__(kK2Threads, kK2Blocks) k_batch(BatchDesc d) {
   jb = jb < 0 ? 0 : jb;
   jd = jd > nsteps ? nsteps : jd;
   const uint8_t* p = d.base + range_lo + lane * kChunkBytes;
+  // K2 follows its verdict-initialisation kernel with programmatic
+  // serialisation (launch_batch): the prologue above -- offsets, the record
+  // search, the first batch -- overlaps it; verdict stores start only after
+  // it has completed.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   for (int j = 0; j < nsteps; ++j, p += kStepBytes) {
     Chunk v[kU];
     uint32_t nsw = 0;
@@ -498,9 +534,50 @@ int batch_blocks_per_sm() {
   return b < 1 ? 1 : b;
 }
 
+// verdicts[0 .. n) = 1, 16 bytes per store; dependents (K2 / K2L, launched
+// with programmatic serialisation) may start at once and wait for this
+// grid's completion only before their first verdict store.
+__global__ void k_init_verdicts(uint8_t* __restrict__ v, uint64_t n) {
+  asm volatile("griddepcontrol.launch_dependents;");
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t head = (16 - ((uintptr_t)v & 15)) & 15;  // bytes before the first 16-byte boundary
+  if (i < head && i < n) v[i] = 1;
+  const uint64_t body = n > head ? (n - head) / 16 : 0;
+  const uint4 ones = make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u);
+  for (uint64_t k = i; k < body; k += (uint64_t)gridDim.x * blockDim.x)
+    reinterpret_cast<uint4*>(v + head)[k] = ones;
+  const uint64_t tail0 = head + body * 16;
+  if (tail0 + i < n && i < 16) v[tail0 + i] = 1;
+}
+
+static void init_verdicts(uint8_t* v, uint64_t n, cudaStream_t st) {
+  const uint64_t vecs = n / 16 + 1;
+  uint64_t blocks = (vecs + 255) / 256;
+  if (blocks > 1184) blocks = 1184;
+  k_init_verdicts<<<(unsigned)(blocks ? blocks : 1), 256, 0, st>>>(v, n);
+}
+
+template <class... Args>
+static void launch_pdl(void (*kernel)(Args...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 void launch_batch(const uint8_t* data, uint64_t n, const uint64_t* d_offsets, uint64_t n_records,
                   uint8_t* d_verdicts, cudaStream_t st, bool states) {
-  if (n_records == 0 || n == 0) return;
+  if (n_records == 0) return;
+  init_verdicts(d_verdicts, n_records, st);
+  if (n == 0) return;
   if (!states && launch_batch_large(data, n, d_offsets, n_records, d_verdicts, st)) return;
   BatchDesc d;
   const uintptr_t up = (uintptr_t)data;
@@ -517,9 +594,9 @@ void launch_batch(const uint8_t* data, uint64_t n, const uint64_t* d_offsets, ui
   if (warps > max_steps) warps = max_steps;
   const int64_t blocks = (warps * 32 + kK2Threads - 1) / kK2Threads;
   if (states)
-    k_batch<true><<<(unsigned)blocks, kK2Threads, 0, st>>>(d);
+    launch_pdl(k_batch<true>, dim3((unsigned)blocks), dim3(kK2Threads), 0, st, d);
   else
-    k_batch<false><<<(unsigned)blocks, kK2Threads, 0, st>>>(d);
+    launch_pdl(k_batch<false>, dim3((unsigned)blocks), dim3(kK2Threads), 0, st, d);
 }
 
 // Per-record segment states (utf8v_state.h) from K2's state-mode output

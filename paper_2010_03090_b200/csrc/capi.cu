@@ -760,10 +760,9 @@ int utf8v_cuda_validate_batch_async(const uint8_t* d_data, uint64_t n, const uin
   if (st) return st;
   cudaStream_t s = (cudaStream_t)stream;
   if (n > 0 && !d_data) return fail(UTF8V_ERR_ARG, "NULL data");
-  CK(cudaMemsetAsync(d_verdicts, 1, n_records, s));
   // No host round trip: the kernel reads the first/last offsets itself.
   u8v::launch_batch(d_data, n, d_offsets, n_records, d_verdicts, s);
-  ++t_launches;
+  t_launches += n > 0 ? 2 : 1;  // verdict initialisation + K2 / K2L
   return check_launch("batch kernel");
 }
 
@@ -799,9 +798,8 @@ int utf8v_cuda_validate_batch(const uint8_t* data, size_t n, const uint64_t* off
     st = stage_h2d(*c, data, n);
     if (st) return st;
   }
-  CK(cudaMemsetAsync(d_ver, 1, n_records, c->s_comp));
   u8v::launch_batch(n > 0 ? c->d_stage : nullptr, n, d_off, n_records, d_ver, c->s_comp);
-  ++t_launches;
+  t_launches += n > 0 ? 2 : 1;
   st = check_launch("batch kernel");
   if (st) return st;
   CK(cudaMemcpyAsync(verdicts, d_ver, n_records, cudaMemcpyDeviceToHost, c->s_comp));
@@ -922,10 +920,9 @@ int utf8v_cuda_batch_states_async(const uint8_t* d_data, uint64_t n, const uint6
   cudaStream_t s = (cudaStream_t)stream;
   uint8_t* d_clean = nullptr;
   CK(cudaMallocAsync(&d_clean, n_records, s));
-  CK(cudaMemsetAsync(d_clean, 1, n_records, s));
   u8v::launch_batch(d_data, n, d_offsets, n_records, d_clean, s, true);
   u8v::launch_record_states(d_data, n, d_offsets, n_records, d_clean, reinterpret_cast<u8v_state*>(d_states), s);
-  t_launches += 2;
+  t_launches += n > 0 ? 3 : 2;
   CK(cudaFreeAsync(d_clean, s));
   return check_launch("batch state kernels");
 }

@@ -57,7 +57,8 @@ void launch_locate(const StreamDesc& d, uint64_t n, const unsigned long long* fi
                    unsigned long long* out_offset, int* out_kind, cudaStream_t st);
 
 // batch.cu
-// Caller sets d_verdicts[] = 1 first.  Asynchronous: the kernel reads
+// Writes d_verdicts[] fully: an initialisation kernel sets them to 1, then K2
+// (or K2L) stores 0 for failing records.  Asynchronous: the kernel reads
 // offsets[0] and offsets[n_records] itself (clamped to the n data bytes).
 // states = true: K2 in segment-state mode -- d_verdicts[r] = 1 iff none of
 // record r's interior lanes [start+3, end-1) is flagged (no boundary checks;

@@ -219,12 +219,32 @@ __device__ __forceinline__ void note_first_step(unsigned long long* first_step, 
   if ((int)(threadIdx.x & 31) == __ffs(m) - 1) atomicMin(first_step, (unsigned long long)cstep);
 }
 
+// Lane 0 takes the next ticket of the CTA's step pool (a predicated
+// atom.shared: the compiler's warp-aggregated atomicAdd -- ballot, popc,
+// leader election and convergence barriers -- cost ~40 instructions per step,
+// 9 % of K1's; profiles/r02_ncu_k_validate_source.txt).
+__device__ __forceinline__ unsigned take_ticket(unsigned pool_addr, int lane, unsigned keep) {
+  unsigned t = keep;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.eq.s32 p, %1, 0;\n\t@p atom.shared.add.u32 %0, [%2], 1;\n\t}"
+      : "+r"(t)
+      : "r"(lane), "r"(pool_addr)
+      : "memory");
+  return t;
+}
+
 template <bool kTrack>
 __device__ __forceinline__ void sweep(const StreamDesc& d, uint32_t* __restrict__ flag) {
   __shared__ unsigned s_ticket;
+  __shared__ unsigned s_zero[32];
   if (threadIdx.x == 0) s_ticket = 0;
+  if (threadIdx.x < 32) s_zero[threadIdx.x] = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31;
+  // The pool's shared address plus a per-lane zero read from shared memory:
+  // ptxas cannot prove the address warp-uniform, so it does not wrap the
+  // single-lane atom in its warp-aggregation sequence.
+  const unsigned pool_addr = (unsigned)__cvta_generic_to_shared(&s_ticket) + s_zero[lane];
   const int64_t sb = kStepChunks * (int64_t)kChunkBytes;
   int64_t int_b, int_d;
   interior_steps(d, &int_b, &int_d);
@@ -239,7 +259,7 @@ __device__ __forceinline__ void sweep(const StreamDesc& d, uint32_t* __restrict_
   int unused = kU;
   unsigned step = blockIdx.x + G * (threadIdx.x >> 5);
   unsigned next = 0;
-  if (step < nsteps && lane == 0) next = atomicAdd(&s_ticket, 1u);
+  if (step < nsteps) next = take_ticket(pool_addr, lane, next);
   while (step < nsteps) {
     uint32_t e;
     if (step >= ib && step < id) {
@@ -261,7 +281,7 @@ __device__ __forceinline__ void sweep(const StreamDesc& d, uint32_t* __restrict_
     }
     const unsigned t = __shfl_sync(0xFFFFFFFFu, next, 0);
     step = blockIdx.x + G * (kK1Warps + t);
-    if (step < nsteps && lane == 0) next = atomicAdd(&s_ticket, 1u);
+    if (step < nsteps) next = take_ticket(pool_addr, lane, next);
   }
   const unsigned any = __reduce_or_sync(0xFFFFFFFFu, acc);
   if (lane == 0 && any) {
@@ -508,6 +528,9 @@ __global__ void __launch_bounds__(kThreads, 4)
     s_off[i] = d.off32 + (int64_t)(o < (uint64_t)nb ? o : (uint64_t)nb);
   }
   __syncthreads();
+  // launched after the verdict initialisation with programmatic
+  // serialisation (launch_batch): verdict stores wait for it
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int lane = threadIdx.x & 31;
   // Record boundaries: thread g of the grid takes start(g), g <= N (record
   // g-1 = [a, s) ends there, record g = [s, b) starts there).
@@ -696,7 +719,17 @@ bool launch_batch_large(const uint8_t* data, uint64_t n, const uint64_t* d_offse
   const int64_t need = ((int64_t)n_records + kThreads) / kThreads;  // boundary threads: N + 1
   if (blocks < need) blocks = need;
   const size_t smem = (n_records + 1) * sizeof(int64_t);
-  k_batch_large<<<(unsigned)blocks, kThreads, smem, st>>>(d, d_offsets, (int)n_records, d_verdicts);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)blocks);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_batch_large, d, d_offsets, (int)n_records, d_verdicts);  // after k_init_verdicts
   return true;
 }
 

@@ -108,7 +108,7 @@ def main():
     ap.add_argument("--round", default="r01")
     ap.add_argument("--rep", action="append", default=[], help="kernel=path.ncu-rep")
     ap.add_argument("--launches")
-    ap.add_argument("--command", default="python bench.py --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 1")
+    ap.add_argument("--command", default="python bench.py")
     a = ap.parse_args()
     prof = ROOT / "profiles"
     prof.mkdir(exist_ok=True)
@@ -130,6 +130,7 @@ def main():
         summary["launches"] = f"{a.round}_launches.json"
         for k, p in l["kernels"].items():
             print(f"  {k}: n={p['count']} mean={p['mean_us']:.1f}us share={p['share']:.3f}")
+    summary["source"] = f"{a.round} ncu --set full capture, scripts/gpu_profile.sh"
     summary_path.write_text(json.dumps(summary, indent=1) + "\n")
 
 
