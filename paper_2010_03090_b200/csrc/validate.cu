@@ -519,6 +519,7 @@ __device__ __forceinline__ void attribute_large(const StreamDesc& d, int64_t cst
   }
 }
 
+constexpr int kK2LThreads = kThreads;
 __global__ void __launch_bounds__(kThreads, 4)
     k_batch_large(StreamDesc d, const uint64_t* __restrict__ offsets, int N, uint8_t* __restrict__ verdicts) {
   extern __shared__ int64_t s_off[];  // start(r) in base coordinates, clamped to the data
@@ -630,7 +631,7 @@ static const DevInfo& dev_info() {
     DevInfo& i = g_info[dev];
     i.k1_ctas = sms * blocks_per_sm((const void*)k_validate, kK1Threads, 0);
     i.k2_warps = sms * batch_blocks_per_sm() * (batch_threads() / 32);
-    i.k2l_warps = sms * blocks_per_sm((const void*)k_batch_large, kThreads, 0) * (kThreads / 32);
+    i.k2l_warps = sms * blocks_per_sm((const void*)k_batch_large, kK2LThreads, 0) * (kK2LThreads / 32);
   });
   return g_info[dev];
 }
@@ -716,12 +717,12 @@ bool launch_batch_large(const uint8_t* data, uint64_t n, const uint64_t* d_offse
   const int64_t spw = (d.steps + warps - 1) / warps;
   warps = (d.steps + spw - 1) / spw;
   int64_t blocks = (warps * 32 + kThreads - 1) / kThreads;
-  const int64_t need = ((int64_t)n_records + kThreads) / kThreads;  // boundary threads: N + 1
+  const int64_t need = ((int64_t)n_records + kK2LThreads) / kK2LThreads;  // boundary threads: N + 1
   if (blocks < need) blocks = need;
   const size_t smem = (n_records + 1) * sizeof(int64_t);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)blocks);
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(kK2LThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute at[1];
