@@ -4,8 +4,8 @@ stream of 0 B .. 48 MiB from the C1 mix (starting anywhere, so possibly
 inside a character), plants 0..4 errors (random bytes, lone leads,
 truncations, garbage runs), and checks validate_lookup and
 validate_lookup_verdict (device and host input: K1, the tracking K1 + K3)
-and a stream session fed in random pieces against the oracle's verdict,
-offset and kind."""
+a stream session fed in random pieces, and segment states of random pieces
+merged in random order, against the oracle's verdict, offset and kind."""
 import sys
 import time
 from pathlib import Path
@@ -61,6 +61,15 @@ while time.time() - t0 < budget:
             s.feed(d[prev:int(c)] if rng.random() < 0.5 else h[prev:int(c)])
             prev = int(c)
         assert s.finish() is exp[0], (trials, n, a, cuts)
+    # segment states of random pieces (host or device), merged in a random
+    # order of adjacent pairs (utf8v_state combine is associative)
+    cuts = [int(c) for c in np.sort(rng.integers(0, n + 1, int(rng.integers(0, 6))))]
+    bounds = [0] + cuts + [n]
+    states = [u8.segment_state(d[x:y] if rng.random() < 0.5 else h[x:y]) for x, y in zip(bounds, bounds[1:])]
+    while len(states) > 1:
+        i = int(rng.integers(0, len(states) - 1))
+        states[i:i + 2] = [u8.combine_states(states[i], states[i + 1])]
+    assert u8.state_valid(states[0]) is exp[0] and states[0].len == n, (trials, n, a, cuts)
     trials += 1
     nbytes += n
     invalid += int(not exp[0])
