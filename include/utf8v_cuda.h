@@ -170,11 +170,11 @@ int utf8v_cuda_validate_batch_async(const uint8_t* d_data, uint64_t n, const uin
  * pieces are not copied) by one K1 launch whose first thread also evaluates
  * the <= 4 lanes straddling the previous piece (csrc/stream_edge.cuh).  Pieces may have any length,
  * including 0.  A device piece is read asynchronously on the session's own
- * stream: work issued after feed() on the legacy default stream (and every
- * blocking stream) is ordered after that read, and the piece must otherwise
- * stay valid and unmodified until finish() returns.  Host pieces are
- * consumed before feed returns.  finish() resets the session.  feed and
- * finish leave the caller's current device unchanged. */
+ * stream (consecutive feeds overlap): it must stay valid and unmodified until
+ * finish() returns (the Python LookupStream keeps a reference to every
+ * device piece until then).  Host pieces are consumed before feed returns.
+ * finish() resets the session.  feed and finish leave the caller's current
+ * device unchanged. */
 typedef struct utf8v_cuda_stream utf8v_cuda_stream;
 int utf8v_cuda_stream_create(utf8v_cuda_stream** out);
 int utf8v_cuda_stream_feed(utf8v_cuda_stream* s, const uint8_t* p, size_t n, int is_device);

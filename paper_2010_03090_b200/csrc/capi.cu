@@ -1042,7 +1042,6 @@ struct utf8v_cuda_stream {
   size_t cap = 0;
   uint64_t total = 0;
   cudaEvent_t ev_legacy = nullptr;  // see after_legacy()
-  cudaEvent_t ev_fed = nullptr;     // a device piece's K1, for the legacy stream to wait on
 };
 
 int utf8v_cuda_stream_create(utf8v_cuda_stream** out) {
@@ -1056,7 +1055,6 @@ int utf8v_cuda_stream_create(utf8v_cuda_stream** out) {
   if (cudaStreamCreateWithFlags(&s->s, cudaStreamNonBlocking) != cudaSuccess ||
       cudaMalloc(&s->d_state, 64) != cudaSuccess || cudaMallocHost(&s->h_res, 64) != cudaSuccess ||
       cudaEventCreateWithFlags(&s->ev_legacy, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&s->ev_fed, cudaEventDisableTiming) != cudaSuccess ||
       cudaMemsetAsync(s->d_state, 0, 64, s->s) != cudaSuccess) {
     const cudaError_t e = cudaGetLastError();
     utf8v_cuda_stream_destroy(s);
@@ -1109,16 +1107,10 @@ int utf8v_cuda_stream_feed(utf8v_cuda_stream* s, const uint8_t* p, size_t n, int
   }
   ++t_launches;
   s->total += n;
-  if (is_device) {
-    // The piece is read asynchronously: work the caller issues later on the
-    // legacy default stream (and every blocking stream) waits for this K1, so
-    // a buffer freed and reused there is not overwritten under it.  Work on
-    // non-blocking streams must keep the piece until finish() returns.
-    CK(cudaEventRecord(s->ev_fed, s->s));
-    CK(cudaStreamWaitEvent(cudaStreamLegacy, s->ev_fed, 0));
-  } else {
-    CK(cudaStreamSynchronize(s->s));  // the caller may reuse its buffer
-  }
+  // A device piece is read asynchronously (and consecutive feeds overlap):
+  // it must stay valid and unmodified until finish() returns.  A host piece
+  // is consumed here: the caller may reuse its buffer.
+  if (!is_device) CK(cudaStreamSynchronize(s->s));
   return check_launch("stream feed");
 }
 
@@ -1146,7 +1138,6 @@ void utf8v_cuda_stream_destroy(utf8v_cuda_stream* s) {
   if (s->d_state) cudaFree(s->d_state);
   if (s->h_res) cudaFreeHost(s->h_res);
   if (s->ev_legacy) cudaEventDestroy(s->ev_legacy);
-  if (s->ev_fed) cudaEventDestroy(s->ev_fed);
   if (s->s) cudaStreamDestroy(s->s);
   delete s;
 }

@@ -314,15 +314,14 @@ __global__ void __launch_bounds__(kK1Threads, 1) k_validate(StreamDesc d, uint32
   // Dependents (a following K1 launched with PDL, see launch_k1) may start
   // as soon as every CTA of this grid has started.
   asm volatile("griddepcontrol.launch_dependents;");
-  if (d.session != nullptr) {
-    // A session feed: only the edge thread, which reads the carry the
-    // previous feed wrote, waits for that feed.
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      asm volatile("griddepcontrol.wait;" ::: "memory");
-      stream_edge_piece(d.session, d.base + d.off32, (uint64_t)(d.hi - d.lo), 0);
-    }
-  }
   sweep<false>(d, flag);
+  if (d.session != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {
+    // A session feed: only the edge thread, which reads the carry the
+    // previous feed wrote, waits for that feed -- after its own share of
+    // the sweep, so no CTA's sweep waits behind the previous piece.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    stream_edge_piece(d.session, d.base + d.off32, (uint64_t)(d.hi - d.lo), 0);
+  }
 #ifdef U8V_TIMELINE
   if ((threadIdx.x & 31) == 0 && g_timeline != nullptr) {
     unsigned smid;

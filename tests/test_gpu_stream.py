@@ -106,32 +106,23 @@ def test_large_device_stream_and_launch_count():
         assert s.finish() is False
 
 
-def test_device_piece_reused_on_the_default_stream_after_feed():
-    """A device piece is read asynchronously; work the caller issues after
-    feed() on the legacy default stream is ordered after that read, so
-    overwriting (or freeing and reusing) the piece there cannot change the
-    verdict (utf8v_cuda_stream_feed, include/utf8v_cuda.h)."""
-    import ctypes as C
+def test_device_pieces_outlive_the_callers_references():
+    """A device piece is read asynchronously until finish(): LookupStream
+    keeps every piece alive, so temporaries the caller drops right after
+    feed() are not freed and reused under the session (the caching
+    allocator would hand their blocks to the next allocations, which are
+    overwritten at once)."""
     import torch
-    from paper_2010_03090_b200 import _lib, configs
-    lib = _lib.load()
+    from paper_2010_03090_b200 import configs
+    u8 = _u8()
     torch.cuda.set_device(0)
-    assert torch.cuda.current_stream().cuda_stream == 0  # torch's default stream is the legacy one
-    h = C.c_void_p()
-    _lib.check(lib.utf8v_cuda_stream_create(C.byref(h)))
-    try:
+    with u8.LookupStream() as s:
         for trial in range(4):
-            pieces = [configs.gen_c1(64 << 20, seed=30 + trial + k) for k in range(2)]
-            # each piece on its own is a valid stream; concatenated at a
-            # character boundary they stay valid
-            for t in pieces:
-                _lib.check(lib.utf8v_cuda_stream_feed(h, t.data_ptr(), t.numel(), 1))
-                t.fill_(0xFF)  # right after feed, on the default stream
-            ok = C.c_uint8(9)
-            _lib.check(lib.utf8v_cuda_stream_finish(h, C.byref(ok)))
-            assert ok.value == 1, trial
-    finally:
-        lib.utf8v_cuda_stream_destroy(h)
+            for k in range(3):
+                s.feed(configs.gen_c1(32 << 20, seed=60 + trial + k))  # a temporary, dropped at once
+                junk = torch.full((32 << 20,), 0xFF, dtype=torch.uint8, device="cuda")  # may reuse freed blocks
+                del junk
+            assert s.finish() is True, trial
 
 
 def test_stream_calls_keep_the_callers_device():
