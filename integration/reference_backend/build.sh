@@ -8,6 +8,7 @@
 #   unit_tests   proj/tests/test_{lookup,oracle,tables}.cpp, unchanged, with
 #                the doctest stand-in of doctest_shim/ (doctest is not in this
 #                image)
+#   roster       prints the roster detect_backends() built (roster.cpp)
 # The one registration line is applied to a copy of proj/src/lookup.cpp in
 # baseline/accept/src/ (never committed): after `found` is declared in
 # detect_backends(), the cuda entry goes first when a device answers, so the
@@ -41,4 +42,5 @@ $CXX $FLAGS -o "$OUT/acceptance" "$REF/tests/acceptance.cpp" "${objs[@]}" "${LIN
 $CXX $FLAGS -I"$ROOT/integration/reference_backend/doctest_shim" -o "$OUT/unit_tests" \
     "$REF/tests/doctest_main.cpp" "$REF/tests/test_lookup.cpp" "$REF/tests/test_oracle.cpp" \
     "$REF/tests/test_tables.cpp" "${objs[@]}" "${LINK[@]}"
-echo "built $OUT/acceptance $OUT/unit_tests"
+$CXX $FLAGS -o "$OUT/roster" "$ROOT/integration/reference_backend/roster.cpp" "${objs[@]}" "${LINK[@]}"
+echo "built $OUT/acceptance $OUT/unit_tests $OUT/roster"

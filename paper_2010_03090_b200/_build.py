@@ -114,11 +114,22 @@ def build_test_helpers() -> None:
               "-pthread"])
 
 
+def build_reference_tests() -> None:
+    """The reference's own unit tests and acceptance gate with the cuda entry
+    first in its roster (integration/reference_backend/build.sh; outputs in
+    the git-ignored baseline/accept/).  A no-op without the reference
+    checkout: the GPU box uses the prebuilt binaries."""
+    script = ROOT / "integration" / "reference_backend" / "build.sh"
+    if script.exists() and Path("/root/reference/proj/src/lookup.cpp").exists():
+        _run(["bash", str(script)])
+
+
 def build_all(force: bool = False, verbose: bool = False) -> None:
     build_cuda(force=force, verbose=verbose)
     build_cli()
     build_oracle()
     build_test_helpers()
+    build_reference_tests()
 
 
 if __name__ == "__main__":
