@@ -1097,11 +1097,9 @@ int utf8v_cuda_stream_feed(utf8v_cuda_stream* s, const uint8_t* p, size_t n, int
   if (desc.steps > 0) {
     desc.session = s->d_state;
     // Device pieces overlap the previous feed's K1 (the only other work on
-    // the session stream); a host piece's K1 follows its own H2D copy.
-    if (is_device)
-      u8v::launch_validate_piece(desc, s->d_state + 1, s->s);
-    else
-      u8v::launch_validate(desc, s->d_state + 1, s->s);
+    // the session stream); a host piece's K1 follows its own H2D copy (PDL
+    // does not reach across a copy).
+    u8v::launch_validate_piece(desc, s->d_state + 1, s->s);
   } else {
     u8v::launch_stream_edge(s->d_state, d, n, 0, s->s);
   }

@@ -29,8 +29,9 @@ struct StreamDesc {
   int64_t c_begin, c_end;  // chunks evaluated: [c_begin, c_end)
   int64_t steps;           // ceil((c_end - c_begin) / kStepChunks)
   u8v_consts k;  // runtime multipliers (FMA-pipe routing, utf8v_swar.h)
-  uint32_t* session;  // non-null: K1's first thread also runs the stream-session
-                      // edge of this piece (stream_edge.cuh) on session[0..1]
+  uint32_t* session;  // a stream-session piece (launch_validate_piece): K1's first
+                      // thread also runs the edge of this piece (stream_edge.cuh)
+                      // on session[0..1]
   unsigned long long* first_step;  // non-null: K1 records its first flagged step
                                    // there (atomicMin of the step's first chunk)
   uint32_t* const* peer_flags;     // n_peers device pointers (other GPUs' flag words,

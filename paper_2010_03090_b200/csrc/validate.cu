@@ -315,13 +315,6 @@ __global__ void __launch_bounds__(kK1Threads, 1) k_validate(StreamDesc d, uint32
   // as soon as every CTA of this grid has started.
   asm volatile("griddepcontrol.launch_dependents;");
   sweep<false>(d, flag);
-  if (d.session != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {
-    // A session feed: only the edge thread, which reads the carry the
-    // previous feed wrote, waits for that feed -- after its own share of
-    // the sweep, so no CTA's sweep waits behind the previous piece.
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    stream_edge_piece(d.session, d.base + d.off32, (uint64_t)(d.hi - d.lo), 0);
-  }
 #ifdef U8V_TIMELINE
   if ((threadIdx.x & 31) == 0 && g_timeline != nullptr) {
     unsigned smid;
@@ -332,6 +325,20 @@ __global__ void __launch_bounds__(kK1Threads, 1) k_validate(StreamDesc d, uint32
     g_timeline[3 * w + 2] = smid;
   }
 #endif
+}
+
+// K1 for a stream-session feed (launch_validate_piece): the piece's own
+// lanes, then the edge thread -- which reads the carry the previous feed
+// wrote -- waits for that feed, after its own share of the sweep, so no
+// CTA's sweep waits behind the previous piece.  (A separate entry keeps the
+// session code out of k_validate.)
+__global__ void __launch_bounds__(kK1Threads, 1) k_validate_piece(StreamDesc d, uint32_t* __restrict__ flag) {
+  asm volatile("griddepcontrol.launch_dependents;");
+  sweep<false>(d, flag);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    stream_edge_piece(d.session, d.base + d.off32, (uint64_t)(d.hi - d.lo), 0);
+  }
 }
 
 // K1 for the verdict path: also records the first flagged step
@@ -701,7 +708,7 @@ void launch_validate(const StreamDesc& d, uint32_t* flag, cudaStream_t st) {
 }
 
 void launch_validate_piece(const StreamDesc& d, uint32_t* flag, cudaStream_t st) {
-  launch_k1(k_validate, d, flag, st);
+  launch_k1(k_validate_piece, d, flag, st);
 }
 
 bool launch_batch_large(const uint8_t* data, uint64_t n, const uint64_t* d_offsets, uint64_t n_records,
