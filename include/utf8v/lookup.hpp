@@ -14,6 +14,9 @@
 //   validate_lookup_verdict  -- first error offset and kind, bit-exact with
 //                               oracle_validate (proj/src/oracle.cpp:10-44)
 //   validate_lookup_batch    -- one verdict per record of a CSR batch
+//   lookup_stream            -- one stream validated in pieces, in order
+//   segment_state            -- segments validated anywhere, merged later
+//   shard_comm               -- a stream sharded over GPUs, combined by NCCL
 #pragma once
 
 #include <cstddef>
@@ -72,6 +75,46 @@ class lookup_stream {
   void feed(bytes_view piece);
   bool finish();
   std::uint64_t bytes_fed() const;
+
+ private:
+  void* handle_ = nullptr;
+};
+
+// A segment validated on its own (any device, any order): its composable
+// state (utf8v_state, include/utf8v_cuda.h).  combine() is associative, so
+// states of consecutive segments merge in any grouping; valid() of the
+// whole stream's state is its verdict -- the order-free counterpart of
+// threading fsm_state (proj/include/utf8v/fsm.hpp:15-20).
+struct segment_state {
+  std::uint64_t len = 0;
+  std::uint32_t flag = 0;
+  std::uint8_t head[4] = {0, 0, 0, 0};
+  std::uint8_t tail[4] = {0, 0, 0, 0};
+  std::uint32_t reserved = 0;
+
+  static segment_state of(bytes_view segment);   // host bytes, validated on the GPU
+  segment_state then(const segment_state& next) const;  // this segment followed by `next`
+  bool valid() const;                            // verdict of a whole-stream state
+};
+std::vector<segment_state> batch_states(bytes_view data, std::span<const std::uint64_t> offsets);
+
+// One rank of a stream sharded over GPUs (one process per GPU), the verdict
+// combined with NCCL from the native layer.  The unique id
+// comes from rank 0 (unique_id()) through the caller's bootstrap.  The shard
+// is this rank's bytes with the look-back head and lookahead tail of
+// sharding.plan, lanes [lane_lo, lane_hi) in its own coordinates.
+class shard_comm {
+ public:
+  static std::vector<std::uint8_t> unique_id();
+  shard_comm(std::span<const std::uint8_t> id, int nranks, int rank);
+  ~shard_comm();
+  shard_comm(const shard_comm&) = delete;
+  shard_comm& operator=(const shard_comm&) = delete;
+  // Collective: the whole stream's verdict / first error (shard_offset = the
+  // stream offset of shard[0]).
+  bool validate(bytes_view shard, std::uint64_t lane_lo, std::uint64_t lane_hi);
+  verdict validate_verdict(bytes_view shard, std::uint64_t lane_lo, std::uint64_t lane_hi,
+                           std::uint64_t shard_offset);
 
  private:
   void* handle_ = nullptr;

@@ -114,4 +114,69 @@ std::uint64_t lookup_stream::bytes_fed() const {
   return utf8v_cuda_stream_bytes(static_cast<const utf8v_cuda_stream*>(handle_));
 }
 
+static_assert(sizeof(segment_state) == sizeof(utf8v_state), "segment_state mirrors utf8v_state");
+
+segment_state segment_state::of(bytes_view segment) {
+  segment_state s;
+  const int st = utf8v_cuda_segment_state(segment.data(), segment.size(), 0, reinterpret_cast<utf8v_state*>(&s));
+  if (st != UTF8V_OK) raise(st);
+  return s;
+}
+
+segment_state segment_state::then(const segment_state& next) const {
+  segment_state r;
+  utf8v_state_combine(reinterpret_cast<const utf8v_state*>(this), reinterpret_cast<const utf8v_state*>(&next),
+                      reinterpret_cast<utf8v_state*>(&r));
+  return r;
+}
+
+bool segment_state::valid() const { return utf8v_state_valid(reinterpret_cast<const utf8v_state*>(this)) != 0; }
+
+std::vector<segment_state> batch_states(bytes_view data, std::span<const std::uint64_t> offsets) {
+  if (offsets.empty()) return {};
+  std::vector<segment_state> out(offsets.size() - 1);
+  const int st = utf8v_cuda_batch_states(data.data(), data.size(), offsets.data(), offsets.size() - 1, 0,
+                                         reinterpret_cast<utf8v_state*>(out.data()));
+  if (st != UTF8V_OK) raise(st);
+  return out;
+}
+
+std::vector<std::uint8_t> shard_comm::unique_id() {
+  std::vector<std::uint8_t> id(UTF8V_COMM_ID_BYTES);
+  const int st = utf8v_cuda_comm_unique_id(id.data());
+  if (st != UTF8V_OK) raise(st);
+  return id;
+}
+
+shard_comm::shard_comm(std::span<const std::uint8_t> id, int nranks, int rank) {
+  if (id.size() != UTF8V_COMM_ID_BYTES) throw cuda_error(UTF8V_ERR_ARG, "utf8v: unique id must be 128 bytes");
+  utf8v_cuda_comm* c = nullptr;
+  const int st = utf8v_cuda_comm_init_rank(id.data(), nranks, rank, &c);
+  if (st != UTF8V_OK) raise(st);
+  handle_ = c;
+}
+
+shard_comm::~shard_comm() { utf8v_cuda_comm_destroy(static_cast<utf8v_cuda_comm*>(handle_)); }
+
+bool shard_comm::validate(bytes_view shard, std::uint64_t lane_lo, std::uint64_t lane_hi) {
+  std::uint8_t ok = 0;
+  const int st = utf8v_cuda_validate_shard_allreduce(static_cast<utf8v_cuda_comm*>(handle_), shard.data(),
+                                                     shard.size(), lane_lo, lane_hi, 0, &ok);
+  if (st != UTF8V_OK) raise(st);
+  return ok != 0;
+}
+
+verdict shard_comm::validate_verdict(bytes_view shard, std::uint64_t lane_lo, std::uint64_t lane_hi,
+                                     std::uint64_t shard_offset) {
+  std::uint8_t ok = 0;
+  std::uint64_t off = 0;
+  int kind = -1;
+  const int st = utf8v_cuda_verdict_shard_allreduce(static_cast<utf8v_cuda_comm*>(handle_), shard.data(),
+                                                    shard.size(), lane_lo, lane_hi, shard_offset, 0, &ok, &off,
+                                                    &kind);
+  if (st != UTF8V_OK) raise(st);
+  if (ok) return verdict::ok();
+  return verdict::fail(static_cast<std::size_t>(off), static_cast<error_kind>(kind));
+}
+
 }  // namespace utf8v

@@ -294,6 +294,59 @@ TEST(stream, "a stream fed in pieces gives the verdict of the whole (fsm.hpp:15-
   }
 }
 
+TEST(states, "segment states merged in any grouping give the verdict of the whole (fsm.hpp:15-20)") {
+  bytes buf(1 << 14);
+  std::uint64_t s = 11;
+  for (std::uint64_t seed = 1; seed <= 25; ++seed) {
+    for (int strategy = -1; strategy < 7; ++strategy) {
+      const std::size_t n = strategy < 0 ? orc_generate_valid(0xF, 2000, seed, buf.data(), buf.size())
+                                         : orc_generate_invalid(0xF, 2000, seed, strategy, buf.data(), buf.size());
+      if (n == static_cast<std::size_t>(-1)) continue;
+      const bytes b(buf.begin(), buf.begin() + static_cast<std::ptrdiff_t>(n));
+      // cut into pieces of 0..600 bytes, validated one by one (in reverse)
+      std::vector<std::pair<std::size_t, std::size_t>> cuts;
+      for (std::size_t at = 0; at < n;) {
+        const std::size_t len = std::min<std::size_t>(n - at, xorshift(s) % 601);
+        cuts.emplace_back(at, len);
+        at += len;
+      }
+      std::vector<utf8v::segment_state> st(cuts.size());
+      for (std::size_t i = cuts.size(); i-- > 0;)
+        st[i] = utf8v::segment_state::of(utf8v::bytes_view(b.data() + cuts[i].first, cuts[i].second));
+      // right fold and left fold must agree (associativity) and give the verdict
+      utf8v::segment_state left, right;
+      for (const auto& x : st) left = left.then(x);
+      for (std::size_t i = st.size(); i-- > 0;) right = st[i].then(right);
+      CHECK(left.valid() == oracle_ok(b));
+      CHECK(right.valid() == oracle_ok(b));
+      CHECK(left.len == n && right.len == n);
+      // the pieces as records of a batch: per-record states equal the segment states
+      std::vector<std::uint64_t> offs{0};
+      for (const auto& c : cuts) offs.push_back(c.first + c.second);
+      const auto bs = utf8v::batch_states(b, offs);
+      CHECK(bs.size() == st.size());
+      for (std::size_t i = 0; i < bs.size() && i < st.size(); ++i)
+        CHECK(std::memcmp(&bs[i], &st[i], sizeof(utf8v::segment_state)) == 0);
+    }
+  }
+}
+
+TEST(shard_comm, "a one-rank NCCL shard communicator gives the stream's verdict and first error") {
+  const auto id = utf8v::shard_comm::unique_id();
+  utf8v::shard_comm comm(id, 1, 0);
+  bytes buf(1 << 16);
+  for (std::uint64_t seed = 1; seed <= 6; ++seed) {
+    for (int strategy = -1; strategy < 7; ++strategy) {
+      const std::size_t n = strategy < 0 ? orc_generate_valid(0xF, 30000, seed, buf.data(), buf.size())
+                                         : orc_generate_invalid(0xF, 30000, seed, strategy, buf.data(), buf.size());
+      if (n == static_cast<std::size_t>(-1)) continue;
+      const bytes b(buf.begin(), buf.begin() + static_cast<std::ptrdiff_t>(n));
+      CHECK(comm.validate(b, 0, n + 3) == oracle_ok(b));
+      CHECK(comm.validate_verdict(b, 0, n + 3, 0) == oracle_verdict(b));
+    }
+  }
+}
+
 TEST(threads, "validators are callable concurrently (bench.cpp:112-118)") {
   std::vector<bytes> inputs;
   std::vector<utf8v::verdict> want;
