@@ -4,7 +4,10 @@ Each trial draws a record count, a length distribution (lognormal with a
 random median and spread, empty records mixed in), content from the C1 mix,
 a per-record corruption rate and kinds (random byte, lead at the record end,
 stray continuation at its start, a cut inside a character), an alignment
-shift and device or host input; every verdict is compared with the oracle."""
+shift and device or host input; every verdict is compared with the oracle.
+About 30 % of the batches also check per-record segment states (a sample
+against the CPU model, the device fold of all of them against the oracle's
+verdict of the records' concatenation)."""
 import sys
 import time
 from pathlib import Path
@@ -17,14 +20,16 @@ import torch
 
 import paper_2010_03090_b200 as u8
 from paper_2010_03090_b200 import configs
+from paper_2010_03090_b200 import _lib
 from tests import _native as nat
+from tests.test_states import leaf
 
 budget = float(sys.argv[1]) if len(sys.argv) > 1 else 60.0
 seed = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 rng = np.random.default_rng(seed)
 pool = configs.gen_c1(256 << 20, seed=seed).cpu().numpy()
 t0 = time.time()
-trials = records = invalid = 0
+trials = records = invalid = states_checked = 0
 paths = {"K2": 0, "K2L": 0}
 while time.time() - t0 < budget:
     n_rec = int(rng.choice([1, 2, 7, 64, 500, 2048, 5000, 50000, 200000]))
@@ -77,10 +82,26 @@ while time.time() - t0 < budget:
         print(f"MISMATCH trial {trials}: n_rec={n_rec} median={median:.0f} rate={rate} lead={lead} "
               f"records {bad[:10]}", flush=True)
         sys.exit(1)
+    if rng.random() < 0.3:
+        # per-record segment states (K2 in state mode): a sample equals the
+        # CPU model, and the in-order device fold of all of them is the
+        # verdict of the records' concatenation
+        st = u8.batch_states(data, offs)
+        for r in rng.integers(0, n_rec, size=min(n_rec, 100)):
+            rec = data[int(offs[r]):int(offs[r + 1])].tobytes()
+            assert bytes(u8.SegmentState.from_buffer_copy(st[r:r + 1].tobytes())) == bytes(leaf(rec)), (trials, r)
+        d_st = torch.from_numpy(st.view(np.uint8).copy()).cuda()
+        d_out = torch.zeros(24, dtype=torch.uint8, device="cuda")
+        _lib.check(_lib.load().utf8v_cuda_states_reduce_async(d_st.data_ptr(), n_rec, d_out.data_ptr(),
+                                                              torch.cuda.current_stream().cuda_stream))
+        whole = u8.SegmentState.from_buffer_copy(d_out.cpu().numpy().tobytes())
+        cat = data[int(offs[0]):int(offs[-1])]
+        assert u8.state_valid(whole) == (nat.oracle_verdict(cat, threads=16)[0] if cat.size else True), trials
+        states_checked += 1
     large = n_rec <= 2048 and data.size // n_rec >= (64 << 10)
     paths["K2L" if large else "K2"] += 1
     trials += 1
     records += n_rec
     invalid += int((want == 0).sum())
 print(f"stress ok: {trials} batches ({paths}), {records} records ({invalid} invalid), "
-      f"{time.time() - t0:.0f} s, seed {seed}", flush=True)
+      f"{states_checked} with per-record states, {time.time() - t0:.0f} s, seed {seed}", flush=True)
