@@ -445,9 +445,10 @@ __global__ void k_locate_step(StreamDesc d, uint64_t n, const unsigned long long
 // the record's first three lanes or lies past the data, plus one boundary
 // check per record start.  With few records (launch_batch dispatches here
 // for <= kLargeMaxRecords records of >= 64 KiB on average) the sweep is K1's
-// own round-robin loop with no record cursor; the interior loop breaks out
-// at a flagged step (rare: a few per invalid record), which is attributed
-// out of the loop, so the loop keeps K1's registers.  A flagged lane whose
+// own: one 1024-thread CTA per SM drawing steps from a shared pool, no
+// record cursor (C2 back to back over two copies: 51.4 -> 49.2 us against
+// four static 8-warp CTAs per SM, tools/k2cmp.py).  A flagged step (rare: a
+// few per invalid record) is attributed out of line.  A flagged lane whose
 // four chunks lie inside one record settles that record directly; the
 // others recompute the step in natural lane order and find each flagged
 // lane's record by binary search over the offsets held in shared memory.
@@ -525,23 +526,23 @@ __device__ __forceinline__ void attribute_large(const StreamDesc& d, int64_t cst
   }
 }
 
-constexpr int kK2LThreads = kThreads;
-__global__ void __launch_bounds__(kThreads, 4)
+constexpr int kK2LThreads = kK1Threads;
+__global__ void __launch_bounds__(kK1Threads, 1)
     k_batch_large(StreamDesc d, const uint64_t* __restrict__ offsets, int N, uint8_t* __restrict__ verdicts) {
   extern __shared__ int64_t s_off[];  // start(r) in base coordinates, clamped to the data
+  __shared__ unsigned s_ticket;
+  __shared__ unsigned s_zero[32];
   const int64_t nb = d.hi - d.lo;
   for (int i = threadIdx.x; i <= N; i += blockDim.x) {
     const uint64_t o = __ldg(offsets + i);
     s_off[i] = d.off32 + (int64_t)(o < (uint64_t)nb ? o : (uint64_t)nb);
   }
+  if (threadIdx.x == 0) s_ticket = 0;
+  if (threadIdx.x < 32) s_zero[threadIdx.x] = 0;
   __syncthreads();
-  // launched after the verdict initialisation with programmatic
-  // serialisation (launch_batch): verdict stores wait for it
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const int lane = threadIdx.x & 31;
-  // Record boundaries: thread g of the grid takes start(g), g <= N (record
-  // g-1 = [a, s) ends there, record g = [s, b) starts there).
-  const int64_t g = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  const int64_t g = (int64_t)blockIdx.x * kK1Threads + threadIdx.x;
   if (g <= N) {
     const int64_t s = s_off[g], lo = s_off[0], hi = s_off[N];
     const int64_t a = g > 0 ? s_off[g - 1] : s, b = g < N ? s_off[g + 1] : s;
@@ -557,50 +558,39 @@ __global__ void __launch_bounds__(kThreads, 4)
     if ((f & 1u) && g > 0) verdicts[g - 1] = 0;
     if ((f & 2u) && g < N) verdicts[g] = 0;
   }
-  // The sweep: K1's loop; a flagged step is attributed out of line.
-  const int64_t warp = g >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * kThreads) >> 5;
+  const unsigned pool_addr = (unsigned)__cvta_generic_to_shared(&s_ticket) + s_zero[lane];
   const int64_t sb = kStepChunks * (int64_t)kChunkBytes;
   int64_t int_b, int_d;
   interior_steps(d, &int_b, &int_d);
+  const unsigned G = gridDim.x, nsteps = (unsigned)d.steps;
+  const unsigned ib = (unsigned)int_b, id = (unsigned)int_d;
+  const uint8_t* const base = d.base + d.c_begin * kChunkBytes;
   bool was_ascii = true;
   int unused = kU;
-  for (int64_t step = warp; step < d.steps; step += nwarps) {
-    uint32_t e = 0;
-    int64_t cs;
-    if (step >= int_b && step < int_d) {
-      // K1's interior loop; it stops at a flagged step, which is attributed
-      // below (out of the loop, so the loop keeps K1's registers), and the
-      // outer loop resumes with the next step.
-      const int n = (int)((int_d - 1 - step) / nwarps) + 1;
-      const int64_t stride = nwarps * sb;
-      const uint8_t* p = d.base + (d.c_begin + step * kStepChunks) * kChunkBytes;
-      int j = 0;
-      for (; j < n; ++j, p += stride) {
-        Chunk v[kU];
+  unsigned step = blockIdx.x + G * (threadIdx.x >> 5);
+  unsigned next = 0;
+  if (step < nsteps) next = take_ticket(pool_addr, lane, next);
+  while (step < nsteps) {
+    uint32_t e;
+    if (step >= ib && step < id) {
+      const uint8_t* p = base + (int64_t)step * sb;
+      Chunk v[kU];
 #pragma unroll
-        for (int i = 0; i < kU; ++i) v[i] = ld_chunk(p + (lane + 32 * i) * kChunkBytes);
-        uint32_t carry_word = 0, nsw = 0;
-        ld_word_if(lane == 31, p - 4, carry_word);
-        ld_word_if(lane == 0, p + sb, nsw);
-        e = step_errors<false, false>(d, v, 0, lane, carry_word, nsw, unused, was_ascii);
-        if (__any_sync(0xFFFFFFFFu, e != 0u)) break;
-      }
-      if (j == n) {
-        step += (int64_t)(n - 1) * nwarps;
-        continue;
-      }
-      step += (int64_t)j * nwarps;
-      cs = (int64_t)((p - d.base) / kChunkBytes);
+      for (int i = 0; i < kU; ++i) v[i] = ld_chunk(p + (lane + 32 * i) * kChunkBytes);
+      uint32_t carry_word = 0, nsw = 0;
+      ld_word_if(lane == 31, p - 4, carry_word);
+      ld_word_if(lane == 0, p + sb, nsw);
+      e = step_errors<false, false>(d, v, 0, lane, carry_word, nsw, unused, was_ascii);
     } else {
       e = any_step_errors<false>(d, step, false, lane, unused, was_ascii);
-      if (!__any_sync(0xFFFFFFFFu, e != 0u)) continue;
-      cs = d.c_begin + step * kStepChunks;
     }
-    attribute_large(d, cs, e, s_off, N, verdicts);
+    if (__any_sync(0xFFFFFFFFu, e != 0u))
+      attribute_large(d, d.c_begin + (int64_t)step * kStepChunks, e, s_off, N, verdicts);
+    const unsigned t = __shfl_sync(0xFFFFFFFFu, next, 0);
+    step = blockIdx.x + G * (kK1Warps + t);
+    if (step < nsteps) next = take_ticket(pool_addr, lane, next);
   }
 }
-
 }  // namespace u8v
 
 // ---- host-side launchers (called by capi.cu) ------------------------------
@@ -613,7 +603,6 @@ namespace {
 struct DevInfo {
   int k1_ctas = 1;    // resident K1 CTAs (kK1Threads each) on the device
   int k2_warps = 1;   // resident K2 warps (batch.cu)
-  int k2l_warps = 1;  // resident K2L warps
 };
 constexpr int kMaxDev = 64;
 DevInfo g_info[kMaxDev];
@@ -637,7 +626,6 @@ static const DevInfo& dev_info() {
     DevInfo& i = g_info[dev];
     i.k1_ctas = sms * blocks_per_sm((const void*)k_validate, kK1Threads, 0);
     i.k2_warps = sms * batch_blocks_per_sm() * (batch_threads() / 32);
-    i.k2l_warps = sms * blocks_per_sm((const void*)k_batch_large, kK2LThreads, 0) * (kK2LThreads / 32);
   });
   return g_info[dev];
 }
@@ -717,12 +705,7 @@ bool launch_batch_large(const uint8_t* data, uint64_t n, const uint64_t* d_offse
   // Lanes [0, n) of the data buffer: lanes past offsets[N] are ignored and
   // the last record's end is settled by the boundary check at offsets[N].
   const StreamDesc d = make_desc(data, n, 0, n);
-  int64_t warps = dev_info().k2l_warps;
-  if (warps > d.steps) warps = d.steps;
-  if (warps < 1) warps = 1;
-  const int64_t spw = (d.steps + warps - 1) / warps;
-  warps = (d.steps + spw - 1) / spw;
-  int64_t blocks = (warps * 32 + kThreads - 1) / kThreads;
+  int64_t blocks = k1_grid(d);
   const int64_t need = ((int64_t)n_records + kK2LThreads) / kK2LThreads;  // boundary threads: N + 1
   if (blocks < need) blocks = need;
   const size_t smem = (n_records + 1) * sizeof(int64_t);
