@@ -295,9 +295,10 @@ int utf8v_cuda_p2p_reset(utf8v_cuda_p2p* g);
 void utf8v_cuda_p2p_destroy(utf8v_cuda_p2p* g);
 
 /* Frees this thread's per-device resources (streams, the bounded host-input
- * ring of 4 x (32 MiB + 32 B) device bytes, pinned staging, the batch stage);
- * the next call on the thread recreates what it needs.  Also done when the
- * thread exits. */
+ * ring of 4 x (32 MiB + 32 B) device bytes, pinned staging, the batch stage),
+ * and those of the library's persistent shard workers
+ * (utf8v_cuda_validate_sharded); the next call recreates what it needs.
+ * A thread's resources are also freed when it exits. */
 void utf8v_cuda_release_thread_resources(void);
 
 /* Number of kernel launches the last call on this thread enqueued. */

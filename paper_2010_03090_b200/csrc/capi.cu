@@ -361,6 +361,11 @@ class ShardPool {
     static ShardPool* pool = new ShardPool();  // never destroyed: workers outlive exit
     return *pool;
   }
+  // Workers created so far (0 if the pool was never used).
+  int size() {
+    std::lock_guard<std::mutex> turn(call_m_);
+    return (int)workers_.size();
+  }
   // fn(g) for g in [0, n), slot g on worker g; returns when all are done.
   void run(int n, const std::function<void(int)>& fn) {
     std::lock_guard<std::mutex> turn(call_m_);
@@ -564,6 +569,14 @@ int utf8v_cuda_last_launch_count(void) { return t_launches; }
 
 void utf8v_cuda_release_thread_resources(void) {
   for (int d = 0; d < kMaxDevices; ++d) t_ctx[d].release();
+  // The persistent shard workers of utf8v_cuda_validate_sharded hold
+  // per-thread contexts too: release theirs as well.
+  ShardPool& pool = ShardPool::get();
+  const int n = pool.size();
+  if (n > 0)
+    pool.run(n, [](int) {
+      for (int d = 0; d < kMaxDevices; ++d) t_ctx[d].release();
+    });
 }
 
 }  // extern "C"

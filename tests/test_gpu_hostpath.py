@@ -139,3 +139,23 @@ def test_host_input_hbm_is_bounded():
     lib.utf8v_cuda_release_thread_resources()
     free3, _ = torch.cuda.mem_get_info()
     assert free3 >= free0 - (4 << 20)
+
+
+def test_release_frees_the_shard_workers_contexts():
+    """utf8v_cuda_validate_sharded runs its shards on persistent worker
+    threads; utf8v_cuda_release_thread_resources frees their contexts too."""
+    import torch
+    from paper_2010_03090_b200 import _lib, configs
+    lib = _lib.load()
+    h = configs.gen_c1(96 * MiB, seed=44).cpu().numpy()
+    lib.utf8v_cuda_release_thread_resources()
+    torch.cuda.synchronize()
+    free0, _ = torch.cuda.mem_get_info()
+    ok = C.c_uint8(9)
+    _lib.check(lib.utf8v_cuda_validate_sharded(h.ctypes.data, h.size, 3, 0, C.byref(ok)))
+    assert ok.value == 1
+    free1, _ = torch.cuda.mem_get_info()
+    assert free0 - free1 >= 3 * (2 * MiB), "the workers hold their device rings"
+    lib.utf8v_cuda_release_thread_resources()
+    free2, _ = torch.cuda.mem_get_info()
+    assert free2 >= free0 - (4 << 20), ((free0 - free2) >> 20)
