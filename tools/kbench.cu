@@ -147,6 +147,39 @@ __device__ __forceinline__ uint32_t word(uint32_t w, Carry& c, const Cfg& k) {
   }
 }
 
+// V30: the reference's own formulation (classify with the three 16-entry
+// nibble tables T1[prev1 >> 4] & T2[prev1 & 15] & T3[cur >> 4], then the
+// 2/3/4-byte continuation cross-check, proj/include/utf8v/lookup_kernel.hpp:
+// 21-46, tables proj/include/utf8v/tables.hpp:60-99) in 32-bit SWAR: each
+// 16-entry lookup is two PRMTs over the table's four words and a select by
+// the nibble's bit 3.  The north_star's suggested formulation, kept here as
+// the measured comparison for DESIGN.md §2 ("nibble tables" deviation).
+__device__ __forceinline__ uint32_t nib_sel(uint32_t nib) {  // byte-lane nibbles -> PRMT selector
+  uint32_t x = nib & 0x07070707u;
+  x = (x | (x >> 4)) & 0x00770077u;
+  return (x | (x >> 8)) & 0x00007777u;
+}
+__device__ __forceinline__ uint32_t lookup16(uint32_t t0, uint32_t t1, uint32_t t2, uint32_t t3, uint32_t nib) {
+  const uint32_t sel = nib_sel(nib);
+  const uint32_t lo = __byte_perm(t0, t1, sel), hi = __byte_perm(t2, t3, sel);
+  const uint32_t m = ((nib >> 3) & 0x01010101u) * 0xFFu;
+  return (hi & m) | (lo & ~m);
+}
+__device__ __forceinline__ uint32_t word_nib(uint32_t w, Carry& c) {
+  const uint32_t prev1 = __funnelshift_l(c.p, w, 8), prev2 = __funnelshift_l(c.p, w, 16);
+  const uint32_t prev3 = __funnelshift_l(c.p, w, 24);
+  const uint32_t c1 = lookup16(0x02020202u, 0x02020202u, 0x80808080u, 0x49150121u, (prev1 >> 4) & 0x0F0F0F0Fu);
+  const uint32_t c2 = lookup16(0x8383A3E7u, 0xCBCBCB8Bu, 0xCBCBCBCBu, 0xCBCBDBCBu, prev1 & 0x0F0F0F0Fu);
+  const uint32_t c3 = lookup16(0x01010101u, 0x01010101u, 0xBABAAEE6u, 0x01010101u, (w >> 4) & 0x0F0F0F0Fu);
+  const uint32_t cls = c1 & c2 & c3;
+  // bit 7 of each byte: prev2 >= E0 | prev3 >= F0
+  const uint32_t e2 = prev2 & (prev2 << 1) & (prev2 << 2);
+  const uint32_t e3 = prev3 & (prev3 << 1) & (prev3 << 2) & (prev3 << 3);
+  const uint32_t err = ((e2 | e3) & 0x80808080u) ^ cls;
+  c.p = w;
+  return (((err & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | err) & 0x80808080u;  // any bit of a byte -> its bit 7
+}
+
 // V4: R evaluated at the lead's own lane: key from w (s2 = w<<2 gives a5..a0)
 // and the next byte's bits 5,4 via a right funnel with the next word.
 __device__ __forceinline__ uint32_t word4(uint32_t w, uint32_t wn, Carry& c, const Cfg& k) {
@@ -346,6 +379,9 @@ __device__ __forceinline__ void body(const uint8_t* base, int64_t steps, int64_t
         const uint32_t nextw = __shfl_down_sync(0xFFFFFFFFu, v[i][0], 1);
 #pragma unroll
         for (int j = 0; j < 8; ++j) e |= word6(v[i][j], j < 7 ? v[i][j + 1] : nextw, c, k);
+      } else if (V == 30) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) e |= word_nib(v[i][j], c);
       } else if (V == 7) {
         const uint32_t nextw = __shfl_down_sync(0xFFFFFFFFu, v[i][0], 1);
 #pragma unroll
@@ -1164,6 +1200,9 @@ KB_KERNEL(6, 4, 3)
 KB_KERNEL(6, 2, 4)
 KB_KERNEL(7, 4, 3)
 KB_KERNEL(8, 4, 3)
+KB_KERNEL(30, 4, 3)
+KB_KERNEL(30, 4, 4)
+KB_KERNEL(30, 2, 4)
 KB_KERNEL(8, 2, 4)
 KB_KERNEL(8, 4, 2)
 KB_KERNEL(8, 1, 6)
@@ -1201,7 +1240,8 @@ static const Entry kEntries[] = {
     {"v4_u2_b4", k_v4_u2_b4, 2}, {"v0_u4_b3", k_v0_u4_b3, 4}, {"v4_u4_b3", k_v4_u4_b3, 4},
     {"v4_u2_b5", k_v4_u2_b5, 2}, {"v5_u2_b4", k_v5_u2_b4, 2}, {"v5_u4_b3", k_v5_u4_b3, 4},
     {"v6_u4_b3", k_v6_u4_b3, 4}, {"v6_u2_b4", k_v6_u2_b4, 2}, {"v7_u4_b3", k_v7_u4_b3, 4},
-    {"v8_u4_b3", k_v8_u4_b3, 4}, {"v8_u2_b4", k_v8_u2_b4, 2}, {"v8_u4_b2", k_v8_u4_b2, 4}, {"v8_u1_b6", k_v8_u1_b6, 1},
+    {"v30_nibble_tables_u4_b3", k_v30_u4_b3, 4}, {"v30_nibble_tables_u4_b4", k_v30_u4_b4, 4},
+    {"v30_nibble_tables_u2_b4", k_v30_u2_b4, 2}, {"v8_u4_b3", k_v8_u4_b3, 4}, {"v8_u2_b4", k_v8_u2_b4, 2}, {"v8_u4_b2", k_v8_u4_b2, 4}, {"v8_u1_b6", k_v8_u1_b6, 1},
     {"v9_u4_b3", k_v9_u4_b3, 4}, {"v9_u2_b4", k_v9_u2_b4, 2},
     {"v10_u4_b3", k_v10_u4_b3, 4}, {"v10_u4_b4", k_v10_u4_b4, 4}, {"v10_u2_b4", k_v10_u2_b4, 2},
     {"v11_u4_b4", k_v11_u4_b4, 4}, {"v13_u4_b4", k_v13_u4_b4, 4},
