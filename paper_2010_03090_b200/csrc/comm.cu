@@ -109,6 +109,7 @@ struct utf8v_cuda_comm {
   int dev = 0, nranks = 1, rank = 0;
   ncclComm_t nccl = nullptr;
   cudaStream_t s = nullptr;
+  cudaEvent_t ev_legacy = nullptr;  // orders device input after the legacy default stream
   uint32_t* d_buf = nullptr;  // [0] local flag, [1] global flag, [2..3] 64-bit MIN key, [4..5] result
   uint32_t* h_buf = nullptr;  // pinned
 };
@@ -126,6 +127,7 @@ namespace {
 
 int comm_alloc(utf8v_cuda_comm* c) {
   CK(cudaStreamCreateWithFlags(&c->s, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&c->ev_legacy, cudaEventDisableTiming));
   CK(cudaMalloc(&c->d_buf, 64));
   CK(cudaMemset(c->d_buf, 0, 64));
   CK(cudaMallocHost(&c->h_buf, 64));
@@ -140,6 +142,7 @@ void comm_free(utf8v_cuda_comm* c) {
   if (c->nccl && g_nccl.CommDestroy) g_nccl.CommDestroy(c->nccl);
   if (c->d_buf) cudaFree(c->d_buf);
   if (c->h_buf) cudaFreeHost(c->h_buf);
+  if (c->ev_legacy) cudaEventDestroy(c->ev_legacy);
   if (c->s) cudaStreamDestroy(c->s);
   cudaGetLastError();
   delete c;
@@ -247,11 +250,8 @@ int utf8v_cuda_validate_shard_allreduce(utf8v_cuda_comm* c, const uint8_t* p, ui
     CK(cudaMemsetAsync(c->d_buf, 0, 8, c->s));
     // Device input is ordered after the legacy default stream (as the other
     // synchronous entry points).
-    cudaEvent_t ev;
-    CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-    cudaEventRecord(ev, cudaStreamLegacy);
-    cudaStreamWaitEvent(c->s, ev, 0);
-    cudaEventDestroy(ev);
+    CK(cudaEventRecord(c->ev_legacy, cudaStreamLegacy));
+    CK(cudaStreamWaitEvent(c->s, c->ev_legacy, 0));
     if (n > 0 && lane_lo < lane_hi) {
       if (!p) return fail(UTF8V_ERR_ARG, "NULL data");
       u8v::launch_validate(u8v::make_desc(p, n, lane_lo, lane_hi), c->d_buf, c->s);
