@@ -304,6 +304,19 @@ void utf8v_cuda_release_thread_resources(void);
 /* Number of kernel launches the last call on this thread enqueued. */
 int utf8v_cuda_last_launch_count(void);
 
+/* The small-call server (host inputs of at most UTF8V_CUDA_SERVE_MAX bytes to
+ * utf8v_cuda_validate / _validate_verdict / _validate_lanes /
+ * _validate_verdict_lanes): one resident CTA answers requests posted in mapped
+ * pinned memory, without a launch or a stream synchronisation per call.  It
+ * exits after UTF8V_CUDA_SERVE_IDLE_US (default 100) microseconds without a
+ * request, and before any other grid-wide launch of this library;
+ * UTF8V_CUDA_SERVE=0 turns it off.  Replaces nothing in the reference: it is
+ * the latency path of validate_lookup (proj/src/lookup.cpp:39-41) on short
+ * buffers.  Diagnostics: server launches and requests served on this thread
+ * and the current device since the thread's resources were created. */
+#define UTF8V_CUDA_SERVE_MAX 65536
+int utf8v_cuda_serve_stats(uint64_t* out_launches, uint64_t* out_requests);
+
 #ifdef __cplusplus
 }
 #endif

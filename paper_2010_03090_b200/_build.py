@@ -25,7 +25,7 @@ LIB = PKG / "libutf8v_cuda.so"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC,-O3",
                      f"-I{ROOT / 'include'}", "--expt-relaxed-constexpr"]
-CU_SOURCES = ["validate.cu", "batch.cu", "lanes.cu", "gen.cu", "stream.cu", "capi.cu", "comm.cu"]
+CU_SOURCES = ["validate.cu", "batch.cu", "lanes.cu", "gen.cu", "stream.cu", "capi.cu", "comm.cu", "serve.cu"]
 CXX_SOURCES = ["lookup.cpp"]
 
 

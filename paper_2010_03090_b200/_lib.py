@@ -29,6 +29,7 @@ SIGNATURES: dict[str, tuple] = {
     "utf8v_cuda_abi_version": (C.c_int, []),
     "utf8v_cuda_last_error": (C.c_char_p, []),
     "utf8v_cuda_last_launch_count": (C.c_int, []),
+    "utf8v_cuda_serve_stats": (C.c_int, [_u64p, _u64p]),
     "utf8v_cuda_release_thread_resources": (None, []),
     "utf8v_cuda_validate": (C.c_int, [C.c_void_p, C.c_size_t, C.c_int, _u8p]),
     "utf8v_cuda_validate_verdict": (C.c_int, [C.c_void_p, C.c_size_t, C.c_int, _u8p, _u64p,

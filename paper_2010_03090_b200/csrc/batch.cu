@@ -29,6 +29,7 @@
 
 #include "chunk.cuh"
 #include "kernels.cuh"
+#include "serve.h"
 #include "utf8v_state.h"
 #include "utf8v_swar.h"
 
@@ -592,6 +593,7 @@ static void launch_pdl(void (*kernel)(Args...), dim3 grid, dim3 block, size_t sm
 void launch_batch(const uint8_t* data, uint64_t n, const uint64_t* d_offsets, uint64_t n_records,
                   uint8_t* d_verdicts, cudaStream_t st, bool states) {
   if (n_records == 0) return;
+  serve_quiesce();  // K2's grid holds the resident CTAs of every SM (static partition)
   init_verdicts(d_verdicts, n_records, st);
   if (n == 0) return;
   if (!states && launch_batch_large(data, n, d_offsets, n_records, d_verdicts, st)) return;

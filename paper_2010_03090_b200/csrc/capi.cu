@@ -18,6 +18,7 @@
 #include "../../include/utf8v_cuda.h"
 #include "capi_internal.h"
 #include "kernels.cuh"
+#include "serve.h"
 
 namespace u8v_capi {
 
@@ -123,6 +124,7 @@ struct Ctx {
   uint8_t* h_small = nullptr;   // mapped pinned: K1 reads it over PCIe (zero copy)
   uint8_t* dh_small = nullptr;  // its device address
   uint8_t* d_small = nullptr;   // device copy for the small verdict path
+  u8v::Server srv;              // the small-call server (serve.cu), <= kServeMax bytes
   // Batch from host memory: the whole data array (kept up to kKeepStage).
   uint8_t* d_stage = nullptr;
   size_t stage_cap = 0;
@@ -135,6 +137,7 @@ struct Ctx {
     int cur = -1;
     cudaGetDevice(&cur);
     cudaSetDevice(dev);
+    srv.release();
     if (s_comp) cudaStreamSynchronize(s_comp);
     if (s_copy) cudaStreamSynchronize(s_copy);
     for (void* p : {(void*)d_flag, (void*)d_pos, (void*)d_kind, (void*)d_lanes, (void*)d_ok, (void*)d_stage,
@@ -567,6 +570,18 @@ const char* utf8v_cuda_last_error(void) { return t_err.c_str(); }
 
 int utf8v_cuda_last_launch_count(void) { return t_launches; }
 
+int utf8v_cuda_serve_stats(uint64_t* out_launches, uint64_t* out_requests) {
+  if (!out_launches || !out_requests) return fail(UTF8V_ERR_ARG, "NULL output");
+  int dev = -1;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) {
+    cudaGetLastError();
+    return fail(UTF8V_ERR_NO_DEVICE, "no CUDA device");
+  }
+  *out_launches = t_ctx[dev].srv.launches;
+  *out_requests = t_ctx[dev].srv.requests;
+  return UTF8V_OK;
+}
+
 void utf8v_cuda_release_thread_resources(void) {
   for (int d = 0; d < kMaxDevices; ++d) t_ctx[d].release();
   // The persistent shard workers of utf8v_cuda_validate_sharded hold
@@ -590,6 +605,15 @@ int flag_lanes(const uint8_t* p, uint64_t n, uint64_t lane_lo, uint64_t lane_hi,
   Ctx* c;
   int st = get_ctx(&c);
   if (st) return st;
+  if (!is_device && n <= u8v::kServeMax && u8v::serve_enabled()) {
+    st = c->srv.ensure(c->dev);
+    if (st) return st;
+    u8v::ServeReply r;
+    st = c->srv.call(p, n, lane_lo, lane_hi, false, &r);
+    if (st) return st;
+    *out = r.flag;
+    return UTF8V_OK;
+  }
   if (!is_device && n <= kZeroCopy) return validate_small(*c, p, n, lane_lo, lane_hi, out);
   CK(cudaMemsetAsync(c->d_flag, 0, 4, c->s_comp));
   if (is_device) {
@@ -673,6 +697,19 @@ int verdict_lanes(const uint8_t* p, uint64_t n, uint64_t lane_lo, uint64_t lane_
     st = after_legacy(c->s_comp, c->ev_legacy);
     if (st) return st;
     return device_verdict(c, p, n, lane_lo, lane_hi, out_valid, out_offset, out_kind);
+  }
+  if (n <= u8v::kServeMax && u8v::serve_enabled()) {
+    st = c->srv.ensure(c->dev);
+    if (st) return st;
+    u8v::ServeReply r;
+    st = c->srv.call(p, n, lane_lo, lane_hi, true, &r);
+    if (st) return st;
+    if (!r.flag) return UTF8V_OK;
+    if (r.kind < 0) return fail(UTF8V_ERR_CUDA, "flagged input but the window decode found no error");
+    *out_valid = 0;
+    *out_offset = r.offset;
+    *out_kind = r.kind;
+    return UTF8V_OK;
   }
   if (n <= kSmall) {
     st = ensure_small(*c);

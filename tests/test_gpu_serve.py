@@ -1,0 +1,253 @@
+"""The small-call server (csrc/serve.cu): host inputs of at most
+UTF8V_CUDA_SERVE_MAX bytes answered by a resident CTA polling a mailbox in
+mapped pinned memory.  Verdicts and first-error positions against the
+oracle (proj/src/oracle.cpp:10-44), lane ranges against the SWAR checker,
+exhaustive short inputs, the idle exit and relaunch, the epoch that clears
+servers before grid-wide kernels, device synchronisation bounded by the idle
+limit, concurrent callers, and UTF8V_CUDA_SERVE=0."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+import pytest
+
+from tests import _native as nat
+
+pytestmark = pytest.mark.gpu
+
+SERVE_MAX = 65536
+BAD = [[0xC0, 0x80], [0xC1, 0xBF], [0xE0, 0x80, 0x80], [0xED, 0xA0, 0x80], [0xF4, 0x90, 0x80, 0x80],
+       [0xF0, 0x8F, 0xBF, 0xBF], [0x80], [0xBF], [0xF5], [0xFF], [0xE1, 0x41], [0xF0, 0x9F, 0x98],
+       [0xE2, 0x82], [0xC3]]
+
+
+def _lib():
+    from paper_2010_03090_b200 import _lib
+    return _lib, _lib.load()
+
+
+def _stats():
+    L, lib = _lib()
+    a, b = C.c_uint64(0), C.c_uint64(0)
+    L.check(lib.utf8v_cuda_serve_stats(C.byref(a), C.byref(b)))
+    return a.value, b.value
+
+
+def _validate(buf: np.ndarray) -> bool:
+    L, lib = _lib()
+    ok = C.c_uint8(9)
+    L.check(lib.utf8v_cuda_validate(buf.ctypes.data, buf.size, 0, C.byref(ok)))
+    return bool(ok.value)
+
+
+def _verdict(buf: np.ndarray):
+    L, lib = _lib()
+    ok, off, kind = C.c_uint8(9), C.c_uint64(0), C.c_int(-7)
+    L.check(lib.utf8v_cuda_validate_verdict(buf.ctypes.data, buf.size, 0, C.byref(ok), C.byref(off),
+                                            C.byref(kind)))
+    return (True, None, None) if ok.value else (False, off.value, kind.value)
+
+
+def _text(n: int, seed: int) -> np.ndarray:
+    # valid mixed-length text, cut to n bytes (a cut character is a
+    # too-short error at the end: the oracle decides either way)
+    raw = nat.generate_valid(0b1111, n + 8, seed)
+    return np.frombuffer(raw[:n], np.uint8).copy()
+
+
+SIZES = [1, 2, 3, 4, 5, 15, 16, 17, 31, 32, 33, 35, 63, 64, 65, 100, 255, 256, 257, 1000, 4093, 4096, 4099,
+         8191, 16383, 16384, 16387, 32768, 40000, 65531, 65532, 65533, 65534, 65535, 65536]
+
+
+@pytest.mark.parametrize("n", SIZES)
+def test_sizes_and_errors_vs_oracle(n):
+    rng = np.random.default_rng(n)
+    _, req0 = _stats()
+    base = _text(n, seed=n)
+    cases = [base]
+    for _ in range(12):
+        b = base.copy()
+        seq = BAD[int(rng.integers(len(BAD)))]
+        at = int(rng.integers(0, n))
+        b[at:at + len(seq)] = seq[:n - at]
+        cases.append(b)
+    for at in (0, n - 1, n - 2, n - 3):  # errors at the very edges
+        if at >= 0:
+            b = base.copy()
+            b[at] = 0xF0
+            cases.append(b)
+    for b in cases:
+        want = nat.oracle_verdict(b)
+        assert _validate(b) == want[0]
+        assert _verdict(b) == want
+    _, req1 = _stats()
+    assert req1 - req0 == 2 * len(cases)    # every call went through the server
+
+
+def test_random_fuzz_vs_oracle():
+    rng = np.random.default_rng(11)
+    for it in range(3000):
+        n = int(rng.integers(1, 600)) if it % 3 else int(rng.integers(1, SERVE_MAX + 1))
+        b = _text(n, seed=1000 + it)
+        for _ in range(int(rng.integers(0, 3))):
+            seq = BAD[int(rng.integers(len(BAD)))]
+            at = int(rng.integers(0, n))
+            b[at:at + len(seq)] = seq[:n - at]
+        want = nat.oracle_verdict(b)
+        assert _verdict(b) == want, (it, n)
+        assert _validate(b) == want[0]
+
+
+@pytest.mark.parametrize("length", [1, 2])
+def test_exhaustive_short_inputs_through_the_server(length):
+    data, ver = nat.exhaustive(length)
+    L, lib = _lib()
+    ok = C.c_uint8(9)
+    for i in range(ver.size):
+        b = data[i * length:(i + 1) * length]
+        L.check(lib.utf8v_cuda_validate(b.ctypes.data, length, 0, C.byref(ok)))
+        assert ok.value == ver[i], bytes(b).hex()
+
+
+def test_lane_ranges_vs_swar_checker():
+    L, lib = _lib()
+    rng = np.random.default_rng(5)
+    flag = C.c_uint32(9)
+    ok, off, kind = C.c_uint8(9), C.c_uint64(0), C.c_int(-7)
+    for it in range(800):
+        n = int(rng.integers(1, 2000)) if it % 2 else int(rng.integers(1, SERVE_MAX + 1))
+        b = _text(n, seed=50_000 + it)
+        if it % 3:
+            seq = BAD[int(rng.integers(len(BAD)))]
+            at = int(rng.integers(0, n))
+            b[at:at + len(seq)] = seq[:n - at]
+        lo = int(rng.integers(0, n + 4))
+        hi = int(rng.integers(lo, n + 4))
+        L.check(lib.utf8v_cuda_validate_lanes(b.ctypes.data, n, lo, hi, 0, C.byref(flag)))
+        want = nat.swar().swar_lanes(b.ctypes.data, n, lo, hi)
+        assert bool(flag.value) == bool(want), (n, lo, hi)
+        # the verdict of a lane range: the first error the range flags
+        L.check(lib.utf8v_cuda_validate_verdict_lanes(b.ctypes.data, n, lo, hi, 0, C.byref(ok), C.byref(off),
+                                                      C.byref(kind)))
+        assert bool(ok.value) == (not want)
+        if not ok.value:
+            # same answer as the device-input path (K1 tracking + K3)
+            import torch
+            d = torch.from_numpy(b).cuda()
+            ok2, off2, kind2 = C.c_uint8(9), C.c_uint64(0), C.c_int(-7)
+            L.check(lib.utf8v_cuda_validate_verdict_lanes(d.data_ptr(), n, lo, hi, 1, C.byref(ok2), C.byref(off2),
+                                                          C.byref(kind2)))
+            assert (ok.value, off.value, kind.value) == (ok2.value, off2.value, kind2.value)
+
+
+def test_idle_exit_and_relaunch():
+    b = _text(4096, seed=3)
+    want = nat.oracle_verdict(b)
+    assert _verdict(b) == want
+    l0, r0 = _stats()
+    for _ in range(200):
+        _validate(b)
+    l1, r1 = _stats()
+    assert r1 - r0 == 200 and l1 == l0     # resident across back-to-back calls
+    for _ in range(5):
+        time.sleep(0.005)                  # > the 100 us idle limit
+        assert _verdict(b) == want         # the relaunched server takes the pending request
+    l2, _ = _stats()
+    assert l2 - l1 == 5                    # one relaunch per idle gap
+
+
+def test_grid_kernels_clear_the_server_and_sync_is_bounded():
+    import torch
+    big = torch.full((256 << 20,), 0x41, dtype=torch.uint8, device="cuda")
+    L, lib = _lib()
+    ok = C.c_uint8(9)
+    # baseline: a 256 MiB device call with no server around
+    L.check(lib.utf8v_cuda_validate(big.data_ptr(), big.numel(), 1, C.byref(ok)))
+    t = time.perf_counter()
+    for _ in range(5):
+        L.check(lib.utf8v_cuda_validate(big.data_ptr(), big.numel(), 1, C.byref(ok)))
+    base = (time.perf_counter() - t) / 5
+    small = np.frombuffer(b"small input \xc3\xa9" * 50, np.uint8).copy()
+    worst = 0.0
+    for _ in range(5):
+        assert _validate(small)            # server resident now
+        t = time.perf_counter()
+        L.check(lib.utf8v_cuda_validate(big.data_ptr(), big.numel(), 1, C.byref(ok)))
+        worst = max(worst, time.perf_counter() - t)
+        assert ok.value == 1
+    assert worst < base + 0.002, (worst, base)  # the K1 grid did not wait for a server's SM
+    assert _validate(small)
+    t = time.perf_counter()
+    torch.cuda.synchronize()               # waits for the server's idle exit at most
+    assert time.perf_counter() - t < 0.05
+
+
+def test_concurrent_callers_and_grid_kernels():
+    import torch
+    errors = []
+    big = torch.from_numpy(_text(32 << 20, seed=77)).cuda()
+    want_big = nat.oracle_verdict(big.cpu().numpy(), threads=8)[0]
+
+    def small_worker(k):
+        try:
+            rng = np.random.default_rng(k)
+            for it in range(300):
+                n = int(rng.integers(1, 20000))
+                b = _text(n, seed=k * 10_000 + it)
+                if it % 2:
+                    b[int(rng.integers(0, n))] = 0xC0
+                if _verdict(b) != nat.oracle_verdict(b):
+                    errors.append((k, it))
+            _, lib = _lib()
+            lib.utf8v_cuda_release_thread_resources()
+        except Exception as e:  # noqa: BLE001
+            errors.append(repr(e))
+
+    def big_worker():
+        try:
+            torch.cuda.set_device(0)
+            L, lib = _lib()
+            ok = C.c_uint8(9)
+            for _ in range(40):
+                L.check(lib.utf8v_cuda_validate(big.data_ptr(), big.numel(), 1, C.byref(ok)))
+                if bool(ok.value) != want_big:
+                    errors.append("big")
+            lib.utf8v_cuda_release_thread_resources()
+        except Exception as e:  # noqa: BLE001
+            errors.append(repr(e))
+
+    ts = [threading.Thread(target=small_worker, args=(k,)) for k in range(6)] + [threading.Thread(target=big_worker)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=300)
+    assert not any(t.is_alive() for t in ts)
+    assert not errors, errors[:5]
+
+
+def test_server_disabled_by_env():
+    code = (
+        "import ctypes as C, numpy as np\n"
+        "from paper_2010_03090_b200 import _lib\n"
+        "lib = _lib.load()\n"
+        "b = np.frombuffer(b'abc\\xc3\\xa9' * 100, np.uint8).copy()\n"
+        "ok = C.c_uint8(9)\n"
+        "_lib.check(lib.utf8v_cuda_validate(b.ctypes.data, b.size, 0, C.byref(ok)))\n"
+        "assert ok.value == 1\n"
+        "b[7] = 0xC0\n"
+        "_lib.check(lib.utf8v_cuda_validate(b.ctypes.data, b.size, 0, C.byref(ok)))\n"
+        "assert ok.value == 0\n"
+        "a, r = C.c_uint64(9), C.c_uint64(9)\n"
+        "_lib.check(lib.utf8v_cuda_serve_stats(C.byref(a), C.byref(r)))\n"
+        "assert (a.value, r.value) == (0, 0), (a.value, r.value)\n"
+        "print('ok')\n")
+    env = dict(os.environ, UTF8V_CUDA_SERVE="0")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
