@@ -204,6 +204,109 @@ __device__ __forceinline__ void attribute_step(RecView d, int64_t s0, int64_t hi
   }
 }
 
+
+// The usual flagged step of a mostly-valid batch, settled without building
+// the attribution window: one lane (src) has flagged chunks, they lie inside
+// one record at least three bytes past its start and before the data end --
+// one verdict store.  The record is found directly in the two consecutive
+// batches of starts the warp holds (T, the taken batch in shared memory, and
+// nx, the next one, both relative to range_lo): no start in (ql, qh], the
+// last start <= ql.  Chunk granularity ([ql, qh] spans src's flagged chunks);
+// anything else (a flagged chunk near a record start, dense records, several
+// flagged lanes) returns false for the exact attribution.
+__device__ __forceinline__ bool settle_fast(const RecView& d, const int* T, int nx, int64_t rb, int s0, int hi_rel,
+                                            uint32_t e0, uint32_t e1, uint32_t e2, uint32_t e3, int src) {
+  const int lane = threadIdx.x & 31;
+  const int cl = 2 * lane + (e0 ? 0 : (e1 ? 1 : (e2 ? 64 : 65)));
+  const int ch = 2 * lane + (e3 ? 65 : (e2 ? 64 : (e1 ? 1 : 0)));
+  const int ql = s0 + __shfl_sync(0xFFFFFFFFu, cl, src) * kChunkBytes;
+  const int qh = s0 + __shfl_sync(0xFFFFFFFFu, ch, src) * kChunkBytes + kChunkBytes - 1;
+  const unsigned nl = __ballot_sync(0xFFFFFFFFu, nx <= ql);
+  if (nl != __ballot_sync(0xFFFFFFFFu, nx <= qh) || nl == 0xFFFFFFFFu) return false;
+  int start;
+  int64_t r;
+  if (nl) {
+    const int L = 31 - __clz(nl);
+    start = __shfl_sync(0xFFFFFFFFu, nx, L);
+    r = rb + L;
+  } else {
+    const int tv = T[lane];
+    const unsigned tl = __ballot_sync(0xFFFFFFFFu, tv <= ql);
+    if (tl == 0u || tl != __ballot_sync(0xFFFFFFFFu, tv <= qh)) return false;
+    const int L = 31 - __clz(tl);
+    start = __shfl_sync(0xFFFFFFFFu, tv, L);
+    r = rb - 32 + L;
+  }
+  if (ql < start + 3 || qh >= hi_rel) return false;
+  if (lane == 0 && r < d.n_records) d.verdicts[r] = 0;
+  return true;
+}
+
+// attribute_step when exactly one lane (src) of the warp has flagged bits
+// and settle_fast did not apply.  Its masks are broadcast and the warp walks
+// their bits together, one flagged lane q per iteration: its window slot is
+// the last lane whose start is <= q (one ballot: the window is ascending),
+// instead of the 5-round shuffle search per round of attribute_step.
+template <bool kState>
+__device__ __forceinline__ void attribute_lane(RecView d, int64_t s0, int64_t hi, uint32_t e0, uint32_t e1,
+                                               uint32_t e2, uint32_t e3, int o, int64_t r0, int src) {
+  const int lane = threadIdx.x & 31;
+  const int hi_rel = rel32(hi, s0);
+  uint32_t f0 = __shfl_sync(0xFFFFFFFFu, e0, src), f1 = __shfl_sync(0xFFFFFFFFu, e1, src);
+  uint32_t f2 = __shfl_sync(0xFFFFFFFFu, e2, src), f3 = __shfl_sync(0xFFFFFFFFu, e3, src);
+  const bool full = __all_sync(0xFFFFFFFFu, o < kStepChunks * kChunkBytes);
+  while ((f0 | f1 | f2 | f3) != 0u) {  // warp-uniform
+    // chunks of lane src in the paired layout: 2 src, 2 src + 1, 64 + 2 src, 64 + 2 src + 1
+    int c = 2 * src;
+    uint32_t e;
+    if (f0) {
+      e = f0;
+      f0 &= f0 - 1;
+    } else if (f1) {
+      e = f1;
+      f1 &= f1 - 1;
+      c += 1;
+    } else if (f2) {
+      e = f2;
+      f2 &= f2 - 1;
+      c += 64;
+    } else {
+      e = f3;
+      f3 &= f3 - 1;
+      c += 65;
+    }
+    const int q = c * kChunkBytes + (int)u8v_perm_byte((unsigned)(__ffs(e) - 1));
+    const unsigned le = __ballot_sync(0xFFFFFFFFu, o <= q);
+    const int L = le ? 31 - __clz(le) : 0;
+    const int start = __shfl_sync(0xFFFFFFFFu, o, L);
+    const int nxt = kState ? __shfl_sync(0xFFFFFFFFu, o, (L + 1) & 31) : 0;
+    if (lane == 0 && q < hi_rel && q >= start) {
+      int64_t r = r0 + L;
+      int64_t st_abs = s0 + start;
+      int64_t end_abs = s0 + nxt;
+      if (full && L == 31) {  // dense records: as attribute_step
+        const int64_t qa = s0 + q;
+        int64_t a = r, span = 4;
+        while (a + span <= d.n_records && rec_start(d, a + span) <= qa) {
+          a += span;
+          span <<= 1;
+        }
+        int64_t b = a + span - 1 < d.n_records ? a + span - 1 : d.n_records;
+        while (a < b) {
+          const int64_t mid = (a + b + 1) >> 1;
+          if (rec_start(d, mid) <= qa) a = mid;
+          else b = mid - 1;
+        }
+        r = a;
+        st_abs = rec_start(d, r);
+      }
+      if (kState && (L == 31 || r != r0 + L)) end_abs = rec_start(d, r + 1);
+      if (r < d.n_records && s0 + q - st_abs >= 3 && (!kState || s0 + q < end_abs - 1)) d.verdicts[r] = 0;
+    }
+  }
+}
+
+
 // Record boundaries, a batch of 32 starts at a time (lane L: start rb + L
 // at o, relative to the warp's range_lo, a multiple of 32).  The taken
 // batch waits in shared memory, not registers (the sweep needs them all):
@@ -215,6 +318,7 @@ __device__ __forceinline__ void attribute_step(RecView d, int64_t s0, int64_t hi
 struct WarpCtx {
   int64_t lo, hi, c_end, range_lo, rb;
   int prev_last, range_rel;
+  int hi_rel;  // hi - range_lo (clamped, rel32)
   int taken;  // a batch sits in the slot (starts rb-32 .. rb-1)
 };
 
@@ -379,6 +483,7 @@ __global__ void __launch_bounds__(kK2Threads, kK2Blocks) k_batch(BatchDesc d) {
   cx->prev_last = prev_last;
   cx->taken = 0;
   cx->range_rel = range_rel;
+  cx->hi_rel = rel32(d.hi, range_lo);
   bool pend = false;
   bool was_ascii = true;
 
@@ -454,12 +559,23 @@ __global__ void __launch_bounds__(kK2Threads, kK2Blocks) k_batch(BatchDesc d) {
         any |= err[i];
       }
       was_ascii = __all_sync(0xFFFFFFFFu, h7 == 0);
-      if (__any_sync(0xFFFFFFFFu, any != 0u)) {
+#ifdef U8V_K2_NO_ATTR  // DEVELOPMENT (tools/kvar.sh): the sweep without attribution
+      const unsigned flagged = __ballot_sync(0xFFFFFFFFu, any == 0xFFFFFFFFu);
+#else
+      const unsigned flagged = __ballot_sync(0xFFFFFFFFu, any != 0u);
+#endif
+      if (flagged) {
         // Window: lane L = start(r0 + L) - s0 with start(r0) <= s0 (or r0 = 0):
         // the taken batch's last start (< s0, else that batch would not have
         // been taken) followed by the next batch's first 31.
         const int s0 = j * kStepBytes;
         const int64_t rbc = cx->rb;
+#ifndef U8V_K2_NO_LANE_PATH
+        if (!kState && (flagged & (flagged - 1)) == 0 && cx->taken &&
+            settle_fast(rv, sl->o, nx, rbc, s0, cx->hi_rel, err[0], err[1], err[2], err[3], __ffs(flagged) - 1))
+          goto settled;
+#endif
+        {
         int o;
         int64_t r0;
         if (cx->taken) {
@@ -479,9 +595,17 @@ __global__ void __launch_bounds__(kK2Threads, kK2Blocks) k_batch(BatchDesc d) {
           o = (rbc == 0 ? nx : (lane == 0 ? cx->prev_last : up)) - s0;
           r0 = rbc == 0 ? 0 : rbc - 1;
         }
-        attribute_step<kState>(rv, cx->range_lo + s0, cx->hi, err[0], err[1], err[2], err[3], o, r0);
+#ifndef U8V_K2_NO_LANE_PATH
+        if ((flagged & (flagged - 1)) == 0)
+          attribute_lane<kState>(rv, cx->range_lo + s0, cx->hi, err[0], err[1], err[2], err[3], o, r0,
+                                 __ffs(flagged) - 1);
+        else
+#endif
+          attribute_step<kState>(rv, cx->range_lo + s0, cx->hi, err[0], err[1], err[2], err[3], o, r0);
+        }
       }
     }
+  settled:
     if (lane == 31) carry_word = v[kU - 1].w[kChunkWords - 1];
 
     // Boundary batches: the pending one is checked a step after it was
