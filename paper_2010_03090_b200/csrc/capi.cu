@@ -265,6 +265,35 @@ int ensure_small(Ctx& c) {
   return UTF8V_OK;
 }
 
+// Stream-ordered scratch of the batch entry points from a per-device pool
+// that keeps up to kPoolKeep bytes mapped between calls: the default pool
+// returns its memory at every synchronisation, and mapping it again cost
+// ~0.4 ms per small host batch call.
+constexpr uint64_t kPoolKeep = 256ull << 20;
+cudaMemPool_t g_pool[kMaxDevices];
+std::once_flag g_pool_once[kMaxDevices];
+
+int pool_alloc(void** p, size_t bytes, cudaStream_t s) {
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  cudaError_t err = cudaSuccess;
+  std::call_once(g_pool_once[dev], [dev, &err] {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    err = cudaMemPoolCreate(&g_pool[dev], &props);
+    if (err == cudaSuccess) {
+      uint64_t keep = kPoolKeep;
+      err = cudaMemPoolSetAttribute(g_pool[dev], cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  });
+  if (err != cudaSuccess) return fail(UTF8V_ERR_CUDA, "cudaMemPoolCreate", err);
+  if (!g_pool[dev]) return fail(UTF8V_ERR_CUDA, "no memory pool (an earlier creation failed)");
+  CK(cudaMallocFromPoolAsync(p, bytes, g_pool[dev], s));
+  return UTF8V_OK;
+}
+
 int check_launch(const char* what) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(UTF8V_ERR_CUDA, what, e);
@@ -839,10 +868,21 @@ int utf8v_cuda_validate_batch(const uint8_t* data, size_t n, const uint64_t* off
   Ctx* c;
   int st = get_ctx(&c);
   if (st) return st;
+  if (u8v::serve_enabled() && n_records <= u8v::kServeMaxRecords &&
+      offsets[n_records] - offsets[0] <= u8v::kServeMax) {  // small batch: the server
+    st = c->srv.ensure(c->dev);
+    if (st) return st;
+    return c->srv.call_batch(data, offsets, n_records, verdicts);
+  }
   uint64_t* d_off = nullptr;
   uint8_t* d_ver = nullptr;
-  CK(cudaMallocAsync(&d_off, (n_records + 1) * 8, c->s_comp));
-  CK(cudaMallocAsync(&d_ver, n_records, c->s_comp));
+  st = pool_alloc((void**)&d_off, (n_records + 1) * 8, c->s_comp);
+  if (st) return st;
+  st = pool_alloc((void**)&d_ver, n_records, c->s_comp);
+  if (st) {
+    cudaFreeAsync(d_off, c->s_comp);
+    return st;
+  }
   CK(cudaMemcpyAsync(d_off, offsets, (n_records + 1) * 8, cudaMemcpyHostToDevice, c->s_comp));
   if (n > 0) {
     st = stage_h2d(*c, data, n);
@@ -969,7 +1009,8 @@ int utf8v_cuda_batch_states_async(const uint8_t* d_data, uint64_t n, const uint6
   if (st) return st;
   cudaStream_t s = (cudaStream_t)stream;
   uint8_t* d_clean = nullptr;
-  CK(cudaMallocAsync(&d_clean, n_records, s));
+  st = pool_alloc((void**)&d_clean, n_records, s);
+  if (st) return st;
   u8v::launch_batch(d_data, n, d_offsets, n_records, d_clean, s, true);
   u8v::launch_record_states(d_data, n, d_offsets, n_records, d_clean, reinterpret_cast<u8v_state*>(d_states), s);
   t_launches += n > 0 ? 3 : 2;
@@ -998,8 +1039,13 @@ int utf8v_cuda_batch_states(const uint8_t* data, size_t n, const uint64_t* offse
   if (offsets[n_records] > n) return fail(UTF8V_ERR_ARG, "offsets exceed data size");
   uint64_t* d_off = nullptr;
   utf8v_state* d_st = nullptr;
-  CK(cudaMallocAsync(&d_off, (n_records + 1) * 8, c->s_comp));
-  CK(cudaMallocAsync(&d_st, n_records * sizeof(utf8v_state), c->s_comp));
+  st = pool_alloc((void**)&d_off, (n_records + 1) * 8, c->s_comp);
+  if (st) return st;
+  st = pool_alloc((void**)&d_st, n_records * sizeof(utf8v_state), c->s_comp);
+  if (st) {
+    cudaFreeAsync(d_off, c->s_comp);
+    return st;
+  }
   CK(cudaMemcpyAsync(d_off, offsets, (n_records + 1) * 8, cudaMemcpyHostToDevice, c->s_comp));
   if (n > 0) {
     st = stage_h2d(*c, data, n);

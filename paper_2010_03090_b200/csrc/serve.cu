@@ -60,25 +60,37 @@ constexpr int kServeThreads = 1024;
 constexpr unsigned kStageBytes = kServeMax + 2 * kChunkBytes;
 constexpr int kLoads = (kStageBytes / 16 + kServeThreads - 1) / kServeThreads;  // uint4 per thread
 
-// Request word: n (bits 0-16), lane_lo (17-33), lane_hi (34-50), verdict
-// mode (51), sequence (52-63, never 0).
-__host__ __device__ __forceinline__ unsigned req_seq(unsigned long long r) { return (unsigned)(r >> 52); }
+// Request word: n (bits 0-16), lane_lo or the record count (17-33), lane_hi
+// (34-50), mode (51-52), sequence (53-63, never 0).
+enum { kModeFlag = 0, kModeVerdict = 1, kModeBatch = 2 };
+constexpr unsigned kSeqMax = 2047;
+__host__ __device__ __forceinline__ unsigned req_seq(unsigned long long r) { return (unsigned)(r >> 53); }
 __host__ __device__ __forceinline__ unsigned req_n(unsigned long long r) { return (unsigned)(r & 0x1FFFF); }
 __host__ __device__ __forceinline__ unsigned req_lo(unsigned long long r) { return (unsigned)((r >> 17) & 0x1FFFF); }
 __host__ __device__ __forceinline__ unsigned req_hi(unsigned long long r) { return (unsigned)((r >> 34) & 0x1FFFF); }
-__host__ __device__ __forceinline__ bool req_verdict(unsigned long long r) { return (r >> 51) & 1; }
+__host__ __device__ __forceinline__ unsigned req_mode(unsigned long long r) { return (unsigned)((r >> 51) & 3); }
 // Reply word: flag (bit 0), kind + 1 (bits 1-4, 0 = none), offset (5-21),
-// sequence (52-63).
+// sequence (53-63).
 
-// Mailbox layout in the mapped pinned buffer (one 64-byte line per word).
+// Mailbox layout in the mapped pinned buffer (one 64-byte line per word;
+// batch mode: the records' 32-bit offsets and the verdicts the server
+// writes back).
 constexpr size_t kReqOff = 0, kRespOff = 64, kExitOff = 128, kDataOff = 256;
-constexpr size_t kMailboxBytes = kDataOff + kStageBytes + 64;
+constexpr size_t kOffsOff = kDataOff + kStageBytes + 64;
+constexpr size_t kVerOff = kOffsOff + 4 * (kServeMaxRecords + 1 + 15);
+constexpr size_t kMailboxBytes = kVerOff + kServeMaxRecords + 64;
+// Shared memory: the staged bytes, then (batch mode) offsets and verdicts.
+constexpr size_t kSmemOffs = kStageBytes;
+constexpr size_t kSmemVer = kSmemOffs + 4 * (kServeMaxRecords + 1 + 3);
+constexpr size_t kSmemBytes = kSmemVer + kServeMaxRecords;
 
 struct ServeArgs {
   const unsigned long long* req;
   unsigned long long* resp;
   unsigned long long* exit_word;
   const uint4* data;
+  const uint32_t* offs;  // batch mode: R + 1 offsets (relative to the data)
+  uint32_t* verdicts;    // batch mode: R verdict bytes (mapped host memory)
   const unsigned long long* epoch;
   unsigned long long epoch0;
   unsigned long long idle_ns;
@@ -95,6 +107,63 @@ __device__ __forceinline__ unsigned long long ld_relaxed_sys(const unsigned long
 }
 __device__ __forceinline__ void st_relaxed_sys(unsigned long long* p, unsigned long long v) {
   asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Batch mode (the K2 decomposition of batch.cu over shared memory; proven
+// against per-record validation by tests/test_swar.py::test_k2_*): every
+// flagged lane of the unbounded stream is attributed to its record unless
+// it is one of that record's first three lanes or lies past the data, and
+// every record start (and the data end) runs u8v_boundary_errors on the
+// bytes around it.  R records, offsets s_off[0..R] relative to the staged
+// bytes (s_off[0] = 0, s_off[R] = n); verdicts in s_ver.
+__device__ __forceinline__ unsigned last_start_le(const uint32_t* s_off, unsigned R, unsigned q) {
+  unsigned a = 0, b = R - 1;  // largest r in [0, R-1] with s_off[r] <= q (s_off[0] = 0 <= q)
+  while (a < b) {
+    const unsigned m = (a + b + 1) >> 1;
+    if (s_off[m] <= q) a = m;
+    else b = m - 1;
+  }
+  return a;
+}
+
+__device__ void serve_batch(const uint8_t* s_bytes, const uint32_t* sw, const uint32_t* s_off, uint8_t* s_ver,
+                            unsigned n, unsigned R, u8v_consts k) {
+  const unsigned t = threadIdx.x;
+  const unsigned c_end = (n + kChunkBytes - 1) / kChunkBytes;
+  for (unsigned c = t; c < c_end; c += kServeThreads) {
+    Chunk v;
+#pragma unroll
+    for (int j = 0; j < kChunkWords; ++j) v.w[j] = sw[c * kChunkWords + j];
+    const uint32_t prev = c ? sw[c * kChunkWords - 1] : 0u;
+    const uint32_t next = sw[(c + 1) * kChunkWords];
+    uint32_t hi7;
+    uint32_t e = chunk_errors<true>(v, prev, next, k, (int64_t)c * kChunkBytes, 0, n, &hi7);
+    while (e) {  // natural order: bit i = lane 32c + i
+      const unsigned q = c * kChunkBytes + (unsigned)(__ffs(e) - 1);
+      e &= e - 1;
+      const unsigned r = last_start_le(s_off, R, q);
+      if (q - s_off[r] >= 3) s_ver[r] = 0;
+    }
+  }
+  for (unsigned rr = t; rr <= R; rr += kServeThreads) {
+    const unsigned o = s_off[rr];
+    uint64_t w8 = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int q = (int)o - 4 + j;
+      if (q >= 0 && q < (int)n) w8 |= (uint64_t)s_bytes[q] << (8 * j);
+    }
+    int ka = rr > 0 ? (int)s_off[rr - 1] - ((int)o - 4) : 4;
+    int kb = rr < R ? (int)s_off[rr + 1] - ((int)o - 4) : 4;
+    ka = ka < 0 ? 0 : (ka > 4 ? 4 : ka);
+    kb = kb < 4 ? 4 : (kb > 8 ? 8 : kb);
+    const uint32_t f = u8v_boundary_errors(w8, (unsigned)ka, (unsigned)kb, k);
+    if ((f & 1u) && rr > 0) s_ver[rr - 1] = 0;
+    if ((f & 2u) && rr < R) s_ver[rr] = 0;
+  }
 }
 __device__ __forceinline__ unsigned long long global_ns() {
   unsigned long long t;
@@ -115,6 +184,8 @@ __device__ __forceinline__ uint4 keep_bytes(uint4 q, unsigned keep) {
 
 __global__ void __launch_bounds__(kServeThreads, 1) k_serve(ServeArgs a) {
   extern __shared__ uint4 s_buf[];
+  uint32_t* const s_off = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(s_buf) + kSmemOffs);
+  uint8_t* const s_ver = reinterpret_cast<uint8_t*>(s_buf) + kSmemVer;
   __shared__ unsigned long long s_req;
   __shared__ unsigned s_first;
   const unsigned t = threadIdx.x;
@@ -143,7 +214,8 @@ __global__ void __launch_bounds__(kServeThreads, 1) k_serve(ServeArgs a) {
       return;
     }
     last = req_seq(r);
-    const unsigned n = req_n(r), L0 = req_lo(r), L1 = req_hi(r);
+    const unsigned mode = req_mode(r);
+    const unsigned n = req_n(r), L0 = mode == kModeBatch ? 0u : req_lo(r), L1 = mode == kModeBatch ? n : req_hi(r);
     const unsigned c_end = (L1 + kChunkBytes - 1) / kChunkBytes;
     const unsigned lim16 = (c_end + 1) * (kChunkBytes / 16);  // uint4 words staged
     // Every load is issued before any is used: one PCIe round trip for up
@@ -153,6 +225,11 @@ __global__ void __launch_bounds__(kServeThreads, 1) k_serve(ServeArgs a) {
     for (int j = 0; j < kLoads; ++j) {
       const unsigned i = t + j * kServeThreads;
       q[j] = (i < lim16 && i * 16 < n) ? __ldcv(a.data + i) : make_uint4(0, 0, 0, 0);
+    }
+    if (mode == kModeBatch) {  // offsets in (their loads overlap the bytes'), verdicts initialised
+      const unsigned R = req_lo(r);
+      for (unsigned i = t; i <= R; i += kServeThreads) s_off[i] = __ldcv(a.offs + i);
+      for (unsigned i = t; i < R; i += kServeThreads) s_ver[i] = 1;
     }
 #pragma unroll
     for (int j = 0; j < kLoads; ++j) {
@@ -165,6 +242,22 @@ __global__ void __launch_bounds__(kServeThreads, 1) k_serve(ServeArgs a) {
     }
     __syncthreads();
     const uint32_t* sw = reinterpret_cast<const uint32_t*>(s_buf);
+    if (mode == kModeBatch) {
+      const unsigned R = req_lo(r);
+      serve_batch(reinterpret_cast<const uint8_t*>(s_buf), sw, s_off, s_ver, n, R, a.k);
+      __syncthreads();
+      uint32_t bad = 0;
+      for (unsigned i = t; i < (R + 3) / 4; i += kServeThreads) {
+        const uint32_t w = reinterpret_cast<const uint32_t*>(s_ver)[i];
+        bad |= ~w & 0x01010101u & (i * 4 + 4 <= R ? 0xFFFFFFFFu : (0xFFFFFFFFu >> (8 * (i * 4 + 4 - R))));
+        a.verdicts[i] = w;  // mapped host memory
+      }
+      bad = __syncthreads_or(bad);
+      if (t == 0) st_release_sys(a.resp, ((unsigned long long)last << 53) | (bad ? 1 : 0));  // after every verdict store
+      t0 = global_ns();
+      __syncthreads();
+      continue;
+    }
     uint32_t any = 0;
     for (unsigned c = L0 / kChunkBytes + t; c < c_end; c += kServeThreads) {
       Chunk v;
@@ -185,8 +278,8 @@ __global__ void __launch_bounds__(kServeThreads, 1) k_serve(ServeArgs a) {
     }
     any = __syncthreads_or(any);
     if (t == 0) {
-      unsigned long long w = ((unsigned long long)last << 52) | any;
-      if (any && req_verdict(r)) {
+      unsigned long long w = ((unsigned long long)last << 53) | any;
+      if (any && mode == kModeVerdict) {
         unsigned long long off = 0;
         int kind = -1;
         locate_chunk(reinterpret_cast<const uint8_t*>(s_buf), n, 0, L0, s_first, &off, &kind);
@@ -257,7 +350,7 @@ int Server::launch() {
   int st = epoch_words(dev, &eh, &ed);
   if (st) return st;
   std::call_once(g_attr_once[dev], [] {
-    cudaFuncSetAttribute(k_serve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kStageBytes);
+    cudaFuncSetAttribute(k_serve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
   });
   uint8_t* dh = mailbox_d;
   ServeArgs a;
@@ -265,15 +358,17 @@ int Server::launch() {
   a.resp = reinterpret_cast<unsigned long long*>(dh + kRespOff);
   a.exit_word = reinterpret_cast<unsigned long long*>(dh + kExitOff);
   a.data = reinterpret_cast<const uint4*>(dh + kDataOff);
+  a.offs = reinterpret_cast<const uint32_t*>(dh + kOffsOff);
+  a.verdicts = reinterpret_cast<uint32_t*>(dh + kVerOff);
   a.epoch = ed;
   a.epoch0 = __atomic_load_n(eh, __ATOMIC_ACQUIRE);
   a.idle_ns = idle_ns;
   a.gen = ++gen;
-  a.last_seq = seq == 1 ? 4095u : seq - 1;  // the pending request (seq) is new to it
+  a.last_seq = seq == 1 ? kSeqMax : seq - 1;  // the pending request (seq) is new to it
   a.first_req = __atomic_load_n(reinterpret_cast<unsigned long long*>(mailbox_h + kReqOff), __ATOMIC_ACQUIRE);
   a.k = u8v_make_consts();
   g_any_server.store(true, std::memory_order_relaxed);
-  k_serve<<<1, kServeThreads, kStageBytes, stream>>>(a);
+  k_serve<<<1, kServeThreads, kSmemBytes, stream>>>(a);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return u8v_capi::fail(UTF8V_ERR_CUDA, "server launch", e);
   ++launches;
@@ -296,14 +391,9 @@ int Server::ensure(int device) {
   return UTF8V_OK;
 }
 
-int Server::call(const uint8_t* p, size_t n, uint64_t lane_lo, uint64_t lane_hi, bool verdict, ServeReply* out) {
-  if (n == 0 || n > kServeMax || lane_hi > n + 3 || lane_lo > lane_hi)
-    return u8v_capi::fail(UTF8V_ERR_ARG, "server request out of range");
-  memcpy(mailbox_h + kDataOff, p, n);
-  seq = seq % 4095 + 1;
-  const unsigned long long w = (unsigned long long)n | ((unsigned long long)lane_lo << 17) |
-                               ((unsigned long long)lane_hi << 34) | ((unsigned long long)(verdict ? 1 : 0) << 51) |
-                               ((unsigned long long)seq << 52);
+int Server::post(unsigned long long w, unsigned long long* reply) {
+  seq = seq % kSeqMax + 1;
+  w |= (unsigned long long)seq << 53;
   auto* req = reinterpret_cast<unsigned long long*>(mailbox_h + kReqOff);
   auto* resp = reinterpret_cast<unsigned long long*>(mailbox_h + kRespOff);
   auto* exit_word = reinterpret_cast<unsigned long long*>(mailbox_h + kExitOff);
@@ -315,20 +405,18 @@ int Server::call(const uint8_t* p, size_t n, uint64_t lane_lo, uint64_t lane_hi,
   ++requests;
   for (unsigned long long spins = 1;; ++spins) {
     unsigned long long r = __atomic_load_n(resp, __ATOMIC_ACQUIRE);
-    if ((unsigned)(r >> 52) != seq && __atomic_load_n(exit_word, __ATOMIC_ACQUIRE) == gen) {
+    if ((unsigned)(r >> 53) != seq && __atomic_load_n(exit_word, __ATOMIC_ACQUIRE) == gen) {
       // The server exited (idle or epoch); it wrote any reply before that.
       r = __atomic_load_n(resp, __ATOMIC_ACQUIRE);
-      if ((unsigned)(r >> 52) != seq) {
+      if ((unsigned)(r >> 53) != seq) {
         alive = false;
         const int st = launch();
         if (st) return st;
         continue;
       }
     }
-    if ((unsigned)(r >> 52) == seq) {
-      out->flag = (uint32_t)(r & 1);
-      out->kind = (int)((r >> 1) & 0xF) - 1;
-      out->offset = (r >> 5) & 0x1FFFF;
+    if ((unsigned)(r >> 53) == seq) {
+      *reply = r;
       return UTF8V_OK;
     }
     if ((spins & 0xFFFFF) == 0) {  // a failed server never replies
@@ -336,6 +424,37 @@ int Server::call(const uint8_t* p, size_t n, uint64_t lane_lo, uint64_t lane_hi,
       if (e != cudaSuccess && e != cudaErrorNotReady) return u8v_capi::fail(UTF8V_ERR_CUDA, "server", e);
     }
   }
+}
+
+int Server::call(const uint8_t* p, size_t n, uint64_t lane_lo, uint64_t lane_hi, bool verdict, ServeReply* out) {
+  if (n == 0 || n > kServeMax || lane_hi > n + 3 || lane_lo > lane_hi)
+    return u8v_capi::fail(UTF8V_ERR_ARG, "server request out of range");
+  memcpy(mailbox_h + kDataOff, p, n);
+  const unsigned long long w = (unsigned long long)n | ((unsigned long long)lane_lo << 17) |
+                               ((unsigned long long)lane_hi << 34) |
+                               ((unsigned long long)(verdict ? kModeVerdict : kModeFlag) << 51);
+  unsigned long long r = 0;
+  const int st = post(w, &r);
+  if (st) return st;
+  out->flag = (uint32_t)(r & 1);
+  out->kind = (int)((r >> 1) & 0xF) - 1;
+  out->offset = (r >> 5) & 0x1FFFF;
+  return UTF8V_OK;
+}
+
+int Server::call_batch(const uint8_t* data, const uint64_t* offsets, size_t n_records, uint8_t* verdicts) {
+  const uint64_t base = offsets[0], n = offsets[n_records] - base;
+  if (n_records == 0 || n_records > kServeMaxRecords || n > kServeMax)
+    return u8v_capi::fail(UTF8V_ERR_ARG, "server batch out of range");
+  if (n) memcpy(mailbox_h + kDataOff, data + base, n);
+  auto* offs = reinterpret_cast<uint32_t*>(mailbox_h + kOffsOff);
+  for (size_t r = 0; r <= n_records; ++r) offs[r] = (uint32_t)(offsets[r] - base);
+  const unsigned long long w = n | ((unsigned long long)n_records << 17) | ((unsigned long long)kModeBatch << 51);
+  unsigned long long r = 0;
+  const int st = post(w, &r);
+  if (st) return st;
+  memcpy(verdicts, mailbox_h + kVerOff, n_records);
+  return UTF8V_OK;
 }
 
 void Server::release() {

@@ -10,6 +10,7 @@
 namespace u8v {
 
 constexpr size_t kServeMax = 64u << 10;
+constexpr size_t kServeMaxRecords = 4096;  // batch requests: records per request
 
 struct ServeReply {
   uint32_t flag = 0;    // some lane of the range is flagged
@@ -24,7 +25,7 @@ struct Server {
   cudaStream_t stream = nullptr;
   uint8_t* mailbox_h = nullptr;
   uint8_t* mailbox_d = nullptr;
-  unsigned seq = 0;                 // last request posted (1..4095)
+  unsigned seq = 0;                 // last request posted (1..2047)
   unsigned long long gen = 0;       // generation of the last server launched
   unsigned long long idle_ns = 0;
   bool alive = false;               // a server of generation `gen` may be running
@@ -35,10 +36,15 @@ struct Server {
   // Flag of lanes [lane_lo, lane_hi) of p[0..n) (1 <= n <= kServeMax); in
   // verdict mode also the first error's (offset, kind).  Synchronous.
   int call(const uint8_t* p, size_t n, uint64_t lane_lo, uint64_t lane_hi, bool verdict, ServeReply* out);
+  // One verdict per record of a host batch whose records span at most
+  // kServeMax bytes (offsets[n_records] - offsets[0]), 1 <= n_records <=
+  // kServeMaxRecords; offsets already checked non-decreasing.  Synchronous.
+  int call_batch(const uint8_t* data, const uint64_t* offsets, size_t n_records, uint8_t* verdicts);
   void release();
 
  private:
   int launch();
+  int post(unsigned long long w, unsigned long long* reply);  // w without its sequence
 };
 
 // False when UTF8V_CUDA_SERVE=0.

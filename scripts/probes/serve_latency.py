@@ -42,3 +42,38 @@ for n in (16, 256, 4096, 16384, 65536):
 a, r = C.c_uint64(0), C.c_uint64(0)
 lib.utf8v_cuda_serve_stats(C.byref(a), C.byref(r))
 print("server launches", a.value, "requests", r.value)
+
+# Host batches (utf8v_cuda_validate_batch on host arrays): per-call latency.
+for n_rec, rec in ((16, 64), (100, 100), (1000, 60), (256, 256)):
+    raw = nat.generate_valid(0b0111, n_rec * rec, 9)[: n_rec * rec]
+    b = np.frombuffer(raw, np.uint8).copy()
+    offs = np.arange(0, n_rec * rec + 1, rec, dtype=np.uint64)
+    offs[-1] = b.size
+    ver = np.empty(n_rec, np.uint8)
+    fn = lambda: lib.utf8v_cuda_validate_batch(b.ctypes.data, b.size, offs.ctypes.data, n_rec, 0, ver.ctypes.data)
+    for _ in range(20):
+        fn()
+    ts = []
+    for _ in range(500):
+        t0 = time.perf_counter()
+        fn()
+        ts.append(time.perf_counter() - t0)
+    ts.sort()
+    print(f"batch {n_rec:5d} x {rec:4d} B: min {ts[0]*1e6:6.2f} med {ts[len(ts)//2]*1e6:6.2f} us", flush=True)
+# Larger host batches (K2 over staged copies; scratch from the library's pool).
+for n_rec, rec in ((10000, 100), (5000, 1000)):
+    raw = nat.generate_valid(0b0111, n_rec * rec, 9)[: n_rec * rec]
+    b = np.frombuffer(raw, np.uint8).copy()
+    offs = np.arange(0, n_rec * rec + 1, rec, dtype=np.uint64)
+    offs[-1] = b.size
+    ver = np.empty(n_rec, np.uint8)
+    fn = lambda: lib.utf8v_cuda_validate_batch(b.ctypes.data, b.size, offs.ctypes.data, n_rec, 0, ver.ctypes.data)
+    for _ in range(5):
+        fn()
+    ts = []
+    for _ in range(50):
+        t0 = time.perf_counter()
+        fn()
+        ts.append(time.perf_counter() - t0)
+    ts.sort()
+    print(f"batch {n_rec:5d} x {rec:4d} B: min {ts[0]*1e6:7.1f} med {ts[len(ts)//2]*1e6:7.1f} us", flush=True)

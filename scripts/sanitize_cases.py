@@ -51,3 +51,20 @@ ok = C.c_uint8()
 _lib.check(lib.utf8v_cuda_validate_sharded(h.ctypes.data, h.size, 3, 0, C.byref(ok)))
 assert ok.value == 1
 print("sanitize cases ok")
+
+# Small-call server: host inputs <= 64 KiB (validate, verdict, lane ranges),
+# including the idle exit and relaunch.
+import time
+for n in (1, 3, 31, 32, 33, 4097, 16384, 65536):
+    raw = (b"ab\xc3\xa9\xe2\x82\xac" * (n // 7 + 1))[:n]
+    hb = np.frombuffer(raw, np.uint8).copy()
+    ok = C.c_uint8(9)
+    _lib.check(lib.utf8v_cuda_validate(hb.ctypes.data, n, 0, C.byref(ok)))
+    hb[n // 2] = 0xC0
+    vok, off, kind = C.c_uint8(9), C.c_uint64(0), C.c_int(-1)
+    _lib.check(lib.utf8v_cuda_validate_verdict(hb.ctypes.data, n, 0, C.byref(vok), C.byref(off), C.byref(kind)))
+    assert vok.value == 0
+    f = C.c_uint32(9)
+    _lib.check(lib.utf8v_cuda_validate_lanes(hb.ctypes.data, n, n // 3, n + 3, 0, C.byref(f)))
+    time.sleep(0.001)
+print("sanitize cases done")

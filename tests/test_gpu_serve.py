@@ -251,3 +251,99 @@ def test_server_disabled_by_env():
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+# ---- batch requests (host arrays, records spanning <= 64 KiB, <= 4096 records)
+
+SERVE_MAX_RECORDS = 4096
+# byte values that matter at record boundaries: ASCII, continuations, every
+# lead class and the rare-pair followers
+EDGE_BYTES = np.array([0x00, 0x41, 0x7F, 0x80, 0x8F, 0x90, 0x9F, 0xA0, 0xBF, 0xC0, 0xC1, 0xC2, 0xDF, 0xE0, 0xE1,
+                       0xED, 0xEF, 0xF0, 0xF4, 0xF5], np.uint8)
+
+
+def _batch(data: np.ndarray, offs: np.ndarray) -> np.ndarray:
+    L, lib = _lib()
+    ver = np.full(offs.size - 1, 7, np.uint8)
+    L.check(lib.utf8v_cuda_validate_batch(data.ctypes.data if data.size else None, data.size, offs.ctypes.data,
+                                          offs.size - 1, 0, ver.ctypes.data))
+    return ver
+
+
+def test_batch_tiny_records_vs_oracle():
+    rng = np.random.default_rng(21)
+    _, req0 = _stats()
+    calls = 0
+    for trial in range(2000):
+        R = int(rng.integers(1, 200))
+        lens = rng.integers(0, 7, R)
+        lead, tail = int(rng.integers(0, 5)), int(rng.integers(0, 5))
+        data = EDGE_BYTES[rng.integers(0, EDGE_BYTES.size, lead + int(lens.sum()) + tail)]
+        offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64) + np.uint64(lead)
+        got = _batch(data, offs)
+        calls += 1
+        want = nat.oracle_batch(data, offs)
+        assert np.array_equal(got, want), (trial, got, want)
+    _, req1 = _stats()
+    assert req1 - req0 == calls
+
+
+def test_batch_text_records_with_errors_vs_oracle():
+    rng = np.random.default_rng(22)
+    for trial in range(300):
+        parts = []
+        for _ in range(int(rng.integers(1, 600))):
+            k = int(rng.integers(0, 5))
+            if k == 0:
+                parts.append(b"")
+            elif k == 1:
+                parts.append(nat.generate_valid(15, int(rng.integers(1, 200)), int(rng.integers(1, 1 << 30))))
+            elif k == 2:
+                parts.append(nat.generate_invalid(15, int(rng.integers(1, 200)), int(rng.integers(1, 1 << 30)),
+                                                  int(rng.integers(0, 6))))
+            elif k == 3:
+                b = bytearray(nat.generate_valid(15, int(rng.integers(4, 120)), int(rng.integers(1, 1 << 30))))
+                b[int(rng.integers(0, len(b)))] = int(EDGE_BYTES[rng.integers(0, EDGE_BYTES.size)])
+                parts.append(bytes(b))
+            else:
+                parts.append(bytes([0xE9, 0x8F]))  # truncated at the record end
+        data = np.frombuffer(b"".join(parts), np.uint8).copy()
+        offs = np.concatenate([[0], np.cumsum([len(p) for p in parts])]).astype(np.uint64)
+        if data.size > SERVE_MAX:
+            continue
+        assert np.array_equal(_batch(data, offs), nat.oracle_batch(data, offs)), trial
+
+
+@pytest.mark.parametrize("R,span", [(1, 65536), (4096, 65536), (4096, 4096), (4096, 0), (1, 0), (4097, 65536),
+                                    (100, 65537), (3000, 65000)])
+def test_batch_limits(R, span):
+    rng = np.random.default_rng(R + span)
+    raw = nat.generate_valid(15, span + 8, 31)[:span] if span else b""
+    data = np.frombuffer(raw, np.uint8).copy()
+    cuts = np.sort(rng.integers(0, span + 1, R - 1)) if R > 1 else np.array([], np.int64)
+    offs = np.concatenate([[0], cuts, [span]]).astype(np.uint64)
+    if span:
+        data[rng.integers(0, span, 5)] = 0xC0
+    _, req0 = _stats()
+    got = _batch(data, offs)
+    _, req1 = _stats()
+    assert np.array_equal(got, nat.oracle_batch(data, offs))
+    served = R <= SERVE_MAX_RECORDS and span <= SERVE_MAX
+    assert (req1 - req0) == (1 if served else 0)   # larger batches take K2
+
+
+def test_batch_then_grid_kernels_and_sync():
+    import torch
+    data = np.frombuffer(nat.generate_valid(15, 5000, 3), np.uint8).copy()
+    offs = np.array([0, 100, 2000, data.size], np.uint64)
+    want = nat.oracle_batch(data, offs)
+    big = torch.full((64 << 20,), 0x41, dtype=torch.uint8, device="cuda")
+    L, lib = _lib()
+    ok = C.c_uint8(9)
+    for _ in range(20):
+        assert np.array_equal(_batch(data, offs), want)
+        L.check(lib.utf8v_cuda_validate(big.data_ptr(), big.numel(), 1, C.byref(ok)))
+        assert ok.value == 1
+    t = time.perf_counter()
+    torch.cuda.synchronize()
+    assert time.perf_counter() - t < 0.05
