@@ -485,6 +485,7 @@ __global__ void __launch_bounds__(kK2Threads, kK2Blocks) k_batch(BatchDesc d) {
   cx->range_rel = range_rel;
   cx->hi_rel = rel32(d.hi, range_lo);
   bool pend = false;
+  int fire = 0;
   bool was_ascii = true;
 
   // Steps [jb, jd) are interior (all bytes real, lookahead word in range):
@@ -610,7 +611,15 @@ __global__ void __launch_bounds__(kK2Threads, kK2Blocks) k_batch(BatchDesc d) {
 
     // Boundary batches: the pending one is checked a step after it was
     // taken; the trigger reads nx a step after it was loaded (no stall).
+#ifdef U8V_K2_OLD_TRIGGER
     if (pend || __shfl_sync(0xFFFFFFFFu, nx, kTrigger) < (j + 1) * kStepBytes) {
+#else
+    // `fire`: the next step with boundary work -- the step after a take (the
+    // pending batch is checked then), else the step whose end passes the
+    // next batch's trigger start (computed when the block last ran, a step
+    // after nx was loaded): one compare per step.
+    if (j >= fire) {
+#endif
       if (pend) {
         check_batch<kState>(rv, sl, nx, cx->rb - 32, cx->range_rel, d.k);
         pend = false;
@@ -625,6 +634,8 @@ __global__ void __launch_bounds__(kK2Threads, kK2Blocks) k_batch(BatchDesc d) {
         cx->rb = rbc + 32;
         nx = rel32(rec_start(rv, rbc + 32 + lane), cx->range_lo);
       }
+      // (the loop left nx's trigger start >= (j + 1) * kStepBytes > 0)
+      fire = pend ? j + 1 : (int)((unsigned)__shfl_sync(0xFFFFFFFFu, nx, kTrigger) / (unsigned)kStepBytes);
     }
   }
   // The range's remaining boundaries.
