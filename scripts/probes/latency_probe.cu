@@ -418,6 +418,36 @@ int main(int argc, char** argv) {
     }
     report("G  host memcpy 16 KiB into WC pinned + sfence", t);
   }
+
+  // I: the launch path with a large dynamic shared-memory request (the
+  // server's 86 KB), after a grid that used little shared memory, vs none.
+  {
+    cudaFuncSetAttribute(k_read, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 << 10);
+    uint8_t* dbig;
+    CK(cudaMalloc(&dbig, 64 << 20));
+    for (int smem : {0, 86 << 10}) {
+      for (int after_grid : {0, 1}) {
+        t.clear();
+        for (int i = 0; i < 400; ++i) {
+          if (after_grid) {
+            CK(cudaMemsetAsync(dbig, i, 64 << 20, s));  // a grid-wide kernel of the runtime
+            CK(cudaStreamSynchronize(s));
+          }
+          double a = now_us();
+          memcpy(hdata, user.data(), 16384);
+          const uint32_t v = (uint32_t)(i + 1) & 0x7fffffffu;
+          k_read<<<1, 1024, smem, s>>>(ddata, 16384 / 16, dflag, v);
+          while ((*hflag & 0x7fffffffu) != v) {
+          }
+          t.push_back(now_us() - a);
+        }
+        CK(cudaStreamSynchronize(s));
+        char w[96];
+        snprintf(w, sizeof w, "I  16 KiB launch+spin, dyn smem %6d, after grid %d", smem, after_grid);
+        report(w, t);
+      }
+    }
+  }
   // idle exit: the server returns by itself after idle_ns
   memset(box, 0, sizeof(Box));
   double a = now_us();
