@@ -236,6 +236,25 @@ __global__ void k_server3(Box* b, Box* rb, const uint4* data, int poll_warps, in
   }
 }
 
+
+// J: G CTAs each read 1/G of the bytes (zero copy); the last CTA to finish
+// (global counter) stores the flag.
+__global__ void k_read_multi(const uint4* p, int n16, volatile uint32_t* f, uint32_t v, unsigned* count) {
+  uint32_t acc = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += gridDim.x * blockDim.x) {
+    uint4 q = __ldcv(p + i);
+    acc |= q.x | q.y | q.z | q.w;
+  }
+  acc = __syncthreads_or(acc & 0x80808080u);
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(count, 1u) == gridDim.x - 1) {
+      *count = 0;
+      *f = v | (acc ? 0x80000000u : 0);
+    }
+  }
+}
+
 static void report(const char* what, std::vector<double>& v) {
   std::sort(v.begin(), v.end());
   printf("%-58s min %7.2f  med %7.2f  p99 %7.2f us\n", what, v[0], v[v.size() / 2], v[v.size() * 99 / 100]);
@@ -444,6 +463,32 @@ int main(int argc, char** argv) {
         CK(cudaStreamSynchronize(s));
         char w[96];
         snprintf(w, sizeof w, "I  16 KiB launch+spin, dyn smem %6d, after grid %d", smem, after_grid);
+        report(w, t);
+      }
+    }
+  }
+
+  // J: the read part spread over G SMs (is one SM's outstanding sysmem
+  // read count the limit?)
+  {
+    unsigned* cnt;
+    CK(cudaMalloc(&cnt, 4));
+    CK(cudaMemset(cnt, 0, 4));
+    for (int n : {16384, 65536}) {
+      for (int G : {1, 2, 4, 8, 16}) {
+        t.clear();
+        for (int i = 0; i < 1000; ++i) {
+          double a = now_us();
+          memcpy(hdata, user.data(), n);
+          const uint32_t v = (uint32_t)(i + 1) & 0x7fffffffu;
+          k_read_multi<<<G, 1024, 0, s>>>(ddata, n / 16, dflag, v, cnt);
+          while ((*hflag & 0x7fffffffu) != v) {
+          }
+          t.push_back(now_us() - a);
+        }
+        CK(cudaStreamSynchronize(s));
+        char w[96];
+        snprintf(w, sizeof w, "J  %6d B over %2d CTAs, launch + spin", n, G);
         report(w, t);
       }
     }
