@@ -13,6 +13,8 @@ Python face of libutf8v_cuda.so, mirroring the reference's Lookup API
     validate_lookup_sharded(d, g)  host input over g GPUs in this process
     segment_state(d) / combine_states(a, b) / state_valid(s) / batch_states(d, offsets)
                                  composable per-segment states (order-free stitching)
+    serve_stats()                (launches, requests) of this thread's small-call server
+                                 (host inputs <= 64 KiB, csrc/serve.cu)
 
 `data` is host bytes (bytes / bytearray / memoryview / numpy uint8) or a CUDA
 torch.uint8 tensor (device-resident, validated in place).  All compute runs on
@@ -35,7 +37,7 @@ __all__ = [
     "LookupStream", "validate_lookup_sharded",
     "validate_lanes_async", "validate_batch_async", "WIDTH",
     "SegmentState", "STATE_DTYPE", "empty_state", "combine_states", "state_valid", "fold_states",
-    "segment_state", "batch_states",
+    "segment_state", "batch_states", "serve_stats",
 ]
 
 WIDTH = _lib.WIDTH
@@ -387,3 +389,13 @@ class LookupStream:
             self.close()
         except Exception:
             pass
+
+
+def serve_stats() -> tuple[int, int]:
+    """(server launches, requests served) on this thread and the current
+    device: host inputs of at most 64 KiB (and host batches of at most 4096
+    records spanning at most 64 KiB) are answered by a resident CTA polling a
+    mapped-memory mailbox (utf8v_cuda_serve_stats, include/utf8v_cuda.h)."""
+    launches, requests = C.c_uint64(0), C.c_uint64(0)
+    _lib.check(_lib.load().utf8v_cuda_serve_stats(C.byref(launches), C.byref(requests)))
+    return launches.value, requests.value

@@ -231,6 +231,14 @@ def test_concurrent_callers_and_grid_kernels():
     assert not errors, errors[:5]
 
 
+def test_python_serve_stats():
+    import paper_2010_03090_b200 as u8
+    l0, r0 = u8.serve_stats()
+    assert u8.validate_lookup(b"caf\xc3\xa9") is True
+    l1, r1 = u8.serve_stats()
+    assert r1 == r0 + 1 and l1 >= l0
+
+
 def test_server_disabled_by_env():
     code = (
         "import ctypes as C, numpy as np\n"
