@@ -65,7 +65,9 @@ extern "C" {
  *      (utf8v_cuda_batch_scratch_bytes removed); host input crosses PCIe
  *      through a bounded device ring; utf8v_cuda_release_thread_resources;
  *      device stream pieces are ordered before later legacy-stream work;
- *      composable segment states (utf8v_state) */
+ *      composable segment states (utf8v_state)
+ *   6  the small-call server answers host inputs <= UTF8V_CUDA_SERVE_MAX
+ *      bytes and small host batches (utf8v_cuda_serve_stats) */
 int utf8v_cuda_abi_version(void);
 
 /* Human-readable text of the last error on this thread ("" if none). */

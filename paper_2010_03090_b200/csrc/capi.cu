@@ -593,7 +593,7 @@ int stage_h2d(Ctx& c, const uint8_t* p, size_t n) {
 
 extern "C" {
 
-int utf8v_cuda_abi_version(void) { return 5; }
+int utf8v_cuda_abi_version(void) { return 6; }
 
 const char* utf8v_cuda_last_error(void) { return t_err.c_str(); }
 

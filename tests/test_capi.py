@@ -41,7 +41,7 @@ def test_library_exports_every_declared_symbol():
 def test_abi_version_and_empty_input_without_device():
     from paper_2010_03090_b200 import _lib
     lib = _lib.load()
-    assert lib.utf8v_cuda_abi_version() == 5
+    assert lib.utf8v_cuda_abi_version() == 6
     out = C.c_uint8(0)
     # n == 0 is valid text without touching the device (test_lookup.cpp:192)
     assert lib.utf8v_cuda_validate(None, 0, 0, C.byref(out)) == 0 and out.value == 1
