@@ -17,6 +17,12 @@
 //   lookup_stream            -- one stream validated in pieces, in order
 //   segment_state            -- segments validated anywhere, merged later
 //   shard_comm               -- a stream sharded over GPUs, combined by NCCL
+// Latency: host inputs of at most 64 KiB (and host batches of at most 4096
+// records spanning at most 64 KiB) are answered by the small-call server, one
+// resident CTA per calling thread and device that polls a mapped-memory
+// mailbox (3.5-7.4 us per call instead of a launch and a synchronisation);
+// it exits after 100 us without a request (UTF8V_CUDA_SERVE_IDLE_US) and is
+// turned off by UTF8V_CUDA_SERVE=0 (include/utf8v_cuda.h).
 #pragma once
 
 #include <cstddef>
