@@ -634,9 +634,12 @@ int flag_lanes(const uint8_t* p, uint64_t n, uint64_t lane_lo, uint64_t lane_hi,
   Ctx* c;
   int st = get_ctx(&c);
   if (st) return st;
+  bool serve = false;
   if (!is_device && n <= u8v::kServeMax && u8v::serve_enabled()) {
-    st = c->srv.ensure(c->dev);
+    st = c->srv.ensure(c->dev, &serve);
     if (st) return st;
+  }
+  if (serve) {
     u8v::ServeReply r;
     st = c->srv.call(p, n, lane_lo, lane_hi, false, &r);
     if (st) return st;
@@ -727,9 +730,12 @@ int verdict_lanes(const uint8_t* p, uint64_t n, uint64_t lane_lo, uint64_t lane_
     if (st) return st;
     return device_verdict(c, p, n, lane_lo, lane_hi, out_valid, out_offset, out_kind);
   }
+  bool serve = false;
   if (n <= u8v::kServeMax && u8v::serve_enabled()) {
-    st = c->srv.ensure(c->dev);
+    st = c->srv.ensure(c->dev, &serve);
     if (st) return st;
+  }
+  if (serve) {
     u8v::ServeReply r;
     st = c->srv.call(p, n, lane_lo, lane_hi, true, &r);
     if (st) return st;
@@ -870,9 +876,10 @@ int utf8v_cuda_validate_batch(const uint8_t* data, size_t n, const uint64_t* off
   if (st) return st;
   if (u8v::serve_enabled() && n_records <= u8v::kServeMaxRecords &&
       offsets[n_records] - offsets[0] <= u8v::kServeMax) {  // small batch: the server
-    st = c->srv.ensure(c->dev);
+    bool serve = false;
+    st = c->srv.ensure(c->dev, &serve);
     if (st) return st;
-    return c->srv.call_batch(data, offsets, n_records, verdicts);
+    if (serve) return c->srv.call_batch(data, offsets, n_records, verdicts);
   }
   uint64_t* d_off = nullptr;
   uint8_t* d_ver = nullptr;

@@ -300,6 +300,7 @@ std::mutex g_epoch_mu;
 std::atomic<unsigned long long*> g_epoch_h[kMaxDev];  // host view (set once)
 unsigned long long* g_epoch_d[kMaxDev];  // device view
 std::once_flag g_attr_once[kMaxDev];
+std::atomic<int> g_servers[kMaxDev];  // threads holding a server, per device
 
 bool env_disabled() {
   const char* e = getenv("UTF8V_CUDA_SERVE");
@@ -376,18 +377,37 @@ int Server::launch() {
   return UTF8V_OK;
 }
 
-int Server::ensure(int device) {
-  if (mailbox_h) return UTF8V_OK;
+int Server::ensure(int device, bool* usable) {
+  *usable = false;
+  if (mailbox_h) {
+    *usable = true;
+    return UTF8V_OK;
+  }
+  if (device < 0 || device >= kMaxDev) return UTF8V_OK;
+  // At most kMaxServersPerDevice threads hold a server on a device (each
+  // server CTA fills an SM); the others launch a kernel per call.
+  if (g_servers[device].fetch_add(1) >= kMaxServersPerDevice) {
+    g_servers[device].fetch_sub(1);
+    return UTF8V_OK;
+  }
   dev = device;
   idle_ns = env_idle_ns();
-  CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
   void* p = nullptr;
-  CK(cudaHostAlloc(&p, kMailboxBytes, cudaHostAllocMapped));
-  memset(p, 0, kMailboxBytes);
   void* dp = nullptr;
-  CK(cudaHostGetDevicePointer(&dp, p, 0));
+  cudaError_t e = cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaHostAlloc(&p, kMailboxBytes, cudaHostAllocMapped);
+  if (e == cudaSuccess) e = cudaHostGetDevicePointer(&dp, p, 0);
+  if (e != cudaSuccess) {
+    if (p) cudaFreeHost(p);
+    if (stream) cudaStreamDestroy(stream);
+    stream = nullptr;
+    g_servers[device].fetch_sub(1);
+    return u8v_capi::fail(UTF8V_ERR_CUDA, "small-call server set-up", e);
+  }
+  memset(p, 0, kMailboxBytes);
   mailbox_h = static_cast<uint8_t*>(p);
   mailbox_d = static_cast<uint8_t*>(dp);
+  *usable = true;
   return UTF8V_OK;
 }
 
@@ -469,6 +489,7 @@ void Server::release() {
   }
   cudaFreeHost(mailbox_h);
   cudaGetLastError();
+  g_servers[dev].fetch_sub(1);
   *this = Server();
 }
 

@@ -11,6 +11,7 @@ namespace u8v {
 
 constexpr size_t kServeMax = 64u << 10;
 constexpr size_t kServeMaxRecords = 4096;  // batch requests: records per request
+constexpr int kMaxServersPerDevice = 32;   // threads holding a server on one device
 
 struct ServeReply {
   uint32_t flag = 0;    // some lane of the range is flagged
@@ -32,7 +33,10 @@ struct Server {
   unsigned long long launches = 0;  // server launches by this thread (diagnostics)
   unsigned long long requests = 0;
 
-  int ensure(int device);
+  // Sets up this thread's server on `device` (mailbox, stream) unless
+  // kMaxServersPerDevice other threads hold one there: *usable says whether
+  // the caller may use it (else it launches a kernel per call).
+  int ensure(int device, bool* usable);
   // Flag of lanes [lane_lo, lane_hi) of p[0..n) (1 <= n <= kServeMax); in
   // verdict mode also the first error's (offset, kind).  Synchronous.
   int call(const uint8_t* p, size_t n, uint64_t lane_lo, uint64_t lane_hi, bool verdict, ServeReply* out);

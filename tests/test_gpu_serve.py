@@ -355,3 +355,37 @@ def test_batch_then_grid_kernels_and_sync():
     t = time.perf_counter()
     torch.cuda.synchronize()
     assert time.perf_counter() - t < 0.05
+
+
+def test_server_cap_per_device():
+    # at most 32 threads hold a server on a device; the rest launch a kernel
+    # per call -- every verdict still equals the oracle
+    n_threads = 40
+    barrier = threading.Barrier(n_threads)
+    stats, errors = [None] * n_threads, []
+
+    def worker(k):
+        try:
+            rng = np.random.default_rng(k)
+            barrier.wait()
+            for it in range(20):
+                b = _text(int(rng.integers(1, 5000)), seed=k * 100 + it)
+                if it % 2:
+                    b[int(rng.integers(0, b.size))] = 0xC0
+                if _verdict(b) != nat.oracle_verdict(b):
+                    errors.append((k, it))
+            stats[k] = _stats()
+            barrier.wait()  # every thread still holds its server here
+            _lib()[1].utf8v_cuda_release_thread_resources()
+        except Exception as e:  # noqa: BLE001
+            errors.append(repr(e))
+
+    ts = [threading.Thread(target=worker, args=(k,)) for k in range(n_threads)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=300)
+    assert not errors, errors[:5]
+    served = [s for s in stats if s and s[1] > 0]
+    assert len(served) <= 32 and all(s[1] == 20 for s in served)
+    assert sum(1 for s in stats if s == (0, 0)) == n_threads - len(served)
