@@ -853,3 +853,30 @@ def test_concurrent_callers_mixed_entry_points(torch):
     for t in ts:
         t.join()
     assert not errors, errors[:3]
+
+
+@pytest.mark.parametrize("path", ["K2L", "K2"])
+def test_batch_offsets_past_4_gib(path, torch):
+    # 64-bit positions: a 5 GiB data array whose records (and injected
+    # errors) lie beyond 2^32 bytes, through K2L (few large records) and K2
+    # (many records: the large one surrounded by 40 k small ones), vs the
+    # multi-threaded oracle per record.
+    G = 1 << 30
+    n = 5 * G + 12345
+    d = configs.gen_c1(n, seed=77)
+    rng = np.random.default_rng(5)
+    if path == "K2L":
+        cuts = [0, 100, 4 * G + 777, 4 * G + (1 << 29), n]
+    else:
+        small = np.sort(rng.integers(4 * G + (1 << 28), n, 40_000)).tolist()
+        cuts = [0, 100, 4 * G + 777] + small + [n]
+    offs = np.array(cuts, np.uint64)
+    for at in (4 * G + 5_000, 4 * G + (1 << 28) + 3, n - 2):  # errors past 2^32
+        d[at] = 0xC0
+    h = d.cpu().numpy()
+    want = nat.oracle_batch(h, offs, threads=16)
+    assert (want == 0).sum() >= 2
+    got = u8.validate_lookup_batch(d, torch.from_numpy(offs.view(np.int64)).cuda())
+    assert np.array_equal(got, want), np.nonzero(got != want)[0][:10]
+    del d
+    torch.cuda.empty_cache()
