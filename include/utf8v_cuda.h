@@ -297,8 +297,10 @@ int utf8v_cuda_p2p_reset(utf8v_cuda_p2p* g);
 void utf8v_cuda_p2p_destroy(utf8v_cuda_p2p* g);
 
 /* Frees this thread's per-device resources (streams, the bounded host-input
- * ring of 4 x (32 MiB + 32 B) device bytes, pinned staging, the batch stage),
- * and those of the library's persistent shard workers
+ * ring of 4 x (32 MiB + 32 B) device bytes, pinned staging, the batch stage,
+ * the small-call server and its mailbox), the unused batch scratch the
+ * library's per-device memory pools keep mapped, and the resources of the
+ * library's persistent shard workers
  * (utf8v_cuda_validate_sharded); the next call recreates what it needs.
  * A thread's resources are also freed when it exits. */
 void utf8v_cuda_release_thread_resources(void);

@@ -613,6 +613,11 @@ int utf8v_cuda_serve_stats(uint64_t* out_launches, uint64_t* out_requests) {
 
 void utf8v_cuda_release_thread_resources(void) {
   for (int d = 0; d < kMaxDevices; ++d) t_ctx[d].release();
+  // Unused batch scratch the per-device pools keep mapped goes back too
+  // (memory other threads still hold stays allocated).
+  for (int d = 0; d < kMaxDevices; ++d)
+    if (g_pool[d]) cudaMemPoolTrimTo(g_pool[d], 0);
+  cudaGetLastError();
   // The persistent shard workers of utf8v_cuda_validate_sharded hold
   // per-thread contexts too: release theirs as well.
   ShardPool& pool = ShardPool::get();
