@@ -235,6 +235,22 @@ __device__ __forceinline__ unsigned take_ticket(unsigned pool_addr, int lane, un
   return t;
 }
 
+#ifdef U8V_K2P_SKELETON
+// DEVELOPMENT (tools/kvar.sh builds only): the memory traffic of a pooled K2
+// -- per step, the step's first-record index from a step table (with the
+// data), then the record starts of the step (after the chunk math), and with
+// U8V_K2P_SKELETON >= 2 the 8 bytes around each start -- folded into the
+// flag so nothing is dropped.  scripts/probes/k2p_skeleton.py.
+__device__ const unsigned* g_k2p_table;
+__device__ const uint64_t* g_k2p_offsets;
+__device__ unsigned g_k2p_n;
+extern "C" int u8v_k2p_set(const unsigned* table, const uint64_t* offsets, unsigned n) {
+  cudaMemcpyToSymbol(g_k2p_table, &table, sizeof(table));
+  cudaMemcpyToSymbol(g_k2p_offsets, &offsets, sizeof(offsets));
+  return (int)cudaMemcpyToSymbol(g_k2p_n, &n, sizeof(n));
+}
+#endif
+
 template <bool kTrack>
 __device__ __forceinline__ void sweep(const StreamDesc& d, uint32_t* __restrict__ flag) {
   __shared__ unsigned s_ticket;
@@ -272,7 +288,24 @@ __device__ __forceinline__ void sweep(const StreamDesc& d, uint32_t* __restrict_
       uint32_t carry_word = 0, nsw = 0;
       ld_word_if(lane == 31, p - 4, carry_word);
       ld_word_if(lane == 0, p + sb, nsw);
+#ifdef U8V_K2P_SKELETON
+      const unsigned t0 = __ldg(g_k2p_table + step), t1 = __ldg(g_k2p_table + step + 1);
+#endif
       e = step_errors_pairs(d, v, lane, carry_word, nsw, was_ascii);
+#ifdef U8V_K2P_SKELETON
+      const unsigned r = t0 + lane;
+      if (r <= t1 && r <= g_k2p_n) {
+        const uint64_t o = __ldg(g_k2p_offsets + r);
+#if U8V_K2P_SKELETON >= 2
+        const uint8_t* q = d.base + d.off32 + o;
+        uint32_t a = 0, b = 0;
+        if (o >= 4) a = *(const uint32_t*)((uintptr_t)(q - 4) & ~(uintptr_t)3);
+        b = *(const uint32_t*)((uintptr_t)q & ~(uintptr_t)3);
+        e |= (a & b) == 0xFFFFFFFFu ? 0x80000000u : 0u;
+#endif
+        e |= (uint32_t)(o >> 62);
+      }
+#endif
     } else {
       e = any_step_errors<false>(d, step, false, lane, unused, was_ascii);
     }
