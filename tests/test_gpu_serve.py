@@ -390,3 +390,22 @@ def test_server_cap_per_device():
     served = [s for s in stats if s and s[1] > 0]
     assert len(served) <= 32 and all(s[1] == 20 for s in served)
     assert sum(1 for s in stats if s == (0, 0)) == n_threads - len(served)
+
+
+def test_server_slots_return_at_thread_exit():
+    # 100 short-lived threads one after another, each with a server: the
+    # per-device slot goes back when a thread exits (thread_local release),
+    # so the 101st thread still gets one
+    b = np.frombuffer("déjà vu ✓".encode() * 20, np.uint8).copy()
+    stats = []
+
+    def worker():
+        for _ in range(3):
+            assert _validate(b)
+        stats.append(_stats())
+
+    for _ in range(101):
+        t = threading.Thread(target=worker)
+        t.start()
+        t.join()
+    assert len(stats) == 101 and all(s[1] == 3 and s[0] >= 1 for s in stats), stats[-3:]
